@@ -1,0 +1,160 @@
+/*
+ * pipefill.h — C ABI of the B200-native PipeFill fill-job executor (libpipefill.so).
+ *
+ * The reference (`bubblefill`, /root/reference/pkg) is a pure-Python planner and
+ * simulator: it has no FFI, no kernels and no device code. Its executor is a
+ * time model — ExecutionPlan.range_wall_us / range_busy_us
+ * (pkg/src/bubblefill/partition.py:118-132) consumed by the simulator's
+ * dispatch loop (pkg/src/bubblefill/sim.py:222-235). Each entry point below
+ * replaces a piece of that time model (or of the paper's DeepSpeed executor,
+ * PAPER.md:45-47,422-434) with real sm_100a execution. The cited reference
+ * line is the behaviour the entry point realises on the device.
+ *
+ * Conventions (all entry points):
+ *   - plain pointers and sizes only; device pointers are raw CUDA addresses,
+ *     `stream` is a cudaStream_t passed as void*; NULL = legacy default stream.
+ *   - return 0 (PF_OK) or a negative PF_ERR_* code; no exceptions cross the
+ *     ABI. pf_last_error() returns a thread-local message for the last failure.
+ *   - every compute kernel is asynchronous and PREEMPTIBLE through pf_ctl_t:
+ *     it polls the stage's bubble flag at work-unit (tile / row-block) granularity
+ *     and yields when the flag reads 0. Completion vs. yield is read back
+ *     afterwards from the control words (pf_ctl_t.cursor, .abort).
+ *   - tensors are bf16 row-major unless stated; accumulation is fp32.
+ */
+#ifndef PIPEFILL_H
+#define PIPEFILL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PF_ABI_VERSION 1
+
+#define PF_OK 0
+#define PF_ERR_INVALID (-1)     /* bad argument / shape / alignment */
+#define PF_ERR_CUDA (-2)        /* a CUDA runtime/driver call failed */
+#define PF_ERR_UNSUPPORTED (-3) /* no sm_100a device, or shape outside the kernel's envelope */
+#define PF_ERR_OOM (-4)         /* arena exhausted (fill job can never spill past its arena) */
+
+/* Preemption control for one kernel launch.
+ *   flag   : device u32, nonzero while the stage is inside a bubble. Set by the
+ *            engine's BUBBLE instruction, cleared by the main job's recv completion
+ *            (SURVEY §5 "Distributed comm backend"). NULL = run to
+ *            completion (non-preemptible, used by parity tests and profiling).
+ *   abort  : device u32, sticky. A launch that observes flag==0 sets it and exits;
+ *            any later launch of the same chain that sees abort!=0 exits at once
+ *            without touching its cursor. Required when flag != NULL.
+ *   cursor : device u32 work-claim counter of THIS launch. Work units are claimed
+ *            in increasing order, and a claimed unit always completes, so units
+ *            [0, min(*cursor, units)) are done: the resume cursor. Relaunching the
+ *            same call with the same cursor continues where it stopped. Must be 0
+ *            for a fresh launch. Required when flag != NULL.                      */
+typedef struct pf_ctl {
+  const uint32_t* flag;
+  uint32_t* abort;
+  uint32_t* cursor;
+} pf_ctl_t;
+
+/* ---- runtime --------------------------------------------------------------- */
+int pf_abi_version(void);
+const char* pf_last_error(void);
+/* Fails with PF_ERR_UNSUPPORTED unless the current device is sm_100 (B200). */
+int pf_device_check(int* sm_count_out);
+
+/* ---- fixed fill-job arena (no reference code) -------------
+ * One cudaMalloc of `bytes`, taken outside the framework caching allocator,
+ * sized from measured bubble free memory (min over bubbles of
+ * BubbleSpec.free_mem_bytes, pkg/src/bubblefill/pipeline.py:100-121). Bump
+ * allocation only; a request that does not fit returns PF_ERR_OOM instead of
+ * growing, so the fill job cannot take memory from the main job.                */
+typedef struct pf_arena pf_arena_t;
+int pf_arena_create(uint64_t bytes, pf_arena_t** out);
+int pf_arena_alloc(pf_arena_t* arena, uint64_t bytes, uint64_t align, void** out_dev_ptr);
+int pf_arena_mark(pf_arena_t* arena, uint64_t* out_mark);
+int pf_arena_release(pf_arena_t* arena, uint64_t mark); /* pop back to a mark */
+int pf_arena_reset(pf_arena_t* arena);
+int pf_arena_stats(pf_arena_t* arena, uint64_t* capacity, uint64_t* used, uint64_t* high_water);
+int pf_arena_base(pf_arena_t* arena, void** out_dev_ptr);
+int pf_arena_destroy(pf_arena_t* arena);
+
+/* ---- bubble flag (the BUBBLE instruction) -------------------
+ * pf_flag_create allocates a zeroed device u32. pf_flag_write_on_stream enqueues a
+ * stream-ordered 32-bit store (cuStreamWriteValue32): the engine writes 1 at the
+ * BUBBLE instruction and 0 after the recv that ends the bubble, on its comm stream.
+ * pf_flag_clear_at enqueues a one-thread kernel that spins on %globaltimer until
+ * `deadline_ns` and then stores 0: the 1-GPU stand-in for the neighbour's send
+ * (artificial bubbles, BASELINE.json north_star).                                */
+int pf_flag_create(uint32_t** out_dev_flag);
+int pf_flag_destroy(uint32_t* dev_flag);
+int pf_flag_write_on_stream(uint32_t* dev_flag, uint32_t value, void* stream);
+int pf_flag_clear_at(uint32_t* dev_flag, uint64_t deadline_ns, void* stream);
+/* Enqueue a kernel that spins until %globaltimer >= deadline_ns (timer-driven recv). */
+int pf_wait_until(uint64_t deadline_ns, void* stream);
+/* Enqueue a kernel writing the device %globaltimer (ns) into *dev_out. */
+int pf_read_globaltimer(uint64_t* dev_out, void* stream);
+
+/* ---- weight / activation staging ------------ */
+int pf_host_alloc_pinned(uint64_t bytes, void** out_host_ptr);
+int pf_host_free_pinned(void* host_ptr);
+int pf_stage_h2d(void* dst_dev, const void* src_pinned_host, uint64_t bytes, void* stream);
+int pf_stage_d2h(void* dst_pinned_host, const void* src_dev, uint64_t bytes, void* stream);
+
+/* ---- fill-job kernels (the partitioned forward) -------------- */
+
+/* Epilogue bits for pf_gemm. */
+#define PF_EPI_BIAS 1u     /* + bias[N]                                   */
+#define PF_EPI_GELU 2u     /* exact erf GELU (nn.GELU(approximate='none')) */
+#define PF_EPI_RESIDUAL 4u /* + residual[M,N] after the activation        */
+
+/* Y[M,N] = epi(X[M,K] · W[N,K]^T): nn.Linear layout. tcgen05.mma (kind::f16,
+ * fp32 accumulators in TMEM), TMA-fed 4-stage mbarrier pipeline, persistent CTAs,
+ * preemptible at output-tile granularity. K % 8 == 0, N % 8 == 0 (16 B rows).
+ * Work units = ceil(M/128) * ceil(N/BN) tiles; pf_gemm_units reports them.        */
+int pf_gemm(const void* X, const void* W, const void* bias, const void* residual, void* Y,
+            int M, int N, int K, uint32_t epilogue, const pf_ctl_t* ctl, void* stream);
+int pf_gemm_units(int M, int N, int K, uint32_t* out_units);
+
+/* Y = LayerNorm(X + residual) * gamma + beta, per row of `cols` (residual may be
+ * NULL). fp32 statistics, two-pass variance. Work units = ceil(rows/rows_per_unit). */
+int pf_layernorm(const void* X, const void* residual, const void* gamma, const void* beta,
+                 void* Y, int rows, int cols, float eps, const pf_ctl_t* ctl, void* stream);
+/* Y = X * rsqrt(mean((X+res)^2) + eps) * gamma. */
+int pf_rmsnorm(const void* X, const void* residual, const void* gamma, void* Y, int rows,
+               int cols, float eps, const pf_ctl_t* ctl, void* stream);
+int pf_norm_units(int rows, int cols, uint32_t* out_units);
+
+/* Row softmax: Y = softmax(X * scale) over `cols`, bf16 in/out, fp32 math.          */
+int pf_softmax(const void* X, void* Y, int rows, int cols, float scale, const pf_ctl_t* ctl,
+               void* stream);
+int pf_softmax_units(int rows, int cols, uint32_t* out_units);
+
+/* Non-causal multi-head attention over a packed QKV tensor, as produced by one
+ * [h -> 3h] projection: QKV[batch, seq, 3, heads, head_dim] -> O[batch, seq, heads,
+ * head_dim]. O = softmax(Q K^T * scale + mask) V per (batch, head). mask_add may be
+ * NULL or an additive fp32 [batch, seq] key mask. seq <= 128, head_dim == 64.
+ * Work units = batch * heads.                                                       */
+int pf_attention(const void* QKV, const float* mask_add, void* O, int batch, int seq,
+                 int heads, int head_dim, float scale, const pf_ctl_t* ctl, void* stream);
+int pf_attention_units(int batch, int seq, int heads, int head_dim, uint32_t* out_units);
+
+/* BERT embeddings: Y[t] = LN(word[ids[t]] + pos[t % seq] + type[tt[t]]) (tt may be
+ * NULL = segment 0). ids/tt int32 [batch*seq].                                       */
+int pf_embedding_ln(const int32_t* ids, const int32_t* type_ids, const void* word,
+                    const void* pos, const void* type, const void* gamma, const void* beta,
+                    void* Y, int batch, int seq, int hidden, int vocab, float eps,
+                    const pf_ctl_t* ctl, void* stream);
+
+/* ---- chain control ------------------------------------------------------------
+ * Resets the per-node cursors of a chain when the chain has not been aborted
+ * (a one-thread kernel: `if (!*abort) cursors[0..n) = 0`), and counts completed
+ * chain runs (`if (!*abort) ++*done`). Used to bracket one batch of a partition. */
+int pf_chain_begin(uint32_t* cursors, int n, const uint32_t* abort, void* stream);
+int pf_chain_end(uint32_t* done_counter, const uint32_t* abort, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIPEFILL_H */

@@ -1,0 +1,113 @@
+"""ORACLE — test infrastructure only. Never imported by the product path.
+
+CPU fp32 restatement of the fill job's forward pass, the "reference CPU torch
+execution" the north star (BASELINE.json) names as the numerics oracle for the
+executor kernels. Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference leg may import this module.
+
+Parity status: UNPINNED by the reference. The reference package has no tensor
+code at all (no torch/numpy math on the executor path), so there
+is no golden vector for fill-job numerics. The semantics restated here are those
+the paper gives for the fill executor — an nn.Sequential run partition by
+partition over layer-index boundaries (partition.py:89-132) —
+with BERT's standard post-LN encoder layer (exact erf GELU, LayerNorm eps 1e-12,
+softmax attention in fp32). Tolerances (north star): bf16 path rel 2e-2 of this.
+
+Explicit ops only: no nn.TransformerEncoderLayer fast path, no SDPA.
+"""
+
+from __future__ import annotations
+
+import math
+from typing import Optional
+
+import torch
+
+
+def linear(x: torch.Tensor, w: torch.Tensor, b: Optional[torch.Tensor] = None, *,
+           gelu: bool = False, residual: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """y = [gelu](x @ w.T + b) [+ residual], fp32."""
+    y = x.float() @ w.float().T
+    if b is not None:
+        y = y + b.float()
+    if gelu:
+        y = 0.5 * y * (1.0 + torch.erf(y / math.sqrt(2.0)))
+    if residual is not None:
+        y = y + residual.float()
+    return y
+
+
+def layernorm(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, eps: float) -> torch.Tensor:
+    x = x.float()
+    mean = x.mean(-1, keepdim=True)
+    var = ((x - mean) ** 2).mean(-1, keepdim=True)
+    return (x - mean) / torch.sqrt(var + eps) * gamma.float() + beta.float()
+
+
+def rmsnorm(x: torch.Tensor, gamma: torch.Tensor, eps: float) -> torch.Tensor:
+    x = x.float()
+    return x * torch.rsqrt((x * x).mean(-1, keepdim=True) + eps) * gamma.float()
+
+
+def softmax(x: torch.Tensor, scale: float = 1.0) -> torch.Tensor:
+    z = x.float() * scale
+    z = z - z.max(-1, keepdim=True).values
+    e = torch.exp(z)
+    return e / e.sum(-1, keepdim=True)
+
+
+def attention(qkv: torch.Tensor, heads: int, mask_add: Optional[torch.Tensor] = None,
+              scale: Optional[float] = None) -> torch.Tensor:
+    """qkv [B, S, 3*hidden] packed as (3, heads, d) -> [B, S, hidden]."""
+    b, s, three_h = qkv.shape
+    hidden = three_h // 3
+    d = hidden // heads
+    if scale is None:
+        scale = d ** -0.5
+    t = qkv.float().view(b, s, 3, heads, d)
+    q = t[:, :, 0].permute(0, 2, 1, 3)  # [B, H, S, d]
+    k = t[:, :, 1].permute(0, 2, 1, 3)
+    v = t[:, :, 2].permute(0, 2, 1, 3)
+    scores = (q @ k.transpose(-1, -2)) * scale
+    if mask_add is not None:
+        scores = scores + mask_add.float()[:, None, None, :]
+    p = softmax(scores)
+    o = p @ v  # [B, H, S, d]
+    return o.permute(0, 2, 1, 3).reshape(b, s, hidden)
+
+
+def embedding_ln(ids: torch.Tensor, word: torch.Tensor, pos: torch.Tensor, typ: torch.Tensor,
+                 gamma: torch.Tensor, beta: torch.Tensor, eps: float,
+                 type_ids: Optional[torch.Tensor] = None) -> torch.Tensor:
+    b, s = ids.shape
+    x = word.float()[ids.long()] + pos.float()[:s][None, :, :]
+    tt = torch.zeros_like(ids) if type_ids is None else type_ids
+    x = x + typ.float()[tt.long()]
+    return layernorm(x, gamma, beta, eps)
+
+
+def bert_layer(x: torch.Tensor, p: dict, heads: int, eps: float = 1e-12,
+               mask_add: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """One post-LN BERT encoder layer on [B, S, h] with weights dict `p` (fp32 math)."""
+    b, s, h = x.shape
+    x2 = x.float().reshape(b * s, h)
+    qkv = linear(x2, p["qkv_w"], p["qkv_b"]).reshape(b, s, 3 * h)
+    ctx = attention(qkv, heads, mask_add).reshape(b * s, h)
+    a = linear(ctx, p["out_w"], p["out_b"], residual=x2)
+    a = layernorm(a, p["ln1_g"], p["ln1_b"], eps)
+    f = linear(a, p["ffn1_w"], p["ffn1_b"], gelu=True)
+    o = linear(f, p["ffn2_w"], p["ffn2_b"], residual=a)
+    o = layernorm(o, p["ln2_g"], p["ln2_b"], eps)
+    return o.reshape(b, s, h)
+
+
+def bert_embeddings(ids: torch.Tensor, p: dict, eps: float = 1e-12) -> torch.Tensor:
+    return embedding_ln(ids, p["word"], p["pos"], p["type"], p["ln_g"], p["ln_b"], eps)
+
+
+def run_sequential(modules: list, x, lo: int, hi: int):
+    """Run modules[lo:hi] in order — one partition of the linearized model
+    (ExecutionPlan partition [lo, hi), pkg/src/bubblefill/partition.py:64-86)."""
+    for i in range(lo, hi):
+        x = modules[i](x)
+    return x

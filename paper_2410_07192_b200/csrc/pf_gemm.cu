@@ -1,0 +1,442 @@
+// pf_gemm.cu — preemptible persistent tcgen05 GEMM with fused bias / GELU / residual.
+//
+//   Y[M,N] = epi( X[M,K] · W[N,K]^T )      (nn.Linear weight layout, bf16 in, fp32 acc)
+//
+// This is the fill job's dominant kernel (QKV / attention-out / FFN1 / FFN2 of
+// every BERT layer, SURVEY §2.1 "gemm_bias_gelu"). The reference has no kernel:
+// its executor is the time model ExecutionPlan.range_busy_us
+// (pkg/src/bubblefill/partition.py:126-132); this kernel is what that time is
+// spent on.
+//
+// Structure (one CTA per SM, persistent, 384 threads):
+//   warp 0      tile scheduler + TMA producer (A/B k-blocks into a STAGES-deep ring)
+//   warp 1      MMA issuer: one lane issues tcgen05.mma 128xBNx16 into TMEM
+//   warp 2      TMEM allocator (2 accumulator buffers of BN fp32 columns)
+//   warp 3      idle
+//   warps 4-11  epilogue: tcgen05.ld -> bias/GELU/residual -> bf16 -> global
+// The scheduler claims output tiles from the launch's cursor only while the
+// bubble flag is set (pf::claim_unit), so the kernel yields within one tile
+// of the flag clearing and the claimed-tile prefix is the resume cursor.
+#include <stdio.h>
+
+#include "pf_common.cuh"
+
+namespace pf {
+namespace gemm {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = 128 B rows -> SWIZZLE_128B
+constexpr int UMMA_K = 16;
+constexpr int NUM_THREADS = 384;
+constexpr int EPI_WARP0 = 4;
+constexpr int NUM_EPI_WARPS = 8;
+constexpr int SCHED_SLOTS = 8;
+constexpr int SMEM_BUDGET = 200 * 1024;
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (SMEM_BUDGET / STAGE_BYTES) > 6 ? 6 : (SMEM_BUDGET / STAGE_BYTES);
+  static constexpr int TMEM_COLS = (2 * BN <= 256) ? 256 : 512;
+  static constexpr int COLS_PER_EPI_WARP = BN / 2;  // two warps share each 32-lane group
+  static constexpr int CHUNKS = COLS_PER_EPI_WARP / 32;
+  // barriers + sched ring + tmem addr live after the operand ring
+  static constexpr int BAR_BYTES = (2 * STAGES + 4 + 2 * SCHED_SLOTS) * 8 + SCHED_SLOTS * 4 + 16;
+  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + BAR_BYTES;
+  static_assert(BN % 64 == 0 && BN <= 256, "BN");
+  static_assert(COLS_PER_EPI_WARP % 32 == 0, "epilogue chunking");
+};
+
+struct Params {
+  __nv_bfloat16* Y;
+  const __nv_bfloat16* bias;
+  const __nv_bfloat16* residual;
+  int M, N, K;
+  uint32_t epi;
+  int tiles_m, tiles_n;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                Params p, Ctl ctl) {
+  using C = Cfg<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-B alignment for the swizzled operand tiles
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* full_bar = bars;
+  uint64_t* empty_bar = bars + C::STAGES;
+  uint64_t* tfull_bar = bars + 2 * C::STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint64_t* sfull_bar = tempty_bar + 2;
+  uint64_t* sempty_bar = sfull_bar + SCHED_SLOTS;
+  int* sched_tile = reinterpret_cast<int*>(sempty_bar + SCHED_SLOTS);
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(sched_tile + SCHED_SLOTS);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+
+  if (chain_aborted(ctl)) return;  // uniform across the CTA: nothing allocated yet
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], NUM_EPI_WARPS);
+    }
+    for (int s = 0; s < SCHED_SLOTS; ++s) {
+      mbar_init(&sfull_bar[s], 1);
+      mbar_init(&sempty_bar[s], 1 + NUM_EPI_WARPS);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_base_smem, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_smem;
+
+  const int num_tiles = p.tiles_m * p.tiles_n;
+  const int num_kb = (p.K + BK - 1) / BK;
+
+  if (warp == 0) {
+    // ---------------- scheduler + TMA producer ----------------
+    int slot = 0;
+    uint32_t sphase = 0;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int it = 0;; ++it) {
+      int tile = -1;
+      if (lane == 0) tile = claim_unit(ctl, num_tiles, it);
+      tile = __shfl_sync(0xffffffffu, tile, 0);
+      mbar_wait(&sempty_bar[slot], sphase ^ 1u);
+      if (lane == 0) {
+        sched_tile[slot] = tile;
+        mbar_arrive(&sfull_bar[slot]);
+      }
+      if (++slot == SCHED_SLOTS) {
+        slot = 0;
+        sphase ^= 1u;
+      }
+      if (tile < 0) break;
+      const int tm = tile % p.tiles_m;
+      const int tn = tile / p.tiles_m;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&empty_bar[stage], phase ^ 1u);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+          tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full_bar[stage], kb * BK, tm * BM);
+          tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full_bar[stage], kb * BK, tn * BN);
+        }
+        __syncwarp();
+        if (++stage == C::STAGES) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, false, false);
+    int slot = 0;
+    uint32_t sphase = 0;
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t aphase = 0;
+    while (true) {
+      mbar_wait(&sfull_bar[slot], sphase);
+      const int tile = sched_tile[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sempty_bar[slot]);
+      if (++slot == SCHED_SLOTS) {
+        slot = 0;
+        sphase ^= 1u;
+      }
+      if (tile < 0) break;
+      mbar_wait(&tempty_bar[acc], aphase ^ 1u);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; ++k) {
+            // K advance inside the 128-B swizzle atom: +32 B per UMMA_K step
+            const uint64_t ad = umma_desc_sw128_kmajor(a_addr + k * UMMA_K * 2);
+            const uint64_t bd = umma_desc_sw128_kmajor(b_addr + k * UMMA_K * 2);
+            umma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs retire
+        }
+        __syncwarp();
+        if (++stage == C::STAGES) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+      if (lane == 0) umma_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        aphase ^= 1u;
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ---------------- epilogue ----------------
+    const int e = warp - EPI_WARP0;
+    const int lane_grp = warp & 3;  // TMEM lanes [32*lane_grp, +32) are visible to this warp
+    const int col_half = e >> 2;
+    int slot = 0;
+    uint32_t sphase = 0;
+    int acc = 0;
+    uint32_t aphase = 0;
+    const bool has_bias = (p.epi & PF_EPI_BIAS) != 0;
+    const bool has_gelu = (p.epi & PF_EPI_GELU) != 0;
+    const bool has_res = (p.epi & PF_EPI_RESIDUAL) != 0;
+    while (true) {
+      mbar_wait(&sfull_bar[slot], sphase);
+      const int tile = sched_tile[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sempty_bar[slot]);
+      if (++slot == SCHED_SLOTS) {
+        slot = 0;
+        sphase ^= 1u;
+      }
+      if (tile < 0) break;
+      const int tm = tile % p.tiles_m;
+      const int tn = tile / p.tiles_m;
+      mbar_wait(&tfull_bar[acc], aphase);
+      tc_fence_after();
+      const int row = tm * BM + lane_grp * 32 + lane;
+      const bool row_ok = row < p.M;
+#pragma unroll 1
+      for (int c = 0; c < C::CHUNKS; ++c) {
+        const int col_in_tile = col_half * C::COLS_PER_EPI_WARP + c * 32;
+        const uint32_t taddr =
+            tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(acc * BN + col_in_tile);
+        uint32_t r[32];
+        __syncwarp();
+        tmem_ld_32x32b_x32(taddr, r);
+        tmem_ld_wait();
+        const int col0 = tn * BN + col_in_tile;
+        if (row_ok && col0 < p.N) {
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        const bool full = col0 + 32 <= p.N;
+        if (has_bias) {
+          if (full) {
+            const uint4* bp = reinterpret_cast<const uint4*>(p.bias + col0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint4 b4 = __ldg(bp + q);
+              const uint32_t bw[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+              for (int h = 0; h < 4; ++h) {
+                float2 f = unpack_bf16x2(bw[h]);
+                v[q * 8 + h * 2] += f.x;
+                v[q * 8 + h * 2 + 1] += f.y;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < p.N) v[j] += __bfloat162float(p.bias[col0 + j]);
+          }
+        }
+        if (has_gelu) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+        }
+        __nv_bfloat16* yrow = p.Y + (size_t)row * p.N;
+        if (has_res) {
+          const __nv_bfloat16* rrow = p.residual + (size_t)row * p.N;
+          if (full) {
+            const uint4* rp = reinterpret_cast<const uint4*>(rrow + col0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint4 r4 = rp[q];
+              const uint32_t rw[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+              for (int h = 0; h < 4; ++h) {
+                float2 f = unpack_bf16x2(rw[h]);
+                v[q * 8 + h * 2] += f.x;
+                v[q * 8 + h * 2 + 1] += f.y;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < p.N) v[j] += __bfloat162float(rrow[col0 + j]);
+          }
+        }
+        if (full) {
+          uint4* yp = reinterpret_cast<uint4*>(yrow + col0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 o;
+            o.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
+            o.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
+            o.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
+            o.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
+            yp[q] = o;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col0 + j < p.N) yrow[col0 + j] = __float2bfloat16_rn(v[j]);
+        }
+        }  // row_ok && col0 < N
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        aphase ^= 1u;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem_base, C::TMEM_COLS);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+// 2-D bf16 row-major [rows, cols] tensor, box [box_rows, 64 cols], 128-B swizzle.
+static int make_tmap(CUtensorMap* map, const void* base, int rows, int cols, int box_rows) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return set_error(PF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(PF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return PF_OK;
+}
+
+// BN choice: minimise (waves x BN), the per-SM tensor-pipe time, on 148 SMs.
+static int pick_bn(int M, int N) {
+  const int sms = device_sm_count();
+  const int cands[3] = {256, 192, 128};
+  int best = 256;
+  long best_cost = -1;
+  for (int bn : cands) {
+    long tiles = (long)((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+    long waves = (tiles + sms - 1) / sms;
+    long cost = waves * bn;
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = bn;
+    }
+  }
+  return best;
+}
+
+template <int BN>
+static int launch(const void* X, const void* W, const void* bias, const void* residual, void* Y,
+                  int M, int N, int K, uint32_t epi, const pf_ctl_t* ctl, cudaStream_t stream) {
+  using C = Cfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    PF_CUDA(cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::SMEM_BYTES));
+    attr_set = true;
+  }
+  CUtensorMap ta, tb;
+  PF_TRY(make_tmap(&ta, X, M, K, BM));
+  PF_TRY(make_tmap(&tb, W, N, K, BN));
+  Params p;
+  p.Y = reinterpret_cast<__nv_bfloat16*>(Y);
+  p.bias = reinterpret_cast<const __nv_bfloat16*>(bias);
+  p.residual = reinterpret_cast<const __nv_bfloat16*>(residual);
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.epi = epi;
+  p.tiles_m = (M + BM - 1) / BM;
+  p.tiles_n = (N + BN - 1) / BN;
+  const int tiles = p.tiles_m * p.tiles_n;
+  const int sms = device_sm_count();
+  const int grid = tiles < sms ? tiles : sms;
+  gemm_kernel<BN><<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(ta, tb, p, make_ctl(ctl));
+  PF_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+}  // namespace gemm
+}  // namespace pf
+
+extern "C" int pf_gemm_units(int M, int N, int K, uint32_t* out_units) {
+  using namespace pf;
+  if (!out_units || M <= 0 || N <= 0 || K <= 0) return set_error(PF_ERR_INVALID, "pf_gemm_units");
+  const int bn = gemm::pick_bn(M, N);
+  *out_units = (uint32_t)(((M + gemm::BM - 1) / gemm::BM) * ((N + bn - 1) / bn));
+  return PF_OK;
+}
+
+extern "C" int pf_gemm(const void* X, const void* W, const void* bias, const void* residual,
+                       void* Y, int M, int N, int K, uint32_t epilogue, const pf_ctl_t* ctl,
+                       void* stream) {
+  using namespace pf;
+  if (!X || !W || !Y || M <= 0 || N <= 0 || K <= 0)
+    return set_error(PF_ERR_INVALID, "pf_gemm: null pointer or non-positive shape");
+  if (K % 8 != 0 || N % 8 != 0)
+    return set_error(PF_ERR_INVALID, "pf_gemm: K and N must be multiples of 8 (16-B rows)");
+  if ((epilogue & PF_EPI_BIAS) && !bias) return set_error(PF_ERR_INVALID, "pf_gemm: bias is NULL");
+  if ((epilogue & PF_EPI_RESIDUAL) && !residual)
+    return set_error(PF_ERR_INVALID, "pf_gemm: residual is NULL");
+  if (((uintptr_t)X | (uintptr_t)W | (uintptr_t)Y | (uintptr_t)bias | (uintptr_t)residual) & 15u)
+    return set_error(PF_ERR_INVALID, "pf_gemm: pointers must be 16-B aligned");
+  PF_TRY(validate_ctl(ctl));
+  if (!device_is_sm100()) return set_error(PF_ERR_UNSUPPORTED, "pf_gemm: needs an sm_100 device");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  switch (gemm::pick_bn(M, N)) {
+    case 256:
+      return gemm::launch<256>(X, W, bias, residual, Y, M, N, K, epilogue, ctl, s);
+    case 192:
+      return gemm::launch<192>(X, W, bias, residual, Y, M, N, K, epilogue, ctl, s);
+    default:
+      return gemm::launch<128>(X, W, bias, residual, Y, M, N, K, epilogue, ctl, s);
+  }
+}

@@ -1,0 +1,230 @@
+"""Tensor-level wrappers over the sm_100a fill-job kernels (libpipefill.so).
+
+torch is used here for device memory and stream handles only; every op below
+is one call through the C ABI (include/pipefill.h) into a hand-written kernel.
+Each op takes an optional :class:`KernelCtl` that makes the launch preemptible
+by the stage's bubble flag (see pf_ctl_t).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from . import native
+from .native import PF_EPI_BIAS, PF_EPI_GELU, PF_EPI_RESIDUAL, PfCtl
+
+
+@dataclass
+class KernelCtl:
+    """Device addresses of one launch's preemption words (flag, abort, cursor)."""
+
+    flag: int = 0
+    abort: int = 0
+    cursor: int = 0
+
+    def as_struct(self) -> PfCtl:
+        return PfCtl(self.flag or None, self.abort or None, self.cursor or None)
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream: Optional[torch.cuda.Stream]) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _ctl_ref(ctl: Optional[KernelCtl]):
+    return None if ctl is None else ctypes.byref(ctl.as_struct())
+
+
+def _check_bf16_cuda(name: str, t: torch.Tensor) -> None:
+    if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous bf16 CUDA tensor, got {t.dtype} {t.device}")
+
+
+def gemm_units(m: int, n: int, k: int) -> int:
+    out = ctypes.c_uint32(0)
+    native.call("pf_gemm_units", m, n, k, ctypes.byref(out))
+    return out.value
+
+
+def norm_units(rows: int, cols: int) -> int:
+    out = ctypes.c_uint32(0)
+    native.call("pf_norm_units", rows, cols, ctypes.byref(out))
+    return out.value
+
+
+def attention_units(batch: int, seq: int, heads: int, head_dim: int) -> int:
+    out = ctypes.c_uint32(0)
+    native.call("pf_attention_units", batch, seq, heads, head_dim, ctypes.byref(out))
+    return out.value
+
+
+def linear(
+    x: torch.Tensor,
+    weight: torch.Tensor,
+    bias: Optional[torch.Tensor] = None,
+    *,
+    gelu: bool = False,
+    residual: Optional[torch.Tensor] = None,
+    out: Optional[torch.Tensor] = None,
+    ctl: Optional[KernelCtl] = None,
+    stream: Optional[torch.cuda.Stream] = None,
+) -> torch.Tensor:
+    """out = [GELU](x @ weight.T + bias) [+ residual] — tcgen05 GEMM (pf_gemm)."""
+    _check_bf16_cuda("x", x)
+    _check_bf16_cuda("weight", weight)
+    k = x.shape[-1]
+    m = x.numel() // k
+    n = weight.shape[0]
+    if weight.shape[1] != k:
+        raise ValueError(f"weight shape {tuple(weight.shape)} does not match in_features {k}")
+    epi = 0
+    if bias is not None:
+        _check_bf16_cuda("bias", bias)
+        epi |= PF_EPI_BIAS
+    if gelu:
+        epi |= PF_EPI_GELU
+    if residual is not None:
+        _check_bf16_cuda("residual", residual)
+        epi |= PF_EPI_RESIDUAL
+    if out is None:
+        out = torch.empty(*x.shape[:-1], n, dtype=torch.bfloat16, device=x.device)
+    native.call(
+        "pf_gemm", x.data_ptr(), weight.data_ptr(), _ptr(bias), _ptr(residual), out.data_ptr(),
+        m, n, k, epi, _ctl_ref(ctl), _stream(stream),
+    )
+    return out
+
+
+def layernorm(
+    x: torch.Tensor,
+    gamma: torch.Tensor,
+    beta: torch.Tensor,
+    eps: float = 1e-12,
+    *,
+    residual: Optional[torch.Tensor] = None,
+    out: Optional[torch.Tensor] = None,
+    ctl: Optional[KernelCtl] = None,
+    stream: Optional[torch.cuda.Stream] = None,
+) -> torch.Tensor:
+    """out = LayerNorm(x [+ residual]) (pf_layernorm)."""
+    _check_bf16_cuda("x", x)
+    cols = x.shape[-1]
+    rows = x.numel() // cols
+    if out is None:
+        out = torch.empty_like(x)
+    native.call(
+        "pf_layernorm", x.data_ptr(), _ptr(residual), gamma.data_ptr(), beta.data_ptr(),
+        out.data_ptr(), rows, cols, float(eps), _ctl_ref(ctl), _stream(stream),
+    )
+    return out
+
+
+def rmsnorm(
+    x: torch.Tensor,
+    gamma: torch.Tensor,
+    eps: float = 1e-6,
+    *,
+    residual: Optional[torch.Tensor] = None,
+    out: Optional[torch.Tensor] = None,
+    ctl: Optional[KernelCtl] = None,
+    stream: Optional[torch.cuda.Stream] = None,
+) -> torch.Tensor:
+    """out = RMSNorm(x [+ residual]) (pf_rmsnorm)."""
+    _check_bf16_cuda("x", x)
+    cols = x.shape[-1]
+    rows = x.numel() // cols
+    if out is None:
+        out = torch.empty_like(x)
+    native.call(
+        "pf_rmsnorm", x.data_ptr(), _ptr(residual), gamma.data_ptr(), out.data_ptr(), rows, cols,
+        float(eps), _ctl_ref(ctl), _stream(stream),
+    )
+    return out
+
+
+def softmax(
+    x: torch.Tensor,
+    scale: float = 1.0,
+    *,
+    out: Optional[torch.Tensor] = None,
+    ctl: Optional[KernelCtl] = None,
+    stream: Optional[torch.cuda.Stream] = None,
+) -> torch.Tensor:
+    """out = softmax(scale * x, dim=-1) (pf_softmax)."""
+    _check_bf16_cuda("x", x)
+    cols = x.shape[-1]
+    rows = x.numel() // cols
+    if out is None:
+        out = torch.empty_like(x)
+    native.call(
+        "pf_softmax", x.data_ptr(), out.data_ptr(), rows, cols, float(scale), _ctl_ref(ctl),
+        _stream(stream),
+    )
+    return out
+
+
+def attention(
+    qkv: torch.Tensor,
+    heads: int,
+    *,
+    mask_add: Optional[torch.Tensor] = None,
+    scale: Optional[float] = None,
+    out: Optional[torch.Tensor] = None,
+    ctl: Optional[KernelCtl] = None,
+    stream: Optional[torch.cuda.Stream] = None,
+) -> torch.Tensor:
+    """Multi-head attention over packed qkv [batch, seq, 3*hidden] -> [batch, seq, hidden]."""
+    _check_bf16_cuda("qkv", qkv)
+    batch, seq, three_h = qkv.shape
+    hidden = three_h // 3
+    head_dim = hidden // heads
+    if scale is None:
+        scale = head_dim ** -0.5
+    if mask_add is not None:
+        if mask_add.dtype != torch.float32 or mask_add.shape != (batch, seq):
+            raise ValueError("mask_add must be fp32 [batch, seq]")
+        mask_add = mask_add.contiguous()
+    if out is None:
+        out = torch.empty(batch, seq, hidden, dtype=torch.bfloat16, device=qkv.device)
+    native.call(
+        "pf_attention", qkv.data_ptr(), _ptr(mask_add), out.data_ptr(), batch, seq, heads,
+        head_dim, float(scale), _ctl_ref(ctl), _stream(stream),
+    )
+    return out
+
+
+def embedding_ln(
+    ids: torch.Tensor,
+    word: torch.Tensor,
+    pos: torch.Tensor,
+    type_emb: torch.Tensor,
+    gamma: torch.Tensor,
+    beta: torch.Tensor,
+    eps: float = 1e-12,
+    *,
+    type_ids: Optional[torch.Tensor] = None,
+    out: Optional[torch.Tensor] = None,
+    ctl: Optional[KernelCtl] = None,
+    stream: Optional[torch.cuda.Stream] = None,
+) -> torch.Tensor:
+    """BERT embeddings + LayerNorm (pf_embedding_ln); ids int32 [batch, seq]."""
+    if ids.dtype != torch.int32 or not ids.is_cuda:
+        raise ValueError("ids must be int32 on CUDA")
+    batch, seq = ids.shape
+    hidden = word.shape[1]
+    if out is None:
+        out = torch.empty(batch, seq, hidden, dtype=torch.bfloat16, device=ids.device)
+    native.call(
+        "pf_embedding_ln", ids.data_ptr(), _ptr(type_ids), word.data_ptr(), pos.data_ptr(),
+        type_emb.data_ptr(), gamma.data_ptr(), beta.data_ptr(), out.data_ptr(), batch, seq, hidden,
+        word.shape[0], float(eps), _ctl_ref(ctl), _stream(stream),
+    )
+    return out
