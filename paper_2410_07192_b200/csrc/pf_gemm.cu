@@ -43,7 +43,8 @@ struct Cfg {
   static constexpr int COLS_PER_EPI_WARP = BN / 2;  // two warps share each 32-lane group
   static constexpr int CHUNKS = COLS_PER_EPI_WARP / 32;
   // barriers + sched ring + tmem addr live after the operand ring
-  static constexpr int BAR_BYTES = (2 * STAGES + 4 + 2 * SCHED_SLOTS) * 8 + SCHED_SLOTS * 4 + 16;
+  static constexpr int BAR_BYTES = (2 * STAGES + 4 + 2 * SCHED_SLOTS) * 8 + SCHED_SLOTS * 4 + 16 +
+                                   NUM_EPI_WARPS * COLS_PER_EPI_WARP * 2;
   static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + BAR_BYTES;
   static_assert(BN % 64 == 0 && BN <= 256, "BN");
   static_assert(COLS_PER_EPI_WARP % 32 == 0, "epilogue chunking");
@@ -54,11 +55,10 @@ struct Params {
   const __nv_bfloat16* bias;
   const __nv_bfloat16* residual;
   int M, N, K;
-  uint32_t epi;
   int tiles_m, tiles_n;
 };
 
-template <int BN>
+template <int BN, uint32_t EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 Params p, Ctl ctl) {
@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* sempty_bar = sfull_bar + SCHED_SLOTS;
   int* sched_tile = reinterpret_cast<int*>(sempty_bar + SCHED_SLOTS);
   uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(sched_tile + SCHED_SLOTS);
+  __nv_bfloat16* bias_smem = reinterpret_cast<__nv_bfloat16*>(tmem_base_smem + 4);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -198,16 +199,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= EPI_WARP0) {
     // ---------------- epilogue ----------------
+    constexpr bool HAS_BIAS = (EPI & PF_EPI_BIAS) != 0;
+    constexpr bool HAS_GELU = (EPI & PF_EPI_GELU) != 0;
+    constexpr bool HAS_RES = (EPI & PF_EPI_RESIDUAL) != 0;
     const int e = warp - EPI_WARP0;
     const int lane_grp = warp & 3;  // TMEM lanes [32*lane_grp, +32) are visible to this warp
     const int col_half = e >> 2;
+    __nv_bfloat16* my_bias = bias_smem + e * C::COLS_PER_EPI_WARP;
     int slot = 0;
     uint32_t sphase = 0;
     int acc = 0;
     uint32_t aphase = 0;
-    const bool has_bias = (p.epi & PF_EPI_BIAS) != 0;
-    const bool has_gelu = (p.epi & PF_EPI_GELU) != 0;
-    const bool has_res = (p.epi & PF_EPI_RESIDUAL) != 0;
     while (true) {
       mbar_wait(&sfull_bar[slot], sphase);
       const int tile = sched_tile[slot];
@@ -220,11 +222,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (tile < 0) break;
       const int tm = tile % p.tiles_m;
       const int tn = tile / p.tiles_m;
-      mbar_wait(&tfull_bar[acc], aphase);
-      tc_fence_after();
       const int row = tm * BM + lane_grp * 32 + lane;
       const bool row_ok = row < p.M;
-#pragma unroll 1
+      const int col_base = tn * BN + col_half * C::COLS_PER_EPI_WARP;
+      // Stage this warp's bias slice in shared memory while the MMAs run.
+      if (HAS_BIAS) {
+        for (int j = lane * 8; j < C::COLS_PER_EPI_WARP; j += 32 * 8) {
+          uint4 b4 = make_uint4(0, 0, 0, 0);
+          if (col_base + j + 8 <= p.N) {
+            b4 = __ldg(reinterpret_cast<const uint4*>(p.bias + col_base + j));
+          } else {
+            __nv_bfloat16 tmp[8];
+            for (int q = 0; q < 8; ++q)
+              tmp[q] = col_base + j + q < p.N ? p.bias[col_base + j + q] : __float2bfloat16(0.f);
+            b4 = *reinterpret_cast<uint4*>(tmp);
+          }
+          *reinterpret_cast<uint4*>(my_bias + j) = b4;
+        }
+        __syncwarp();
+      }
+      const __nv_bfloat16* rrow = HAS_RES ? p.residual + (size_t)row * p.N : nullptr;
+      uint4 res_cur[4], res_nxt[4];
+      if (HAS_RES && row_ok && col_base + 32 <= p.N) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) res_cur[q] = reinterpret_cast<const uint4*>(rrow + col_base)[q];
+      }
+      mbar_wait(&tfull_bar[acc], aphase);
+      tc_fence_after();
+#pragma unroll
       for (int c = 0; c < C::CHUNKS; ++c) {
         const int col_in_tile = col_half * C::COLS_PER_EPI_WARP + c * 32;
         const uint32_t taddr =
@@ -232,19 +257,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t r[32];
         __syncwarp();
         tmem_ld_32x32b_x32(taddr, r);
-        tmem_ld_wait();
-        const int col0 = tn * BN + col_in_tile;
-        if (row_ok && col0 < p.N) {
-        float v[32];
+        const int col0 = col_base + c * 32;
+        if (HAS_RES && c + 1 < C::CHUNKS && row_ok && col0 + 64 <= p.N) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        const bool full = col0 + 32 <= p.N;
-        if (has_bias) {
-          if (full) {
-            const uint4* bp = reinterpret_cast<const uint4*>(p.bias + col0);
+          for (int q = 0; q < 4; ++q) res_nxt[q] = reinterpret_cast<const uint4*>(rrow + col0 + 32)[q];
+        }
+        tmem_ld_wait();
+        if (row_ok && col0 < p.N) {
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          const bool full = col0 + 32 <= p.N;
+          if (HAS_BIAS) {
+            const uint4* bp = reinterpret_cast<const uint4*>(my_bias + c * 32);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              uint4 b4 = __ldg(bp + q);
+              uint4 b4 = bp[q];
               const uint32_t bw[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
               for (int h = 0; h < 4; ++h) {
@@ -253,55 +281,51 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 v[q * 8 + h * 2 + 1] += f.y;
               }
             }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (col0 + j < p.N) v[j] += __bfloat162float(p.bias[col0 + j]);
           }
-        }
-        if (has_gelu) {
+          if (HAS_GELU) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
-        }
-        __nv_bfloat16* yrow = p.Y + (size_t)row * p.N;
-        if (has_res) {
-          const __nv_bfloat16* rrow = p.residual + (size_t)row * p.N;
+            for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
+          }
+          __nv_bfloat16* yrow = p.Y + (size_t)row * p.N;
+          if (HAS_RES) {
+            if (full) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t rw[4] = {res_cur[q].x, res_cur[q].y, res_cur[q].z, res_cur[q].w};
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                  float2 f = unpack_bf16x2(rw[h]);
+                  v[q * 8 + h * 2] += f.x;
+                  v[q * 8 + h * 2 + 1] += f.y;
+                }
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (col0 + j < p.N) v[j] += __bfloat162float(rrow[col0 + j]);
+            }
+          }
           if (full) {
-            const uint4* rp = reinterpret_cast<const uint4*>(rrow + col0);
+            uint4* yp = reinterpret_cast<uint4*>(yrow + col0);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              uint4 r4 = rp[q];
-              const uint32_t rw[4] = {r4.x, r4.y, r4.z, r4.w};
-#pragma unroll
-              for (int h = 0; h < 4; ++h) {
-                float2 f = unpack_bf16x2(rw[h]);
-                v[q * 8 + h * 2] += f.x;
-                v[q * 8 + h * 2 + 1] += f.y;
-              }
+              uint4 o;
+              o.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
+              o.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
+              o.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
+              o.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
+              yp[q] = o;
             }
           } else {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (col0 + j < p.N) v[j] += __bfloat162float(rrow[col0 + j]);
+              if (col0 + j < p.N) yrow[col0 + j] = __float2bfloat16_rn(v[j]);
           }
         }
-        if (full) {
-          uint4* yp = reinterpret_cast<uint4*>(yrow + col0);
+        if (HAS_RES) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 o;
-            o.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
-            o.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
-            o.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
-            o.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
-            yp[q] = o;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (col0 + j < p.N) yrow[col0 + j] = __float2bfloat16_rn(v[j]);
+          for (int q = 0; q < 4; ++q) res_cur[q] = res_nxt[q];
         }
-        }  // row_ok && col0 < N
       }
       tc_fence_before();
       __syncwarp();
@@ -373,16 +397,24 @@ static int pick_bn(int M, int N) {
   return best;
 }
 
-template <int BN>
-static int launch(const void* X, const void* W, const void* bias, const void* residual, void* Y,
-                  int M, int N, int K, uint32_t epi, const pf_ctl_t* ctl, cudaStream_t stream) {
+template <int BN, uint32_t EPI>
+static int launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid,
+                      const pf_ctl_t* ctl, cudaStream_t stream) {
   using C = Cfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
-    PF_CUDA(cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    PF_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  C::SMEM_BYTES));
     attr_set = true;
   }
+  gemm_kernel<BN, EPI><<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(ta, tb, p, make_ctl(ctl));
+  PF_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+template <int BN>
+static int launch(const void* X, const void* W, const void* bias, const void* residual, void* Y,
+                  int M, int N, int K, uint32_t epi, const pf_ctl_t* ctl, cudaStream_t stream) {
   CUtensorMap ta, tb;
   PF_TRY(make_tmap(&ta, X, M, K, BM));
   PF_TRY(make_tmap(&tb, W, N, K, BN));
@@ -393,15 +425,21 @@ static int launch(const void* X, const void* W, const void* bias, const void* re
   p.M = M;
   p.N = N;
   p.K = K;
-  p.epi = epi;
   p.tiles_m = (M + BM - 1) / BM;
   p.tiles_n = (N + BN - 1) / BN;
   const int tiles = p.tiles_m * p.tiles_n;
   const int sms = device_sm_count();
   const int grid = tiles < sms ? tiles : sms;
-  gemm_kernel<BN><<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(ta, tb, p, make_ctl(ctl));
-  PF_CUDA(cudaGetLastError());
-  return PF_OK;
+  switch (epi & 7u) {
+    case 0: return launch_epi<BN, 0>(ta, tb, p, grid, ctl, stream);
+    case 1: return launch_epi<BN, 1>(ta, tb, p, grid, ctl, stream);
+    case 2: return launch_epi<BN, 2>(ta, tb, p, grid, ctl, stream);
+    case 3: return launch_epi<BN, 3>(ta, tb, p, grid, ctl, stream);
+    case 4: return launch_epi<BN, 4>(ta, tb, p, grid, ctl, stream);
+    case 5: return launch_epi<BN, 5>(ta, tb, p, grid, ctl, stream);
+    case 6: return launch_epi<BN, 6>(ta, tb, p, grid, ctl, stream);
+    default: return launch_epi<BN, 7>(ta, tb, p, grid, ctl, stream);
+  }
 }
 
 }  // namespace gemm
