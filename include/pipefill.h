@@ -85,14 +85,17 @@ int pf_arena_destroy(pf_arena_t* arena);
  * stream-ordered 32-bit store (cuStreamWriteValue32): the engine writes 1 at the
  * BUBBLE instruction and 0 after the recv that ends the bubble, on its comm stream.
  * pf_flag_clear_at enqueues a one-thread kernel that spins on %globaltimer until
- * `deadline_ns` and then stores 0: the 1-GPU stand-in for the neighbour's send
- * (artificial bubbles, BASELINE.json north_star).                                */
+ * *base_ns + offset_ns and then stores 0: the 1-GPU stand-in for the neighbour's
+ * send that ends the bubble (artificial bubbles, BASELINE.json north_star).       */
 int pf_flag_create(uint32_t** out_dev_flag);
 int pf_flag_destroy(uint32_t* dev_flag);
 int pf_flag_write_on_stream(uint32_t* dev_flag, uint32_t value, void* stream);
-int pf_flag_clear_at(uint32_t* dev_flag, uint64_t deadline_ns, void* stream);
-/* Enqueue a kernel that spins until %globaltimer >= deadline_ns (timer-driven recv). */
-int pf_wait_until(uint64_t deadline_ns, void* stream);
+int pf_flag_clear_at(uint32_t* dev_flag, const uint64_t* base_ns, uint64_t offset_ns,
+                     uint64_t* stamp_out, void* stream);
+/* Enqueue a one-thread kernel that spins until %globaltimer >= (*base_ns + offset_ns)
+ * (base_ns may be NULL = 0): the timer-driven stand-in for a recv. If stamp_out is
+ * non-NULL it receives the %globaltimer value at release. dev_flag may be NULL.     */
+int pf_wait_until(const uint64_t* base_ns, uint64_t offset_ns, uint64_t* stamp_out, void* stream);
 /* Enqueue a kernel writing the device %globaltimer (ns) into *dev_out. */
 int pf_read_globaltimer(uint64_t* dev_out, void* stream);
 
@@ -101,6 +104,13 @@ int pf_host_alloc_pinned(uint64_t bytes, void** out_host_ptr);
 int pf_host_free_pinned(void* host_ptr);
 int pf_stage_h2d(void* dst_dev, const void* src_pinned_host, uint64_t bytes, void* stream);
 int pf_stage_d2h(void* dst_pinned_host, const void* src_dev, uint64_t bytes, void* stream);
+/* Chain-aware copy for activation offload/reload between partitions and for a
+ * batch's inputs/results: a grid-stride 16-B copy kernel between any
+ * two UVA addresses (HBM or mapped pinned host memory), gated by pf_ctl_t like the
+ * compute kernels, so copies queued behind a yielded kernel never clobber the
+ * buffers its resume needs. bytes % 16 == 0, 16-B aligned. Atomic work unit.     */
+int pf_copy(void* dst, const void* src, uint64_t bytes, const pf_ctl_t* ctl, void* stream);
+int pf_copy_units(uint64_t bytes, uint32_t* out_units);
 
 /* ---- fill-job kernels (the partitioned forward) -------------- */
 

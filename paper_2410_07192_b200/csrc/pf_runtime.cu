@@ -67,16 +67,22 @@ bool device_is_sm100() {
 // ---------------------------------------------------------------------------
 // small kernels
 
-__global__ void flag_clear_at_kernel(uint32_t* flag, uint64_t deadline_ns) {
+__global__ void flag_clear_at_kernel(uint32_t* flag, const uint64_t* base, uint64_t offset,
+                                     uint64_t* stamp) {
+  const uint64_t deadline = (base ? *(volatile const uint64_t*)base : 0ull) + offset;
   uint64_t now;
   do {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-    if (now >= deadline_ns) break;
-    __nanosleep(500);
+    if (now >= deadline) break;
+    __nanosleep(256);
   } while (true);
   if (flag) {
     __threadfence();
     atomicExch(flag, 0u);
+  }
+  if (stamp) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    *stamp = now;
   }
 }
 
@@ -94,6 +100,44 @@ __global__ void chain_begin_kernel(uint32_t* cursors, int n, const uint32_t* abo
 __global__ void chain_end_kernel(uint32_t* done, const uint32_t* abort) {
   if (abort && ld_volatile_u32(abort) != 0u) return;
   *done += 1u;
+}
+
+constexpr int COPY_THREADS = 256;
+constexpr uint64_t COPY_BYTES_PER_CTA = 256 * 1024;
+
+__global__ void __launch_bounds__(COPY_THREADS) copy_kernel(uint4* __restrict__ dst,
+                                                            const uint4* __restrict__ src,
+                                                            uint64_t n16, Ctl ctl) {
+  __shared__ int s_go;
+  if (threadIdx.x == 0) {
+    int go = 1;
+    if (chain_aborted(ctl)) go = 0;
+    else if (ctl.flag != nullptr && ld_acquire_u32(ctl.flag) == 0u) {
+      atomicExch(ctl.abort, 1u);
+      go = 0;
+    }
+    s_go = go;
+  }
+  __syncthreads();
+  if (!s_go) return;
+  const uint64_t per = COPY_BYTES_PER_CTA / 16;
+  const uint64_t lo = (uint64_t)blockIdx.x * per;
+  const uint64_t hi = lo + per < n16 ? lo + per : n16;
+  constexpr int U = 4;
+  uint64_t i = lo + threadIdx.x;
+  for (; i + (U - 1) * COPY_THREADS < hi; i += U * COPY_THREADS) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = src[i + u * COPY_THREADS];
+#pragma unroll
+    for (int u = 0; u < U; ++u) dst[i + u * COPY_THREADS] = v[u];
+  }
+  for (; i < hi; i += COPY_THREADS) dst[i] = src[i];
+  __syncthreads();
+  if (threadIdx.x == 0 && ctl.cursor != nullptr) {
+    __threadfence_system();
+    atomicAdd(ctl.cursor, 1u);
+  }
 }
 
 __global__ void flag_write_kernel(uint32_t* flag, uint32_t v) {
@@ -253,15 +297,18 @@ int pf_flag_write_on_stream(uint32_t* flag, uint32_t value, void* stream) {
   return PF_OK;
 }
 
-int pf_flag_clear_at(uint32_t* flag, uint64_t deadline_ns, void* stream) {
+int pf_flag_clear_at(uint32_t* flag, const uint64_t* base_ns, uint64_t offset_ns,
+                     uint64_t* stamp_out, void* stream) {
   using namespace pf;
-  flag_clear_at_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(flag, deadline_ns);
+  flag_clear_at_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(flag, base_ns,
+                                                                            offset_ns, stamp_out);
   PF_CUDA(cudaGetLastError());
   return PF_OK;
 }
 
-int pf_wait_until(uint64_t deadline_ns, void* stream) {
-  return pf_flag_clear_at(nullptr, deadline_ns, stream);
+int pf_wait_until(const uint64_t* base_ns, uint64_t offset_ns, uint64_t* stamp_out,
+                  void* stream) {
+  return pf_flag_clear_at(nullptr, base_ns, offset_ns, stamp_out, stream);
 }
 
 int pf_read_globaltimer(uint64_t* dev_out, void* stream) {
@@ -277,7 +324,7 @@ int pf_read_globaltimer(uint64_t* dev_out, void* stream) {
 int pf_host_alloc_pinned(uint64_t bytes, void** out) {
   using namespace pf;
   if (!out || bytes == 0) return set_error(PF_ERR_INVALID, "pf_host_alloc_pinned: bad arguments");
-  PF_CUDA(cudaHostAlloc(out, bytes, cudaHostAllocPortable));
+  PF_CUDA(cudaHostAlloc(out, bytes, cudaHostAllocPortable | cudaHostAllocMapped));
   return PF_OK;
 }
 
@@ -299,6 +346,28 @@ int pf_stage_d2h(void* dst, const void* src, uint64_t bytes, void* stream) {
   if (!dst || !src) return set_error(PF_ERR_INVALID, "pf_stage_d2h: null pointer");
   PF_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost,
                           reinterpret_cast<cudaStream_t>(stream)));
+  return PF_OK;
+}
+
+int pf_copy_units(uint64_t bytes, uint32_t* out) {
+  using namespace pf;
+  if (!out) return set_error(PF_ERR_INVALID, "pf_copy_units: null out");
+  *out = (uint32_t)((bytes + COPY_BYTES_PER_CTA - 1) / COPY_BYTES_PER_CTA);
+  return PF_OK;
+}
+
+int pf_copy(void* dst, const void* src, uint64_t bytes, const pf_ctl_t* ctl, void* stream) {
+  using namespace pf;
+  if (!dst || !src) return set_error(PF_ERR_INVALID, "pf_copy: null pointer");
+  if ((bytes & 15u) || (((uintptr_t)dst | (uintptr_t)src) & 15u))
+    return set_error(PF_ERR_INVALID, "pf_copy: bytes and pointers must be 16-B aligned");
+  PF_TRY(validate_ctl(ctl));
+  if (bytes == 0) return PF_OK;
+  const uint64_t grid = (bytes + COPY_BYTES_PER_CTA - 1) / COPY_BYTES_PER_CTA;
+  copy_kernel<<<(unsigned)grid, COPY_THREADS, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src), bytes / 16,
+      make_ctl(ctl));
+  PF_CUDA(cudaGetLastError());
   return PF_OK;
 }
 

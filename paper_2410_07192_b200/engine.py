@@ -1,0 +1,300 @@
+"""Pipeline engine with PipeFill's BUBBLE instruction, on CUDA streams.
+
+The main job is the user's pipeline-parallel training job (the paper augments
+DeepSpeed's engine). This engine executes one stage's
+instruction list from ``schedule.stage_program`` — GPipe or 1F1B, F/B per
+microbatch, with BUBBLE instructions before the first backward and after the
+last one — on three streams:
+
+* main (high priority): the stage's forward/backward compute and optimizer step;
+* comm (high priority): the recv that ends each wait. A BUBBLE instruction
+  writes 1 to the stage's device flag (stream-ordered 32-bit store) and records
+  the bubble-start event the fill stream waits on; the recv completion then
+  writes 0 ("the recv's completion, stream-ordered on the comm
+  stream, clears the stage's device bubble flag");
+* fill (lowest priority, owned by executor.Executor): the fill job's kernels,
+  which poll the flag at tile granularity and yield.
+
+Two transports provide the recv:
+
+* ``TimerLink`` — the 1-GPU stand-in (artificial bubbles, BASELINE north star):
+  every recv completes at its analytic arrival time in the p-stage schedule,
+  measured from a device %globaltimer anchor, via a one-thread spin kernel;
+* ``NcclLink`` — real P2P activations/gradients between adjacent stages over
+  NVLink with torch.distributed (NCCL), one process per GPU.
+
+Main-job compute (``GPTStage``) is plain torch (cuBLAS / SDPA): it is the
+job being filled, not the product.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Optional
+
+import torch
+import torch.nn.functional as F
+from torch import nn
+
+from . import native
+from .executor import BubbleSlot, Executor
+from .schedule import BubbleKind, Instr, PipelineConfig, program_timeline, stage_program
+
+US = 1000  # ns per us
+
+
+# --------------------------------------------------------------------------- main job
+
+
+@dataclass(frozen=True)
+class GPTStageConfig:
+    hidden: int = 4096
+    heads: int = 32
+    ffn: int = 16384
+    layers: int = 5
+    seq: int = 2048
+    micro_batch: int = 2
+
+    @property
+    def params(self) -> int:
+        h, f = self.hidden, self.ffn
+        return self.layers * (4 * h * h + 2 * h * f + 9 * h + f)
+
+
+GPT_8B_STAGE = GPTStageConfig()  # 8-stage split of a 40-layer h=4096 GPT
+GPT2_SMALL_STAGE = GPTStageConfig(hidden=768, heads=12, ffn=3072, layers=3, seq=1024, micro_batch=8)
+
+
+class _Block(nn.Module):
+    def __init__(self, c: GPTStageConfig):
+        super().__init__()
+        self.c = c
+        self.ln1 = nn.LayerNorm(c.hidden)
+        self.qkv = nn.Linear(c.hidden, 3 * c.hidden)
+        self.proj = nn.Linear(c.hidden, c.hidden)
+        self.ln2 = nn.LayerNorm(c.hidden)
+        self.up = nn.Linear(c.hidden, c.ffn)
+        self.down = nn.Linear(c.ffn, c.hidden)
+
+    def forward(self, x):
+        b, s, h = x.shape
+        q, k, v = self.qkv(self.ln1(x)).view(b, s, 3, self.c.heads, h // self.c.heads).unbind(2)
+        a = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2),
+                                           is_causal=True)
+        x = x + self.proj(a.transpose(1, 2).reshape(b, s, h))
+        return x + self.down(F.gelu(self.up(self.ln2(x)), approximate="tanh"))
+
+
+class GPTStage(nn.Module):
+    """One pipeline stage of a GPT-style decoder (bf16, AdamW), trained by microbatch."""
+
+    def __init__(self, c: GPTStageConfig, seed: int = 0, device: str = "cuda"):
+        super().__init__()
+        torch.manual_seed(seed)
+        self.c = c
+        self.blocks = nn.ModuleList(_Block(c) for _ in range(c.layers))
+        for n, p in self.named_parameters():
+            if p.dim() > 1:
+                nn.init.normal_(p, std=0.02)
+        self.to(device=device, dtype=torch.bfloat16)
+        self.opt = torch.optim.AdamW(self.parameters(), lr=1e-4, fused=True)
+        self._saved: dict[int, tuple[torch.Tensor, torch.Tensor]] = {}
+
+    def forward_mb(self, mb: int, x: torch.Tensor) -> torch.Tensor:
+        x = x.detach().requires_grad_(True)
+        y = x
+        for blk in self.blocks:
+            y = blk(y)
+        self._saved[mb] = (x, y)
+        return y.detach()
+
+    def backward_mb(self, mb: int, grad_out: Optional[torch.Tensor]) -> torch.Tensor:
+        x, y = self._saved.pop(mb)
+        if grad_out is None:  # last stage: scalar loss on the stage output
+            loss = y.float().pow(2).mean()
+            loss.backward()
+            self.last_loss = loss.detach()
+        else:
+            y.backward(grad_out)
+        return x.grad
+
+    def step(self) -> None:
+        self.opt.step()
+        self.opt.zero_grad(set_to_none=False)
+
+
+# --------------------------------------------------------------------------- device helpers
+
+
+class DeviceWords:
+    """A small device u64 scratch (timestamps) + the stage's bubble flag."""
+
+    def __init__(self, n_stamps: int = 8192):
+        self.flag = ctypes.c_void_p()
+        native.call("pf_flag_create", ctypes.byref(self.flag))
+        self.stamps = torch.zeros(n_stamps, dtype=torch.int64, device="cuda")
+        self.anchor = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self.n = 0
+
+    def stamp_ptr(self) -> int:
+        if self.n >= self.stamps.numel():
+            raise RuntimeError("timestamp buffer full")
+        p = self.stamps.data_ptr() + 8 * self.n
+        self.n += 1
+        return p
+
+    def close(self):
+        native.call("pf_flag_destroy", self.flag)
+
+
+@dataclass
+class IterationRecord:
+    iteration: int
+    stage: int
+    anchor_off_ns: int  # nominal iteration start relative to the run anchor
+    end_stamp: int  # index into stamps: end of the last main-job op
+    bubbles: list[tuple[int, int, int]] = field(default_factory=list)  # (kind, set idx, clear idx)
+
+
+# --------------------------------------------------------------------------- links
+
+
+class TimerLink:
+    """1-GPU stand-in for the neighbours: every recv completes at its arrival time
+    in the analytic p-stage timeline (with measured t_fwd/t_bwd), anchored at a
+    device timestamp. Activations/gradients are fixed synthetic tensors."""
+
+    def __init__(self, words: DeviceWords, comm: torch.cuda.Stream):
+        self.w = words
+        self.comm = comm
+
+    def wait_until(self, stream: torch.cuda.Stream, offset_ns: int) -> None:
+        native.call("pf_wait_until", self.w.anchor.data_ptr(), int(offset_ns), None, stream.cuda_stream)
+
+    def bubble_end(self, offset_ns: int, stamp: int) -> None:
+        native.call("pf_flag_clear_at", self.w.flag, self.w.anchor.data_ptr(), int(offset_ns), stamp,
+                    self.comm.cuda_stream)
+
+
+# --------------------------------------------------------------------------- engine
+
+
+class StageEngine:
+    """Runs one stage's program iteration by iteration; BUBBLE hands the bubble to
+    the executor (if any). Emulated-neighbour (TimerLink) version for 1 GPU."""
+
+    def __init__(self, config: PipelineConfig, stage_id: int, model: GPTStage,
+                 executor: Optional[Executor] = None):
+        self.cfg = config
+        self.stage = stage_id
+        self.model = model
+        self.executor = executor
+        lo, hi = torch.cuda.Stream.priority_range()
+        self.main = torch.cuda.Stream(priority=hi)
+        self.comm = torch.cuda.Stream(priority=hi)
+        self.words = DeviceWords()
+        self.link = TimerLink(self.words, self.comm)
+        c = model.c
+        g = torch.Generator(device="cuda").manual_seed(1234 + stage_id)
+        shape = (c.micro_batch, c.seq, c.hidden)
+        self.x_in = [torch.randn(shape, generator=g, device="cuda").to(torch.bfloat16) * 0.5
+                     for _ in range(config.num_microbatches)]
+        self.g_in = [torch.randn(shape, generator=g, device="cuda").to(torch.bfloat16) * 1e-3
+                     for _ in range(config.num_microbatches)]
+        self.last_stage = stage_id == config.num_stages - 1
+        self.timeline = program_timeline(config, stage_id)
+        self.records: list[IterationRecord] = []
+        self.outputs: list[torch.Tensor] = []
+
+    def set_anchor(self, lead_ms: float = 5.0) -> None:
+        """Anchor = device time now + lead (host enqueues ahead within the lead)."""
+        with torch.cuda.stream(self.main):
+            native.call("pf_read_globaltimer", self.words.anchor.data_ptr(), self.main.cuda_stream)
+            self.words.anchor.add_(int(lead_ms * 1e6))
+        self.comm.wait_stream(self.main)
+
+    def run_iteration(self, it: int, fill: bool, keep_outputs: bool = False) -> IterationRecord:
+        cfg = self.cfg
+        base = it * cfg.period_us * US
+        rec = IterationRecord(it, self.stage, base, -1)
+        prev_end_us = None
+        main, comm = self.main, self.comm
+        flag = self.words.flag.value
+        for ins, start_us, end_us in self.timeline:
+            if ins.op == "BUBBLE":
+                ev = torch.cuda.Event()
+                ev.record(main)
+                comm.wait_event(ev)
+                set_idx = self.words.n
+                native.call("pf_flag_write_on_stream", flag, 1, comm.cuda_stream)
+                native.call("pf_read_globaltimer", self.words.stamp_ptr(), comm.cuda_stream)
+                start_ev = torch.cuda.Event()
+                start_ev.record(comm)
+                clear_idx = self.words.n
+                self.link.bubble_end(base + end_us * US, self.words.stamp_ptr())
+                end_ev = torch.cuda.Event()
+                end_ev.record(comm)
+                kind = 0 if ins.kind is BubbleKind.FWD_BWD else 1
+                rec.bubbles.append((kind, set_idx, clear_idx))
+                if fill and self.executor is not None:
+                    self.executor.fill(BubbleSlot(kind, start_ev, flag))
+                main.wait_event(end_ev)
+                prev_end_us = end_us
+                continue
+            # F / B: wait for the (emulated) recv if the schedule idles before it
+            if prev_end_us is None or start_us > prev_end_us:
+                self.link.wait_until(main, base + start_us * US)
+            with torch.cuda.stream(main):
+                if ins.op == "F":
+                    y = self.model.forward_mb(ins.mb, self.x_in[ins.mb])
+                    if keep_outputs:
+                        self.outputs.append(y)
+                else:
+                    self.model.backward_mb(ins.mb, None if self.last_stage else self.g_in[ins.mb])
+                if ins == self._last_compute():
+                    self.model.step()
+                    rec.end_stamp = self.words.n
+                    native.call("pf_read_globaltimer", self.words.stamp_ptr(), main.cuda_stream)
+            prev_end_us = end_us
+        self.records.append(rec)
+        return rec
+
+    def _last_compute(self) -> Instr:
+        return [ins for ins, _, _ in self.timeline if ins.op != "BUBBLE"][-1]
+
+    def timings(self) -> dict:
+        """Per-iteration main-job span and per-bubble durations from device stamps (ns)."""
+        torch.cuda.synchronize()
+        st = self.words.stamps.cpu()
+        anchor = int(self.words.anchor.item())
+        iters, bubbles = [], []
+        for r in self.records:
+            iters.append(int(st[r.end_stamp]) - (anchor + r.anchor_off_ns))
+            for kind, si, ci in r.bubbles:
+                bubbles.append((r.iteration, kind, int(st[si]), int(st[ci])))
+        return {"iter_ns": iters, "bubbles": bubbles, "anchor": anchor}
+
+
+def measure_stage_times(model: GPTStage, reps: int = 5, warmup: int = 2) -> tuple[float, float]:
+    """t_fwd / t_bwd of one microbatch on this stage (ms, CUDA events): the
+    per-stage timings PipelineConfig takes (pipeline.py:48-97)."""
+    c = model.c
+    x = (torch.randn(c.micro_batch, c.seq, c.hidden, device="cuda") * 0.5).to(torch.bfloat16)
+    g = (torch.randn(c.micro_batch, c.seq, c.hidden, device="cuda") * 1e-3).to(torch.bfloat16)
+    tf, tb = [], []
+    for i in range(warmup + reps):
+        a, b, d = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        a.record()
+        model.forward_mb(0, x)
+        b.record()
+        model.backward_mb(0, g)
+        d.record()
+        torch.cuda.synchronize()
+        if i >= warmup:
+            tf.append(a.elapsed_time(b))
+            tb.append(b.elapsed_time(d))
+    model.opt.zero_grad(set_to_none=False)
+    tf.sort()
+    tb.sort()
+    return tf[len(tf) // 2], tb[len(tb) // 2]

@@ -67,8 +67,8 @@ _SIGNATURES: dict[str, tuple] = {
     "pf_flag_create": (c_int, [POINTER(c_void_p)]),
     "pf_flag_destroy": (c_int, [c_void_p]),
     "pf_flag_write_on_stream": (c_int, [c_void_p, c_uint32, c_void_p]),
-    "pf_flag_clear_at": (c_int, [c_void_p, c_uint64, c_void_p]),
-    "pf_wait_until": (c_int, [c_uint64, c_void_p]),
+    "pf_flag_clear_at": (c_int, [c_void_p, c_void_p, c_uint64, c_void_p, c_void_p]),
+    "pf_wait_until": (c_int, [c_void_p, c_uint64, c_void_p, c_void_p]),
     "pf_read_globaltimer": (c_int, [c_void_p, c_void_p]),
     "pf_host_alloc_pinned": (c_int, [c_uint64, POINTER(c_void_p)]),
     "pf_host_free_pinned": (c_int, [c_void_p]),
@@ -103,6 +103,8 @@ _SIGNATURES: dict[str, tuple] = {
         [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
          c_int, c_int, c_int, c_float, POINTER(PfCtl), c_void_p],
     ),
+    "pf_copy": (c_int, [c_void_p, c_void_p, c_uint64, POINTER(PfCtl), c_void_p]),
+    "pf_copy_units": (c_int, [c_uint64, POINTER(c_uint32)]),
     "pf_chain_begin": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
     "pf_chain_end": (c_int, [c_void_p, c_void_p, c_void_p]),
 }

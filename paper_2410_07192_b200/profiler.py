@@ -1,0 +1,101 @@
+"""Measure a fill model's LayerProfile on B200 (the planner's input).
+
+The reference only synthesizes profiles from a cost model (workload.py:216-271);
+PipeFill "relies on profiles of the fill job model's layer execution times and
+memory consumption". Here each module k of the fill
+nn.Sequential is timed on the device with CUDA events inside a full-model
+chain (so inter-kernel gaps are charged to the module that follows them), at
+every batch size, and its memory is the arena bytes the executor really uses
+(weights + the module's workspace + activation buffers). The result is a
+ModelProfile whose layer k is module k, serialized with model_to_json — the
+reference's profile wire format.
+"""
+
+from __future__ import annotations
+
+from typing import Sequence
+
+import torch
+
+from .arena import Arena
+from .fillmodels import ExecContext, FillSequential, synthetic_ids
+from .profiles import JobKind, LayerProfile, ModelProfile
+
+FIXED_TRANSIENT_BYTES = 1 << 20  # control block, cursors, alignment slack
+
+
+def _module_mem(model: FillSequential, i: int, b: int) -> tuple[int, int]:
+    cfg = model.cfg
+    w = model[i].weight_bytes()
+    ws = sum(2 * v for v in model[i].workspace(b, cfg.seq).values())
+    act = 2 * b * cfg.seq * cfg.hidden + 2 * b * cfg.hidden + 4 * b * cfg.seq
+    return w, ws + act + FIXED_TRANSIENT_BYTES
+
+
+def measure_profile(model: FillSequential, batch_sizes: Sequence[int], reps: int = 5,
+                    warmup: int = 2, name: str | None = None) -> ModelProfile:
+    cfg = model.cfg
+    bmax = max(batch_sizes)
+    weights = sum((model[i].weight_bytes() + 255) // 256 * 256 for i in range(len(model)))
+    need = model.workspace(0, len(model), bmax)
+    need["hidden"] = bmax * cfg.seq * cfg.hidden
+    arena = Arena(weights + 2 * sum(need.values()) + 4 * bmax * cfg.seq + (64 << 20))
+    stream = torch.cuda.Stream()
+    try:
+        for mod in model:
+            mod.stage(arena, stream)
+        ws = {k: arena.alloc((v,), torch.bfloat16) for k, v in need.items()}
+        ids_dev = arena.alloc((bmax, cfg.seq), torch.int32)
+        times: dict[int, list[float]] = {}
+        for b in sorted(batch_sizes):
+            ids_dev[:b].copy_(synthetic_ids(0, 0, b, cfg.seq, cfg.vocab))
+            per_rep = []
+            for r in range(warmup + reps):
+                evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(model) + 1)]
+                with torch.cuda.stream(stream):
+                    ctx = ExecContext(stream, ws)
+                    x = ids_dev[:b]
+                    evs[0].record(stream)
+                    for i, mod in enumerate(model):
+                        x = mod(x, ctx)
+                        evs[i + 1].record(stream)
+                stream.synchronize()
+                if r >= warmup:
+                    per_rep.append([evs[i].elapsed_time(evs[i + 1]) for i in range(len(model))])
+            med = []
+            for i in range(len(model)):
+                col = sorted(p[i] for p in per_rep)
+                med.append(col[len(col) // 2])
+            times[b] = med
+    finally:
+        torch.cuda.synchronize()
+        for mod in model:
+            mod.unstage()
+        arena.close()
+
+    layers = []
+    sizes = sorted(batch_sizes)
+    for i in range(len(model)):
+        w, _ = _module_mem(model, i, 1)
+        exec_ms, mem = {}, {}
+        prev_t, prev_m = 0.0, 0
+        for b in sizes:
+            # enforce the profile contract (non-decreasing in batch size) against timer noise
+            t = max(times[b][i], prev_t, 1e-3)
+            m = max(w + _module_mem(model, i, b)[1], prev_m)
+            exec_ms[b], mem[b] = t, m
+            prev_t, prev_m = t, m
+        flops = _module_flops(model, i)
+        layers.append(LayerProfile(exec_time_ms=exec_ms, mem_bytes=mem, weight_bytes=w,
+                                   flops_per_sample=flops))
+    params = sum(model[i].weight_bytes() // 2 for i in range(len(model)))
+    return ModelProfile(name=name or f"{cfg.name}-infer-b200", layers=tuple(layers), param_count=params,
+                        kind_allowed=frozenset({JobKind.BATCH_INFERENCE}))
+
+
+def _module_flops(model: FillSequential, i: int) -> float:
+    cfg = model.cfg
+    if i == 0:
+        return 0.0
+    s, h, f = cfg.seq, cfg.hidden, cfg.ffn
+    return 2.0 * s * (4 * h * h + 2 * h * f) + 4.0 * s * s * h

@@ -1,0 +1,149 @@
+"""The Executor running Coordinator WorkItems on B200: numerics vs the CPU fp32 oracle,
+multi-partition plans (weight staging + activation offload), and preemption/resume."""
+
+import ctypes
+import math
+
+import pytest
+import torch
+
+from oracle import fill_ref
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL_BF16 = 2e-2
+
+
+@pytest.fixture(scope="module")
+def pf():
+    import paper_2410_07192_b200 as pf
+    from paper_2410_07192_b200 import native
+
+    native.require_device()
+    return pf
+
+
+def tiny_cfg():
+    from paper_2410_07192_b200.fillmodels import BertConfig
+
+    return BertConfig("bert_tiny", vocab=1000, hidden=256, heads=4, ffn=1024, layers=3)
+
+
+def oracle_cls(model, ids):
+    x = fill_ref.bert_embeddings(ids, model.oracle_params(0), model.cfg.eps)
+    for i in range(1, len(model)):
+        x = fill_ref.bert_layer(x, model.oracle_params(i), model.cfg.heads, model.cfg.eps)
+    return x[:, 0, :]
+
+
+def plan_item(pf, model, samples, free_mem, sizes=(4, 8)):
+    from paper_2410_07192_b200.profiles import JobSpec, LayerProfile, ModelProfile, JobKind
+
+    layers = []
+    for i in range(len(model)):
+        w = model[i].weight_bytes()
+        layers.append(LayerProfile({b: 0.01 * b for b in sizes}, {b: w + 1_000_000 * b for b in sizes}, w, 1.0))
+    prof = ModelProfile("tiny", tuple(layers), 1, frozenset({JobKind.BATCH_INFERENCE}))
+    cyc = pf.BubbleCycle((pf.BubbleSpec(1000, 1000, free_mem, pf.BubbleKind.FWD_BWD),
+                          pf.BubbleSpec(500, 500, free_mem, pf.BubbleKind.FILL_DRAIN)), 10_000, 0)
+    coord = pf.Coordinator(0, cyc, 1)
+    job = JobSpec("j0", 0.0, prof, JobKind.BATCH_INFERENCE, samples)
+    plan = coord.admit(job)
+    return coord.request_work(0, 0.0), plan
+
+
+def run_to_completion(ex, bubbles_fn, max_bubbles=500):
+    k = 0
+    while ex.busy and k < max_bubbles:
+        ex.fill(bubbles_fn(k))
+        k += 1
+    ex.settle()
+    torch.cuda.synchronize()
+    assert not ex.busy
+    return k
+
+
+def test_executor_single_partition_matches_oracle(pf):
+    from paper_2410_07192_b200.executor import BubbleSlot, Executor
+    from paper_2410_07192_b200.fillmodels import bert, synthetic_ids
+
+    model = bert(tiny_cfg(), seed=3)
+    item, plan = plan_item(pf, model, samples=37, free_mem=8_000_000_000)
+    assert len(plan.partitions) == 1
+    ex = Executor(256 << 20, job_seed=5)
+    ex.load(item, model)
+    run_to_completion(ex, lambda k: BubbleSlot(k % 2, None, 0))
+    got = ex.results().float()
+    ids = synthetic_ids(5, 0, 37, model.cfg.seq, model.cfg.vocab)
+    ref = oracle_cls(model, ids)
+    err = ((got - ref).abs().max() / ref.abs().max()).item()
+    assert err < REL_TOL_BF16, err
+    assert ex.samples_completed == 37
+    ex.close()
+
+
+def test_executor_multi_partition_offload_matches_single(pf):
+    """A memory cap forces a multi-partition plan: weights are staged per partition and
+    activations offloaded/reloaded through pinned host memory; results must be
+    bit-identical to the single-partition run."""
+    from paper_2410_07192_b200.executor import BubbleSlot, Executor
+    from paper_2410_07192_b200.fillmodels import bert
+
+    model = bert(tiny_cfg(), seed=4)
+    item1, plan1 = plan_item(pf, model, samples=20, free_mem=8_000_000_000)
+    w_emb = model[0].weight_bytes()
+    w_layer = model[1].weight_bytes()
+    # room for the embedding alone or two layers -> >= 2 partitions
+    item2, plan2 = plan_item(pf, model, samples=20, free_mem=max(w_emb, 2 * w_layer) + 4_000_000)
+    assert len(plan2.partitions) >= 2, plan2
+    outs = []
+    for item in (item1, item2):
+        ex = Executor(256 << 20, job_seed=9)
+        ex.load(item, model)
+        run_to_completion(ex, lambda k: BubbleSlot(k % 2, None, 0))
+        outs.append(ex.results().clone())
+        ex.close()
+    assert torch.equal(outs[0], outs[1])
+
+
+def test_executor_preemption_resume_is_exact(pf):
+    """Bubbles that close mid-batch (timer-cleared flag) must yield, resume at the
+    first incomplete kernel, and produce results identical to an unpreempted run."""
+    from paper_2410_07192_b200 import native
+    from paper_2410_07192_b200.executor import BubbleSlot, Executor
+    from paper_2410_07192_b200.fillmodels import bert
+
+    model = bert(tiny_cfg(), seed=6)
+    item, _ = plan_item(pf, model, samples=48, free_mem=8_000_000_000, sizes=(8, 16))
+    ex0 = Executor(256 << 20, job_seed=2)
+    ex0.load(item, model)
+    run_to_completion(ex0, lambda k: BubbleSlot(k % 2, None, 0))
+    ref = ex0.results().clone()
+    ex0.close()
+
+    flag = ctypes.c_void_p()
+    native.call("pf_flag_create", ctypes.byref(flag))
+    anchor = torch.zeros(1, dtype=torch.int64, device="cuda")
+    comm = torch.cuda.Stream()
+    ex = Executor(256 << 20, job_seed=2)
+    ex.load(item, model)
+
+    def bubble(k):
+        # the "main job" busy for a while (host enqueues the fill meanwhile), then
+        # open the bubble and close it 50-350 us later
+        with torch.cuda.stream(comm):
+            torch.cuda._sleep(400_000)
+        native.call("pf_read_globaltimer", anchor.data_ptr(), comm.cuda_stream)
+        native.call("pf_flag_write_on_stream", flag, 1, comm.cuda_stream)
+        ev = torch.cuda.Event()
+        ev.record(comm)
+        native.call("pf_flag_clear_at", flag, anchor.data_ptr(), 50_000 + 100_000 * (k % 4), None,
+                    comm.cuda_stream)
+        return BubbleSlot(k % 2, ev, flag.value)
+
+    n = run_to_completion(ex, bubble, max_bubbles=2000)
+    aborted = sum(r.aborted for r in ex.records)
+    assert aborted > 0, "bubbles were long enough to never preempt; shorten them"
+    assert torch.equal(ex.results(), ref), (n, aborted)
+    ex.close()
+    native.call("pf_flag_destroy", flag)
