@@ -4,7 +4,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Xptxas -v --expt-relaxed-constexpr
 PKG := paper_2410_07192_b200
 SRCS := $(wildcard $(PKG)/csrc/*.cu)
-HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/pipefill.h
+HDRS := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/pipefill.h
 LIB := $(PKG)/libpipefill.so
 
 all: $(LIB)

@@ -1,0 +1,402 @@
+"""bench.py — PipeFill fill-job executor on B200: fill samples/s in bubbles.
+
+Metric (BASELINE.json): "fill-job samples/s in bubbles at <=2% main-job slowdown;
+% bubble time filled". Workload (BASELINE.json configs[1], per GPU): one stage of
+an 8-stage 1F1B GPT-style 8B main job (h=4096, 5 layers/stage, FFN 16384, seq 2048,
+microbatch 2, 8 microbatches, bf16, AdamW) with BERT-large batch-inference fill
+jobs (seq 128) planned by the PipeFill DP partitioner from a B200-measured profile.
+
+At N=1 the neighbouring stages are artificial (BASELINE north star "1 GPU (fill
+executor alone, artificial bubbles)"): every recv completes at its arrival time in
+the analytic 8-stage timeline built from the MEASURED t_fwd/t_bwd of this GPU, so
+the bubbles are real idle windows of a real main-job iteration. Step k runs one
+main-job iteration of stage (rank + k*N) mod 8, cycling through the pipeline. One
+step = one iteration with both of its bubbles filled.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Rank 0 prints ONE JSON line. `value` is device-timed (%globaltimer stamps of the
+iterations, max over ranks); `e2e` is host wall clock around the same steps
+through the public API (Coordinator -> WorkItem -> Executor, inputs from and results
+to pinned host memory, host readback included).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fill-job samples/s in bubbles at ≤2% main-job slowdown; % bubble time filled"
+P_STAGES = 8
+M_MICRO = 8
+FILL_BATCH_SIZES = (8, 16, 32, 64, 128)
+FILL_FRACTION = 0.68
+
+
+def load_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        d["source"] = "MEASURED_PEAKS.json"
+        return d
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._thr = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._thr.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._thr.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and
+                          r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# --------------------------------------------------------------------------- reference arm
+
+
+def cpu_fill_throughput(batch: int, reps: int, threads: int | None = None) -> dict:
+    """The oracle CPU execution of the fill job (BERT-large fp32 forward, torch CPU)."""
+    import torch
+
+    from oracle import fill_ref
+    from paper_2410_07192_b200.fillmodels import BERT_LARGE, bert, synthetic_ids
+
+    if threads:
+        torch.set_num_threads(threads)
+    model = bert(BERT_LARGE, seed=0)
+    params = [model.oracle_params(i) for i in range(len(model))]
+    cfg = model.cfg
+    times = []
+    for r in range(reps):
+        ids = synthetic_ids(0, r * batch, batch, cfg.seq, cfg.vocab)
+        t0 = time.perf_counter()
+        with torch.no_grad():
+            x = fill_ref.bert_embeddings(ids, params[0], cfg.eps)
+            for i in range(1, len(model)):
+                x = fill_ref.bert_layer(x, params[i], cfg.heads, cfg.eps)
+            _ = x[:, 0, :].sum().item()
+        times.append(time.perf_counter() - t0)
+    return {"times": times, "batch": batch, "threads": torch.get_num_threads()}
+
+
+def run_reference(args) -> None:
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import torch
+
+    threads = os.cpu_count() or 1
+    batch = 4
+    res = cpu_fill_throughput(batch, args.warmup + args.steps, threads)
+    timed = res["times"][args.warmup:]
+    value = batch * len(timed) / sum(timed)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * sum(timed) / len(timed), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "bert_large fill inference, seq 128, CPU oracle (no bubbles: whole CPU)",
+                   "global_batch": batch, "seq_len": 128},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": res["threads"], "kind": "port",
+                         "sample": f"{len(timed)} batches of {batch} BERT-large sequences, torch CPU fp32 "
+                                   f"(oracle/fill_ref.py; the reference has no fill-compute code)"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    _ = torch
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--fill", default="bert_large", choices=("bert_large", "bert_base"))
+    ap.add_argument("--main", default="gpt8b", choices=("gpt8b", "gpt2small"))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--out", default=None, help="also write the JSON line to this file")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2410_07192_b200 as pf
+    from paper_2410_07192_b200 import native
+    from paper_2410_07192_b200.engine import (GPT2_SMALL_STAGE, GPT_8B_STAGE, GPTStage, StageEngine,
+                                              measure_stage_times)
+    from paper_2410_07192_b200.executor import Executor
+    from paper_2410_07192_b200.fillmodels import BERT_BASE, BERT_LARGE, bert
+    from paper_2410_07192_b200.profiler import measure_profile
+
+    native.require_device()
+    peaks = load_peaks()
+
+    # ---- main job and its measured stage timings
+    gcfg = GPT_8B_STAGE if args.main == "gpt8b" else GPT2_SMALL_STAGE
+    main_model = GPTStage(gcfg, seed=rank)
+    tf_ms, tb_ms = measure_stage_times(main_model)
+
+    # ---- fill job: BERT with a B200-measured profile
+    fcfg = BERT_LARGE if args.fill == "bert_large" else BERT_BASE
+    fill_model = bert(fcfg, seed=0)
+    profile = measure_profile(fill_model, FILL_BATCH_SIZES)
+
+    # ---- bubble characterization: free memory with the main job at its peak
+    probe_cfg = pf.PipelineConfig(P_STAGES, M_MICRO, tf_ms, tb_ms, pf.ScheduleKind.ONE_F_ONE_B,
+                                  1, 1, FILL_FRACTION)
+    probe = StageEngine(probe_cfg, 0, main_model, None)  # stage 0 holds the most activations
+    probe.set_anchor()
+    probe.run_iteration(0, fill=False)
+    torch.cuda.synchronize()
+    free_b, total_b = torch.cuda.mem_get_info()
+    reserved = torch.cuda.max_memory_reserved()
+    free_mem = int(max(0, total_b - reserved - (4 << 30)) * 0.9)  # safety margin
+    arena_bytes = min(free_mem, 24 << 30)
+    pcfg = pf.PipelineConfig(P_STAGES, M_MICRO, tf_ms, tb_ms, pf.ScheduleKind.ONE_F_ONE_B,
+                             arena_bytes, arena_bytes, FILL_FRACTION)
+
+    executor = Executor(arena_bytes, job_seed=rank)
+    engines: dict[int, StageEngine] = {}
+    coords: dict[int, pf.Coordinator] = {}
+    items: dict[int, object] = {}
+
+    def engine_for(s: int) -> StageEngine:
+        if s not in engines:
+            engines[s] = StageEngine(pcfg, s, main_model, executor)
+            # the stage's Coordinator; a long-running fill job split into 16K-sample ranges
+            coords[s] = pf.Coordinator(s, pf.build_bubble_cycle(pcfg, s), 1,
+                                       pf.OrderingPolicy("concurrent", 16384))
+            job = pf.JobSpec(f"fill-{s}", 0.0, profile, pf.JobKind.BATCH_INFERENCE, 10_000_000)
+            coords[s].admit(job)
+        return engines[s]
+
+    def next_work():
+        s = items["stage"]
+        prev = items.get("item")
+        if prev is not None and not executor.busy:
+            coords[s].on_range_done(0, prev, 0.0)
+        item = coords[s].request_work(0, 0.0)
+        items["item"] = item
+        return None if item is None else (item, fill_model)
+
+    executor.work_source = next_work
+
+    def run_step(k: int, fill: bool, stage: int | None = None) -> dict:
+        s = (rank + k * world) % P_STAGES if stage is None else stage
+        eng = engine_for(s)
+        if fill and items.get("stage") != s:
+            if items.get("item") is not None and items.get("stage") is not None:
+                coords[items["stage"]].worker_job[0] = None  # abandon the partial range
+            items["stage"], items["item"] = s, None
+            executor.item = None  # force next_work() at the first bubble
+        eng.reset_stamps()
+        eng.set_anchor()
+        rec = eng.run_iteration(0, fill=fill)
+        if fill:
+            executor.settle()
+        t = eng.record_timing(rec)
+        t["stage"] = s
+        return t
+
+    # ---- fill-off iterations: the main job's own iteration time per stage (one
+    # untimed + one timed iteration of every stage the timed fill-on steps visit)
+    n_total = args.warmup + args.steps
+    off = {}
+    for s_ in sorted({(rank + k * world) % P_STAGES for k in range(args.warmup, n_total)}):
+        for rep in range(2):
+            t = run_step(s_, fill=False, stage=s_)
+            if rep:
+                off.setdefault(s_, []).append(t["main_end"] - t["start"])
+
+    # ---- fill-on: warmup, then the timed steps
+    for k in range(args.warmup):
+        run_step(k, fill=True)
+    executor.timing = True
+    executor.gemm_samples = []
+    n_rec0 = len(executor.records)
+    launches0 = executor.kernel_launches + sum(e.launches for e in engines.values())
+    h2d0, d2h0 = executor.h2d_bytes, executor.d2h_bytes
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    steps = []
+    with ClockSampler(local) as clocks:
+        w0 = time.perf_counter()
+        for k in range(args.warmup, n_total):
+            steps.append(run_step(k, fill=True))
+        torch.cuda.synchronize()
+        checksum = float(executor.results().float().sum())  # host reads the results
+        w1 = time.perf_counter()
+    recs = executor.records[n_rec0:]
+    launches = executor.kernel_launches + sum(e.launches for e in engines.values()) - launches0
+
+    # ---- accounting from device timestamps
+    # sample-equivalents: a batch that passed partition [lo, hi) counts as the share of
+    # the model's FLOPs in that partition (= completed samples in steady state)
+    samples = sum(r.samples_done * r.model_fraction for r in recs)
+    completed = sum(r.samples_completed for r in recs)
+    device_s = sum(t["step_end"] - t["start"] for t in steps) / 1e9
+    bubble_ns = busy_ns = 0
+    rec_iter = iter(recs)
+    for t in steps:
+        for kind, t_set, t_clr in t["bubbles"]:
+            bubble_ns += t_clr - t_set
+            r = next(rec_iter, None)
+            if r is not None and r.fill_end_ns > 0:
+                lo, hi = max(r.fill_start_ns, t_set), min(r.fill_end_ns, t_clr)
+                busy_ns += max(0, hi - lo)
+    idle_total_ns = sum(pf.build_bubble_cycle(pcfg, t["stage"]).total_idle_us * 1000 for t in steps)
+    on_iter = {}
+    for t in steps:
+        on_iter.setdefault(t["stage"], []).append(t["main_end"] - t["start"])
+    slow = [statistics.mean(on_iter[s]) / statistics.mean(off[s]) - 1 for s in on_iter if s in off]
+    slowdown = statistics.mean(slow) if slow else None
+    gemm_flops = sum(f for f, _ in executor.gemm_samples)
+    gemm_ms = sum(ms for _, ms in executor.gemm_samples)
+    gemm_launches = len(executor.gemm_samples)
+    executor.timing = False
+
+    # ---- aggregate over ranks (max time, summed work)
+    agg = torch.tensor([samples, completed, busy_ns, bubble_ns, idle_total_ns, gemm_flops, gemm_ms,
+                        launches, w1 - w0, device_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        sums = agg.clone()
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+        maxs = agg.clone()
+        dist.all_reduce(maxs, op=dist.ReduceOp.MAX)
+        agg = torch.cat([sums[:8], maxs[8:]])
+    (samples_all, completed_all, busy_all, bubble_all, idle_all, gflops_all, gms_all, launches_all,
+     wall_s, dev_s) = agg.tolist()
+    value = samples_all / dev_s if dev_s > 0 else 0.0
+    e2e = samples_all / wall_s if wall_s > 0 else 0.0
+    achieved = gflops_all / (gms_all / 1e3) / 1e12 if gms_all > 0 else 0.0
+    peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res = cpu_fill_throughput(batch=4, reps=3, threads=os.cpu_count())
+        t = res["times"][1:]
+        cpu = {"value": 4 * len(t) / sum(t), "unit": "samples/s", "cores": res["threads"], "kind": "port",
+               "sample": "2 batches x 4 BERT-large seq-128 sequences, torch CPU fp32 oracle "
+                         "(oracle/fill_ref.py), after 1 warm-up batch"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000 * dev_s / max(1, len(steps)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init weights, synthetic token ids / activations)",
+            "config": {
+                "workload": f"8-stage 1F1B GPT-style {'8B' if args.main == 'gpt8b' else 'GPT-2-small'} "
+                            f"main job (one stage per GPU, artificial neighbours) + "
+                            f"{fcfg.name} batch-inference fill (seq {fcfg.seq})",
+                "main_stage": {"hidden": gcfg.hidden, "layers": gcfg.layers, "ffn": gcfg.ffn,
+                               "seq": gcfg.seq, "micro_batch": gcfg.micro_batch,
+                               "microbatches": M_MICRO, "stages": P_STAGES,
+                               "t_fwd_ms": tf_ms, "t_bwd_ms": tb_ms},
+                "fill": {"model": fcfg.name, "seq_len": fcfg.seq, "profiled_batch_sizes": list(FILL_BATCH_SIZES),
+                         "fill_fraction": FILL_FRACTION, "arena_bytes": arena_bytes,
+                         "plans": {str(s): pf.plan_to_dict(c.executables[f"fill-{s}"]) for s, c in coords.items()}},
+                "stages_run": [t["stage"] for t in steps],
+                "l2": "inputs larger than L2 (BERT-large weights 0.67 GB streamed per batch; main job 1B params)",
+            },
+            "bubble_time_filled": busy_all / bubble_all if bubble_all else 0.0,
+            "bubble_time_filled_of_total_idle": busy_all / idle_all if idle_all else 0.0,
+            "main_job_slowdown": slowdown,
+            "per_stage_iter_ms": {str(st): {"fill_off": statistics.mean(off.get(st, [0])) / 1e6,
+                                            "fill_on": statistics.mean(v) / 1e6} for st, v in on_iter.items()},
+            "bubbles_preempted": sum(1 for r in recs if r.aborted),
+            "bubbles_filled": len(recs),
+            "fill_sample_equivalents": samples_all,
+            "fill_samples_completed": int(completed_all),
+            "value_definition": "sample-equivalents/s: completed batches x share of the model's FLOPs in "
+                                "the batch's partition, over device time of the timed iterations",
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak if peak else None, "traffic": None,
+                         "kernel": "pf_gemm (tcgen05)", "launches_timed": gemm_launches,
+                         "peak_source": peaks["source"] + " bf16_tflops_sustained"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e, "unit": "samples/s",
+                    "h2d_bytes_per_step": (executor.h2d_bytes - h2d0) // max(1, len(steps)),
+                    "d2h_bytes_per_step": (executor.d2h_bytes - d2h0) // max(1, len(steps))},
+            "gpu_launches": int(launches_all),
+            "clocks": clocks.summary(),
+            "result_checksum": checksum,
+        }
+        text = json.dumps(line)
+        print(text, flush=True)
+        if args.out:
+            with open(args.out, "w") as fh:
+                fh.write(text + "\n")
+    executor.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -111,6 +111,10 @@ int pf_stage_d2h(void* dst_pinned_host, const void* src_dev, uint64_t bytes, voi
  * buffers its resume needs. bytes % 16 == 0, 16-B aligned. Atomic work unit.     */
 int pf_copy(void* dst, const void* src, uint64_t bytes, const pf_ctl_t* ctl, void* stream);
 int pf_copy_units(uint64_t bytes, uint32_t* out_units);
+/* 2-D variant: `rows` rows of `width` bytes with byte pitches (e.g. gathering the
+ * [CLS] rows of a [batch, seq, hidden] activation straight into pinned host memory). */
+int pf_copy2d(void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch, int64_t width,
+              int64_t rows, const pf_ctl_t* ctl, void* stream);
 
 /* ---- fill-job kernels (the partitioned forward) -------------- */
 
@@ -163,6 +167,47 @@ int pf_embedding_ln(const int32_t* ids, const int32_t* type_ids, const void* wor
  * chain runs (`if (!*abort) ++*done`). Used to bracket one batch of a partition. */
 int pf_chain_begin(uint32_t* cursors, int n, const uint32_t* abort, void* stream);
 int pf_chain_end(uint32_t* done_counter, const uint32_t* abort, void* stream);
+
+/* ---- recorded chains: one batch of one partition --------------------------------
+ * The Executor records the kernel sequence of "partition [lo, hi) at batch size b"
+ * once (argument checks, TMA descriptors, launch shapes resolved at record time) and
+ * replays it per batch with a single pf_chain_launch: node i gets pf_ctl_t
+ * {flag, abort, cursors + i}; start_node > 0 resumes a yielded batch at its first
+ * incomplete node (no cursor reset); copy nodes with role 1/2 add in_off to their
+ * source / out_off to their destination (the batch's slice of the range's inputs /
+ * outputs). With done != NULL a chain-end marker counts completed batches.
+ * This replaces the reference's per-range time model (partition.py:118-132) with
+ * the actual per-batch launch sequence of the paper's Executor.   */
+typedef struct pf_chain pf_chain_t;
+int pf_chain_create(pf_chain_t** out);
+int pf_chain_destroy(pf_chain_t* chain);
+int pf_chain_add_gemm(pf_chain_t* chain, const void* X, const void* W, const void* bias,
+                      const void* residual, void* Y, int M, int N, int K, uint32_t epilogue);
+int pf_chain_add_layernorm(pf_chain_t* chain, const void* X, const void* residual,
+                           const void* gamma, const void* beta, void* Y, int rows, int cols,
+                           float eps);
+int pf_chain_add_rmsnorm(pf_chain_t* chain, const void* X, const void* residual, const void* gamma,
+                         void* Y, int rows, int cols, float eps);
+int pf_chain_add_softmax(pf_chain_t* chain, const void* X, void* Y, int rows, int cols,
+                         float scale);
+int pf_chain_add_attention(pf_chain_t* chain, const void* QKV, const float* mask_add, void* O,
+                           int batch, int seq, int heads, int head_dim, float scale);
+int pf_chain_add_embedding_ln(pf_chain_t* chain, const int32_t* ids, const int32_t* type_ids,
+                              const void* word, const void* pos, const void* type,
+                              const void* gamma, const void* beta, void* Y, int batch, int seq,
+                              int hidden, int vocab, float eps);
+int pf_chain_add_copy(pf_chain_t* chain, void* dst, int64_t dst_pitch, const void* src,
+                      int64_t src_pitch, int64_t width, int64_t rows, int role);
+int pf_chain_size(pf_chain_t* chain, int* out_nodes);
+/* units = work units of the node; resumable = 1 for claimed-prefix nodes (GEMM tiles),
+ * 0 for atomic nodes that are re-run whole (cursor must be reset to 0 first).       */
+int pf_chain_node_info(pf_chain_t* chain, int node, uint32_t* out_units, int* out_resumable);
+/* Live per-node device timing (CUDA events around every node of the next launches);
+ * pf_chain_node_elapsed returns the last launch's duration of `node` in ms.        */
+int pf_chain_set_timing(pf_chain_t* chain, int enable);
+int pf_chain_node_elapsed(pf_chain_t* chain, int node, float* out_ms);
+int pf_chain_launch(pf_chain_t* chain, const uint32_t* flag, uint32_t* abort, uint32_t* cursors,
+                    uint32_t* done, int start_node, int64_t in_off, int64_t out_off, void* stream);
 
 #ifdef __cplusplus
 }

@@ -11,7 +11,7 @@
 // Q, K, V tiles arrive by one 3-D TMA each from the packed QKV projection output
 // [batch*seq, 3, heads, 64]; no transpose or split kernel runs before attention.
 // Preemption: atomic work unit = one (batch, head); flag checked on entry.
-#include "pf_common.cuh"
+#include "pf_ops.h"
 
 namespace pf {
 namespace attn {
@@ -223,7 +223,62 @@ static EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
+struct AttentionOp final : PreparedOp {
+  CUtensorMap tm;
+  const float* mask = nullptr;
+  __nv_bfloat16* out = nullptr;
+  int batch = 0, seq = 0, heads = 0;
+  float scale_log2 = 0.f;
+  uint32_t units() const override { return (uint32_t)(batch * heads); }
+  bool resumable() const override { return false; }
+  int run(const pf_ctl_t* ctl, cudaStream_t s, int64_t, int64_t) override {
+    attention_kernel<<<batch * heads, THREADS, SMEM_REQUEST, s>>>(tm, mask, out, batch, seq, heads,
+                                                                  scale_log2, make_ctl(ctl));
+    PF_CUDA(cudaGetLastError());
+    return PF_OK;
+  }
+};
+
 }  // namespace attn
+
+int make_attention_op(OpPtr* out, const void* QKV, const float* mask_add, void* O, int batch,
+                      int seq, int heads, int head_dim, float scale) {
+  using namespace attn;
+  if (!QKV || !O || batch <= 0 || heads <= 0 || seq <= 0)
+    return set_error(PF_ERR_INVALID, "pf_attention: bad arguments");
+  if (head_dim != D || seq > S_MAX)
+    return set_error(PF_ERR_UNSUPPORTED, "pf_attention: needs head_dim == 64 and seq <= 128");
+  if (((uintptr_t)QKV | (uintptr_t)O) & 15u)
+    return set_error(PF_ERR_INVALID, "pf_attention: pointers must be 16-B aligned");
+  if (!device_is_sm100()) return set_error(PF_ERR_UNSUPPORTED, "pf_attention: needs sm_100");
+  static bool attr = false;
+  if (!attr) {
+    PF_CUDA(cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 SMEM_REQUEST));
+    attr = true;
+  }
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return set_error(PF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  auto op = std::make_unique<AttentionOp>();
+  // QKV viewed as [batch*seq][3*heads][64]; box = one head slot x 128 tokens
+  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)(3 * heads), (cuuint64_t)batch * seq};
+  cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)3 * heads * D * 2};
+  cuuint32_t box[3] = {(cuuint32_t)D, 1, (cuuint32_t)S_MAX};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(&op->tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(QKV), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(PF_ERR_CUDA, "attention tensor map failed (%d)", (int)r);
+  op->mask = mask_add;
+  op->out = reinterpret_cast<__nv_bfloat16*>(O);
+  op->batch = batch;
+  op->seq = seq;
+  op->heads = heads;
+  op->scale_log2 = scale * 1.4426950408889634f;
+  *out = std::move(op);
+  return PF_OK;
+}
+
 }  // namespace pf
 
 extern "C" int pf_attention_units(int batch, int seq, int heads, int head_dim, uint32_t* out) {
@@ -236,38 +291,8 @@ extern "C" int pf_attention_units(int batch, int seq, int heads, int head_dim, u
 extern "C" int pf_attention(const void* QKV, const float* mask_add, void* O, int batch, int seq,
                             int heads, int head_dim, float scale, const pf_ctl_t* ctl,
                             void* stream) {
-  using namespace pf;
-  using namespace pf::attn;
-  if (!QKV || !O || batch <= 0 || heads <= 0 || seq <= 0)
-    return set_error(PF_ERR_INVALID, "pf_attention: bad arguments");
-  if (head_dim != D || seq > S_MAX)
-    return set_error(PF_ERR_UNSUPPORTED, "pf_attention: needs head_dim == 64 and seq <= 128");
-  if (((uintptr_t)QKV | (uintptr_t)O) & 15u)
-    return set_error(PF_ERR_INVALID, "pf_attention: pointers must be 16-B aligned");
-  PF_TRY(validate_ctl(ctl));
-  if (!device_is_sm100()) return set_error(PF_ERR_UNSUPPORTED, "pf_attention: needs sm_100");
-  static bool attr = false;
-  if (!attr) {
-    PF_CUDA(cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 SMEM_REQUEST));
-    attr = true;
-  }
-  EncodeTiledFn enc = get_encode_fn();
-  if (!enc) return set_error(PF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  // QKV viewed as [batch*seq][3*heads][64]; box = one head slot x 128 tokens
-  CUtensorMap tm;
-  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)(3 * heads), (cuuint64_t)batch * seq};
-  cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)3 * heads * D * 2};
-  cuuint32_t box[3] = {(cuuint32_t)D, 1, (cuuint32_t)S_MAX};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(QKV), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return set_error(PF_ERR_CUDA, "attention tensor map failed (%d)", (int)r);
-  const float scale_log2 = scale * 1.4426950408889634f;
-  attention_kernel<<<batch * heads, THREADS, SMEM_REQUEST, reinterpret_cast<cudaStream_t>(stream)>>>(
-      tm, mask_add, reinterpret_cast<__nv_bfloat16*>(O), batch, seq, heads, scale_log2,
-      make_ctl(ctl));
-  PF_CUDA(cudaGetLastError());
-  return PF_OK;
+  PF_TRY(pf::validate_ctl(ctl));
+  pf::OpPtr op;
+  PF_TRY(pf::make_attention_op(&op, QKV, mask_add, O, batch, seq, heads, head_dim, scale));
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), 0, 0);
 }

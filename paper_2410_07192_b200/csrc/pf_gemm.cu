@@ -19,7 +19,7 @@
 // of the flag clearing and the claimed-tile prefix is the resume cursor.
 #include <stdio.h>
 
-#include "pf_common.cuh"
+#include "pf_ops.h"
 
 namespace pf {
 namespace gemm {
@@ -413,36 +413,82 @@ static int launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const Params
 }
 
 template <int BN>
-static int launch(const void* X, const void* W, const void* bias, const void* residual, void* Y,
-                  int M, int N, int K, uint32_t epi, const pf_ctl_t* ctl, cudaStream_t stream) {
+struct GemmOp final : PreparedOp {
   CUtensorMap ta, tb;
-  PF_TRY(make_tmap(&ta, X, M, K, BM));
-  PF_TRY(make_tmap(&tb, W, N, K, BN));
   Params p;
-  p.Y = reinterpret_cast<__nv_bfloat16*>(Y);
-  p.bias = reinterpret_cast<const __nv_bfloat16*>(bias);
-  p.residual = reinterpret_cast<const __nv_bfloat16*>(residual);
-  p.M = M;
-  p.N = N;
-  p.K = K;
-  p.tiles_m = (M + BM - 1) / BM;
-  p.tiles_n = (N + BN - 1) / BN;
-  const int tiles = p.tiles_m * p.tiles_n;
-  const int sms = device_sm_count();
-  const int grid = tiles < sms ? tiles : sms;
-  switch (epi & 7u) {
-    case 0: return launch_epi<BN, 0>(ta, tb, p, grid, ctl, stream);
-    case 1: return launch_epi<BN, 1>(ta, tb, p, grid, ctl, stream);
-    case 2: return launch_epi<BN, 2>(ta, tb, p, grid, ctl, stream);
-    case 3: return launch_epi<BN, 3>(ta, tb, p, grid, ctl, stream);
-    case 4: return launch_epi<BN, 4>(ta, tb, p, grid, ctl, stream);
-    case 5: return launch_epi<BN, 5>(ta, tb, p, grid, ctl, stream);
-    case 6: return launch_epi<BN, 6>(ta, tb, p, grid, ctl, stream);
-    default: return launch_epi<BN, 7>(ta, tb, p, grid, ctl, stream);
+  uint32_t epi = 0;
+  int grid = 0;
+
+  int prepare(const void* X, const void* W, const void* bias, const void* residual, void* Y, int M,
+              int N, int K, uint32_t e) {
+    PF_TRY(make_tmap(&ta, X, M, K, BM));
+    PF_TRY(make_tmap(&tb, W, N, K, BN));
+    p.Y = reinterpret_cast<__nv_bfloat16*>(Y);
+    p.bias = reinterpret_cast<const __nv_bfloat16*>(bias);
+    p.residual = reinterpret_cast<const __nv_bfloat16*>(residual);
+    p.M = M;
+    p.N = N;
+    p.K = K;
+    p.tiles_m = (M + BM - 1) / BM;
+    p.tiles_n = (N + BN - 1) / BN;
+    const int tiles = p.tiles_m * p.tiles_n;
+    const int sms = device_sm_count();
+    grid = tiles < sms ? tiles : sms;
+    epi = e & 7u;
+    return PF_OK;
+  }
+  uint32_t units() const override { return (uint32_t)(p.tiles_m * p.tiles_n); }
+  bool resumable() const override { return true; }
+  int run(const pf_ctl_t* ctl, cudaStream_t stream, int64_t, int64_t) override {
+    switch (epi) {
+      case 0: return launch_epi<BN, 0>(ta, tb, p, grid, ctl, stream);
+      case 1: return launch_epi<BN, 1>(ta, tb, p, grid, ctl, stream);
+      case 2: return launch_epi<BN, 2>(ta, tb, p, grid, ctl, stream);
+      case 3: return launch_epi<BN, 3>(ta, tb, p, grid, ctl, stream);
+      case 4: return launch_epi<BN, 4>(ta, tb, p, grid, ctl, stream);
+      case 5: return launch_epi<BN, 5>(ta, tb, p, grid, ctl, stream);
+      case 6: return launch_epi<BN, 6>(ta, tb, p, grid, ctl, stream);
+      default: return launch_epi<BN, 7>(ta, tb, p, grid, ctl, stream);
+    }
+  }
+};
+
+}  // namespace gemm
+
+int make_gemm_op(OpPtr* out, const void* X, const void* W, const void* bias, const void* residual,
+                 void* Y, int M, int N, int K, uint32_t epilogue) {
+  if (!X || !W || !Y || M <= 0 || N <= 0 || K <= 0)
+    return set_error(PF_ERR_INVALID, "pf_gemm: null pointer or non-positive shape");
+  if (K % 8 != 0 || N % 8 != 0)
+    return set_error(PF_ERR_INVALID, "pf_gemm: K and N must be multiples of 8 (16-B rows)");
+  if ((epilogue & PF_EPI_BIAS) && !bias) return set_error(PF_ERR_INVALID, "pf_gemm: bias is NULL");
+  if ((epilogue & PF_EPI_RESIDUAL) && !residual)
+    return set_error(PF_ERR_INVALID, "pf_gemm: residual is NULL");
+  if (((uintptr_t)X | (uintptr_t)W | (uintptr_t)Y | (uintptr_t)bias | (uintptr_t)residual) & 15u)
+    return set_error(PF_ERR_INVALID, "pf_gemm: pointers must be 16-B aligned");
+  if (!device_is_sm100()) return set_error(PF_ERR_UNSUPPORTED, "pf_gemm: needs an sm_100 device");
+  switch (gemm::pick_bn(M, N)) {
+    case 256: {
+      auto op = std::make_unique<gemm::GemmOp<256>>();
+      PF_TRY(op->prepare(X, W, bias, residual, Y, M, N, K, epilogue));
+      *out = std::move(op);
+      return PF_OK;
+    }
+    case 192: {
+      auto op = std::make_unique<gemm::GemmOp<192>>();
+      PF_TRY(op->prepare(X, W, bias, residual, Y, M, N, K, epilogue));
+      *out = std::move(op);
+      return PF_OK;
+    }
+    default: {
+      auto op = std::make_unique<gemm::GemmOp<128>>();
+      PF_TRY(op->prepare(X, W, bias, residual, Y, M, N, K, epilogue));
+      *out = std::move(op);
+      return PF_OK;
+    }
   }
 }
 
-}  // namespace gemm
 }  // namespace pf
 
 extern "C" int pf_gemm_units(int M, int N, int K, uint32_t* out_units) {
@@ -457,24 +503,8 @@ extern "C" int pf_gemm(const void* X, const void* W, const void* bias, const voi
                        void* Y, int M, int N, int K, uint32_t epilogue, const pf_ctl_t* ctl,
                        void* stream) {
   using namespace pf;
-  if (!X || !W || !Y || M <= 0 || N <= 0 || K <= 0)
-    return set_error(PF_ERR_INVALID, "pf_gemm: null pointer or non-positive shape");
-  if (K % 8 != 0 || N % 8 != 0)
-    return set_error(PF_ERR_INVALID, "pf_gemm: K and N must be multiples of 8 (16-B rows)");
-  if ((epilogue & PF_EPI_BIAS) && !bias) return set_error(PF_ERR_INVALID, "pf_gemm: bias is NULL");
-  if ((epilogue & PF_EPI_RESIDUAL) && !residual)
-    return set_error(PF_ERR_INVALID, "pf_gemm: residual is NULL");
-  if (((uintptr_t)X | (uintptr_t)W | (uintptr_t)Y | (uintptr_t)bias | (uintptr_t)residual) & 15u)
-    return set_error(PF_ERR_INVALID, "pf_gemm: pointers must be 16-B aligned");
   PF_TRY(validate_ctl(ctl));
-  if (!device_is_sm100()) return set_error(PF_ERR_UNSUPPORTED, "pf_gemm: needs an sm_100 device");
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  switch (gemm::pick_bn(M, N)) {
-    case 256:
-      return gemm::launch<256>(X, W, bias, residual, Y, M, N, K, epilogue, ctl, s);
-    case 192:
-      return gemm::launch<192>(X, W, bias, residual, Y, M, N, K, epilogue, ctl, s);
-    default:
-      return gemm::launch<128>(X, W, bias, residual, Y, M, N, K, epilogue, ctl, s);
-  }
+  OpPtr op;
+  PF_TRY(make_gemm_op(&op, X, W, bias, residual, Y, M, N, K, epilogue));
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), 0, 0);
 }

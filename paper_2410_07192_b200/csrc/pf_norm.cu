@@ -7,7 +7,7 @@
 // bubble flag once on entry and counts itself into the cursor on exit; they are
 // out-of-place and idempotent, so an interrupted launch is simply re-run
 // (cursor reset to 0) — yield latency is one CTA (16 rows, well under 1 us).
-#include "pf_common.cuh"
+#include "pf_ops.h"
 
 namespace pf {
 namespace norm {
@@ -250,7 +250,123 @@ static int check_rows(const void* a, const void* b, const void* c, const void* d
   return PF_OK;
 }
 
+struct NormOp final : PreparedOp {
+  bool rms = false;
+  const __nv_bfloat16 *x = nullptr, *r = nullptr, *g = nullptr, *b = nullptr;
+  __nv_bfloat16* y = nullptr;
+  int rows = 0, cols = 0;
+  float eps = 0.f;
+  uint32_t units() const override { return (uint32_t)grid_for(rows); }
+  bool resumable() const override { return false; }
+  int run(const pf_ctl_t* ctl, cudaStream_t s, int64_t, int64_t) override {
+    if (rms) {
+      PF_NV_DISPATCH(nv_for(cols), (norm_kernel<NV, true><<<grid_for(rows), WARPS * 32, 0, s>>>(
+                                       x, r, g, nullptr, y, rows, cols, eps, make_ctl(ctl))));
+    } else {
+      PF_NV_DISPATCH(nv_for(cols), (norm_kernel<NV, false><<<grid_for(rows), WARPS * 32, 0, s>>>(
+                                       x, r, g, b, y, rows, cols, eps, make_ctl(ctl))));
+    }
+    PF_CUDA(cudaGetLastError());
+    return PF_OK;
+  }
+};
+
+struct SoftmaxOp final : PreparedOp {
+  const __nv_bfloat16* x = nullptr;
+  __nv_bfloat16* y = nullptr;
+  int rows = 0, cols = 0;
+  float scale = 1.f;
+  uint32_t units() const override { return (uint32_t)grid_for(rows); }
+  bool resumable() const override { return false; }
+  int run(const pf_ctl_t* ctl, cudaStream_t s, int64_t, int64_t) override {
+    PF_NV_DISPATCH(nv_for(cols), (softmax_kernel<NV><<<grid_for(rows), WARPS * 32, 0, s>>>(
+                                     x, y, rows, cols, scale, make_ctl(ctl))));
+    PF_CUDA(cudaGetLastError());
+    return PF_OK;
+  }
+};
+
+struct EmbeddingOp final : PreparedOp {
+  const int32_t *ids = nullptr, *tt = nullptr;
+  const __nv_bfloat16 *word = nullptr, *pos = nullptr, *type = nullptr, *g = nullptr, *b = nullptr;
+  __nv_bfloat16* y = nullptr;
+  int rows = 0, seq = 0, hidden = 0, vocab = 0;
+  float eps = 0.f;
+  uint32_t units() const override { return (uint32_t)grid_for(rows); }
+  bool resumable() const override { return false; }
+  int run(const pf_ctl_t* ctl, cudaStream_t s, int64_t, int64_t) override {
+    PF_NV_DISPATCH(nv_for(hidden),
+                   (embedding_ln_kernel<NV><<<grid_for(rows), WARPS * 32, 0, s>>>(
+                       ids, tt, word, pos, type, g, b, y, rows, seq, hidden, vocab, eps,
+                       make_ctl(ctl))));
+    PF_CUDA(cudaGetLastError());
+    return PF_OK;
+  }
+};
+
 }  // namespace norm
+
+using bf = __nv_bfloat16;
+
+int make_norm_op(OpPtr* out, bool rms, const void* X, const void* residual, const void* gamma,
+                 const void* beta, void* Y, int rows, int cols, float eps) {
+  const char* who = rms ? "pf_rmsnorm" : "pf_layernorm";
+  if (!X || !gamma || !Y || (!rms && !beta)) return set_error(PF_ERR_INVALID, "%s: null pointer", who);
+  PF_TRY(norm::check_rows(X, residual, gamma, Y, rows, cols, who));
+  if ((uintptr_t)beta & 15u) return set_error(PF_ERR_INVALID, "%s: beta misaligned", who);
+  auto op = std::make_unique<norm::NormOp>();
+  op->rms = rms;
+  op->x = reinterpret_cast<const bf*>(X);
+  op->r = reinterpret_cast<const bf*>(residual);
+  op->g = reinterpret_cast<const bf*>(gamma);
+  op->b = reinterpret_cast<const bf*>(beta);
+  op->y = reinterpret_cast<bf*>(Y);
+  op->rows = rows;
+  op->cols = cols;
+  op->eps = eps;
+  *out = std::move(op);
+  return PF_OK;
+}
+
+int make_softmax_op(OpPtr* out, const void* X, void* Y, int rows, int cols, float scale) {
+  if (!X || !Y) return set_error(PF_ERR_INVALID, "pf_softmax: null pointer");
+  PF_TRY(norm::check_rows(X, Y, nullptr, nullptr, rows, cols, "pf_softmax"));
+  auto op = std::make_unique<norm::SoftmaxOp>();
+  op->x = reinterpret_cast<const bf*>(X);
+  op->y = reinterpret_cast<bf*>(Y);
+  op->rows = rows;
+  op->cols = cols;
+  op->scale = scale;
+  *out = std::move(op);
+  return PF_OK;
+}
+
+int make_embedding_op(OpPtr* out, const int32_t* ids, const int32_t* tt, const void* word,
+                      const void* pos, const void* type, const void* gamma, const void* beta,
+                      void* Y, int batch, int seq, int hidden, int vocab, float eps) {
+  if (!ids || !word || !pos || !type || !gamma || !beta || !Y || batch <= 0 || seq <= 0 ||
+      vocab <= 0)
+    return set_error(PF_ERR_INVALID, "pf_embedding_ln: bad arguments");
+  const int rows = batch * seq;
+  PF_TRY(norm::check_rows(word, pos, type, Y, rows, hidden, "pf_embedding_ln"));
+  auto op = std::make_unique<norm::EmbeddingOp>();
+  op->ids = ids;
+  op->tt = tt;
+  op->word = reinterpret_cast<const bf*>(word);
+  op->pos = reinterpret_cast<const bf*>(pos);
+  op->type = reinterpret_cast<const bf*>(type);
+  op->g = reinterpret_cast<const bf*>(gamma);
+  op->b = reinterpret_cast<const bf*>(beta);
+  op->y = reinterpret_cast<bf*>(Y);
+  op->rows = rows;
+  op->seq = seq;
+  op->hidden = hidden;
+  op->vocab = vocab;
+  op->eps = eps;
+  *out = std::move(op);
+  return PF_OK;
+}
+
 }  // namespace pf
 
 extern "C" int pf_norm_units(int rows, int cols, uint32_t* out) {
@@ -266,80 +382,35 @@ extern "C" int pf_softmax_units(int rows, int cols, uint32_t* out) {
 extern "C" int pf_layernorm(const void* X, const void* residual, const void* gamma,
                             const void* beta, void* Y, int rows, int cols, float eps,
                             const pf_ctl_t* ctl, void* stream) {
-  using namespace pf;
-  using namespace pf::norm;
-  if (!X || !gamma || !beta || !Y) return set_error(PF_ERR_INVALID, "pf_layernorm: null pointer");
-  PF_TRY(check_rows(X, residual, gamma, Y, rows, cols, "pf_layernorm"));
-  if ((uintptr_t)beta & 15u) return set_error(PF_ERR_INVALID, "pf_layernorm: beta misaligned");
-  PF_TRY(validate_ctl(ctl));
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const auto* x = reinterpret_cast<const __nv_bfloat16*>(X);
-  const auto* r = reinterpret_cast<const __nv_bfloat16*>(residual);
-  const auto* g = reinterpret_cast<const __nv_bfloat16*>(gamma);
-  const auto* b = reinterpret_cast<const __nv_bfloat16*>(beta);
-  auto* y = reinterpret_cast<__nv_bfloat16*>(Y);
-  PF_NV_DISPATCH(nv_for(cols), (norm_kernel<NV, false><<<grid_for(rows), WARPS * 32, 0, s>>>(
-                                   x, r, g, b, y, rows, cols, eps, make_ctl(ctl))));
-  PF_CUDA(cudaGetLastError());
-  return PF_OK;
+  PF_TRY(pf::validate_ctl(ctl));
+  pf::OpPtr op;
+  PF_TRY(pf::make_norm_op(&op, false, X, residual, gamma, beta, Y, rows, cols, eps));
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), 0, 0);
 }
 
 extern "C" int pf_rmsnorm(const void* X, const void* residual, const void* gamma, void* Y,
                           int rows, int cols, float eps, const pf_ctl_t* ctl, void* stream) {
-  using namespace pf;
-  using namespace pf::norm;
-  if (!X || !gamma || !Y) return set_error(PF_ERR_INVALID, "pf_rmsnorm: null pointer");
-  PF_TRY(check_rows(X, residual, gamma, Y, rows, cols, "pf_rmsnorm"));
-  PF_TRY(validate_ctl(ctl));
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const auto* x = reinterpret_cast<const __nv_bfloat16*>(X);
-  const auto* r = reinterpret_cast<const __nv_bfloat16*>(residual);
-  const auto* g = reinterpret_cast<const __nv_bfloat16*>(gamma);
-  auto* y = reinterpret_cast<__nv_bfloat16*>(Y);
-  PF_NV_DISPATCH(nv_for(cols), (norm_kernel<NV, true><<<grid_for(rows), WARPS * 32, 0, s>>>(
-                                   x, r, g, nullptr, y, rows, cols, eps, make_ctl(ctl))));
-  PF_CUDA(cudaGetLastError());
-  return PF_OK;
+  PF_TRY(pf::validate_ctl(ctl));
+  pf::OpPtr op;
+  PF_TRY(pf::make_norm_op(&op, true, X, residual, gamma, nullptr, Y, rows, cols, eps));
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), 0, 0);
 }
 
 extern "C" int pf_softmax(const void* X, void* Y, int rows, int cols, float scale,
                           const pf_ctl_t* ctl, void* stream) {
-  using namespace pf;
-  using namespace pf::norm;
-  if (!X || !Y) return set_error(PF_ERR_INVALID, "pf_softmax: null pointer");
-  PF_TRY(check_rows(X, Y, nullptr, nullptr, rows, cols, "pf_softmax"));
-  PF_TRY(validate_ctl(ctl));
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  PF_NV_DISPATCH(nv_for(cols),
-                 (softmax_kernel<NV><<<grid_for(rows), WARPS * 32, 0, s>>>(
-                     reinterpret_cast<const __nv_bfloat16*>(X),
-                     reinterpret_cast<__nv_bfloat16*>(Y), rows, cols, scale, make_ctl(ctl))));
-  PF_CUDA(cudaGetLastError());
-  return PF_OK;
+  PF_TRY(pf::validate_ctl(ctl));
+  pf::OpPtr op;
+  PF_TRY(pf::make_softmax_op(&op, X, Y, rows, cols, scale));
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), 0, 0);
 }
 
 extern "C" int pf_embedding_ln(const int32_t* ids, const int32_t* type_ids, const void* word,
                                const void* pos, const void* type, const void* gamma,
                                const void* beta, void* Y, int batch, int seq, int hidden,
                                int vocab, float eps, const pf_ctl_t* ctl, void* stream) {
-  using namespace pf;
-  using namespace pf::norm;
-  if (!ids || !word || !pos || !type || !gamma || !beta || !Y || batch <= 0 || seq <= 0 ||
-      vocab <= 0)
-    return set_error(PF_ERR_INVALID, "pf_embedding_ln: bad arguments");
-  const int rows = batch * seq;
-  PF_TRY(check_rows(word, pos, type, Y, rows, hidden, "pf_embedding_ln"));
-  PF_TRY(validate_ctl(ctl));
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  PF_NV_DISPATCH(nv_for(hidden),
-                 (embedding_ln_kernel<NV><<<grid_for(rows), WARPS * 32, 0, s>>>(
-                     ids, type_ids, reinterpret_cast<const __nv_bfloat16*>(word),
-                     reinterpret_cast<const __nv_bfloat16*>(pos),
-                     reinterpret_cast<const __nv_bfloat16*>(type),
-                     reinterpret_cast<const __nv_bfloat16*>(gamma),
-                     reinterpret_cast<const __nv_bfloat16*>(beta),
-                     reinterpret_cast<__nv_bfloat16*>(Y), rows, seq, hidden, vocab, eps,
-                     make_ctl(ctl))));
-  PF_CUDA(cudaGetLastError());
-  return PF_OK;
+  PF_TRY(pf::validate_ctl(ctl));
+  pf::OpPtr op;
+  PF_TRY(pf::make_embedding_op(&op, ids, type_ids, word, pos, type, gamma, beta, Y, batch, seq,
+                               hidden, vocab, eps));
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), 0, 0);
 }

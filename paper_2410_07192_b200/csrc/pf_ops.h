@@ -1,0 +1,37 @@
+// pf_ops.h — host-side "prepared" kernel launches: every argument check, tensor-map
+// encode and launch-shape decision is done once when a chain is recorded; replaying
+// a node is a single kernel launch (pf_chain_launch).
+#pragma once
+
+#include <memory>
+
+#include "pf_common.cuh"
+
+namespace pf {
+
+struct PreparedOp {
+  virtual ~PreparedOp() {}
+  // in_off / out_off: per-launch byte offsets for copy nodes bound to a batch slice
+  virtual int run(const pf_ctl_t* ctl, cudaStream_t s, int64_t in_off, int64_t out_off) = 0;
+  virtual uint32_t units() const = 0;
+  virtual bool resumable() const = 0;  // true: claimed-prefix cursor; false: atomic (re-run whole)
+};
+
+using OpPtr = std::unique_ptr<PreparedOp>;
+
+int make_gemm_op(OpPtr* out, const void* X, const void* W, const void* bias, const void* residual,
+                 void* Y, int M, int N, int K, uint32_t epi);
+int make_norm_op(OpPtr* out, bool rms, const void* X, const void* residual, const void* gamma,
+                 const void* beta, void* Y, int rows, int cols, float eps);
+int make_softmax_op(OpPtr* out, const void* X, void* Y, int rows, int cols, float scale);
+int make_embedding_op(OpPtr* out, const int32_t* ids, const int32_t* tt, const void* word,
+                      const void* pos, const void* type, const void* gamma, const void* beta,
+                      void* Y, int batch, int seq, int hidden, int vocab, float eps);
+int make_attention_op(OpPtr* out, const void* QKV, const float* mask, void* O, int batch, int seq,
+                      int heads, int head_dim, float scale);
+// 2-D copy: `rows` rows of `width` bytes, pitches in bytes; role 1 adds in_off to src,
+// role 2 adds out_off to dst. Any UVA addresses (HBM or mapped pinned host).
+int make_copy_op(OpPtr* out, void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch,
+                 int64_t width, int64_t rows, int role);
+
+}  // namespace pf

@@ -6,7 +6,7 @@
 
 #include <mutex>
 
-#include "pf_common.cuh"
+#include "pf_ops.h"
 
 namespace pf {
 
@@ -105,8 +105,11 @@ __global__ void chain_end_kernel(uint32_t* done, const uint32_t* abort) {
 constexpr int COPY_THREADS = 256;
 constexpr uint64_t COPY_BYTES_PER_CTA = 256 * 1024;
 
-__global__ void __launch_bounds__(COPY_THREADS) copy_kernel(uint4* __restrict__ dst,
+// 2-D copy of `rows` rows x `w16` 16-B words (pitches in 16-B words), flattened
+// row-major and split into CTA chunks; atomic preemption unit = one CTA chunk.
+__global__ void __launch_bounds__(COPY_THREADS) copy_kernel(uint4* __restrict__ dst, int64_t dpitch,
                                                             const uint4* __restrict__ src,
+                                                            int64_t spitch, int64_t w16,
                                                             uint64_t n16, Ctl ctl) {
   __shared__ int s_go;
   if (threadIdx.x == 0) {
@@ -125,19 +128,65 @@ __global__ void __launch_bounds__(COPY_THREADS) copy_kernel(uint4* __restrict__ 
   const uint64_t hi = lo + per < n16 ? lo + per : n16;
   constexpr int U = 4;
   uint64_t i = lo + threadIdx.x;
-  for (; i + (U - 1) * COPY_THREADS < hi; i += U * COPY_THREADS) {
-    uint4 v[U];
+  if (dpitch == w16 && spitch == w16) {
+    for (; i + (U - 1) * COPY_THREADS < hi; i += U * COPY_THREADS) {
+      uint4 v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = src[i + u * COPY_THREADS];
+      for (int u = 0; u < U; ++u) v[u] = src[i + u * COPY_THREADS];
 #pragma unroll
-    for (int u = 0; u < U; ++u) dst[i + u * COPY_THREADS] = v[u];
+      for (int u = 0; u < U; ++u) dst[i + u * COPY_THREADS] = v[u];
+    }
+    for (; i < hi; i += COPY_THREADS) dst[i] = src[i];
+  } else {
+    for (; i < hi; i += COPY_THREADS) {
+      const uint64_t r = i / (uint64_t)w16, c = i % (uint64_t)w16;
+      dst[r * dpitch + c] = src[r * spitch + c];
+    }
   }
-  for (; i < hi; i += COPY_THREADS) dst[i] = src[i];
   __syncthreads();
   if (threadIdx.x == 0 && ctl.cursor != nullptr) {
     __threadfence_system();
     atomicAdd(ctl.cursor, 1u);
   }
+}
+
+struct CopyOp final : PreparedOp {
+  uint8_t* dst = nullptr;
+  const uint8_t* src = nullptr;
+  int64_t dpitch = 0, spitch = 0, width = 0, rows = 0;
+  int role = 0;
+  uint64_t n16() const { return (uint64_t)(width / 16) * (uint64_t)rows; }
+  uint32_t units() const override {
+    return (uint32_t)((n16() * 16 + COPY_BYTES_PER_CTA - 1) / COPY_BYTES_PER_CTA);
+  }
+  bool resumable() const override { return false; }
+  int run(const pf_ctl_t* ctl, cudaStream_t s, int64_t in_off, int64_t out_off) override {
+    const uint8_t* sp = src + (role == 1 ? in_off : 0);
+    uint8_t* dp = dst + (role == 2 ? out_off : 0);
+    if (n16() == 0) return PF_OK;
+    copy_kernel<<<units(), COPY_THREADS, 0, s>>>(
+        reinterpret_cast<uint4*>(dp), dpitch / 16, reinterpret_cast<const uint4*>(sp), spitch / 16,
+        width / 16, n16(), make_ctl(ctl));
+    PF_CUDA(cudaGetLastError());
+    return PF_OK;
+  }
+};
+
+int make_copy_op(OpPtr* out, void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch,
+                 int64_t width, int64_t rows, int role) {
+  if (!dst || !src || width < 0 || rows < 0) return set_error(PF_ERR_INVALID, "pf_copy: bad arguments");
+  if ((width | dst_pitch | src_pitch) & 15 || (((uintptr_t)dst | (uintptr_t)src) & 15u))
+    return set_error(PF_ERR_INVALID, "pf_copy: sizes, pitches and pointers must be 16-B aligned");
+  auto op = std::make_unique<CopyOp>();
+  op->dst = static_cast<uint8_t*>(dst);
+  op->src = static_cast<const uint8_t*>(src);
+  op->dpitch = dst_pitch;
+  op->spitch = src_pitch;
+  op->width = width;
+  op->rows = rows;
+  op->role = role;
+  *out = std::move(op);
+  return PF_OK;
 }
 
 __global__ void flag_write_kernel(uint32_t* flag, uint32_t v) {
@@ -358,17 +407,19 @@ int pf_copy_units(uint64_t bytes, uint32_t* out) {
 
 int pf_copy(void* dst, const void* src, uint64_t bytes, const pf_ctl_t* ctl, void* stream) {
   using namespace pf;
-  if (!dst || !src) return set_error(PF_ERR_INVALID, "pf_copy: null pointer");
-  if ((bytes & 15u) || (((uintptr_t)dst | (uintptr_t)src) & 15u))
-    return set_error(PF_ERR_INVALID, "pf_copy: bytes and pointers must be 16-B aligned");
   PF_TRY(validate_ctl(ctl));
-  if (bytes == 0) return PF_OK;
-  const uint64_t grid = (bytes + COPY_BYTES_PER_CTA - 1) / COPY_BYTES_PER_CTA;
-  copy_kernel<<<(unsigned)grid, COPY_THREADS, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src), bytes / 16,
-      make_ctl(ctl));
-  PF_CUDA(cudaGetLastError());
-  return PF_OK;
+  OpPtr op;
+  PF_TRY(make_copy_op(&op, dst, (int64_t)bytes, src, (int64_t)bytes, (int64_t)bytes, 1, 0));
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), 0, 0);
+}
+
+int pf_copy2d(void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch, int64_t width,
+              int64_t rows, const pf_ctl_t* ctl, void* stream) {
+  using namespace pf;
+  PF_TRY(validate_ctl(ctl));
+  OpPtr op;
+  PF_TRY(make_copy_op(&op, dst, dst_pitch, src, src_pitch, width, rows, 0));
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), 0, 0);
 }
 
 // ---- chain ----------------------------------------------------------------------
@@ -386,6 +437,158 @@ int pf_chain_end(uint32_t* done, const uint32_t* abort, void* stream) {
   if (!done) return set_error(PF_ERR_INVALID, "pf_chain_end: null counter");
   chain_end_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(done, abort);
   PF_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// recorded launch chains: one batch of one partition of the fill model
+
+#include <vector>
+
+struct pf_chain {
+  std::vector<pf::OpPtr> nodes;
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;  // 2 per node when timing is on
+  ~pf_chain() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  }
+};
+
+extern "C" {
+
+int pf_chain_create(pf_chain_t** out) {
+  if (!out) return pf::set_error(PF_ERR_INVALID, "pf_chain_create: null out");
+  *out = new pf_chain();
+  return PF_OK;
+}
+
+int pf_chain_destroy(pf_chain_t* c) {
+  delete c;
+  return PF_OK;
+}
+
+static int chain_push(pf_chain_t* c, int rc, pf::OpPtr& op) {
+  if (rc != PF_OK) return rc;
+  c->nodes.push_back(std::move(op));
+  return PF_OK;
+}
+
+int pf_chain_add_gemm(pf_chain_t* c, const void* X, const void* W, const void* bias,
+                      const void* residual, void* Y, int M, int N, int K, uint32_t epilogue) {
+  if (!c) return pf::set_error(PF_ERR_INVALID, "null chain");
+  pf::OpPtr op;
+  return chain_push(c, pf::make_gemm_op(&op, X, W, bias, residual, Y, M, N, K, epilogue), op);
+}
+
+int pf_chain_add_layernorm(pf_chain_t* c, const void* X, const void* residual, const void* gamma,
+                           const void* beta, void* Y, int rows, int cols, float eps) {
+  if (!c) return pf::set_error(PF_ERR_INVALID, "null chain");
+  pf::OpPtr op;
+  return chain_push(c, pf::make_norm_op(&op, false, X, residual, gamma, beta, Y, rows, cols, eps), op);
+}
+
+int pf_chain_add_rmsnorm(pf_chain_t* c, const void* X, const void* residual, const void* gamma,
+                         void* Y, int rows, int cols, float eps) {
+  if (!c) return pf::set_error(PF_ERR_INVALID, "null chain");
+  pf::OpPtr op;
+  return chain_push(c, pf::make_norm_op(&op, true, X, residual, gamma, nullptr, Y, rows, cols, eps), op);
+}
+
+int pf_chain_add_softmax(pf_chain_t* c, const void* X, void* Y, int rows, int cols, float scale) {
+  if (!c) return pf::set_error(PF_ERR_INVALID, "null chain");
+  pf::OpPtr op;
+  return chain_push(c, pf::make_softmax_op(&op, X, Y, rows, cols, scale), op);
+}
+
+int pf_chain_add_attention(pf_chain_t* c, const void* QKV, const float* mask_add, void* O,
+                           int batch, int seq, int heads, int head_dim, float scale) {
+  if (!c) return pf::set_error(PF_ERR_INVALID, "null chain");
+  pf::OpPtr op;
+  return chain_push(
+      c, pf::make_attention_op(&op, QKV, mask_add, O, batch, seq, heads, head_dim, scale), op);
+}
+
+int pf_chain_add_embedding_ln(pf_chain_t* c, const int32_t* ids, const int32_t* type_ids,
+                              const void* word, const void* pos, const void* type,
+                              const void* gamma, const void* beta, void* Y, int batch, int seq,
+                              int hidden, int vocab, float eps) {
+  if (!c) return pf::set_error(PF_ERR_INVALID, "null chain");
+  pf::OpPtr op;
+  return chain_push(c,
+                    pf::make_embedding_op(&op, ids, type_ids, word, pos, type, gamma, beta, Y,
+                                          batch, seq, hidden, vocab, eps),
+                    op);
+}
+
+int pf_chain_add_copy(pf_chain_t* c, void* dst, int64_t dst_pitch, const void* src,
+                      int64_t src_pitch, int64_t width, int64_t rows, int role) {
+  if (!c) return pf::set_error(PF_ERR_INVALID, "null chain");
+  pf::OpPtr op;
+  return chain_push(c, pf::make_copy_op(&op, dst, dst_pitch, src, src_pitch, width, rows, role), op);
+}
+
+int pf_chain_size(pf_chain_t* c, int* n) {
+  if (!c || !n) return pf::set_error(PF_ERR_INVALID, "pf_chain_size: bad arguments");
+  *n = (int)c->nodes.size();
+  return PF_OK;
+}
+
+int pf_chain_node_info(pf_chain_t* c, int node, uint32_t* units, int* resumable) {
+  if (!c || node < 0 || node >= (int)c->nodes.size())
+    return pf::set_error(PF_ERR_INVALID, "pf_chain_node_info: bad node");
+  if (units) *units = c->nodes[node]->units();
+  if (resumable) *resumable = c->nodes[node]->resumable() ? 1 : 0;
+  return PF_OK;
+}
+
+int pf_chain_set_timing(pf_chain_t* c, int enable) {
+  using namespace pf;
+  if (!c) return set_error(PF_ERR_INVALID, "null chain");
+  if (enable && c->ev.size() < 2 * c->nodes.size()) {
+    while (c->ev.size() < 2 * c->nodes.size()) {
+      cudaEvent_t e;
+      PF_CUDA(cudaEventCreate(&e));
+      c->ev.push_back(e);
+    }
+  }
+  c->timing = enable != 0;
+  return PF_OK;
+}
+
+int pf_chain_node_elapsed(pf_chain_t* c, int node, float* ms) {
+  using namespace pf;
+  if (!c || !ms || node < 0 || 2 * node + 1 >= (int)c->ev.size())
+    return set_error(PF_ERR_INVALID, "pf_chain_node_elapsed: bad node or timing never enabled");
+  PF_CUDA(cudaEventElapsedTime(ms, c->ev[2 * node], c->ev[2 * node + 1]));
+  return PF_OK;
+}
+
+int pf_chain_launch(pf_chain_t* c, const uint32_t* flag, uint32_t* abort, uint32_t* cursors,
+                    uint32_t* done, int start_node, int64_t in_off, int64_t out_off, void* stream) {
+  using namespace pf;
+  if (!c) return set_error(PF_ERR_INVALID, "null chain");
+  const int n = (int)c->nodes.size();
+  if (start_node < 0 || start_node > n)
+    return set_error(PF_ERR_INVALID, "pf_chain_launch: start node %d of %d", start_node, n);
+  if (flag && (!abort || !cursors))
+    return set_error(PF_ERR_INVALID, "pf_chain_launch: preemptible chain needs abort and cursors");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (start_node == 0 && cursors) {
+    chain_begin_kernel<<<1, 128, 0, s>>>(cursors, n, abort);
+    PF_CUDA(cudaGetLastError());
+  }
+  for (int i = start_node; i < n; ++i) {
+    pf_ctl_t ctl{flag, abort, cursors ? cursors + i : nullptr};
+    if (c->timing) PF_CUDA(cudaEventRecord(c->ev[2 * i], s));
+    PF_TRY(c->nodes[i]->run(flag || cursors ? &ctl : nullptr, s, in_off, out_off));
+    if (c->timing) PF_CUDA(cudaEventRecord(c->ev[2 * i + 1], s));
+  }
+  if (done) {
+    chain_end_kernel<<<1, 1, 0, s>>>(done, abort);
+    PF_CUDA(cudaGetLastError());
+  }
   return PF_OK;
 }
 

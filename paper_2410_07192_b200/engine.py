@@ -152,8 +152,9 @@ class DeviceWords:
 class IterationRecord:
     iteration: int
     stage: int
-    anchor_off_ns: int  # nominal iteration start relative to the run anchor
+    anchor_off_ns: int  # nominal iteration start relative to the anchor
     end_stamp: int  # index into stamps: end of the last main-job op
+    anchor_stamp: int = -1  # index into stamps holding the anchor this iteration used
     bubbles: list[tuple[int, int, int]] = field(default_factory=list)  # (kind, set idx, clear idx)
 
 
@@ -202,22 +203,29 @@ class StageEngine:
                      for _ in range(config.num_microbatches)]
         self.g_in = [torch.randn(shape, generator=g, device="cuda").to(torch.bfloat16) * 1e-3
                      for _ in range(config.num_microbatches)]
+        self.main.wait_stream(torch.cuda.current_stream())  # inputs were made on the default stream
         self.last_stage = stage_id == config.num_stages - 1
         self.timeline = program_timeline(config, stage_id)
         self.records: list[IterationRecord] = []
         self.outputs: list[torch.Tensor] = []
+        self.launches = 0  # our kernels (timer / stamp / flag) enqueued by the engine
+        self._anchor_stamp = -1
 
     def set_anchor(self, lead_ms: float = 5.0) -> None:
         """Anchor = device time now + lead (host enqueues ahead within the lead)."""
         with torch.cuda.stream(self.main):
             native.call("pf_read_globaltimer", self.words.anchor.data_ptr(), self.main.cuda_stream)
             self.words.anchor.add_(int(lead_ms * 1e6))
+            self._anchor_stamp = self.words.n
+            self.words.stamps[self.words.n:self.words.n + 1].copy_(self.words.anchor)
+            self.words.n += 1
+        self.launches += 1
         self.comm.wait_stream(self.main)
 
     def run_iteration(self, it: int, fill: bool, keep_outputs: bool = False) -> IterationRecord:
         cfg = self.cfg
         base = it * cfg.period_us * US
-        rec = IterationRecord(it, self.stage, base, -1)
+        rec = IterationRecord(it, self.stage, base, -1, self._anchor_stamp)
         prev_end_us = None
         main, comm = self.main, self.comm
         flag = self.words.flag.value
@@ -235,6 +243,7 @@ class StageEngine:
                 self.link.bubble_end(base + end_us * US, self.words.stamp_ptr())
                 end_ev = torch.cuda.Event()
                 end_ev.record(comm)
+                self.launches += 3
                 kind = 0 if ins.kind is BubbleKind.FWD_BWD else 1
                 rec.bubbles.append((kind, set_idx, clear_idx))
                 if fill and self.executor is not None:
@@ -245,6 +254,7 @@ class StageEngine:
             # F / B: wait for the (emulated) recv if the schedule idles before it
             if prev_end_us is None or start_us > prev_end_us:
                 self.link.wait_until(main, base + start_us * US)
+                self.launches += 1
             with torch.cuda.stream(main):
                 if ins.op == "F":
                     y = self.model.forward_mb(ins.mb, self.x_in[ins.mb])
@@ -256,6 +266,7 @@ class StageEngine:
                     self.model.step()
                     rec.end_stamp = self.words.n
                     native.call("pf_read_globaltimer", self.words.stamp_ptr(), main.cuda_stream)
+                    self.launches += 1
             prev_end_us = end_us
         self.records.append(rec)
         return rec
@@ -263,17 +274,21 @@ class StageEngine:
     def _last_compute(self) -> Instr:
         return [ins for ins, _, _ in self.timeline if ins.op != "BUBBLE"][-1]
 
-    def timings(self) -> dict:
-        """Per-iteration main-job span and per-bubble durations from device stamps (ns)."""
+    def record_timing(self, rec: IterationRecord) -> dict:
+        """Device timestamps of one iteration (ns): nominal start, main-job end, and
+        every bubble's (kind, flag set, flag cleared)."""
         torch.cuda.synchronize()
-        st = self.words.stamps.cpu()
-        anchor = int(self.words.anchor.item())
-        iters, bubbles = [], []
-        for r in self.records:
-            iters.append(int(st[r.end_stamp]) - (anchor + r.anchor_off_ns))
-            for kind, si, ci in r.bubbles:
-                bubbles.append((r.iteration, kind, int(st[si]), int(st[ci])))
-        return {"iter_ns": iters, "bubbles": bubbles, "anchor": anchor}
+        st = self.words.stamps
+        start = int(st[rec.anchor_stamp]) + rec.anchor_off_ns
+        end = int(st[rec.end_stamp])
+        bubbles = [(kind, int(st[si]), int(st[ci])) for kind, si, ci in rec.bubbles]
+        last = max([end] + [c for _, _, c in bubbles])
+        return {"start": start, "main_end": end, "step_end": last, "bubbles": bubbles}
+
+    def reset_stamps(self) -> None:
+        torch.cuda.synchronize()
+        self.words.n = 0
+        self.records = []
 
 
 def measure_stage_times(model: GPTStage, reps: int = 5, warmup: int = 2) -> tuple[float, float]:

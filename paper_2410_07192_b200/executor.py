@@ -9,14 +9,18 @@ Executor process. Here the plan is executed for real:
   nn.Sequential runs ``per_bubble[j].num_batches`` batches of
   ``per_bubble[j].batch_size`` samples in bubble j of every cycle until all of the
   range's samples passed through it (the reference's partition-major order);
-* every kernel is launched on a low-priority fill stream behind the bubble's
-  start event and polls the stage's bubble flag at tile granularity, so the
-  work yields within one tile of the main job's recv completing;
-* a yielded batch is resumed at its first incomplete kernel in the next bubble
-  (tile cursor for GEMMs, whole-node re-run for idempotent nodes);
+* one batch of one partition is a native launch chain (libpipefill pf_chain_*),
+  recorded once per (partition, batch size) with every TMA descriptor and launch
+  shape resolved, and replayed with one call per batch on a low-priority fill
+  stream behind the bubble's start event;
+* every kernel polls the stage's bubble flag at tile granularity, so the work
+  yields within one tile of the main job's recv completing; a yielded batch is
+  resumed at its first incomplete kernel in the next bubble (tile cursor for
+  GEMMs, whole-node re-run for idempotent nodes);
 * weights of the next partition are staged host->HBM with pinned copies on a
   side stream while the main job computes; activations between partitions are
-  offloaded to pinned host memory and reloaded (PAPER.md:47);
+  kept in an HBM activation store inside the arena when it fits (B200: 180 GB),
+  else offloaded to pinned host memory and reloaded (PAPER.md:47);
 * everything lives in a fixed arena sized from the measured bubble free memory,
   so the fill job cannot allocate past it.
 """
@@ -25,18 +29,18 @@ from __future__ import annotations
 
 import ctypes
 from dataclasses import dataclass
-from typing import Optional
+from typing import Callable, Optional
 
 import torch
 
 from . import native
 from .arena import Arena, PinnedBuffer, device_view
 from .coordinator import WorkItem
-from .fillmodels import ATOMIC, ExecContext, FillSequential, synthetic_ids
+from .fillmodels import ExecContext, FillSequential, synthetic_ids
 from .planner import ExecutionPlan
 
-MAX_NODES = 4096  # cursor slots in the control block (24-layer BERT-large: 1 + 24*7 + copies)
-_CTL_WORDS = 64 + MAX_NODES  # [0]=abort, [1]=batches done, [8..16)=timestamps(u64), [64..)=cursors
+_CTL_WORDS = 64 + 4096  # [0]=abort, [1]=batches done, [8..12)=timestamps (2 x u64), [64..)=cursors
+_CURSOR0 = 64
 
 
 @dataclass
@@ -53,11 +57,14 @@ class BubbleRecord:
     index: int
     batches_planned: int
     batches_done: int
-    samples_done: int
+    samples_done: int  # samples through this bubble's partition (completed batches)
     aborted: bool
     fill_start_ns: int = 0
     fill_end_ns: int = 0
     launches: int = 0
+    part: int = 0
+    model_fraction: float = 1.0  # share of the model's FLOPs in this bubble's partition
+    samples_completed: int = 0  # samples that left the LAST partition in this bubble
 
 
 @dataclass
@@ -75,20 +82,61 @@ class _Pending:
     batches: list[tuple[int, int, int]]  # (first sample, count, start node)
     end_event: torch.cuda.Event
     launches: int
+    part: int
     has_resume: bool = False
+
+
+class _Chain:
+    """Owner of one recorded pf_chain_t (partition, batch size)."""
+
+    def __init__(self):
+        self.h = ctypes.c_void_p()
+        native.call("pf_chain_create", ctypes.byref(self.h))
+        self.units: list[tuple[int, bool]] = []
+        self.gemm_flops: dict[int, float] = {}
+        self.timing = False
+
+    def finalize(self) -> None:
+        n = ctypes.c_int(0)
+        native.call("pf_chain_size", self.h, ctypes.byref(n))
+        self.units = []
+        for i in range(n.value):
+            u, r = ctypes.c_uint32(0), ctypes.c_int(0)
+            native.call("pf_chain_node_info", self.h, i, ctypes.byref(u), ctypes.byref(r))
+            self.units.append((u.value, bool(r.value)))
+
+    def set_timing(self, on: bool) -> None:
+        if on != self.timing:
+            native.call("pf_chain_set_timing", self.h, 1 if on else 0)
+            self.timing = on
+
+    def gemm_times(self) -> list[tuple[float, float]]:
+        """(flops, ms) of every GEMM node of the last launch."""
+        out = []
+        ms = ctypes.c_float(0)
+        for node, fl in self.gemm_flops.items():
+            native.call("pf_chain_node_elapsed", self.h, node, ctypes.byref(ms))
+            out.append((fl, ms.value))
+        return out
+
+    def close(self) -> None:
+        if self.h:
+            native.call("pf_chain_destroy", self.h)
+            self.h = ctypes.c_void_p()
 
 
 class Executor:
     """One per GPU (pipeline-stage worker). Not thread-safe; driven by the engine."""
 
-    def __init__(self, arena_bytes: int, *, priority: int = 1, job_seed: int = 0):
+    def __init__(self, arena_bytes: int, *, priority: int = 1, job_seed: int = 0,
+                 activation_store: str = "auto"):
         native.require_device()
         self.arena = Arena(arena_bytes)
         lo_prio, hi_prio = torch.cuda.Stream.priority_range()
-        # fill work on the LOWEST priority; staging on its own stream
         self.stream = torch.cuda.Stream(priority=hi_prio if priority == 0 else lo_prio)
         self.copy_stream = torch.cuda.Stream(priority=lo_prio)
         self.job_seed = job_seed
+        self.activation_store = activation_store  # "auto" (HBM if it fits) | "host"
         self.item: Optional[WorkItem] = None
         self.model: Optional[FillSequential] = None
         self.plan: Optional[ExecutionPlan] = None
@@ -97,77 +145,106 @@ class Executor:
         self.records: list[BubbleRecord] = []
         self.samples_completed = 0  # samples through the LAST partition, all items
         self.kernel_launches = 0
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+        self.timing = False  # live per-GEMM device timing (bench roofline)
+        self.gemm_samples: list[tuple[float, float]] = []  # (flops, ms)
+        # called when the executor runs out of work at a bubble: returns the next
+        # (WorkItem, model) from the stage's Coordinator, or None
+        self.work_source: Optional[Callable[[], Optional[tuple[WorkItem, FillSequential]]]] = None
         self._ctl_host = PinnedBuffer((_CTL_WORDS,), torch.int32)
-        self._staged_part: Optional[int] = None
+        self._chains: dict[tuple[int, int], _Chain] = {}
         self._staged_event: Optional[torch.cuda.Event] = None
-        self._results: Optional[PinnedBuffer] = None
-        self._offload: Optional[PinnedBuffer] = None
+        self._staged_part: Optional[int] = None
+        self._cap = 0  # samples the per-range buffers hold
         self._ids_host: Optional[PinnedBuffer] = None
+        self._results: Optional[PinnedBuffer] = None
+        self._store_host: Optional[PinnedBuffer] = None
+        self._store_dev: Optional[torch.Tensor] = None
+        self._layout_key = None
+        self._flops_frac: list[float] = []
 
     # ------------------------------------------------------------------ loading
 
     def load(self, item: WorkItem, model: FillSequential) -> None:
-        """Take a new WorkItem. `item.reuse` (same job as the previous item,
-        PAPER.md:47) keeps the staged executable and arena layout."""
+        """Take a new WorkItem. The arena layout and recorded chains are kept when
+        the executable is unchanged (the Coordinator's `reuse`)."""
         if self.pending is not None:
             self.settle()
-        same = (item.reuse and self.model is model and self.plan is item.plan)
-        self.item, self.model, self.plan = item, model, item.plan
-        self.progress = _Progress()
         n = item.entry.size
         cfg = model.cfg
-        if not same:
-            self._layout()
-        # per-range host buffers: inputs, results, inter-partition activations
-        self._ids_host = PinnedBuffer((n, cfg.seq), torch.int32)
-        self._ids_host.tensor.copy_(synthetic_ids(self.job_seed, item.entry.lo - 1, n, cfg.seq, cfg.vocab))
-        self._results = PinnedBuffer((n, cfg.hidden), torch.bfloat16)
-        self._offload = (PinnedBuffer((n, cfg.seq, cfg.hidden), torch.bfloat16)
-                         if len(self.plan.partitions) > 1 else None)
-        if not same or self._staged_part != 0:
-            self._stage_partition(0)
+        key = (id(model), id(item.plan))
+        if key != self._layout_key or n > self._cap:
+            self.model, self.plan = model, item.plan
+            self._layout(max(n, self._cap))
+            self._layout_key = key
+        self.item = item
+        self.progress = _Progress()
+        self._ids_host.tensor[:n].copy_(
+            synthetic_ids(self.job_seed, item.entry.lo - 1, n, cfg.seq, cfg.vocab))
+        self._stage_partition(0)
 
-    def _layout(self) -> None:
-        """Carve the arena: control block | weights (largest partition) | workspace."""
-        plan, model = self.plan, self.model
+    def _layout(self, cap: int) -> None:
+        """Arena: control block | weight region (largest partition) | workspace | store."""
+        plan, model, cfg = self.plan, self.model, self.model.cfg
+        self._drop_chains()
+        self.stream.synchronize()  # the arena is about to be re-carved
+        self.copy_stream.synchronize()
         self.arena.reset()
         self._ctl = self.arena.alloc((_CTL_WORDS,), torch.int32)
         self._ctl.zero_()
         max_w = max(sum(_pad256(model[i].weight_bytes()) for i in range(p.lo, p.hi))
                     for p in plan.partitions)
-        self._wmark = self.arena.mark()
         self._wregion = self.arena.alloc((max_w // 2,), torch.bfloat16)
         bmax = max(e.batch_size for p in plan.partitions for e in p.per_bubble)
-        cfg = model.cfg
-        need = {}
+        need: dict[str, int] = {}
         for p in plan.partitions:
             for k, v in model.workspace(p.lo, p.hi, bmax).items():
                 need[k] = max(need.get(k, 0), v)
         need["hidden"] = bmax * cfg.seq * cfg.hidden
-        need["cls"] = bmax * cfg.hidden
         self.ws = {k: self.arena.alloc((v,), torch.bfloat16) for k, v in need.items()}
         self.ids_dev = self.arena.alloc((bmax, cfg.seq), torch.int32)
+        self._cap = cap
+        self._ids_host = PinnedBuffer((cap, cfg.seq), torch.int32)
+        self._results = PinnedBuffer((cap, cfg.hidden), torch.bfloat16)
+        self._store_dev = None
+        self._store_host = None
+        if len(plan.partitions) > 1:
+            store_bytes = cap * cfg.seq * cfg.hidden * 2
+            free = self.arena.capacity - self.arena.stats()["used"]
+            if self.activation_store == "auto" and store_bytes + (64 << 20) <= free:
+                self._store_dev = self.arena.alloc((cap * cfg.seq * cfg.hidden,), torch.bfloat16)
+            else:
+                self._store_host = PinnedBuffer((cap, cfg.seq, cfg.hidden), torch.bfloat16)
+        total = sum(model[i].flops_per_sample() for i in range(len(model))) or 1.0
+        self._flops_frac = [sum(model[i].flops_per_sample() for i in range(p.lo, p.hi)) / total
+                            for p in plan.partitions]
         self._staged_part = None
 
+    def _store_ptr(self) -> int:
+        return self._store_dev.data_ptr() if self._store_dev is not None else self._store_host.ptr
+
     def _stage_partition(self, part: int) -> None:
-        """Stage partition `part`'s weights into the weight region on the copy stream."""
+        """Stage partition `part`'s weights into the weight region on the copy stream
+        (pinned cudaMemcpyAsync), after the fill stream drained the previous partition."""
+        if self._staged_part == part:
+            return
         p = self.plan.partitions[part]
         ptr = self._wregion.data_ptr()
         with torch.cuda.stream(self.copy_stream):
-            if self._staged_event is not None:
-                self.copy_stream.wait_event(self._staged_event)
-            self.copy_stream.wait_stream(self.stream)  # previous partition's kernels are done
+            self.copy_stream.wait_stream(self.stream)
             for i in range(p.lo, p.hi):
                 mod = self.model[i]
                 nbytes = mod.weight_bytes()
                 dflat = device_view(ptr, (nbytes // 2,), torch.bfloat16)
                 native.call("pf_stage_h2d", ptr, mod.host.ptr, nbytes, self.copy_stream.cuda_stream)
-                off = 0
+                self.h2d_bytes += nbytes
                 mod.dev = {}
+                off = 0
                 for name, shape, _ in mod.param_specs():
                     nel = 1
-                    for s in shape:
-                        nel *= s
+                    for s_ in shape:
+                        nel *= s_
                     mod.dev[name] = dflat[off:off + nel].view(*shape)
                     off += nel
                 ptr += _pad256(nbytes)
@@ -175,6 +252,53 @@ class Executor:
         ev.record(self.copy_stream)
         self._staged_event = ev
         self._staged_part = part
+        # recorded chains point at the previous partition's weights: drop them
+        self._drop_chains()
+
+    # ------------------------------------------------------------------ chains
+
+    def _chain(self, part_idx: int, cnt: int) -> _Chain:
+        key = (part_idx, cnt)
+        ch = self._chains.get(key)
+        if ch is not None:
+            return ch
+        model, cfg = self.model, self.model.cfg
+        part = self.plan.partitions[part_idx]
+        s, h = cfg.seq, cfg.hidden
+        ch = _Chain()
+        ctx = ExecContext(self.stream, self.ws, chain=ch.h)
+        # node 0: the batch's input slice (role 1: source + in_off)
+        if part.lo == 0:
+            native.call("pf_chain_add_copy", ch.h, self.ids_dev.data_ptr(), cnt * s * 4,
+                        self._ids_host.ptr, cnt * s * 4, cnt * s * 4, 1, 1)
+            x = self.ids_dev[:cnt]
+        else:
+            x = ctx.buf("hidden", cnt * s * h).view(cnt, s, h)
+            native.call("pf_chain_add_copy", ch.h, x.data_ptr(), cnt * s * h * 2, self._store_ptr(),
+                        cnt * s * h * 2, cnt * s * h * 2, 1, 1)
+        ctx.node = 1
+        for i in range(part.lo, part.hi):
+            before = ctx.node
+            x = model[i](x, ctx)
+            for node, fl in model[i].gemm_node_flops(cnt):
+                ch.gemm_flops[before + node] = fl
+        # last node: the batch's output slice (role 2: destination + out_off)
+        if part.hi == len(model):
+            # [CLS] rows of [cnt, s, h] gathered straight into the pinned results
+            native.call("pf_chain_add_copy", ch.h, self._results.ptr, h * 2, x.data_ptr(), s * h * 2,
+                        h * 2, cnt, 2)
+        else:
+            native.call("pf_chain_add_copy", ch.h, self._store_ptr(), cnt * s * h * 2, x.data_ptr(),
+                        cnt * s * h * 2, cnt * s * h * 2, 1, 2)
+        ch.finalize()
+        self._chains[key] = ch
+        return ch
+
+    def _drop_chains(self) -> None:
+        # safe with launches in flight: kernel parameters are copied at launch time
+        for ch in self._chains.values():
+            ch.close()
+        self._chains = {}
 
     # ------------------------------------------------------------------ bubbles
 
@@ -186,6 +310,10 @@ class Executor:
         """Enqueue this bubble's planned batches (asynchronously). The previous
         bubble is settled first. Returns the settled record of the previous bubble."""
         prev = self.settle() if self.pending is not None else None
+        if not self.busy and self.work_source is not None:
+            nxt = self.work_source()
+            if nxt is not None:
+                self.load(*nxt)
         if not self.busy:
             return prev
         pr = self.progress
@@ -205,100 +333,51 @@ class Executor:
                 start += cnt
         if not batches:
             return prev
+        cfg = self.model.cfg
+        s, h = cfg.seq, cfg.hidden
         st = self.stream
-        ctl = self._ctl
-        base = ctl.data_ptr()
+        base = self._ctl.data_ptr()
         abort_ptr, done_ptr = base, base + 4
-        t_start, t_end = base + 32, base + 40
-        cursors = base + 4 * 64
+        cursors = base + 4 * _CURSOR0
+        flag = slot.flag_ptr or None
         launches = 0
         with torch.cuda.stream(st):
             if slot.start_event is not None:
                 st.wait_event(slot.start_event)
             if self._staged_event is not None:
                 st.wait_event(self._staged_event)
-            # fresh bubble: clear the abort word and the done counter
-            ctl[:2].zero_()
+            self._ctl[:2].zero_()  # fresh bubble: abort word and done counter
             if pr.resume_zero is not None:
-                ctl[64 + pr.resume_zero] = 0
+                self._ctl[_CURSOR0 + pr.resume_zero] = 0
                 pr.resume_zero = None
-            native.call("pf_read_globaltimer", t_start, st.cuda_stream)
+            native.call("pf_read_globaltimer", base + 32, st.cuda_stream)
             for first, cnt, node in batches:
-                launches += self._enqueue_batch(pr.part, first, cnt, node, slot.flag_ptr, abort_ptr,
-                                                cursors, done_ptr)
-            native.call("pf_read_globaltimer", t_end, st.cuda_stream)
+                ch = self._chain(pr.part, cnt)
+                ch.set_timing(self.timing and bool(ch.gemm_flops))
+                if part.lo == 0:
+                    in_off = first * s * 4
+                    self.h2d_bytes += cnt * s * 4 if node == 0 else 0
+                else:
+                    in_off = first * s * h * 2
+                    if self._store_host is not None and node == 0:
+                        self.h2d_bytes += cnt * s * h * 2
+                if part.hi == len(self.model):
+                    out_off = first * h * 2
+                    self.d2h_bytes += cnt * h * 2
+                else:
+                    out_off = first * s * h * 2
+                    if self._store_host is not None:
+                        self.d2h_bytes += cnt * s * h * 2
+                native.call("pf_chain_launch", ch.h, flag, abort_ptr if flag else None,
+                            cursors if flag else None, done_ptr, node, in_off, out_off, st.cuda_stream)
+                launches += len(ch.units) - node + (1 if node == 0 else 0) + 1
+            native.call("pf_read_globaltimer", base + 40, st.cuda_stream)
             launches += 2
         ev = torch.cuda.Event()
         ev.record(st)
-        self.pending = _Pending(slot, batches, ev, launches, has_resume=pr.resume is not None)
+        self.pending = _Pending(slot, batches, ev, launches, pr.part, has_resume=pr.resume is not None)
         self.kernel_launches += launches
         return prev
-
-    def _enqueue_batch(self, part_idx: int, first: int, cnt: int, start_node: int, flag: int,
-                       abort: int, cursors: int, done: int) -> int:
-        """One batch of one partition as a chain of preemptible launches."""
-        model, cfg = self.model, self.model.cfg
-        part = self.plan.partitions[part_idx]
-        st = self.stream
-        s, h = cfg.seq, cfg.hidden
-        ctx = ExecContext(st, self.ws, flag, abort, cursors)
-        ctx.start_node = start_node
-        launches = 0
-        if start_node == 0:
-            native.call("pf_chain_begin", cursors, MAX_NODES, abort, st.cuda_stream)
-            launches += 1
-        # node 0: the batch's input
-        if part.lo == 0:
-            src = self._ids_host.ptr + first * s * 4
-            ids = self.ids_dev[:cnt]
-            if ctx.active():
-                native.call("pf_copy", ids.data_ptr(), src, cnt * s * 4,
-                            ctypes.byref(ctx.ctl().as_struct()) if flag else None, st.cuda_stream)
-                launches += 1
-            else:
-                ctx.skip()
-            x = ids
-        else:
-            hid = ctx.buf("hidden", cnt * s * h).view(cnt, s, h)
-            src = self._offload.ptr + first * s * h * 2
-            if ctx.active():
-                native.call("pf_copy", hid.data_ptr(), src, cnt * s * h * 2,
-                            ctypes.byref(ctx.ctl().as_struct()) if flag else None, st.cuda_stream)
-                launches += 1
-            else:
-                ctx.skip()
-            x = hid
-        for i in range(part.lo, part.hi):
-            x = model[i](x, ctx)
-        # last node: the batch's output
-        last = part.hi == len(model)
-        if last:
-            # CLS rows [cnt, h] (row stride s*h) -> results; one copy per row would be
-            # cnt launches, so gather on the device side via a strided view
-            dst = self._results.ptr + first * h * 2
-            if ctx.active():
-                cls = x[:, 0, :]
-                with torch.cuda.stream(st):
-                    # dedicated buffer: this (non-preemptible) gather never touches
-                    # anything a resumed node reads
-                    staged = self.ws["cls"].view(-1)[: cnt * h].view(cnt, h)
-                    staged.copy_(cls)
-                native.call("pf_copy", dst, staged.data_ptr(), cnt * h * 2,
-                            ctypes.byref(ctx.ctl().as_struct()) if flag else None, st.cuda_stream)
-                launches += 1
-            else:
-                ctx.skip()
-        else:
-            dst = self._offload.ptr + first * s * h * 2
-            if ctx.active():
-                native.call("pf_copy", dst, x.data_ptr(), cnt * s * h * 2,
-                            ctypes.byref(ctx.ctl().as_struct()) if flag else None, st.cuda_stream)
-                launches += 1
-            else:
-                ctx.skip()
-        native.call("pf_chain_end", done, abort, st.cuda_stream)
-        launches += 1 + ctx.launched
-        return launches
 
     def settle(self) -> Optional[BubbleRecord]:
         """Wait for the pending bubble's fill work, read the control block, advance
@@ -310,15 +389,20 @@ class Executor:
         pend.end_event.synchronize()
         words = self._ctl_host
         native.call("pf_stage_d2h", words.ptr, self._ctl.data_ptr(), 4 * _CTL_WORDS,
-                    torch.cuda.current_stream().cuda_stream)
-        torch.cuda.current_stream().synchronize()
+                    self.stream.cuda_stream)
+        self.stream.synchronize()
         w = words.tensor
         aborted = int(w[0]) != 0
         done = int(w[1])
         ts = w[8:12].view(torch.int64)
         pr = self.progress
-        rec = BubbleRecord(pend.slot.index, len(pend.batches), done, 0, aborted,
-                           int(ts[0]), int(ts[1]), pend.launches)
+        rec = BubbleRecord(pend.slot.index, len(pend.batches), done, 0, aborted, int(ts[0]), int(ts[1]),
+                           pend.launches, pend.part, self._flops_frac[pend.part])
+        if self.timing and done > 0 and not aborted:
+            last_cnt = pend.batches[min(done, len(pend.batches)) - 1][1]
+            ch = self._chains.get((pend.part, last_cnt))
+            if ch is not None and ch.timing:
+                self.gemm_samples.extend(ch.gemm_times())
         n_total = self.item.entry.size
         samples = 0
         for k, (first, cnt, node) in enumerate(pend.batches):
@@ -329,66 +413,49 @@ class Executor:
                 else:
                     pr.next_sample = max(pr.next_sample, first + cnt)
             elif k == done and aborted:
-                # first incomplete node of the interrupted batch
-                units = self._node_units(pr.part, cnt)
-                cur = w[64:64 + len(units)]
-                resume_node = len(units)
-                for j, (u, kind) in enumerate(units):
+                ch = self._chains[(pend.part, cnt)]
+                cur = w[_CURSOR0:_CURSOR0 + len(ch.units)]
+                resume_node = len(ch.units)
+                for j, (u, _) in enumerate(ch.units):
                     if int(cur[j]) < u:
                         resume_node = j
                         break
-                # atomic nodes re-run whole: zero their cursor; prefix nodes keep it
-                if resume_node < len(units) and units[resume_node][1] == ATOMIC:
-                    pr.resume_zero = resume_node
                 if not (k == 0 and pend.has_resume):
                     pr.next_sample = max(pr.next_sample, first + cnt)
-                pr.resume = (first, cnt, max(resume_node, node) if resume_node < len(units) else 0)
-                if resume_node >= len(units):
+                if resume_node >= len(ch.units):
                     pr.resume = None  # every node finished; only the end marker was skipped
                     samples += cnt
+                else:
+                    pr.resume = (first, cnt, max(resume_node, node))
+                    if not ch.units[resume_node][1]:
+                        pr.resume_zero = resume_node  # atomic: re-run the whole node
                 break
             else:
                 break
         rec.samples_done = samples
-        part = self.plan.partitions[pr.part]
+        if pend.part == len(self.plan.partitions) - 1:
+            rec.samples_completed = samples
+            self.samples_completed += samples
         if pr.resume is None and pr.next_sample >= n_total:
             if pr.part == len(self.plan.partitions) - 1:
-                self.samples_completed += n_total
                 pr.finished = True
             else:
                 pr.part += 1
                 pr.next_sample = 0
                 self._stage_partition(pr.part)
-        _ = part
         self.records.append(rec)
         return rec
 
-    def _node_units(self, part_idx: int, cnt: int) -> list[tuple[int, str]]:
-        part = self.plan.partitions[part_idx]
-        cfg = self.model.cfg
-        units: list[tuple[int, str]] = []
-        in_bytes = cnt * cfg.seq * (4 if part.lo == 0 else 2 * cfg.hidden)
-        units.append((_copy_units(in_bytes), ATOMIC))
-        units.extend(self.model.node_units(part.lo, part.hi, cnt))
-        out_bytes = cnt * cfg.hidden * 2 if part.hi == len(self.model) else cnt * cfg.seq * cfg.hidden * 2
-        units.append((_copy_units(out_bytes), ATOMIC))
-        return units
-
     def results(self) -> torch.Tensor:
         """[N, hidden] bf16 CLS embeddings of the current range (host, pinned)."""
-        return self._results.tensor
+        return self._results.tensor[: self.item.entry.size]
 
     def close(self) -> None:
         self.settle()
         torch.cuda.synchronize()
+        self._drop_chains()
         self.arena.close()
 
 
 def _pad256(n: int) -> int:
     return (n + 255) // 256 * 256
-
-
-def _copy_units(nbytes: int) -> int:
-    out = ctypes.c_uint32(0)
-    native.call("pf_copy_units", nbytes, ctypes.byref(out))
-    return out.value

@@ -63,18 +63,25 @@ BERT_LARGE = BertConfig("bert_large", hidden=1024, heads=16, ffn=4096, layers=24
 
 
 class ExecContext:
-    """Per-launch-chain state: stream, preemption words, workspace buffers."""
+    """Where a module's kernel nodes go: launched now (eager: tests, profiler) or
+    recorded into a native chain (``chain``: the Executor's per-batch replay path).
+
+    Eager mode carries the preemption words (flag, abort, per-node cursors) and can
+    skip nodes below ``start_node`` (resume)."""
 
     def __init__(self, stream: torch.cuda.Stream, workspace: dict[str, torch.Tensor],
-                 flag: int = 0, abort: int = 0, cursors: int = 0):
+                 flag: int = 0, abort: int = 0, cursors: int = 0, chain: Optional[int] = None):
         self.stream = stream
         self.ws = workspace
         self.flag = flag
         self.abort = abort
         self.cursors = cursors
+        self.chain = chain  # pf_chain_t* (record mode) or None
         self.node = 0
-        self.start_node = 0  # nodes below this are skipped (resume)
+        self.start_node = 0  # nodes below this are skipped (eager resume)
         self.launched = 0
+        # optional live timing of eager GEMM launches: list of (start event, end event, flops)
+        self.gemm_timers: Optional[list] = None
 
     def ctl(self) -> Optional[KernelCtl]:
         idx = self.node
@@ -92,6 +99,66 @@ class ExecContext:
 
     def buf(self, name: str, numel: int) -> torch.Tensor:
         return self.ws[name].view(-1)[:numel]
+
+    # -- nodes -----------------------------------------------------------------
+    def _eager(self, fn, flops: float = 0.0) -> None:
+        if not self.active():
+            self.skip()
+            return
+        timed = flops > 0 and self.gemm_timers is not None
+        if timed:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(self.stream)
+        fn(self.ctl())
+        if timed:
+            e1.record(self.stream)
+            self.gemm_timers.append((e0, e1, flops))
+        self.launched += 1
+
+    def gemm(self, x, w, b, out, *, gelu: bool = False, residual=None) -> None:
+        k = x.shape[-1]
+        m = x.numel() // k
+        n = w.shape[0]
+        if self.chain is not None:
+            epi = (native.PF_EPI_BIAS if b is not None else 0) | (native.PF_EPI_GELU if gelu else 0) \
+                | (native.PF_EPI_RESIDUAL if residual is not None else 0)
+            native.call("pf_chain_add_gemm", self.chain, x.data_ptr(), w.data_ptr(),
+                        None if b is None else b.data_ptr(),
+                        None if residual is None else residual.data_ptr(), out.data_ptr(), m, n, k, epi)
+            self.node += 1
+            return
+        self._eager(lambda c: K.linear(x, w, b, gelu=gelu, residual=residual, out=out, ctl=c,
+                                       stream=self.stream), flops=2.0 * m * n * k)
+
+    def attention(self, qkv, heads: int, out) -> None:
+        if self.chain is not None:
+            b, s, three_h = qkv.shape
+            hd = three_h // 3 // heads
+            native.call("pf_chain_add_attention", self.chain, qkv.data_ptr(), None, out.data_ptr(), b, s,
+                        heads, hd, float(hd ** -0.5))
+            self.node += 1
+            return
+        self._eager(lambda c: K.attention(qkv, heads, out=out, ctl=c, stream=self.stream))
+
+    def layernorm(self, x, g, b, eps: float, out) -> None:
+        if self.chain is not None:
+            cols = x.shape[-1]
+            native.call("pf_chain_add_layernorm", self.chain, x.data_ptr(), None, g.data_ptr(),
+                        b.data_ptr(), out.data_ptr(), x.numel() // cols, cols, float(eps))
+            self.node += 1
+            return
+        self._eager(lambda c: K.layernorm(x, g, b, eps, out=out, ctl=c, stream=self.stream))
+
+    def embedding(self, ids, word, pos, typ, g, b, eps: float, out) -> None:
+        if self.chain is not None:
+            bsz, s = ids.shape
+            native.call("pf_chain_add_embedding_ln", self.chain, ids.data_ptr(), None, word.data_ptr(),
+                        pos.data_ptr(), typ.data_ptr(), g.data_ptr(), b.data_ptr(), out.data_ptr(), bsz, s,
+                        word.shape[1], word.shape[0], float(eps))
+            self.node += 1
+            return
+        self._eager(lambda c: K.embedding_ln(ids, word, pos, typ, g, b, eps, out=out, ctl=c,
+                                             stream=self.stream))
 
 
 class FillModule(nn.Module):
@@ -149,6 +216,14 @@ class FillModule(nn.Module):
     def workspace(self, batch: int, seq: int) -> dict[str, int]:
         return {}
 
+    def flops_per_sample(self) -> float:
+        """Algorithmic forward FLOPs of this module for one sequence."""
+        return 0.0
+
+    def gemm_node_flops(self, batch: int) -> list[tuple[int, float]]:
+        """(node index within this module, algorithmic FLOPs) of its GEMM nodes."""
+        return []
+
     def node_units(self, batch: int, seq: int) -> list[tuple[int, str]]:
         raise NotImplementedError
 
@@ -184,13 +259,8 @@ class BertEmbeddings(FillModule):
     def forward(self, ids: torch.Tensor, ctx: ExecContext) -> torch.Tensor:
         b, s = ids.shape
         out = ctx.buf("hidden", b * s * self.cfg.hidden).view(b, s, self.cfg.hidden)
-        if ctx.active():
-            d = self.dev
-            K.embedding_ln(ids, d["word"], d["pos"], d["type"], d["ln_g"], d["ln_b"], self.cfg.eps,
-                           out=out, ctl=ctx.ctl(), stream=ctx.stream)
-            ctx.launched += 1
-        else:
-            ctx.skip()
+        d = self.dev
+        ctx.embedding(ids, d["word"], d["pos"], d["type"], d["ln_g"], d["ln_b"], self.cfg.eps, out)
         return out
 
 
@@ -218,6 +288,15 @@ class BertLayer(FillModule):
         m, h, f = batch * seq, self.cfg.hidden, self.cfg.ffn
         return {"qkv": m * 3 * h, "ctx": m * h, "a": m * h, "a_ln": m * h, "ffn": m * f, "o": m * h}
 
+    def flops_per_sample(self) -> float:
+        s, h, f = self.cfg.seq, self.cfg.hidden, self.cfg.ffn
+        return 2.0 * s * (4 * h * h + 2 * h * f) + 4.0 * s * s * h
+
+    def gemm_node_flops(self, batch: int) -> list[tuple[int, float]]:
+        m, h, f = batch * self.cfg.seq, self.cfg.hidden, self.cfg.ffn
+        return [(0, 2.0 * m * 3 * h * h), (2, 2.0 * m * h * h), (4, 2.0 * m * h * f),
+                (5, 2.0 * m * f * h)]
+
     def node_units(self, batch, seq):
         m, h, f = batch * seq, self.cfg.hidden, self.cfg.ffn
         return [(K.gemm_units(m, 3 * h, h), PREFIX),
@@ -231,7 +310,7 @@ class BertLayer(FillModule):
     def forward(self, x: torch.Tensor, ctx: ExecContext) -> torch.Tensor:
         b, s, h = x.shape
         m, f = b * s, self.cfg.ffn
-        d, st = self.dev, ctx.stream
+        d = self.dev
         x2 = x.view(m, h)
         qkv = ctx.buf("qkv", m * 3 * h).view(b, s, 3 * h)
         cx = ctx.buf("ctx", m * h).view(m, h)
@@ -239,21 +318,13 @@ class BertLayer(FillModule):
         a_ln = ctx.buf("a_ln", m * h).view(m, h)
         hf = ctx.buf("ffn", m * f).view(m, f)
         o = ctx.buf("o", m * h).view(m, h)
-        steps = [
-            lambda c: K.linear(x2, d["qkv_w"], d["qkv_b"], out=qkv.view(m, 3 * h), ctl=c, stream=st),
-            lambda c: K.attention(qkv, self.cfg.heads, out=cx.view(b, s, h), ctl=c, stream=st),
-            lambda c: K.linear(cx, d["out_w"], d["out_b"], residual=x2, out=a, ctl=c, stream=st),
-            lambda c: K.layernorm(a, d["ln1_g"], d["ln1_b"], self.cfg.eps, out=a_ln, ctl=c, stream=st),
-            lambda c: K.linear(a_ln, d["ffn1_w"], d["ffn1_b"], gelu=True, out=hf, ctl=c, stream=st),
-            lambda c: K.linear(hf, d["ffn2_w"], d["ffn2_b"], residual=a_ln, out=o, ctl=c, stream=st),
-            lambda c: K.layernorm(o, d["ln2_g"], d["ln2_b"], self.cfg.eps, out=x2, ctl=c, stream=st),
-        ]
-        for step in steps:
-            if ctx.active():
-                step(ctx.ctl())
-                ctx.launched += 1
-            else:
-                ctx.skip()
+        ctx.gemm(x2, d["qkv_w"], d["qkv_b"], qkv.view(m, 3 * h))
+        ctx.attention(qkv, self.cfg.heads, cx.view(b, s, h))
+        ctx.gemm(cx, d["out_w"], d["out_b"], a, residual=x2)
+        ctx.layernorm(a, d["ln1_g"], d["ln1_b"], self.cfg.eps, a_ln)
+        ctx.gemm(a_ln, d["ffn1_w"], d["ffn1_b"], hf, gelu=True)
+        ctx.gemm(hf, d["ffn2_w"], d["ffn2_b"], o, residual=a_ln)
+        ctx.layernorm(o, d["ln2_g"], d["ln2_b"], self.cfg.eps, x2)
         return x
 
 

@@ -10,7 +10,7 @@ from __future__ import annotations
 import ctypes
 import os
 import re
-from ctypes import POINTER, c_char_p, c_float, c_int, c_uint32, c_uint64, c_void_p
+from ctypes import POINTER, c_char_p, c_float, c_int, c_int64, c_uint32, c_uint64, c_void_p
 
 LIB_NAME = "libpipefill.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
@@ -105,6 +105,30 @@ _SIGNATURES: dict[str, tuple] = {
     ),
     "pf_copy": (c_int, [c_void_p, c_void_p, c_uint64, POINTER(PfCtl), c_void_p]),
     "pf_copy_units": (c_int, [c_uint64, POINTER(c_uint32)]),
+    "pf_copy2d": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, POINTER(PfCtl),
+                          c_void_p]),
+    "pf_chain_create": (c_int, [POINTER(c_void_p)]),
+    "pf_chain_destroy": (c_int, [c_void_p]),
+    "pf_chain_add_gemm": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
+                                  c_int, c_int, c_uint32]),
+    "pf_chain_add_layernorm": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                       c_int, c_int, c_float]),
+    "pf_chain_add_rmsnorm": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int,
+                                     c_float]),
+    "pf_chain_add_softmax": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_float]),
+    "pf_chain_add_attention": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int,
+                                       c_int, c_float]),
+    "pf_chain_add_embedding_ln": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                          c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int,
+                                          c_float]),
+    "pf_chain_add_copy": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64,
+                                  c_int]),
+    "pf_chain_size": (c_int, [c_void_p, POINTER(c_int)]),
+    "pf_chain_set_timing": (c_int, [c_void_p, c_int]),
+    "pf_chain_node_elapsed": (c_int, [c_void_p, c_int, POINTER(c_float)]),
+    "pf_chain_node_info": (c_int, [c_void_p, c_int, POINTER(c_uint32), POINTER(c_int)]),
+    "pf_chain_launch": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int64,
+                                c_int64, c_void_p]),
     "pf_chain_begin": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
     "pf_chain_end": (c_int, [c_void_p, c_void_p, c_void_p]),
 }
