@@ -172,6 +172,9 @@ def main() -> None:
     ap.add_argument("--fill", default="bert_large", choices=("bert_large", "bert_base"))
     ap.add_argument("--main", default="gpt8b", choices=("gpt8b", "gpt2small"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pipeline", default="emulated", choices=("emulated", "nccl"),
+                    help="emulated: every rank runs stages of an 8-stage pipeline against artificial "
+                         "neighbours; nccl: the N ranks ARE an N-stage pipeline (NCCL P2P over NVLink)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -188,10 +191,11 @@ def main() -> None:
 
     import paper_2410_07192_b200 as pf
     from paper_2410_07192_b200 import native
-    from paper_2410_07192_b200.engine import (GPT2_SMALL_STAGE, GPT_8B_STAGE, GPTStage, StageEngine,
-                                              measure_stage_times)
+    from paper_2410_07192_b200.engine import (GPT2_SMALL_STAGE, GPT_8B_STAGE, GPTStage,
+                                              NcclPipelineEngine, StageEngine, measure_stage_times)
     from paper_2410_07192_b200.executor import Executor
     from paper_2410_07192_b200.fillmodels import BERT_BASE, BERT_LARGE, bert
+    from paper_2410_07192_b200.metrics import FillStats, aggregate, busy_in_bubbles, mean_slowdown
     from paper_2410_07192_b200.profiler import measure_profile
 
     native.require_device()
@@ -222,19 +226,17 @@ def main() -> None:
                              arena_bytes, arena_bytes, FILL_FRACTION)
 
     executor = Executor(arena_bytes, job_seed=rank)
-    engines: dict[int, StageEngine] = {}
     coords: dict[int, pf.Coordinator] = {}
+    engines: dict[int, object] = {}
     items: dict[int, object] = {}
 
-    def engine_for(s: int) -> StageEngine:
-        if s not in engines:
-            engines[s] = StageEngine(pcfg, s, main_model, executor)
+    def coordinator_for(s: int, cfg) -> pf.Coordinator:
+        if s not in coords:
             # the stage's Coordinator; a long-running fill job split into 16K-sample ranges
-            coords[s] = pf.Coordinator(s, pf.build_bubble_cycle(pcfg, s), 1,
+            coords[s] = pf.Coordinator(s, pf.build_bubble_cycle(cfg, s), 1,
                                        pf.OrderingPolicy("concurrent", 16384))
-            job = pf.JobSpec(f"fill-{s}", 0.0, profile, pf.JobKind.BATCH_INFERENCE, 10_000_000)
-            coords[s].admit(job)
-        return engines[s]
+            coords[s].admit(pf.JobSpec(f"fill-{s}", 0.0, profile, pf.JobKind.BATCH_INFERENCE, 10_000_000))
+        return coords[s]
 
     def next_work():
         s = items["stage"]
@@ -246,97 +248,154 @@ def main() -> None:
         return None if item is None else (item, fill_model)
 
     executor.work_source = next_work
-
-    def run_step(k: int, fill: bool, stage: int | None = None) -> dict:
-        s = (rank + k * world) % P_STAGES if stage is None else stage
-        eng = engine_for(s)
-        if fill and items.get("stage") != s:
-            if items.get("item") is not None and items.get("stage") is not None:
-                coords[items["stage"]].worker_job[0] = None  # abandon the partial range
-            items["stage"], items["item"] = s, None
-            executor.item = None  # force next_work() at the first bubble
-        eng.reset_stamps()
-        eng.set_anchor()
-        rec = eng.run_iteration(0, fill=fill)
-        if fill:
-            executor.settle()
-        t = eng.record_timing(rec)
-        t["stage"] = s
-        return t
-
-    # ---- fill-off iterations: the main job's own iteration time per stage (one
-    # untimed + one timed iteration of every stage the timed fill-on steps visit)
     n_total = args.warmup + args.steps
-    off = {}
-    for s_ in sorted({(rank + k * world) % P_STAGES for k in range(args.warmup, n_total)}):
-        for rep in range(2):
-            t = run_step(s_, fill=False, stage=s_)
-            if rep:
-                off.setdefault(s_, []).append(t["main_end"] - t["start"])
+    off: dict[int, list] = {}
 
-    # ---- fill-on: warmup, then the timed steps
-    for k in range(args.warmup):
-        run_step(k, fill=True)
-    executor.timing = True
-    executor.gemm_samples = []
-    n_rec0 = len(executor.records)
-    launches0 = executor.kernel_launches + sum(e.launches for e in engines.values())
-    h2d0, d2h0 = executor.h2d_bytes, executor.d2h_bytes
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    steps = []
-    with ClockSampler(local) as clocks:
-        w0 = time.perf_counter()
-        for k in range(args.warmup, n_total):
-            steps.append(run_step(k, fill=True))
+    if args.pipeline == "nccl":
+        # the N ranks form an N-stage 1F1B pipeline; t_fwd/t_bwd = slowest stage
+        tt = torch.tensor([tf_ms, tb_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tf_ms, tb_ms = tt.tolist()
+        pcfg = pf.PipelineConfig(world, M_MICRO, tf_ms, tb_ms, pf.ScheduleKind.ONE_F_ONE_B,
+                                 arena_bytes, arena_bytes, FILL_FRACTION)
+        eng = NcclPipelineEngine(pcfg, main_model, executor)
+        engines[rank] = eng
+        coordinator_for(rank, pcfg)
+        items["stage"], items["item"] = rank, None
+
+        def run_phase(fill: bool) -> list[dict]:
+            eng.reset_stamps()
+            dist.barrier()
+            eng.set_anchor()
+            recs_ = []
+            for it in range(n_total):
+                recs_.append(eng.run_iteration(it, fill=fill, last=(it == n_total - 1)))
+            if fill:
+                executor.settle()
+            eng.sync()
+            out, prev_end = [], None
+            for it, r in enumerate(recs_):
+                t = eng.record_timing(r)
+                if prev_end is not None and it >= args.warmup:
+                    out.append({"start": prev_end, "main_end": t["main_end"], "step_end": t["main_end"],
+                                "bubbles": t["bubbles"], "stage": rank})
+                prev_end = t["main_end"]
+            return out
+
+        snap = main_model.snapshot()  # both phases train from the same weights and data
+        for t in run_phase(False):
+            off.setdefault(rank, []).append(t["main_end"] - t["start"])
+        losses_off = [float(x) for x in eng.losses]
+        eng.losses = []
+        main_model.restore(snap)
+        del snap
+        executor.timing = True
+        executor.gemm_samples = []
+        n_rec0 = len(executor.records)
+        launches0 = executor.kernel_launches + eng.launches
+        h2d0, d2h0 = executor.h2d_bytes, executor.d2h_bytes
         torch.cuda.synchronize()
-        checksum = float(executor.results().float().sum())  # host reads the results
-        w1 = time.perf_counter()
-    recs = executor.records[n_rec0:]
-    launches = executor.kernel_launches + sum(e.launches for e in engines.values()) - launches0
+        with ClockSampler(local) as clocks:
+            w0 = time.perf_counter()
+            steps = run_phase(True)
+            torch.cuda.synchronize()
+            checksum = float(executor.results().float().sum()) if executor.item is not None else 0.0
+            w1 = time.perf_counter()
+        # host wall clock of the timed iterations only (warmup iterations excluded pro rata)
+        w0 = w1 - (w1 - w0) * args.steps / n_total
+        recs = [r for r in executor.records[n_rec0:]
+                if any(r.tag == b[3] for t in steps for b in t["bubbles"])]
+        launches = executor.kernel_launches + eng.launches - launches0
+        obj = [[losses_off, [float(x) for x in eng.losses]]]
+        dist.broadcast_object_list(obj, src=world - 1)  # the last stage owns the loss
+        losses_off, losses = obj[0]
+    else:
+        def engine_for(s: int) -> StageEngine:
+            if s not in engines:
+                engines[s] = StageEngine(pcfg, s, main_model, executor)
+                coordinator_for(s, pcfg)
+            return engines[s]
+
+        def run_step(k: int, fill: bool, stage: int | None = None) -> dict:
+            s = (rank + k * world) % P_STAGES if stage is None else stage
+            eng = engine_for(s)
+            if fill and items.get("stage") != s:
+                if items.get("item") is not None and items.get("stage") is not None:
+                    coords[items["stage"]].worker_job[0] = None  # abandon the partial range
+                items["stage"], items["item"] = s, None
+                executor.item = None  # force next_work() at the first bubble
+            eng.reset_stamps()
+            eng.set_anchor()
+            rec = eng.run_iteration(0, fill=fill)
+            if fill:
+                executor.settle()
+            t = eng.record_timing(rec)
+            t["stage"] = s
+            return t
+
+        # fill-off iterations: the main job's own iteration time per stage (one
+        # untimed + one timed iteration of every stage the timed fill-on steps visit)
+        for s_ in sorted({(rank + k * world) % P_STAGES for k in range(args.warmup, n_total)}):
+            for rep in range(2):
+                t = run_step(s_, fill=False, stage=s_)
+                if rep:
+                    off.setdefault(s_, []).append(t["main_end"] - t["start"])
+
+        # fill-on: warmup, then the timed steps
+        for k in range(args.warmup):
+            run_step(k, fill=True)
+        executor.timing = True
+        executor.gemm_samples = []
+        n_rec0 = len(executor.records)
+        launches0 = executor.kernel_launches + sum(e.launches for e in engines.values())
+        h2d0, d2h0 = executor.h2d_bytes, executor.d2h_bytes
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        steps = []
+        with ClockSampler(local) as clocks:
+            w0 = time.perf_counter()
+            for k in range(args.warmup, n_total):
+                steps.append(run_step(k, fill=True))
+            torch.cuda.synchronize()
+            checksum = float(executor.results().float().sum())  # host reads the results
+            w1 = time.perf_counter()
+        recs = executor.records[n_rec0:]
+        launches = executor.kernel_launches + sum(e.launches for e in engines.values()) - launches0
+        losses, losses_off = [], []
 
     # ---- accounting from device timestamps
     # sample-equivalents: a batch that passed partition [lo, hi) counts as the share of
     # the model's FLOPs in that partition (= completed samples in steady state)
-    samples = sum(r.samples_done * r.model_fraction for r in recs)
-    completed = sum(r.samples_completed for r in recs)
-    device_s = sum(t["step_end"] - t["start"] for t in steps) / 1e9
-    bubble_ns = busy_ns = 0
-    rec_iter = iter(recs)
+    by_tag = {r.tag: r for r in recs}
+    bubbles, fills = [], []
     for t in steps:
-        for kind, t_set, t_clr in t["bubbles"]:
-            bubble_ns += t_clr - t_set
-            r = next(rec_iter, None)
-            if r is not None and r.fill_end_ns > 0:
-                lo, hi = max(r.fill_start_ns, t_set), min(r.fill_end_ns, t_clr)
-                busy_ns += max(0, hi - lo)
-    idle_total_ns = sum(pf.build_bubble_cycle(pcfg, t["stage"]).total_idle_us * 1000 for t in steps)
-    on_iter = {}
+        for kind, t_set, t_clr, tag in t["bubbles"]:
+            r = by_tag.get(tag)
+            bubbles.append((t_set, t_clr))
+            fills.append((r.fill_start_ns, r.fill_end_ns) if r is not None else (0, 0))
+    on_iter: dict[int, list] = {}
     for t in steps:
         on_iter.setdefault(t["stage"], []).append(t["main_end"] - t["start"])
-    slow = [statistics.mean(on_iter[s]) / statistics.mean(off[s]) - 1 for s in on_iter if s in off]
-    slowdown = statistics.mean(slow) if slow else None
-    gemm_flops = sum(f for f, _ in executor.gemm_samples)
-    gemm_ms = sum(ms for _, ms in executor.gemm_samples)
+    slowdown = mean_slowdown(on_iter, off)
+    stats = FillStats(
+        sample_equivalents=sum(r.samples_done * r.model_fraction for r in recs),
+        samples_completed=sum(r.samples_completed for r in recs),
+        fill_busy_ns=busy_in_bubbles(bubbles, fills),
+        bubble_ns=sum(b1 - b0 for b0, b1 in bubbles),
+        idle_ns=sum(pf.build_bubble_cycle(pcfg, t["stage"]).total_idle_us * 1000 for t in steps),
+        gemm_flops=sum(f for f, _ in executor.gemm_samples),
+        gemm_ms=sum(ms for _, ms in executor.gemm_samples),
+        launches=launches, wall_s=w1 - w0,
+        device_s=sum(t["step_end"] - t["start"] for t in steps) / 1e9)
     gemm_launches = len(executor.gemm_samples)
     executor.timing = False
-
-    # ---- aggregate over ranks (max time, summed work)
-    agg = torch.tensor([samples, completed, busy_ns, bubble_ns, idle_total_ns, gemm_flops, gemm_ms,
-                        launches, w1 - w0, device_s], dtype=torch.float64, device="cuda")
-    if world > 1:
-        sums = agg.clone()
-        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
-        maxs = agg.clone()
-        dist.all_reduce(maxs, op=dist.ReduceOp.MAX)
-        agg = torch.cat([sums[:8], maxs[8:]])
-    (samples_all, completed_all, busy_all, bubble_all, idle_all, gflops_all, gms_all, launches_all,
-     wall_s, dev_s) = agg.tolist()
-    value = samples_all / dev_s if dev_s > 0 else 0.0
-    e2e = samples_all / wall_s if wall_s > 0 else 0.0
-    achieved = gflops_all / (gms_all / 1e3) / 1e12 if gms_all > 0 else 0.0
+    tot = aggregate(stats, device=torch.device("cuda", local))  # summed work, max time over ranks
+    value = tot.value
+    e2e = tot.sample_equivalents / tot.wall_s if tot.wall_s > 0 else 0.0
+    achieved = tot.gemm_tflops
     peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    dev_s = tot.device_s
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -352,12 +411,15 @@ def main() -> None:
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random-init weights, synthetic token ids / activations)",
             "config": {
-                "workload": f"8-stage 1F1B GPT-style {'8B' if args.main == 'gpt8b' else 'GPT-2-small'} "
-                            f"main job (one stage per GPU, artificial neighbours) + "
-                            f"{fcfg.name} batch-inference fill (seq {fcfg.seq})",
+                "workload": (f"{pcfg.num_stages}-stage 1F1B GPT-style main job ({gcfg.layers} layers of "
+                             f"h={gcfg.hidden} per stage; "
+                             + ("one stage per GPU over NCCL P2P" if args.pipeline == "nccl" else
+                                "8B model, artificial neighbours: one emulated stage per GPU-step")
+                             + f") + {fcfg.name} batch-inference fill (seq {fcfg.seq})"),
+                "pipeline": args.pipeline,
                 "main_stage": {"hidden": gcfg.hidden, "layers": gcfg.layers, "ffn": gcfg.ffn,
                                "seq": gcfg.seq, "micro_batch": gcfg.micro_batch,
-                               "microbatches": M_MICRO, "stages": P_STAGES,
+                               "microbatches": M_MICRO, "stages": pcfg.num_stages,
                                "t_fwd_ms": tf_ms, "t_bwd_ms": tb_ms},
                 "fill": {"model": fcfg.name, "seq_len": fcfg.seq, "profiled_batch_sizes": list(FILL_BATCH_SIZES),
                          "fill_fraction": FILL_FRACTION, "arena_bytes": arena_bytes,
@@ -365,15 +427,15 @@ def main() -> None:
                 "stages_run": [t["stage"] for t in steps],
                 "l2": "inputs larger than L2 (BERT-large weights 0.67 GB streamed per batch; main job 1B params)",
             },
-            "bubble_time_filled": busy_all / bubble_all if bubble_all else 0.0,
-            "bubble_time_filled_of_total_idle": busy_all / idle_all if idle_all else 0.0,
+            "bubble_time_filled": tot.bubble_filled,
+            "bubble_time_filled_of_total_idle": tot.idle_filled,
             "main_job_slowdown": slowdown,
             "per_stage_iter_ms": {str(st): {"fill_off": statistics.mean(off.get(st, [0])) / 1e6,
                                             "fill_on": statistics.mean(v) / 1e6} for st, v in on_iter.items()},
             "bubbles_preempted": sum(1 for r in recs if r.aborted),
             "bubbles_filled": len(recs),
-            "fill_sample_equivalents": samples_all,
-            "fill_samples_completed": int(completed_all),
+            "fill_sample_equivalents": tot.sample_equivalents,
+            "fill_samples_completed": int(tot.samples_completed),
             "value_definition": "sample-equivalents/s: completed batches x share of the model's FLOPs in "
                                 "the batch's partition, over device time of the timed iterations",
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -384,9 +446,11 @@ def main() -> None:
             "e2e": {"value": e2e, "unit": "samples/s",
                     "h2d_bytes_per_step": (executor.h2d_bytes - h2d0) // max(1, len(steps)),
                     "d2h_bytes_per_step": (executor.d2h_bytes - d2h0) // max(1, len(steps))},
-            "gpu_launches": int(launches_all),
+            "gpu_launches": int(tot.launches),
             "clocks": clocks.summary(),
             "result_checksum": checksum,
+            "main_job_losses": ({"fill_off": losses_off, "fill_on": losses,
+                                 "identical": losses_off == losses} if losses else None),
         }
         text = json.dumps(line)
         print(text, flush=True)

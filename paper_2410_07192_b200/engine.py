@@ -123,6 +123,28 @@ class GPTStage(nn.Module):
         self.opt.step()
         self.opt.zero_grad(set_to_none=False)
 
+    def snapshot(self) -> dict:
+        """Device copies of parameters and optimizer state (to replay iterations)."""
+        torch.cuda.synchronize()
+        params = [p.detach().clone() for p in self.parameters()]
+        opt = {id(p): {k: (v.clone() if torch.is_tensor(v) else v) for k, v in st.items()}
+               for p, st in self.opt.state.items()}
+        return {"params": params, "opt": opt}
+
+    def restore(self, snap: dict) -> None:
+        torch.cuda.synchronize()
+        with torch.no_grad():
+            for p, q in zip(self.parameters(), snap["params"]):
+                p.copy_(q)
+            for p, st in self.opt.state.items():
+                for k, v in snap["opt"].get(id(p), {}).items():
+                    if torch.is_tensor(v):
+                        st[k].copy_(v)
+                    else:
+                        st[k] = v
+        self.opt.zero_grad(set_to_none=False)
+        torch.cuda.synchronize()
+
 
 # --------------------------------------------------------------------------- device helpers
 
@@ -247,7 +269,7 @@ class StageEngine:
                 kind = 0 if ins.kind is BubbleKind.FWD_BWD else 1
                 rec.bubbles.append((kind, set_idx, clear_idx))
                 if fill and self.executor is not None:
-                    self.executor.fill(BubbleSlot(kind, start_ev, flag))
+                    self.executor.fill(BubbleSlot(kind, start_ev, flag, tag=(id(self), clear_idx)))
                 main.wait_event(end_ev)
                 prev_end_us = end_us
                 continue
@@ -281,8 +303,8 @@ class StageEngine:
         st = self.words.stamps
         start = int(st[rec.anchor_stamp]) + rec.anchor_off_ns
         end = int(st[rec.end_stamp])
-        bubbles = [(kind, int(st[si]), int(st[ci])) for kind, si, ci in rec.bubbles]
-        last = max([end] + [c for _, _, c in bubbles])
+        bubbles = [(kind, int(st[si]), int(st[ci]), (id(self), ci)) for kind, si, ci in rec.bubbles]
+        last = max([end] + [b[2] for b in bubbles])
         return {"start": start, "main_end": end, "step_end": last, "bubbles": bubbles}
 
     def reset_stamps(self) -> None:
@@ -313,3 +335,183 @@ def measure_stage_times(model: GPTStage, reps: int = 5, warmup: int = 2) -> tupl
     tf.sort()
     tb.sort()
     return tf[len(tf) // 2], tb[len(tb) // 2]
+
+
+# --------------------------------------------------------------------------- real pipeline
+
+
+class NcclPipelineEngine:
+    """One rank = one pipeline stage of a real p-stage pipeline (world == p).
+
+    Activations flow s -> s+1 and gradients s+1 -> s over NCCL P2P
+    (torch.distributed, NVLink/NVSwitch). Forward and backward traffic use two
+    separate process groups, so a pending send in one direction can never block
+    a recv in the other (1F1B sends and receives between the same pair in both
+    directions). Each op is posted just in time on the comm stream; the main
+    stream waits on the recv through an event.
+
+    BUBBLE: the comm stream writes flag=1, records the bubble-start event for the
+    fill stream, then waits on the recv that ends the bubble (the first backward's
+    gradient, or the next iteration's first activation) and writes flag=0 — the
+    recv completion clears the flag."""
+
+    def __init__(self, config: PipelineConfig, model: GPTStage, executor: Optional[Executor] = None,
+                 groups=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        if self.world != config.num_stages:
+            raise ValueError(f"real pipeline needs one rank per stage ({config.num_stages}), got {self.world}")
+        self.cfg = config
+        self.stage = self.rank
+        self.model = model
+        self.executor = executor
+        if groups is None:
+            groups = (dist.new_group(list(range(self.world))), dist.new_group(list(range(self.world))))
+        self.g_fwd, self.g_bwd = groups
+        lo, hi = torch.cuda.Stream.priority_range()
+        self.main = torch.cuda.Stream(priority=hi)
+        self.comm = torch.cuda.Stream(priority=hi)
+        self.words = DeviceWords()
+        c = model.c
+        self.shape = (c.micro_batch, c.seq, c.hidden)
+        g = torch.Generator(device="cuda").manual_seed(4321)
+        m = config.num_microbatches
+        self.x_first = [torch.randn(self.shape, generator=g, device="cuda").to(torch.bfloat16) * 0.5
+                        for _ in range(m)] if self.stage == 0 else None
+        self.main.wait_stream(torch.cuda.current_stream())
+        self.last_stage = self.stage == self.world - 1
+        self.prog = stage_program(config, self.stage)
+        self.records: list[IterationRecord] = []
+        self.launches = 0
+        self.losses: list[torch.Tensor] = []
+        self._inflight: list = []  # (work, tensor) kept alive until the iteration is synced
+        self._prefetched: Optional[tuple[torch.Tensor, torch.cuda.Event]] = None
+        self._anchor_stamp = -1
+
+    # ---- P2P helpers (comm stream) ------------------------------------------------
+    def _recv(self, src: int, group) -> tuple[torch.Tensor, torch.cuda.Event]:
+        buf = torch.empty(self.shape, dtype=torch.bfloat16, device="cuda")
+        with torch.cuda.stream(self.comm):
+            buf.record_stream(self.comm)
+            work = self.dist.irecv(buf, src, group=group)
+            work.wait()  # comm stream waits for the NCCL recv
+            ev = torch.cuda.Event()
+            ev.record(self.comm)
+        self._inflight.append((work, buf))
+        return buf, ev
+
+    def _send(self, t: torch.Tensor, dst: int, group) -> None:
+        ev = torch.cuda.Event()
+        ev.record(self.main)
+        with torch.cuda.stream(self.comm):
+            self.comm.wait_event(ev)
+            work = self.dist.isend(t, dst, group=group)
+        self._inflight.append((work, t))
+
+    def _bubble(self, kind: BubbleKind, end_recv: Optional[tuple[int, object]], fill: bool,
+                rec: IterationRecord) -> Optional[tuple[torch.Tensor, torch.cuda.Event]]:
+        """BUBBLE instruction: flag up, hand the bubble to the executor, end it with the recv."""
+        flag = self.words.flag.value
+        ev = torch.cuda.Event()
+        ev.record(self.main)
+        self.comm.wait_event(ev)
+        set_idx = self.words.n
+        native.call("pf_flag_write_on_stream", flag, 1, self.comm.cuda_stream)
+        native.call("pf_read_globaltimer", self.words.stamp_ptr(), self.comm.cuda_stream)
+        start_ev = torch.cuda.Event()
+        start_ev.record(self.comm)
+        got = None
+        if end_recv is not None:
+            got = self._recv(*end_recv)
+        clear_idx = self.words.n
+        native.call("pf_flag_write_on_stream", flag, 0, self.comm.cuda_stream)
+        native.call("pf_read_globaltimer", self.words.stamp_ptr(), self.comm.cuda_stream)
+        end_ev = torch.cuda.Event()
+        end_ev.record(self.comm)
+        self.launches += 2
+        k = 0 if kind is BubbleKind.FWD_BWD else 1
+        rec.bubbles.append((k, set_idx, clear_idx))
+        if fill and self.executor is not None:
+            self.executor.fill(BubbleSlot(k, start_ev, flag, tag=(id(self), clear_idx)))
+        self.main.wait_event(end_ev)
+        return got
+
+    def set_anchor(self) -> None:
+        with torch.cuda.stream(self.main):
+            self._anchor_stamp = self.words.n
+            native.call("pf_read_globaltimer", self.words.stamp_ptr(), self.main.cuda_stream)
+        self.launches += 1
+
+    def run_iteration(self, it: int, fill: bool, last: bool = False) -> IterationRecord:
+        """One training iteration of this stage; `last` = no next iteration (no
+        trailing fill-drain bubble, whose end would be the next iteration's recv)."""
+        s, p = self.stage, self.world
+        rec = IterationRecord(it, s, 0, -1, self._anchor_stamp)
+        pending_grad: dict[int, tuple[torch.Tensor, torch.cuda.Event]] = {}
+        for idx, ins in enumerate(self.prog):
+            if ins.op == "BUBBLE":
+                if ins.kind is BubbleKind.FWD_BWD:
+                    nxt = self.prog[idx + 1]  # the first backward: its gradient ends the bubble
+                    got = self._bubble(ins.kind, (s + 1, self.g_bwd) if not self.last_stage else None,
+                                       fill, rec)
+                    if got is not None:
+                        pending_grad[nxt.mb] = got
+                else:
+                    if last or s == 0:
+                        continue
+                    got = self._bubble(ins.kind, (s - 1, self.g_fwd), fill, rec)
+                    self._prefetched = got
+                continue
+            with torch.cuda.stream(self.main):
+                if ins.op == "F":
+                    if s == 0:
+                        x = self.x_first[ins.mb]
+                    else:
+                        if ins.mb == 0 and self._prefetched is not None:
+                            x, ev = self._prefetched
+                            self._prefetched = None
+                        else:
+                            x, ev = self._recv(s - 1, self.g_fwd)
+                        self.main.wait_event(ev)
+                    y = self.model.forward_mb(ins.mb, x)
+                    if not self.last_stage:
+                        self._send(y, s + 1, self.g_fwd)
+                else:
+                    g = None
+                    if not self.last_stage:
+                        g, ev = pending_grad.pop(ins.mb, None) or self._recv(s + 1, self.g_bwd)
+                        self.main.wait_event(ev)
+                    gin = self.model.backward_mb(ins.mb, g)
+                    if self.last_stage:
+                        self.losses.append(self.model.last_loss)
+                    if s > 0:
+                        self._send(gin, s - 1, self.g_bwd)
+                    if ins == [i for i in self.prog if i.op != "BUBBLE"][-1]:
+                        self.model.step()
+                        rec.end_stamp = self.words.n
+                        native.call("pf_read_globaltimer", self.words.stamp_ptr(), self.main.cuda_stream)
+                        self.launches += 1
+        self.records.append(rec)
+        return rec
+
+    def sync(self) -> None:
+        torch.cuda.synchronize()
+        self._inflight = []
+
+    def record_timing(self, rec: IterationRecord) -> dict:
+        self.sync()
+        st = self.words.stamps
+        start = int(st[rec.anchor_stamp])
+        end = int(st[rec.end_stamp])
+        bubbles = [(kind, int(st[si]), int(st[ci]), (id(self), ci)) for kind, si, ci in rec.bubbles]
+        last = max([end] + [b[2] for b in bubbles])
+        return {"start": start, "main_end": end, "step_end": last, "bubbles": bubbles,
+                "stage": self.stage}
+
+    def reset_stamps(self) -> None:
+        self.sync()
+        self.words.n = 0
+        self.records = []

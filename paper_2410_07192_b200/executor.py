@@ -50,6 +50,7 @@ class BubbleSlot:
     index: int  # bubble position j in the stage's cycle (0 = fwd-bwd, 1 = fill-drain)
     start_event: Optional[torch.cuda.Event]  # fill stream waits for it (flag already set)
     flag_ptr: int  # device address of the stage's bubble flag (0 = not preemptible)
+    tag: object = None  # engine's id for this bubble, copied into the BubbleRecord
 
 
 @dataclass
@@ -65,6 +66,7 @@ class BubbleRecord:
     part: int = 0
     model_fraction: float = 1.0  # share of the model's FLOPs in this bubble's partition
     samples_completed: int = 0  # samples that left the LAST partition in this bubble
+    tag: object = None
 
 
 @dataclass
@@ -397,7 +399,7 @@ class Executor:
         ts = w[8:12].view(torch.int64)
         pr = self.progress
         rec = BubbleRecord(pend.slot.index, len(pend.batches), done, 0, aborted, int(ts[0]), int(ts[1]),
-                           pend.launches, pend.part, self._flops_frac[pend.part])
+                           pend.launches, pend.part, self._flops_frac[pend.part], tag=pend.slot.tag)
         if self.timing and done > 0 and not aborted:
             last_cnt = pend.batches[min(done, len(pend.batches)) - 1][1]
             ch = self._chains.get((pend.part, last_cnt))

@@ -1,0 +1,90 @@
+"""Real 2-stage pipeline over NCCL (needs 2 GPUs: `gpurun --gpus 2`): the recv completion
+ends each bubble, the fill executor runs inside, and the main job's losses are
+bit-identical with filling on and off (the fill job only touches its own arena)."""
+
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+WORKER = r'''
+import os, sys, json, torch, torch.distributed as dist
+sys.path.insert(0, os.environ["ROOT"])
+rank = int(os.environ["RANK"]); world = int(os.environ["WORLD_SIZE"])
+torch.cuda.set_device(rank)
+dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
+torch.backends.cuda.enable_flash_sdp(False); torch.backends.cuda.enable_mem_efficient_sdp(False)
+torch.backends.cuda.enable_math_sdp(True)
+torch.backends.cudnn.deterministic = True
+import paper_2410_07192_b200 as pf
+from paper_2410_07192_b200.engine import GPTStage, GPTStageConfig, NcclPipelineEngine, measure_stage_times
+from paper_2410_07192_b200.executor import Executor
+from paper_2410_07192_b200.fillmodels import BertConfig, bert
+cfg = GPTStageConfig(hidden=512, heads=8, ffn=2048, layers=2, seq=256, micro_batch=2)
+model = GPTStage(cfg, seed=rank)
+tf, tb = measure_stage_times(model, reps=3, warmup=1)
+tt = torch.tensor([tf, tb], device="cuda"); dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+pcfg = pf.PipelineConfig(world, 4, tt[0].item(), tt[1].item(), pf.ScheduleKind.ONE_F_ONE_B, 1 << 30, 1 << 30, 0.68)
+fill = bert(BertConfig("t", vocab=1000, hidden=256, heads=4, ffn=1024, layers=2), seed=1)
+layers = tuple(pf.LayerProfile({8: 0.02, 16: 0.04}, {8: m.weight_bytes() + (8 << 20), 16: m.weight_bytes() + (16 << 20)},
+                               m.weight_bytes(), 1.0) for m in fill)
+prof = pf.ModelProfile("t", layers, 1, frozenset({pf.JobKind.BATCH_INFERENCE}))
+coord = pf.Coordinator(rank, pf.build_bubble_cycle(pcfg, rank), 1, pf.OrderingPolicy("concurrent", 256))
+coord.admit(pf.JobSpec("j", 0.0, prof, pf.JobKind.BATCH_INFERENCE, 100000))
+ex = Executor(256 << 20)
+ex.work_source = lambda: (coord.request_work(0, 0.0), fill)
+eng = NcclPipelineEngine(pcfg, model, ex)
+snap = model.snapshot()
+out = {}
+for fill_on in (False, True):
+    model.restore(snap); eng.losses = []
+    for it in range(4):
+        eng.run_iteration(it, fill=fill_on, last=(it == 3))
+    ex.settle(); eng.sync()
+    out["on" if fill_on else "off"] = [float(x) for x in eng.losses]
+out["filled_bubbles"] = sum(1 for r in ex.records if r.batches_done > 0)
+out["records"] = len(ex.records)
+ex.close()
+print("RESULT", rank, json.dumps(out), flush=True)
+dist.destroy_process_group()
+'''
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_two_stage_nccl_pipeline_fill_keeps_losses_identical(tmp_path):
+    script = tmp_path / "worker.py"
+    script.write_text(WORKER)
+    port = _port()
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", LOCAL_RANK=str(r), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port), ROOT=ROOT, CUBLAS_WORKSPACE_CONFIG=":4096:8")
+        procs.append(subprocess.Popen([sys.executable, str(script)], env=env, stdout=subprocess.PIPE,
+                                      stderr=subprocess.STDOUT, text=True))
+    outs = [p.communicate(timeout=600)[0] for p in procs]
+    for p, o in zip(procs, outs):
+        assert p.returncode == 0, o[-4000:]
+    import json
+
+    res = {}
+    for o in outs:
+        for line in o.splitlines():
+            if line.startswith("RESULT"):
+                _, r, js = line.split(" ", 2)
+                res[int(r)] = json.loads(js)
+    last = res[1]
+    assert len(last["off"]) == 4 * 4 and last["off"] == last["on"], last
+    assert res[0]["filled_bubbles"] > 0 and res[1]["records"] > 0
