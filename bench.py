@@ -176,6 +176,7 @@ def main() -> None:
                     help="emulated: every rank runs stages of an 8-stage pipeline against artificial "
                          "neighbours; nccl: the N ranks ARE an N-stage pipeline (NCCL P2P over NVLink)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
+    ap.add_argument("--save-profile", default=None, help="write the measured fill ModelProfile JSON here")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -210,6 +211,9 @@ def main() -> None:
     fcfg = BERT_LARGE if args.fill == "bert_large" else BERT_BASE
     fill_model = bert(fcfg, seed=0)
     profile = measure_profile(fill_model, FILL_BATCH_SIZES)
+    if args.save_profile and rank == 0:
+        with open(args.save_profile, "w") as fh:
+            fh.write(pf.model_to_json(profile) + "\n")
 
     # ---- bubble characterization: free memory with the main job at its peak
     probe_cfg = pf.PipelineConfig(P_STAGES, M_MICRO, tf_ms, tb_ms, pf.ScheduleKind.ONE_F_ONE_B,
@@ -230,10 +234,10 @@ def main() -> None:
     engines: dict[int, object] = {}
     items: dict[int, object] = {}
 
-    def coordinator_for(s: int, cfg) -> pf.Coordinator:
+    def coordinator_for(s: int, cfg, cycle=None) -> pf.Coordinator:
         if s not in coords:
             # the stage's Coordinator; a long-running fill job split into 16K-sample ranges
-            coords[s] = pf.Coordinator(s, pf.build_bubble_cycle(cfg, s), 1,
+            coords[s] = pf.Coordinator(s, cycle or pf.build_bubble_cycle(cfg, s), 1,
                                        pf.OrderingPolicy("concurrent", 16384))
             coords[s].admit(pf.JobSpec(f"fill-{s}", 0.0, profile, pf.JobKind.BATCH_INFERENCE, 10_000_000))
         return coords[s]
@@ -260,7 +264,6 @@ def main() -> None:
                                  arena_bytes, arena_bytes, FILL_FRACTION)
         eng = NcclPipelineEngine(pcfg, main_model, executor)
         engines[rank] = eng
-        coordinator_for(rank, pcfg)
         items["stage"], items["item"] = rank, None
 
         def run_phase(fill: bool) -> list[dict]:
@@ -283,8 +286,25 @@ def main() -> None:
             return out
 
         snap = main_model.snapshot()  # both phases train from the same weights and data
-        for t in run_phase(False):
+        off_steps = run_phase(False)
+        for t in off_steps:
             off.setdefault(rank, []).append(t["main_end"] - t["start"])
+        # bubble characterization from the fill-off iterations: measured duration of every
+        # BUBBLE (flag set -> recv done) and the measured iteration period
+        meas = {0: [], 1: []}
+        for t in off_steps:
+            for kind, t_set, t_clr, _ in t["bubbles"]:
+                meas[kind].append((t_clr - t_set) // 1000)
+        period_us = int(statistics.median(off[rank]) // 1000)
+        durs = [int(statistics.median(meas[k])) if meas[k] else 0 for k in (0, 1)]
+        analytic = pf.build_bubble_cycle(pcfg, rank)
+        measured_cycle = pf.cycle_from_measurements(
+            rank, max(period_us, sum(durs)), durs, [arena_bytes, arena_bytes], FILL_FRACTION,
+            unfillable_us=max(0, min(analytic.unfillable_us, period_us - sum(durs))))
+        coordinator_for(rank, pcfg, measured_cycle)
+        characterization = {"measured_bubbles_us": durs, "measured_period_us": period_us,
+                            "analytic_bubbles_us": [b.duration_us for b in analytic.bubbles],
+                            "analytic_period_us": analytic.period_us}
         losses_off = [float(x) for x in eng.losses]
         eng.losses = []
         main_model.restore(snap)
@@ -363,6 +383,7 @@ def main() -> None:
         recs = executor.records[n_rec0:]
         launches = executor.kernel_launches + sum(e.launches for e in engines.values()) - launches0
         losses, losses_off = [], []
+        characterization = {"bubbles": "analytic timeline with measured t_fwd/t_bwd (artificial neighbours)"}
 
     # ---- accounting from device timestamps
     # sample-equivalents: a batch that passed partition [lo, hi) counts as the share of
@@ -432,6 +453,7 @@ def main() -> None:
             "main_job_slowdown": slowdown,
             "per_stage_iter_ms": {str(st): {"fill_off": statistics.mean(off.get(st, [0])) / 1e6,
                                             "fill_on": statistics.mean(v) / 1e6} for st, v in on_iter.items()},
+            "bubble_characterization": characterization,
             "bubbles_preempted": sum(1 for r in recs if r.aborted),
             "bubbles_filled": len(recs),
             "fill_sample_equivalents": tot.sample_equivalents,

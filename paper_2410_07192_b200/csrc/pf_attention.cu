@@ -6,8 +6,8 @@
 //       thread-per-query-row softmax straight out of TMEM (tcgen05.ld), P packed to
 //       bf16 into shared memory in the UMMA K-major 128-B-swizzled layout, reusing
 //       the dead Q/K tiles
-//   O = P V          tcgen05.mma 128x64x128 with V as an MN-major operand, TMEM cols
-//       [128,192), normalised by the fp32 row sum in the epilogue
+//   O = P V          tcgen05.mma 128x64x128 with V as an MN-major operand, into TMEM cols
+//       [0,64) over the consumed S, normalised by the fp32 row sum in the epilogue
 // Q, K, V tiles arrive by one 3-D TMA each from the packed QKV projection output
 // [batch*seq, 3, heads, 64]; no transpose or split kernel runs before attention.
 // Preemption: atomic work unit = one (batch, head); flag checked on entry.
@@ -20,10 +20,11 @@ constexpr int S_MAX = 128;
 constexpr int D = 64;
 constexpr int THREADS = 128;
 constexpr int TILE_BYTES = S_MAX * D * 2;  // 16 KB per operand tile
-// Q | K | V tiles (P overwrites Q|K), barriers; padded so at most 2 CTAs share an SM
-// (each allocates 256 of the SM's 512 TMEM columns).
+// Q | K | V tiles (P overwrites Q|K) and barriers: ~49 KB, so 4 CTAs share an SM; each
+// allocates 128 of the SM's 512 TMEM columns (O = PV reuses the consumed S columns).
 constexpr int SMEM_BYTES = 1024 + 3 * TILE_BYTES + 64;
-constexpr int SMEM_REQUEST = 100 * 1024;
+constexpr int SMEM_REQUEST = SMEM_BYTES;
+constexpr int TMEM_COLS = 128;
 
 __global__ void __launch_bounds__(THREADS) attention_kernel(const __grid_constant__ CUtensorMap tm,
                                                             const float* __restrict__ mask_add,
@@ -64,7 +65,7 @@ __global__ void __launch_bounds__(THREADS) attention_kernel(const __grid_constan
   }
   __syncthreads();
   if (!s_go) return;
-  if (warp == 0) tmem_alloc(tmem_slot, 256);
+  if (warp == 0) tmem_alloc(tmem_slot, TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(THREADS) attention_kernel(const __grid_constan
     for (int k = 0; k < S_MAX / 16; ++k) {
       const uint64_t ad = umma_desc_sw128_kmajor(pa + (k >> 2) * TILE_BYTES + (k & 3) * 32);
       const uint64_t bd = umma_desc_sw128_mnmajor(va + k * 2048, TILE_BYTES);
-      umma_bf16_ss(tmem + 128, ad, bd, idesc_o, k > 0 ? 1u : 0u);
+      umma_bf16_ss(tmem, ad, bd, idesc_o, k > 0 ? 1u : 0u);  // over the consumed S
     }
     umma_commit(mma_bar);
   }
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(THREADS) attention_kernel(const __grid_constan
 #pragma unroll 1
   for (int c = 0; c < 2; ++c) {
     uint32_t r[32];
-    tmem_ld_32x32b_x32(tmem + lane_base + 128 + c * 32, r);
+    tmem_ld_32x32b_x32(tmem + lane_base + c * 32, r);
     tmem_ld_wait();
     if (row_ok) {
 #pragma unroll
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(THREADS) attention_kernel(const __grid_constan
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, 256);
+  if (warp == 0) tmem_dealloc(tmem, TMEM_COLS);
   if (tid == 0 && ctl.cursor != nullptr) {
     __threadfence();
     atomicAdd(ctl.cursor, 1u);
