@@ -18,6 +18,7 @@
 // bubble flag is set (pf::claim_unit), so the kernel yields within one tile
 // of the flag clearing and the claimed-tile prefix is the resume cursor.
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "pf_ops.h"
 
@@ -45,7 +46,10 @@ struct Cfg {
   // barriers + sched ring + tmem addr live after the operand ring
   static constexpr int BAR_BYTES = (2 * STAGES + 4 + 2 * SCHED_SLOTS) * 8 + SCHED_SLOTS * 4 + 16 +
                                    NUM_EPI_WARPS * COLS_PER_EPI_WARP * 2;
-  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + BAR_BYTES;
+  // per-epilogue-warp 32x32 bf16 staging tile for the TMA store (1024-B aligned)
+  static constexpr int STG_OFFSET = (STAGES * STAGE_BYTES + BAR_BYTES + 1023) / 1024 * 1024;
+  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STG_OFFSET + NUM_EPI_WARPS * 2048;
+  static_assert(SMEM_BYTES <= 227 * 1024, "smem");
   static_assert(BN % 64 == 0 && BN <= 256, "BN");
   static_assert(COLS_PER_EPI_WARP % 32 == 0, "epilogue chunking");
 };
@@ -64,6 +68,17 @@ struct Params {
 // exceeded L2 (FFN2 at batch 128: A = 134 MB, read 8x).
 constexpr int GROUP_M = 16;
 
+#ifdef PF_GEMM_DIAG
+// [0] MMA wait on full (data), [1] MMA wait on tempty (epilogue), [2] producer wait on empty,
+// [3] epilogue wait on tfull, [4] MMA issue cycles, [5] epilogue busy cycles
+__device__ unsigned long long g_gemm_diag[8];
+#define DIAG_T0() long long _t0 = clock64()
+#define DIAG_ADD(i) atomicAdd(&g_gemm_diag[i], (unsigned long long)(clock64() - _t0))
+#else
+#define DIAG_T0()
+#define DIAG_ADD(i)
+#endif
+
 __device__ __forceinline__ void tile_coords(int tile, const Params& p, int& tm, int& tn) {
   const int per_group = GROUP_M * p.tiles_n;
   const int g = tile / per_group;
@@ -74,10 +89,138 @@ __device__ __forceinline__ void tile_coords(int tile, const Params& p, int& tm, 
   tn = r / rows;
 }
 
+// One epilogue warp's share of an output tile: 32 rows (its TMEM lane group) x
+// CHUNKS*32 columns. Bias is staged in shared memory before the accumulator is ready;
+// TMEM loads are double-buffered; each 32x32 result chunk goes registers -> bias /
+// erf-GELU / residual -> bf16 -> a 64-B-swizzled smem tile -> one TMA bulk store
+// (full-line writes, clipped at the tensor edges) issued by lane 0.
+template <int CHUNKS, uint32_t EPI, bool PAIR>
+__device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap* tmY,
+                                              uint8_t* stg, uint32_t taddr0, uint64_t* tfull,
+                                              uint32_t aphase, int row_base, int col_base,
+                                              __nv_bfloat16* my_bias) {
+  constexpr bool HAS_BIAS = (EPI & PF_EPI_BIAS) != 0;
+  constexpr bool HAS_GELU = (EPI & PF_EPI_GELU) != 0;
+  constexpr bool HAS_RES = (EPI & PF_EPI_RESIDUAL) != 0;
+  constexpr int COLS = CHUNKS * 32;
+  const int lane = lane_id();
+  const int row = row_base + lane;
+  const bool row_ok = row < p.M;
+  if (HAS_BIAS) {
+    for (int j = lane * 8; j < COLS; j += 32 * 8) {
+      uint4 b4 = make_uint4(0, 0, 0, 0);
+      if (col_base + j + 8 <= p.N) {
+        b4 = __ldg(reinterpret_cast<const uint4*>(p.bias + col_base + j));
+      } else {
+        __nv_bfloat16 tmp[8];
+        for (int q = 0; q < 8; ++q)
+          tmp[q] = col_base + j + q < p.N ? p.bias[col_base + j + q] : __float2bfloat16(0.f);
+        b4 = *reinterpret_cast<uint4*>(tmp);
+      }
+      *reinterpret_cast<uint4*>(my_bias + j) = b4;
+    }
+    __syncwarp();
+  }
+  const __nv_bfloat16* rrow = HAS_RES ? p.residual + (size_t)row * p.N : nullptr;
+  {
+    DIAG_T0();
+    if (PAIR) mbar_wait_cluster(tfull, aphase);
+    else mbar_wait(tfull, aphase);
+    if (lane == 0) DIAG_ADD(3);
+  }
+  tc_fence_after();
+  uint32_t rbuf[2][32];
+  __syncwarp();
+  tmem_ld_32x32b_x32(taddr0, rbuf[0]);
+#pragma unroll
+  for (int c = 0; c < CHUNKS; ++c) {
+    const int col0 = col_base + c * 32;
+    uint4 res_cur[4];
+    if (HAS_RES) {
+      // the residual slice of this chunk is fetched while the TMEM load completes
+      if (row_ok && col0 + 32 <= p.N) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) res_cur[q] = reinterpret_cast<const uint4*>(rrow + col0)[q];
+      } else {
+        __nv_bfloat16 tmp[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          tmp[j] = (row_ok && col0 + j < p.N) ? rrow[col0 + j] : __float2bfloat16(0.f);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) res_cur[q] = reinterpret_cast<const uint4*>(tmp)[q];
+      }
+    }
+    __syncwarp();
+    tmem_ld_wait();  // chunk c landed
+    if (c + 1 < CHUNKS) tmem_ld_32x32b_x32(taddr0 + (uint32_t)((c + 1) * 32), rbuf[(c + 1) & 1]);
+    const uint32_t(&r)[32] = rbuf[c & 1];
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+    if (HAS_BIAS) {
+      const uint4* bp = reinterpret_cast<const uint4*>(my_bias + c * 32);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 b4 = bp[q];
+        const uint32_t bw[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          float2 f = unpack_bf16x2(bw[h]);
+          v[q * 8 + h * 2] += f.x;
+          v[q * 8 + h * 2 + 1] += f.y;
+        }
+      }
+    }
+    if (HAS_GELU) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
+    }
+    if (HAS_RES) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t rw[4] = {res_cur[q].x, res_cur[q].y, res_cur[q].z, res_cur[q].w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          float2 f = unpack_bf16x2(rw[h]);
+          v[q * 8 + h * 2] += f.x;
+          v[q * 8 + h * 2 + 1] += f.y;
+        }
+      }
+    }
+    // previous chunk's bulk store must have read the staging tile
+    if (c > 0) {
+      if (lane == 0) bulk_wait_read0();
+      __syncwarp();
+    }
+    // row `lane` of the 32x32 tile = 4 x 16 B; TMA SWIZZLE_64B places 16-B chunk q of
+    // row r at chunk q ^ ((r >> 1) & 3) (conflict-free: 8 distinct bank groups per phase)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 o;
+      o.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
+      o.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
+      o.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
+      o.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
+      const int phys = q ^ ((lane >> 1) & 3);
+#ifndef PF_DIAG_NO_STORE
+      *reinterpret_cast<uint4*>(stg + lane * 64 + phys * 16) = o;
+#else
+      if (o.x == 0x12345678u) *reinterpret_cast<uint4*>(stg + lane * 64 + phys * 16) = o;
+#endif
+    }
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0 && col0 < p.N) {
+      tma_store_2d(tmY, stg, col0, row_base);
+      bulk_commit();
+    }
+  }
+}
+
 template <int BN, uint32_t EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                Params p, Ctl ctl) {
+                const __grid_constant__ CUtensorMap tmY, Params p, Ctl ctl) {
   using C = Cfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment for the swizzled operand tiles
@@ -104,6 +247,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmY);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
@@ -150,7 +294,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int tm, tn;
       tile_coords(tile, p, tm, tn);
       for (int kb = 0; kb < num_kb; ++kb) {
-        mbar_wait(&empty_bar[stage], phase ^ 1u);
+        {
+          DIAG_T0();
+          mbar_wait(&empty_bar[stage], phase ^ 1u);
+          if (lane == 0) DIAG_ADD(2);
+        }
         if (lane == 0) {
           mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
           tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full_bar[stage], kb * BK, tm * BM);
@@ -182,11 +330,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         sphase ^= 1u;
       }
       if (tile < 0) break;
-      mbar_wait(&tempty_bar[acc], aphase ^ 1u);
+      {
+        DIAG_T0();
+        mbar_wait(&tempty_bar[acc], aphase ^ 1u);
+        if (lane == 0) DIAG_ADD(1);
+      }
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
       for (int kb = 0; kb < num_kb; ++kb) {
-        mbar_wait(&full_bar[stage], phase);
+        {
+          DIAG_T0();
+          mbar_wait(&full_bar[stage], phase);
+          if (lane == 0) DIAG_ADD(0);
+        }
         tc_fence_after();
         if (lane == 0) {
           const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
@@ -215,13 +371,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= EPI_WARP0) {
     // ---------------- epilogue ----------------
-    constexpr bool HAS_BIAS = (EPI & PF_EPI_BIAS) != 0;
-    constexpr bool HAS_GELU = (EPI & PF_EPI_GELU) != 0;
-    constexpr bool HAS_RES = (EPI & PF_EPI_RESIDUAL) != 0;
     const int e = warp - EPI_WARP0;
     const int lane_grp = warp & 3;  // TMEM lanes [32*lane_grp, +32) are visible to this warp
     const int col_half = e >> 2;
     __nv_bfloat16* my_bias = bias_smem + e * C::COLS_PER_EPI_WARP;
+    uint8_t* my_stg = smem + C::STG_OFFSET + e * 2048;
     int slot = 0;
     uint32_t sphase = 0;
     int acc = 0;
@@ -238,111 +392,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (tile < 0) break;
       int tm, tn;
       tile_coords(tile, p, tm, tn);
-      const int row = tm * BM + lane_grp * 32 + lane;
-      const bool row_ok = row < p.M;
+      const int row_base = tm * BM + lane_grp * 32;
       const int col_base = tn * BN + col_half * C::COLS_PER_EPI_WARP;
-      // Stage this warp's bias slice in shared memory while the MMAs run.
-      if (HAS_BIAS) {
-        for (int j = lane * 8; j < C::COLS_PER_EPI_WARP; j += 32 * 8) {
-          uint4 b4 = make_uint4(0, 0, 0, 0);
-          if (col_base + j + 8 <= p.N) {
-            b4 = __ldg(reinterpret_cast<const uint4*>(p.bias + col_base + j));
-          } else {
-            __nv_bfloat16 tmp[8];
-            for (int q = 0; q < 8; ++q)
-              tmp[q] = col_base + j + q < p.N ? p.bias[col_base + j + q] : __float2bfloat16(0.f);
-            b4 = *reinterpret_cast<uint4*>(tmp);
-          }
-          *reinterpret_cast<uint4*>(my_bias + j) = b4;
-        }
-        __syncwarp();
-      }
-      const __nv_bfloat16* rrow = HAS_RES ? p.residual + (size_t)row * p.N : nullptr;
-      uint4 res_cur[4], res_nxt[4];
-      if (HAS_RES && row_ok && col_base + 32 <= p.N) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) res_cur[q] = reinterpret_cast<const uint4*>(rrow + col_base)[q];
-      }
-      mbar_wait(&tfull_bar[acc], aphase);
-      tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < C::CHUNKS; ++c) {
-        const int col_in_tile = col_half * C::COLS_PER_EPI_WARP + c * 32;
-        const uint32_t taddr =
-            tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(acc * BN + col_in_tile);
-        uint32_t r[32];
-        __syncwarp();
-        tmem_ld_32x32b_x32(taddr, r);
-        const int col0 = col_base + c * 32;
-        if (HAS_RES && c + 1 < C::CHUNKS && row_ok && col0 + 64 <= p.N) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) res_nxt[q] = reinterpret_cast<const uint4*>(rrow + col0 + 32)[q];
-        }
-        tmem_ld_wait();
-        if (row_ok && col0 < p.N) {
-          float v[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-          const bool full = col0 + 32 <= p.N;
-          if (HAS_BIAS) {
-            const uint4* bp = reinterpret_cast<const uint4*>(my_bias + c * 32);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint4 b4 = bp[q];
-              const uint32_t bw[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-              for (int h = 0; h < 4; ++h) {
-                float2 f = unpack_bf16x2(bw[h]);
-                v[q * 8 + h * 2] += f.x;
-                v[q * 8 + h * 2 + 1] += f.y;
-              }
-            }
-          }
-          if (HAS_GELU) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
-          }
-          __nv_bfloat16* yrow = p.Y + (size_t)row * p.N;
-          if (HAS_RES) {
-            if (full) {
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const uint32_t rw[4] = {res_cur[q].x, res_cur[q].y, res_cur[q].z, res_cur[q].w};
-#pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                  float2 f = unpack_bf16x2(rw[h]);
-                  v[q * 8 + h * 2] += f.x;
-                  v[q * 8 + h * 2 + 1] += f.y;
-                }
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (col0 + j < p.N) v[j] += __bfloat162float(rrow[col0 + j]);
-            }
-          }
-          if (full) {
-            uint4* yp = reinterpret_cast<uint4*>(yrow + col0);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint4 o;
-              o.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
-              o.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
-              o.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
-              o.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
-              yp[q] = o;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (col0 + j < p.N) yrow[col0 + j] = __float2bfloat16_rn(v[j]);
-          }
-        }
-        if (HAS_RES) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) res_cur[q] = res_nxt[q];
-        }
-      }
+      const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) +
+                             (uint32_t)(acc * BN + col_half * C::COLS_PER_EPI_WARP);
+      epilogue_tile<C::CHUNKS, EPI, false>(p, &tmY, my_stg, taddr, &tfull_bar[acc], aphase, row_base,
+                                           col_base, my_bias);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
@@ -351,12 +406,263 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         aphase ^= 1u;
       }
     }
+    if (lane == 0) bulk_wait0();  // outstanding TMA stores of this warp are complete
   }
 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc(tmem_base, C::TMEM_COLS);
+}
+
+
+// ===========================================================================
+// CTA-pair variant (cluster of 2, tcgen05 cta_group::2)
+//
+// A pair computes a 256 x BN output tile: each CTA TMA-loads its own 128 rows of A
+// and HALF of the BN rows of W into its shared memory, and the leader CTA issues
+// tcgen05.mma.cta_group::2 (M=256) that reads both CTAs' operands. Each SM thus
+// streams 128x64 + (BN/2)x64 operand elements per 128xBNx64 of MMA work instead of
+// 128x64 + BNx64: a third less shared-memory / L2 traffic per FLOP, and 6 pipeline
+// stages fit instead of 4. Each CTA's TMEM holds its 128 accumulator rows; both
+// CTAs run the same epilogue on their half. The leader claims tiles (and makes the
+// preemption decision) and forwards each tile index to the peer through DSMEM.
+template <int BN>
+struct Cfg2 {
+  static constexpr int A_BYTES = BM * BK * 2;         // this CTA's 128 rows
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;   // this CTA's half of W's BN rows
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (SMEM_BUDGET / STAGE_BYTES) > 6 ? 6 : (SMEM_BUDGET / STAGE_BYTES);
+  static constexpr int TMEM_COLS = (2 * BN <= 256) ? 256 : 512;
+  static constexpr int COLS_PER_EPI_WARP = BN / 2;
+  static constexpr int CHUNKS = COLS_PER_EPI_WARP / 32;
+  static constexpr int BAR_BYTES = (2 * STAGES + 4 + 2 * SCHED_SLOTS) * 8 + SCHED_SLOTS * 4 + 16 +
+                                   NUM_EPI_WARPS * COLS_PER_EPI_WARP * 2;
+  static constexpr int STG_OFFSET = (STAGES * STAGE_BYTES + BAR_BYTES + 1023) / 1024 * 1024;
+  static constexpr int SMEM_BYTES = 1024 + STG_OFFSET + NUM_EPI_WARPS * 2048;
+  static_assert(SMEM_BYTES <= 227 * 1024, "smem");
+  static_assert(BN % 128 == 0 && BN <= 256, "pair BN");
+};
+
+__device__ __forceinline__ int claim_pair(const Ctl& c, int units, int iter) {
+  if (chain_aborted(c)) return -1;
+  if (c.flag != nullptr) {
+    if (ld_acquire_u32(c.flag) == 0u) {
+      atomicExch(c.abort, 1u);
+      return -1;
+    }
+  }
+  uint32_t u;
+  if (c.cursor != nullptr) {
+    u = atomicAdd(c.cursor, 1u);
+  } else {
+    u = (blockIdx.x >> 1) + (uint32_t)iter * (gridDim.x >> 1);
+  }
+  return u < (uint32_t)units ? (int)u : -1;
+}
+
+template <int BN, uint32_t EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const __grid_constant__ CUtensorMap tmY, Params p, Ctl ctl) {
+  using C = Cfg2<BN>;
+  constexpr int PM = 2 * BM;  // pair tile rows
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* full_bar = bars;
+  uint64_t* empty_bar = bars + C::STAGES;
+  uint64_t* tfull_bar = bars + 2 * C::STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint64_t* sfull_bar = tempty_bar + 2;
+  uint64_t* sempty_bar = sfull_bar + SCHED_SLOTS;
+  int* sched_tile = reinterpret_cast<int*>(sempty_bar + SCHED_SLOTS);
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(sched_tile + SCHED_SLOTS);
+  __nv_bfloat16* bias_smem = reinterpret_cast<__nv_bfloat16*>(tmem_base_smem + 4);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmY);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);   // leader: its arrive.expect_tx (both CTAs' bytes)
+      mbar_init(&empty_bar[s], 1);  // the leader's multicast MMA commit
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);                   // multicast commit
+      mbar_init(&tempty_bar[a], 2 * NUM_EPI_WARPS);  // leader: both CTAs' epilogue warps
+    }
+    for (int s = 0; s < SCHED_SLOTS; ++s) {
+      mbar_init(&sfull_bar[s], 1);
+      // leader: its MMA + epilogue warps (local) and the peer's producer + epilogue (remote)
+      mbar_init(&sempty_bar[s], 2 + 2 * NUM_EPI_WARPS);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair(tmem_base_smem, C::TMEM_COLS);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_smem;
+
+  const int num_tiles = p.tiles_m * p.tiles_n;
+  const int num_kb = (p.K + BK - 1) / BK;
+
+  if (warp == 0) {
+    // ---------------- scheduler (leader) / tile follower (peer) + TMA producer ----------------
+    int slot = 0;
+    uint32_t sphase = 0;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int it = 0;; ++it) {
+      int tile;
+      if (leader) {
+        tile = 0;
+        if (lane == 0) tile = claim_pair(ctl, num_tiles, it);
+        tile = __shfl_sync(0xffffffffu, tile, 0);
+        mbar_wait_cluster(&sempty_bar[slot], sphase ^ 1u);
+        if (lane == 0) {
+          sched_tile[slot] = tile;
+          st_shared_cluster_u32(mapa_shared(smem_u32(&sched_tile[slot]), 1), (uint32_t)tile);
+          mbar_arrive(&sfull_bar[slot]);
+          mbar_arrive_cluster(mapa_shared(smem_u32(&sfull_bar[slot]), 1));
+        }
+      } else {
+        mbar_wait_cluster(&sfull_bar[slot], sphase);
+        tile = sched_tile[slot];
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&sempty_bar[slot]), 0));
+      }
+      if (++slot == SCHED_SLOTS) {
+        slot = 0;
+        sphase ^= 1u;
+      }
+      if (tile < 0) break;
+      int tm, tn;
+      tile_coords(tile, p, tm, tn);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&empty_bar[stage], phase ^ 1u);
+        if (lane == 0) {
+          const uint32_t fb = mapa_shared(smem_u32(&full_bar[stage]), 0);
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * C::STAGE_BYTES);
+          tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, fb, kb * BK, tm * PM + (int)rank * BM);
+          tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, fb, kb * BK, tn * BN + (int)rank * (BN / 2));
+        }
+        __syncwarp();
+        if (++stage == C::STAGES) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      // ---------------- MMA issuer (leader only; M = 256 over both CTAs) ----------------
+      constexpr uint32_t idesc = umma_idesc_bf16(PM, BN, false, false);
+      int slot = 0;
+      uint32_t sphase = 0;
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      while (true) {
+        mbar_wait(&sfull_bar[slot], sphase);
+        const int tile = sched_tile[slot];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty_bar[slot]);
+        if (++slot == SCHED_SLOTS) {
+          slot = 0;
+          sphase ^= 1u;
+        }
+        if (tile < 0) break;
+        mbar_wait_cluster(&tempty_bar[acc], aphase ^ 1u);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
+            const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+            for (int k = 0; k < BK / UMMA_K; ++k) {
+              const uint64_t ad = umma_desc_sw128_kmajor(a_addr + k * UMMA_K * 2);
+              const uint64_t bd = umma_desc_sw128_kmajor(b_addr + k * UMMA_K * 2);
+              umma_bf16_ss_pair(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            }
+            umma_commit_pair(&empty_bar[stage]);  // frees this stage in BOTH CTAs
+          }
+          __syncwarp();
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        if (lane == 0) umma_commit_pair(&tfull_bar[acc]);  // accumulators ready in both CTAs
+        __syncwarp();
+        if (++acc == 2) {
+          acc = 0;
+          aphase ^= 1u;
+        }
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ---------------- epilogue (both CTAs, each on its 128 rows) ----------------
+    const int e = warp - EPI_WARP0;
+    const int lane_grp = warp & 3;
+    const int col_half = e >> 2;
+    __nv_bfloat16* my_bias = bias_smem + e * C::COLS_PER_EPI_WARP;
+    uint8_t* my_stg = smem + C::STG_OFFSET + e * 2048;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
+    int slot = 0;
+    uint32_t sphase = 0;
+    int acc = 0;
+    uint32_t aphase = 0;
+    while (true) {
+      if (leader) mbar_wait(&sfull_bar[slot], sphase);
+      else mbar_wait_cluster(&sfull_bar[slot], sphase);
+      const int tile = sched_tile[slot];
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(&sempty_bar[slot]);
+        else mbar_arrive_cluster(mapa_shared(smem_u32(&sempty_bar[slot]), 0));
+      }
+      if (++slot == SCHED_SLOTS) {
+        slot = 0;
+        sphase ^= 1u;
+      }
+      if (tile < 0) break;
+      int tm, tn;
+      tile_coords(tile, p, tm, tn);
+      const int row_base = tm * PM + (int)rank * BM + lane_grp * 32;
+      const int col_base = tn * BN + col_half * C::COLS_PER_EPI_WARP;
+      const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) +
+                             (uint32_t)(acc * BN + col_half * C::COLS_PER_EPI_WARP);
+      epilogue_tile<C::CHUNKS, EPI, true>(p, &tmY, my_stg, taddr, &tfull_bar[acc], aphase, row_base,
+                                          col_base, my_bias);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader0 + (uint32_t)(acc * 8));
+      if (++acc == 2) {
+        acc = 0;
+        aphase ^= 1u;
+      }
+    }
+    if (lane == 0) bulk_wait0();
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
 }
 
 // ---------------------------------------------------------------------------
@@ -395,6 +701,21 @@ static int make_tmap(CUtensorMap* map, const void* base, int rows, int cols, int
   return PF_OK;
 }
 
+// Output map for the epilogue's TMA stores: box 32 x 32, 64-B swizzle.
+static int make_tmap_store(CUtensorMap* map, const void* base, int rows, int cols) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return set_error(PF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(PF_ERR_CUDA, "output tensor map failed (%d)", (int)r);
+  return PF_OK;
+}
+
 // BN choice: minimise (waves x BN), the per-SM tensor-pipe time, on 148 SMs.
 static int pick_bn(int M, int N) {
   const int sms = device_sm_count();
@@ -414,7 +735,8 @@ static int pick_bn(int M, int N) {
 }
 
 template <int BN, uint32_t EPI>
-static int launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid,
+static int launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty,
+                      const Params& p, int grid,
                       const pf_ctl_t* ctl, cudaStream_t stream) {
   using C = Cfg<BN>;
   static bool attr_set = false;
@@ -423,14 +745,92 @@ static int launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const Params
                                  C::SMEM_BYTES));
     attr_set = true;
   }
-  gemm_kernel<BN, EPI><<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(ta, tb, p, make_ctl(ctl));
+  gemm_kernel<BN, EPI><<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(ta, tb, ty, p, make_ctl(ctl));
   PF_CUDA(cudaGetLastError());
   return PF_OK;
 }
 
+template <int BN, uint32_t EPI>
+static int launch_pair_epi(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty,
+                           const Params& p, int grid,
+                           const pf_ctl_t* ctl, cudaStream_t stream) {
+  using C = Cfg2<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    PF_CUDA(cudaFuncSetAttribute(gemm2_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::SMEM_BYTES));
+    attr_set = true;
+  }
+  gemm2_kernel<BN, EPI><<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(ta, tb, ty, p, make_ctl(ctl));
+  PF_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+// CTA-pair GEMM: 256 x BN tiles per cluster of 2 SMs.
+template <int BN>
+struct GemmPairOp final : PreparedOp {
+  CUtensorMap ta, tb, ty;
+  Params p;
+  uint32_t epi = 0;
+  int grid = 0;
+
+  int prepare(const void* X, const void* W, const void* bias, const void* residual, void* Y, int M,
+              int N, int K, uint32_t e) {
+    PF_TRY(make_tmap(&ta, X, M, K, BM));
+    PF_TRY(make_tmap(&tb, W, N, K, BN / 2));
+    PF_TRY(make_tmap_store(&ty, Y, M, N));
+    p.Y = reinterpret_cast<__nv_bfloat16*>(Y);
+    p.bias = reinterpret_cast<const __nv_bfloat16*>(bias);
+    p.residual = reinterpret_cast<const __nv_bfloat16*>(residual);
+    p.M = M;
+    p.N = N;
+    p.K = K;
+    p.tiles_m = (M + 2 * BM - 1) / (2 * BM);
+    p.tiles_n = (N + BN - 1) / BN;
+    const int tiles = p.tiles_m * p.tiles_n;
+    const int pairs = device_sm_count() / 2;
+    grid = 2 * (tiles < pairs ? tiles : pairs);
+    epi = e & 7u;
+    return PF_OK;
+  }
+  uint32_t units() const override { return (uint32_t)(p.tiles_m * p.tiles_n); }
+  bool resumable() const override { return true; }
+  int run(const pf_ctl_t* ctl, cudaStream_t stream, int64_t, int64_t) override {
+    switch (epi) {
+      case 0: return launch_pair_epi<BN, 0>(ta, tb, ty, p, grid, ctl, stream);
+      case 1: return launch_pair_epi<BN, 1>(ta, tb, ty, p, grid, ctl, stream);
+      case 2: return launch_pair_epi<BN, 2>(ta, tb, ty, p, grid, ctl, stream);
+      case 3: return launch_pair_epi<BN, 3>(ta, tb, ty, p, grid, ctl, stream);
+      case 4: return launch_pair_epi<BN, 4>(ta, tb, ty, p, grid, ctl, stream);
+      case 5: return launch_pair_epi<BN, 5>(ta, tb, ty, p, grid, ctl, stream);
+      case 6: return launch_pair_epi<BN, 6>(ta, tb, ty, p, grid, ctl, stream);
+      default: return launch_pair_epi<BN, 7>(ta, tb, ty, p, grid, ctl, stream);
+    }
+  }
+};
+
+// Variant choice: 0 = single-CTA (BN from pick_bn), 1 = CTA pair BN=256, 2 = CTA pair BN=128.
+// The pair kernel is opt-in (PF_GEMM_PAIR=1): with the TMA-store epilogue the single-CTA
+// kernel is faster on the fill job's K = 1024 GEMMs; the pair kernel wins only at K >= 3072
+// (profiles/r01_gemm_variants.txt).
+static int pick_variant(int M, int N) {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("PF_GEMM_PAIR");
+    mode = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (mode == 0 || M < 2 * BM) return 0;
+  const long pairs = device_sm_count() / 2;
+  const long t256 = (long)((M + 255) / 256) * ((N + 255) / 256);
+  const long t128 = (long)((M + 255) / 256) * ((N + 127) / 128);
+  const long c256 = ((t256 + pairs - 1) / pairs) * 256;
+  const long c128 = ((t128 + pairs - 1) / pairs) * 128;
+  return c256 <= c128 ? 1 : 2;
+}
+
 template <int BN>
 struct GemmOp final : PreparedOp {
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, ty;
   Params p;
   uint32_t epi = 0;
   int grid = 0;
@@ -439,6 +839,7 @@ struct GemmOp final : PreparedOp {
               int N, int K, uint32_t e) {
     PF_TRY(make_tmap(&ta, X, M, K, BM));
     PF_TRY(make_tmap(&tb, W, N, K, BN));
+    PF_TRY(make_tmap_store(&ty, Y, M, N));
     p.Y = reinterpret_cast<__nv_bfloat16*>(Y);
     p.bias = reinterpret_cast<const __nv_bfloat16*>(bias);
     p.residual = reinterpret_cast<const __nv_bfloat16*>(residual);
@@ -457,14 +858,14 @@ struct GemmOp final : PreparedOp {
   bool resumable() const override { return true; }
   int run(const pf_ctl_t* ctl, cudaStream_t stream, int64_t, int64_t) override {
     switch (epi) {
-      case 0: return launch_epi<BN, 0>(ta, tb, p, grid, ctl, stream);
-      case 1: return launch_epi<BN, 1>(ta, tb, p, grid, ctl, stream);
-      case 2: return launch_epi<BN, 2>(ta, tb, p, grid, ctl, stream);
-      case 3: return launch_epi<BN, 3>(ta, tb, p, grid, ctl, stream);
-      case 4: return launch_epi<BN, 4>(ta, tb, p, grid, ctl, stream);
-      case 5: return launch_epi<BN, 5>(ta, tb, p, grid, ctl, stream);
-      case 6: return launch_epi<BN, 6>(ta, tb, p, grid, ctl, stream);
-      default: return launch_epi<BN, 7>(ta, tb, p, grid, ctl, stream);
+      case 0: return launch_epi<BN, 0>(ta, tb, ty, p, grid, ctl, stream);
+      case 1: return launch_epi<BN, 1>(ta, tb, ty, p, grid, ctl, stream);
+      case 2: return launch_epi<BN, 2>(ta, tb, ty, p, grid, ctl, stream);
+      case 3: return launch_epi<BN, 3>(ta, tb, ty, p, grid, ctl, stream);
+      case 4: return launch_epi<BN, 4>(ta, tb, ty, p, grid, ctl, stream);
+      case 5: return launch_epi<BN, 5>(ta, tb, ty, p, grid, ctl, stream);
+      case 6: return launch_epi<BN, 6>(ta, tb, ty, p, grid, ctl, stream);
+      default: return launch_epi<BN, 7>(ta, tb, ty, p, grid, ctl, stream);
     }
   }
 };
@@ -483,6 +884,19 @@ int make_gemm_op(OpPtr* out, const void* X, const void* W, const void* bias, con
   if (((uintptr_t)X | (uintptr_t)W | (uintptr_t)Y | (uintptr_t)bias | (uintptr_t)residual) & 15u)
     return set_error(PF_ERR_INVALID, "pf_gemm: pointers must be 16-B aligned");
   if (!device_is_sm100()) return set_error(PF_ERR_UNSUPPORTED, "pf_gemm: needs an sm_100 device");
+  const int variant = gemm::pick_variant(M, N);
+  if (variant == 1 || variant == 2) {
+    if (variant == 1) {
+      auto op = std::make_unique<gemm::GemmPairOp<256>>();
+      PF_TRY(op->prepare(X, W, bias, residual, Y, M, N, K, epilogue));
+      *out = std::move(op);
+    } else {
+      auto op = std::make_unique<gemm::GemmPairOp<128>>();
+      PF_TRY(op->prepare(X, W, bias, residual, Y, M, N, K, epilogue));
+      *out = std::move(op);
+    }
+    return PF_OK;
+  }
   switch (gemm::pick_bn(M, N)) {
     case 256: {
       auto op = std::make_unique<gemm::GemmOp<256>>();
@@ -507,9 +921,30 @@ int make_gemm_op(OpPtr* out, const void* X, const void* W, const void* bias, con
 
 }  // namespace pf
 
+extern "C" int pf_gemm_diag(unsigned long long* out8, int reset) {
+#ifdef PF_GEMM_DIAG
+  if (out8) cudaMemcpyFromSymbol(out8, pf::gemm::g_gemm_diag, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(pf::gemm::g_gemm_diag, z, sizeof(z));
+  }
+  return PF_OK;
+#else
+  (void)out8;
+  (void)reset;
+  return PF_ERR_UNSUPPORTED;
+#endif
+}
+
 extern "C" int pf_gemm_units(int M, int N, int K, uint32_t* out_units) {
   using namespace pf;
   if (!out_units || M <= 0 || N <= 0 || K <= 0) return set_error(PF_ERR_INVALID, "pf_gemm_units");
+  const int variant = gemm::pick_variant(M, N);
+  if (variant) {
+    const int bnp = variant == 1 ? 256 : 128;
+    *out_units = (uint32_t)(((M + 2 * gemm::BM - 1) / (2 * gemm::BM)) * ((N + bnp - 1) / bnp));
+    return PF_OK;
+  }
   const int bn = gemm::pick_bn(M, N);
   *out_units = (uint32_t)(((M + gemm::BM - 1) / gemm::BM) * ((N + bn - 1) / bn));
   return PF_OK;

@@ -1,0 +1,22 @@
+import ctypes, os, sys, torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2410_07192_b200 import native
+native.LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), os.environ.get("DIAG_LIB", "libpipefill_diag.so"))
+native._SIGNATURES["pf_gemm_diag"] = (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int])
+from paper_2410_07192_b200 import kernels as K
+native.load(native.LIB_PATH)
+native.require_device()
+lib = native.load()
+for (m, n, k, gelu) in [(16384, 3072, 768, False), (16384, 3072, 768, True), (16384, 1024, 4096, False), (8192, 8192, 8192, False)]:
+    x = torch.randn(m, k, device="cuda").bfloat16(); w = (torch.randn(n, k, device="cuda") * k ** -0.5).bfloat16()
+    b = torch.randn(n, device="cuda").bfloat16(); y = torch.empty(m, n, device="cuda").bfloat16()
+    for _ in range(3): K.linear(x, w, b, gelu=gelu, out=y)
+    torch.cuda.synchronize()
+    lib.pf_gemm_diag(None, 1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(); K.linear(x, w, b, gelu=gelu, out=y); e1.record(); torch.cuda.synchronize()
+    d = (ctypes.c_ulonglong * 8)()
+    lib.pf_gemm_diag(d, 0)
+    ms = e0.elapsed_time(e1)
+    cyc = ms * 1e-3 * 1.9e9 * 148
+    print(f"{m}x{n}x{k} gelu={gelu} {ms*1e3:.1f}us  per-SM-cycles~{cyc/148:.0f}  mma_wait_full={d[0]/148:.0f} mma_wait_tempty={d[1]/148:.0f} prod_wait_empty={d[2]/148:.0f} epi_wait_tfull(8 warps)={d[3]/148/8:.0f}")
