@@ -177,6 +177,9 @@ def main() -> None:
                          "neighbours; nccl: the N ranks ARE an N-stage pipeline (NCCL P2P over NVLink)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     ap.add_argument("--save-profile", default=None, help="write the measured fill ModelProfile JSON here")
+    ap.add_argument("--debug", action="store_true", help="per-bubble details to stderr")
+    ap.add_argument("--fill-fraction", type=float, default=FILL_FRACTION,
+                    help="share of each bubble the planner may fill (reference default 0.68)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -217,7 +220,7 @@ def main() -> None:
 
     # ---- bubble characterization: free memory with the main job at its peak
     probe_cfg = pf.PipelineConfig(P_STAGES, M_MICRO, tf_ms, tb_ms, pf.ScheduleKind.ONE_F_ONE_B,
-                                  1, 1, FILL_FRACTION)
+                                  1, 1, args.fill_fraction)
     probe = StageEngine(probe_cfg, 0, main_model, None)  # stage 0 holds the most activations
     probe.set_anchor()
     probe.run_iteration(0, fill=False)
@@ -227,7 +230,7 @@ def main() -> None:
     free_mem = int(max(0, total_b - reserved - (4 << 30)) * 0.9)  # safety margin
     arena_bytes = min(free_mem, 24 << 30)
     pcfg = pf.PipelineConfig(P_STAGES, M_MICRO, tf_ms, tb_ms, pf.ScheduleKind.ONE_F_ONE_B,
-                             arena_bytes, arena_bytes, FILL_FRACTION)
+                             arena_bytes, arena_bytes, args.fill_fraction)
 
     executor = Executor(arena_bytes, job_seed=rank)
     coords: dict[int, pf.Coordinator] = {}
@@ -261,7 +264,7 @@ def main() -> None:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         tf_ms, tb_ms = tt.tolist()
         pcfg = pf.PipelineConfig(world, M_MICRO, tf_ms, tb_ms, pf.ScheduleKind.ONE_F_ONE_B,
-                                 arena_bytes, arena_bytes, FILL_FRACTION)
+                                 arena_bytes, arena_bytes, args.fill_fraction)
         eng = NcclPipelineEngine(pcfg, main_model, executor)
         engines[rank] = eng
         items["stage"], items["item"] = rank, None
@@ -299,7 +302,7 @@ def main() -> None:
         durs = [int(statistics.median(meas[k])) if meas[k] else 0 for k in (0, 1)]
         analytic = pf.build_bubble_cycle(pcfg, rank)
         measured_cycle = pf.cycle_from_measurements(
-            rank, max(period_us, sum(durs)), durs, [arena_bytes, arena_bytes], FILL_FRACTION,
+            rank, max(period_us, sum(durs)), durs, [arena_bytes, arena_bytes], args.fill_fraction,
             unfillable_us=max(0, min(analytic.unfillable_us, period_us - sum(durs))))
         coordinator_for(rank, pcfg, measured_cycle)
         characterization = {"measured_bubbles_us": durs, "measured_period_us": period_us,
@@ -343,7 +346,13 @@ def main() -> None:
                 if items.get("item") is not None and items.get("stage") is not None:
                     coords[items["stage"]].worker_job[0] = None  # abandon the partial range
                 items["stage"], items["item"] = s, None
-                executor.item = None  # force next_work() at the first bubble
+                # hand the stage's next WorkItem to the executor before the iteration
+                # (layout, weight staging and graph recording off the bubbles)
+                nxt = next_work()
+                if nxt is not None:
+                    executor.load(*nxt)
+                executor.prewarm(eng.words.flag.value)
+                torch.cuda.synchronize()
             eng.reset_stamps()
             eng.set_anchor()
             rec = eng.run_iteration(0, fill=fill)
@@ -398,6 +407,17 @@ def main() -> None:
     on_iter: dict[int, list] = {}
     for t in steps:
         on_iter.setdefault(t["stage"], []).append(t["main_end"] - t["start"])
+    if args.debug:
+        for t in steps:
+            print(f"[dbg] rank {rank} stage {t['stage']} main {(t['main_end'] - t['start']) / 1e6:.1f} ms "
+                  f"step {(t['step_end'] - t['start']) / 1e6:.1f} ms", file=sys.stderr)
+            for kind, t_set, t_clr, tag in t["bubbles"]:
+                r = by_tag.get(tag)
+                info = "no fill" if r is None else (
+                    f"fill +{(r.fill_start_ns - t_set) / 1e6:.2f}..+{(r.fill_end_ns - t_set) / 1e6:.2f} ms "
+                    f"part {r.part} batches {r.batches_done}/{r.batches_planned} aborted {r.aborted}")
+                print(f"[dbg]   bubble {kind} at +{(t_set - t['start']) / 1e6:.1f} ms len "
+                      f"{(t_clr - t_set) / 1e6:.2f} ms: {info}", file=sys.stderr)
     slowdown = mean_slowdown(on_iter, off)
     stats = FillStats(
         sample_equivalents=sum(r.samples_done * r.model_fraction for r in recs),
@@ -443,7 +463,7 @@ def main() -> None:
                                "microbatches": M_MICRO, "stages": pcfg.num_stages,
                                "t_fwd_ms": tf_ms, "t_bwd_ms": tb_ms},
                 "fill": {"model": fcfg.name, "seq_len": fcfg.seq, "profiled_batch_sizes": list(FILL_BATCH_SIZES),
-                         "fill_fraction": FILL_FRACTION, "arena_bytes": arena_bytes,
+                         "fill_fraction": args.fill_fraction, "arena_bytes": arena_bytes,
                          "plans": {str(s): pf.plan_to_dict(c.executables[f"fill-{s}"]) for s, c in coords.items()}},
                 "stages_run": [t["stage"] for t in steps],
                 "l2": "inputs larger than L2 (BERT-large weights 0.67 GB streamed per batch; main job 1B params)",

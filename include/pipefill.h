@@ -202,6 +202,21 @@ int pf_chain_size(pf_chain_t* chain, int* out_nodes);
 /* units = work units of the node; resumable = 1 for claimed-prefix nodes (GEMM tiles),
  * 0 for atomic nodes that are re-run whole (cursor must be reset to 0 first).       */
 int pf_chain_node_info(pf_chain_t* chain, int node, uint32_t* out_units, int* out_resumable);
+/* Device-side batch descriptors: with desc set, copy nodes of role 1/2 take their
+ * batch-slice offsets from desc[2 * (*done) + role - 1] (int64 pairs in device memory),
+ * so one recorded graph serves every batch of a bubble.                            */
+int pf_chain_set_desc(pf_chain_t* chain, const int64_t* desc);
+/* In-kernel timing: node i of a launch writes [earliest CTA start, latest CTA end]
+ * (%globaltimer ns) to stamps[2i], stamps[2i+1] (GEMM nodes; reset at chain begin).   */
+int pf_chain_set_stamps(pf_chain_t* chain, uint64_t* stamps);
+/* Record the chain as a CUDA graph with device-side gating: after the chain-begin
+ * marker, every segment [seg_ends[i-1], seg_ends[i]) of nodes sits in a conditional IF
+ * node preceded by a one-thread gate kernel that checks abort / the bubble flag; a
+ * closed bubble skips the remaining segments on the device (no launches). Then one
+ * pf_chain_graph_launch per batch.                                                   */
+int pf_chain_build_graph(pf_chain_t* chain, const uint32_t* flag, uint32_t* abort,
+                         uint32_t* cursors, uint32_t* done, const int* seg_ends, int n_segs);
+int pf_chain_graph_launch(pf_chain_t* chain, void* stream);
 /* Live per-node device timing (CUDA events around every node of the next launches);
  * pf_chain_node_elapsed returns the last launch's duration of `node` in ms.        */
 int pf_chain_set_timing(pf_chain_t* chain, int enable);

@@ -232,7 +232,7 @@ struct AttentionOp final : PreparedOp {
   float scale_log2 = 0.f;
   uint32_t units() const override { return (uint32_t)(batch * heads); }
   bool resumable() const override { return false; }
-  int run(const pf_ctl_t* ctl, cudaStream_t s, int64_t, int64_t) override {
+  int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
     attention_kernel<<<batch * heads, THREADS, SMEM_REQUEST, s>>>(tm, mask, out, batch, seq, heads,
                                                                   scale_log2, make_ctl(ctl));
     PF_CUDA(cudaGetLastError());
@@ -295,5 +295,5 @@ extern "C" int pf_attention(const void* QKV, const float* mask_add, void* O, int
   PF_TRY(pf::validate_ctl(ctl));
   pf::OpPtr op;
   PF_TRY(pf::make_attention_op(&op, QKV, mask_add, O, batch, seq, heads, head_dim, scale));
-  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), 0, 0);
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), pf::LaunchArgs{});
 }

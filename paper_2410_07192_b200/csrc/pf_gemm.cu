@@ -60,7 +60,14 @@ struct Params {
   const __nv_bfloat16* residual;
   int M, N, K;
   int tiles_m, tiles_n;
+  unsigned long long* stamp;  // optional [first CTA start, last CTA end] in ns
 };
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Grouped rasterisation: tiles walk GROUP_M m-blocks x all n-blocks, n fastest, so the
 // CTAs in flight share a band of A rows (read from DRAM once) and all of W (the small,
@@ -243,6 +250,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int lane = lane_id();
 
   if (chain_aborted(ctl)) return;  // uniform across the CTA: nothing allocated yet
+  if (threadIdx.x == 0 && p.stamp) atomicMin(&p.stamp[0], globaltimer_ns());
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -413,6 +421,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc(tmem_base, C::TMEM_COLS);
+  if (threadIdx.x == 0 && p.stamp) atomicMax(&p.stamp[1], globaltimer_ns());
 }
 
 
@@ -487,6 +496,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const int lane = lane_id();
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
+  if (threadIdx.x == 0 && p.stamp) atomicMin(&p.stamp[0], globaltimer_ns());
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -663,6 +673,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   cluster_sync_all();
   tc_fence_after();
   if (warp == 2) tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
+  if (threadIdx.x == 0 && p.stamp) atomicMax(&p.stamp[1], globaltimer_ns());
 }
 
 // ---------------------------------------------------------------------------
@@ -787,6 +798,7 @@ struct GemmPairOp final : PreparedOp {
     p.K = K;
     p.tiles_m = (M + 2 * BM - 1) / (2 * BM);
     p.tiles_n = (N + BN - 1) / BN;
+    p.stamp = nullptr;
     const int tiles = p.tiles_m * p.tiles_n;
     const int pairs = device_sm_count() / 2;
     grid = 2 * (tiles < pairs ? tiles : pairs);
@@ -795,7 +807,9 @@ struct GemmPairOp final : PreparedOp {
   }
   uint32_t units() const override { return (uint32_t)(p.tiles_m * p.tiles_n); }
   bool resumable() const override { return true; }
-  int run(const pf_ctl_t* ctl, cudaStream_t stream, int64_t, int64_t) override {
+  int run(const pf_ctl_t* ctl, cudaStream_t stream, const LaunchArgs& a) override {
+    Params p = this->p;
+    p.stamp = a.stamp;
     switch (epi) {
       case 0: return launch_pair_epi<BN, 0>(ta, tb, ty, p, grid, ctl, stream);
       case 1: return launch_pair_epi<BN, 1>(ta, tb, ty, p, grid, ctl, stream);
@@ -848,6 +862,7 @@ struct GemmOp final : PreparedOp {
     p.K = K;
     p.tiles_m = (M + BM - 1) / BM;
     p.tiles_n = (N + BN - 1) / BN;
+    p.stamp = nullptr;
     const int tiles = p.tiles_m * p.tiles_n;
     const int sms = device_sm_count();
     grid = tiles < sms ? tiles : sms;
@@ -856,7 +871,9 @@ struct GemmOp final : PreparedOp {
   }
   uint32_t units() const override { return (uint32_t)(p.tiles_m * p.tiles_n); }
   bool resumable() const override { return true; }
-  int run(const pf_ctl_t* ctl, cudaStream_t stream, int64_t, int64_t) override {
+  int run(const pf_ctl_t* ctl, cudaStream_t stream, const LaunchArgs& a) override {
+    Params p = this->p;
+    p.stamp = a.stamp;
     switch (epi) {
       case 0: return launch_epi<BN, 0>(ta, tb, ty, p, grid, ctl, stream);
       case 1: return launch_epi<BN, 1>(ta, tb, ty, p, grid, ctl, stream);
@@ -957,5 +974,5 @@ extern "C" int pf_gemm(const void* X, const void* W, const void* bias, const voi
   PF_TRY(validate_ctl(ctl));
   OpPtr op;
   PF_TRY(make_gemm_op(&op, X, W, bias, residual, Y, M, N, K, epilogue));
-  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), 0, 0);
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), pf::LaunchArgs{});
 }

@@ -258,7 +258,7 @@ struct NormOp final : PreparedOp {
   float eps = 0.f;
   uint32_t units() const override { return (uint32_t)grid_for(rows); }
   bool resumable() const override { return false; }
-  int run(const pf_ctl_t* ctl, cudaStream_t s, int64_t, int64_t) override {
+  int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
     if (rms) {
       PF_NV_DISPATCH(nv_for(cols), (norm_kernel<NV, true><<<grid_for(rows), WARPS * 32, 0, s>>>(
                                        x, r, g, nullptr, y, rows, cols, eps, make_ctl(ctl))));
@@ -278,7 +278,7 @@ struct SoftmaxOp final : PreparedOp {
   float scale = 1.f;
   uint32_t units() const override { return (uint32_t)grid_for(rows); }
   bool resumable() const override { return false; }
-  int run(const pf_ctl_t* ctl, cudaStream_t s, int64_t, int64_t) override {
+  int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
     PF_NV_DISPATCH(nv_for(cols), (softmax_kernel<NV><<<grid_for(rows), WARPS * 32, 0, s>>>(
                                      x, y, rows, cols, scale, make_ctl(ctl))));
     PF_CUDA(cudaGetLastError());
@@ -294,7 +294,7 @@ struct EmbeddingOp final : PreparedOp {
   float eps = 0.f;
   uint32_t units() const override { return (uint32_t)grid_for(rows); }
   bool resumable() const override { return false; }
-  int run(const pf_ctl_t* ctl, cudaStream_t s, int64_t, int64_t) override {
+  int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
     PF_NV_DISPATCH(nv_for(hidden),
                    (embedding_ln_kernel<NV><<<grid_for(rows), WARPS * 32, 0, s>>>(
                        ids, tt, word, pos, type, g, b, y, rows, seq, hidden, vocab, eps,
@@ -385,7 +385,7 @@ extern "C" int pf_layernorm(const void* X, const void* residual, const void* gam
   PF_TRY(pf::validate_ctl(ctl));
   pf::OpPtr op;
   PF_TRY(pf::make_norm_op(&op, false, X, residual, gamma, beta, Y, rows, cols, eps));
-  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), 0, 0);
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), pf::LaunchArgs{});
 }
 
 extern "C" int pf_rmsnorm(const void* X, const void* residual, const void* gamma, void* Y,
@@ -393,7 +393,7 @@ extern "C" int pf_rmsnorm(const void* X, const void* residual, const void* gamma
   PF_TRY(pf::validate_ctl(ctl));
   pf::OpPtr op;
   PF_TRY(pf::make_norm_op(&op, true, X, residual, gamma, nullptr, Y, rows, cols, eps));
-  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), 0, 0);
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), pf::LaunchArgs{});
 }
 
 extern "C" int pf_softmax(const void* X, void* Y, int rows, int cols, float scale,
@@ -401,7 +401,7 @@ extern "C" int pf_softmax(const void* X, void* Y, int rows, int cols, float scal
   PF_TRY(pf::validate_ctl(ctl));
   pf::OpPtr op;
   PF_TRY(pf::make_softmax_op(&op, X, Y, rows, cols, scale));
-  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), 0, 0);
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), pf::LaunchArgs{});
 }
 
 extern "C" int pf_embedding_ln(const int32_t* ids, const int32_t* type_ids, const void* word,
@@ -412,5 +412,5 @@ extern "C" int pf_embedding_ln(const int32_t* ids, const int32_t* type_ids, cons
   pf::OpPtr op;
   PF_TRY(pf::make_embedding_op(&op, ids, type_ids, word, pos, type, gamma, beta, Y, batch, seq,
                                hidden, vocab, eps));
-  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), 0, 0);
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), pf::LaunchArgs{});
 }

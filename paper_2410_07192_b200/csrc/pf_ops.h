@@ -9,10 +9,22 @@
 
 namespace pf {
 
+// Per-launch arguments. Copy nodes bound to a batch slice add in_off (role 1, source) or
+// out_off (role 2, destination); with `desc` set they instead read the offsets on the
+// device from desc[2 * (*idx) + role - 1], so one recorded graph serves every batch.
+struct LaunchArgs {
+  int64_t in_off = 0;
+  int64_t out_off = 0;
+  const int64_t* desc = nullptr;
+  const uint32_t* idx = nullptr;
+  // optional in-kernel timing of this node: [0] = earliest CTA start, [1] = latest CTA end
+  // (%globaltimer ns), reset by the chain-begin marker
+  unsigned long long* stamp = nullptr;
+};
+
 struct PreparedOp {
   virtual ~PreparedOp() {}
-  // in_off / out_off: per-launch byte offsets for copy nodes bound to a batch slice
-  virtual int run(const pf_ctl_t* ctl, cudaStream_t s, int64_t in_off, int64_t out_off) = 0;
+  virtual int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs& a) = 0;
   virtual uint32_t units() const = 0;
   virtual bool resumable() const = 0;  // true: claimed-prefix cursor; false: atomic (re-run whole)
 };

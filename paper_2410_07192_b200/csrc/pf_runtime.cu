@@ -92,9 +92,16 @@ __global__ void globaltimer_kernel(uint64_t* out) {
   *out = now;
 }
 
-__global__ void chain_begin_kernel(uint32_t* cursors, int n, const uint32_t* abort) {
+__global__ void chain_begin_kernel(uint32_t* cursors, int n, const uint32_t* abort,
+                                   unsigned long long* stamps) {
   if (abort && ld_volatile_u32(abort) != 0u) return;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) cursors[i] = 0u;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (cursors) cursors[i] = 0u;
+    if (stamps) {
+      stamps[2 * i] = ~0ull;
+      stamps[2 * i + 1] = 0ull;
+    }
+  }
 }
 
 __global__ void chain_end_kernel(uint32_t* done, const uint32_t* abort) {
@@ -110,7 +117,9 @@ constexpr uint64_t COPY_BYTES_PER_CTA = 256 * 1024;
 __global__ void __launch_bounds__(COPY_THREADS) copy_kernel(uint4* __restrict__ dst, int64_t dpitch,
                                                             const uint4* __restrict__ src,
                                                             int64_t spitch, int64_t w16,
-                                                            uint64_t n16, Ctl ctl) {
+                                                            uint64_t n16, Ctl ctl,
+                                                            const int64_t* desc,
+                                                            const uint32_t* idx, int role) {
   __shared__ int s_go;
   if (threadIdx.x == 0) {
     int go = 1;
@@ -123,6 +132,11 @@ __global__ void __launch_bounds__(COPY_THREADS) copy_kernel(uint4* __restrict__ 
   }
   __syncthreads();
   if (!s_go) return;
+  if (desc != nullptr && role != 0) {  // batch slice offset chosen on the device
+    const int64_t off = desc[2 * (int64_t)ld_volatile_u32(idx) + role - 1];
+    if (role == 1) src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(src) + off);
+    else dst = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(dst) + off);
+  }
   const uint64_t per = COPY_BYTES_PER_CTA / 16;
   const uint64_t lo = (uint64_t)blockIdx.x * per;
   const uint64_t hi = lo + per < n16 ? lo + per : n16;
@@ -160,13 +174,14 @@ struct CopyOp final : PreparedOp {
     return (uint32_t)((n16() * 16 + COPY_BYTES_PER_CTA - 1) / COPY_BYTES_PER_CTA);
   }
   bool resumable() const override { return false; }
-  int run(const pf_ctl_t* ctl, cudaStream_t s, int64_t in_off, int64_t out_off) override {
-    const uint8_t* sp = src + (role == 1 ? in_off : 0);
-    uint8_t* dp = dst + (role == 2 ? out_off : 0);
+  int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs& a) override {
+    const bool dev = a.desc != nullptr && role != 0;
+    const uint8_t* sp = src + (role == 1 && !dev ? a.in_off : 0);
+    uint8_t* dp = dst + (role == 2 && !dev ? a.out_off : 0);
     if (n16() == 0) return PF_OK;
     copy_kernel<<<units(), COPY_THREADS, 0, s>>>(
         reinterpret_cast<uint4*>(dp), dpitch / 16, reinterpret_cast<const uint4*>(sp), spitch / 16,
-        width / 16, n16(), make_ctl(ctl));
+        width / 16, n16(), make_ctl(ctl), dev ? a.desc : nullptr, a.idx, role);
     PF_CUDA(cudaGetLastError());
     return PF_OK;
   }
@@ -410,7 +425,7 @@ int pf_copy(void* dst, const void* src, uint64_t bytes, const pf_ctl_t* ctl, voi
   PF_TRY(validate_ctl(ctl));
   OpPtr op;
   PF_TRY(make_copy_op(&op, dst, (int64_t)bytes, src, (int64_t)bytes, (int64_t)bytes, 1, 0));
-  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), 0, 0);
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), pf::LaunchArgs{});
 }
 
 int pf_copy2d(void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch, int64_t width,
@@ -419,7 +434,7 @@ int pf_copy2d(void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch, 
   PF_TRY(validate_ctl(ctl));
   OpPtr op;
   PF_TRY(make_copy_op(&op, dst, dst_pitch, src, src_pitch, width, rows, 0));
-  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), 0, 0);
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), pf::LaunchArgs{});
 }
 
 // ---- chain ----------------------------------------------------------------------
@@ -427,7 +442,8 @@ int pf_copy2d(void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch, 
 int pf_chain_begin(uint32_t* cursors, int n, const uint32_t* abort, void* stream) {
   using namespace pf;
   if (!cursors || n <= 0) return set_error(PF_ERR_INVALID, "pf_chain_begin: bad arguments");
-  chain_begin_kernel<<<1, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(cursors, n, abort);
+  chain_begin_kernel<<<1, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(cursors, n, abort,
+                                                                             nullptr);
   PF_CUDA(cudaGetLastError());
   return PF_OK;
 }
@@ -451,10 +467,33 @@ struct pf_chain {
   std::vector<pf::OpPtr> nodes;
   bool timing = false;
   std::vector<cudaEvent_t> ev;  // 2 per node when timing is on
+  const int64_t* desc = nullptr;  // device batch-slice offsets (see LaunchArgs)
+  unsigned long long* stamps = nullptr;  // device [start, end] per node (in-kernel timing)
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
   ~pf_chain() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
   }
 };
+
+namespace pf {
+// Segment gate of a chain graph: the following conditional IF body (one module's
+// kernels) runs only while the chain is live and the bubble is open. A closed bubble
+// sets the sticky abort, so every later gate and the chain-end marker see it.
+__global__ void chain_gate_kernel(cudaGraphConditionalHandle h, const uint32_t* flag,
+                                  uint32_t* abort) {
+  unsigned go = 1u;
+  if (abort != nullptr && ld_volatile_u32(abort) != 0u) {
+    go = 0u;
+  } else if (flag != nullptr && ld_acquire_u32(flag) == 0u) {
+    atomicExch(abort, 1u);
+    go = 0u;
+  }
+  cudaGraphSetConditional(h, go);
+}
+}  // namespace pf
 
 extern "C" {
 
@@ -543,6 +582,129 @@ int pf_chain_node_info(pf_chain_t* c, int node, uint32_t* units, int* resumable)
   return PF_OK;
 }
 
+int pf_chain_set_stamps(pf_chain_t* c, uint64_t* stamps) {
+  if (!c) return pf::set_error(PF_ERR_INVALID, "null chain");
+  c->stamps = reinterpret_cast<unsigned long long*>(stamps);
+  return PF_OK;
+}
+
+int pf_chain_set_desc(pf_chain_t* c, const int64_t* desc) {
+  if (!c) return pf::set_error(PF_ERR_INVALID, "null chain");
+  c->desc = desc;
+  return PF_OK;
+}
+
+// Record the chain as a CUDA graph: chain-begin marker, then per segment a gate kernel
+// and a conditional IF node whose body is the segment's kernels (stream-captured),
+// then the chain-end marker. A batch whose bubble closed costs one gate launch per
+// remaining segment instead of one kernel launch per remaining node.
+int pf_chain_build_graph(pf_chain_t* c, const uint32_t* flag, uint32_t* abort, uint32_t* cursors,
+                         uint32_t* done, const int* seg_ends, int n_segs) {
+  using namespace pf;
+  if (!c || !seg_ends || n_segs <= 0) return set_error(PF_ERR_INVALID, "pf_chain_build_graph: bad arguments");
+  const int n = (int)c->nodes.size();
+  if (seg_ends[n_segs - 1] != n) return set_error(PF_ERR_INVALID, "segments must end at the chain size");
+  if (flag && (!abort || !cursors)) return set_error(PF_ERR_INVALID, "preemptible graph needs abort and cursors");
+  if (c->exec) {
+    cudaGraphExecDestroy(c->exec);
+    c->exec = nullptr;
+  }
+  if (c->graph) {
+    cudaGraphDestroy(c->graph);
+    c->graph = nullptr;
+  }
+  cudaGraph_t g;
+  PF_CUDA(cudaGraphCreate(&g, 0));
+  cudaStream_t cap;
+  PF_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  int rc = PF_OK;
+  cudaGraphNode_t prev = nullptr;
+  auto add_kernel = [&](void* fn, dim3 grid, dim3 block, void** args) -> int {
+    cudaKernelNodeParams kp = {};
+    kp.func = fn;
+    kp.gridDim = grid;
+    kp.blockDim = block;
+    kp.sharedMemBytes = 0;
+    kp.kernelParams = args;
+    cudaGraphNode_t nd;
+    PF_CUDA(cudaGraphAddKernelNode(&nd, g, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
+    prev = nd;
+    return PF_OK;
+  };
+  do {
+    if (cursors || c->stamps) {
+      uint32_t* cur = cursors;
+      int nn = n;
+      const uint32_t* ab = abort;
+      unsigned long long* st = c->stamps;
+      void* args[] = {&cur, &nn, &ab, &st};
+      if ((rc = add_kernel((void*)chain_begin_kernel, dim3(1), dim3(128), args)) != PF_OK) break;
+    }
+    int lo = 0;
+    for (int sgi = 0; sgi < n_segs && rc == PF_OK; ++sgi) {
+      const int hi = seg_ends[sgi];
+      cudaGraphConditionalHandle h;
+      if ((rc = check_cuda(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault),
+                           "cudaGraphConditionalHandleCreate")) != PF_OK)
+        break;
+      const uint32_t* fl = flag;
+      uint32_t* ab = abort;
+      void* gargs[] = {&h, &fl, &ab};
+      if ((rc = add_kernel((void*)chain_gate_kernel, dim3(1), dim3(1), gargs)) != PF_OK) break;
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeIf;
+      cp.conditional.size = 1;
+      cudaGraphNode_t cn;
+      if ((rc = check_cuda(cudaGraphAddNode(&cn, g, &prev, 1, &cp), "cudaGraphAddNode(cond)")) != PF_OK)
+        break;
+      prev = cn;
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      if ((rc = check_cuda(cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0,
+                                                         cudaStreamCaptureModeThreadLocal),
+                           "cudaStreamBeginCaptureToGraph")) != PF_OK)
+        break;
+      for (int i = lo; i < hi && rc == PF_OK; ++i) {
+        pf_ctl_t ctl{flag, abort, cursors ? cursors + i : nullptr};
+        LaunchArgs la;
+        la.desc = c->desc;
+        la.idx = done;
+        la.stamp = c->stamps ? c->stamps + 2 * i : nullptr;
+        if (c->timing) rc = check_cuda(cudaEventRecord(c->ev[2 * i], cap), "event");
+        if (rc == PF_OK) rc = c->nodes[i]->run(flag || cursors ? &ctl : nullptr, cap, la);
+        if (rc == PF_OK && c->timing) rc = check_cuda(cudaEventRecord(c->ev[2 * i + 1], cap), "event");
+      }
+      cudaGraph_t out_g;
+      int rc2 = check_cuda(cudaStreamEndCapture(cap, &out_g), "cudaStreamEndCapture");
+      if (rc == PF_OK) rc = rc2;
+      lo = hi;
+    }
+    if (rc != PF_OK) break;
+    if (done) {
+      uint32_t* d = done;
+      const uint32_t* ab = abort;
+      void* args[] = {&d, &ab};
+      if ((rc = add_kernel((void*)chain_end_kernel, dim3(1), dim3(1), args)) != PF_OK) break;
+    }
+    rc = check_cuda(cudaGraphInstantiate(&c->exec, g, 0), "cudaGraphInstantiate");
+  } while (false);
+  cudaStreamDestroy(cap);
+  if (rc != PF_OK) {
+    cudaGraphDestroy(g);
+    return rc;
+  }
+  c->graph = g;
+  return PF_OK;
+}
+
+int pf_chain_graph_launch(pf_chain_t* c, void* stream) {
+  using namespace pf;
+  if (!c || !c->exec) return set_error(PF_ERR_INVALID, "pf_chain_graph_launch: no graph built");
+  PF_CUDA(cudaGraphLaunch(c->exec, reinterpret_cast<cudaStream_t>(stream)));
+  return PF_OK;
+}
+
 int pf_chain_set_timing(pf_chain_t* c, int enable) {
   using namespace pf;
   if (!c) return set_error(PF_ERR_INVALID, "null chain");
@@ -575,14 +737,20 @@ int pf_chain_launch(pf_chain_t* c, const uint32_t* flag, uint32_t* abort, uint32
   if (flag && (!abort || !cursors))
     return set_error(PF_ERR_INVALID, "pf_chain_launch: preemptible chain needs abort and cursors");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (start_node == 0 && cursors) {
-    chain_begin_kernel<<<1, 128, 0, s>>>(cursors, n, abort);
+  if (start_node == 0 && (cursors || c->stamps)) {
+    chain_begin_kernel<<<1, 128, 0, s>>>(cursors, n, abort, c->stamps);
     PF_CUDA(cudaGetLastError());
   }
   for (int i = start_node; i < n; ++i) {
     pf_ctl_t ctl{flag, abort, cursors ? cursors + i : nullptr};
     if (c->timing) PF_CUDA(cudaEventRecord(c->ev[2 * i], s));
-    PF_TRY(c->nodes[i]->run(flag || cursors ? &ctl : nullptr, s, in_off, out_off));
+    LaunchArgs la;
+    la.in_off = in_off;
+    la.out_off = out_off;
+    la.desc = c->desc;
+    la.idx = done;
+    la.stamp = c->stamps ? c->stamps + 2 * i : nullptr;
+    PF_TRY(c->nodes[i]->run(flag || cursors ? &ctl : nullptr, s, la));
     if (c->timing) PF_CUDA(cudaEventRecord(c->ev[2 * i + 1], s));
   }
   if (done) {

@@ -41,6 +41,8 @@ from .planner import ExecutionPlan
 
 _CTL_WORDS = 64 + 4096  # [0]=abort, [1]=batches done, [8..12)=timestamps (2 x u64), [64..)=cursors
 _CURSOR0 = 64
+MAX_BATCHES = 64  # per bubble (device batch descriptors)
+MAX_NODES = 4096
 
 
 @dataclass
@@ -89,14 +91,16 @@ class _Pending:
 
 
 class _Chain:
-    """Owner of one recorded pf_chain_t (partition, batch size)."""
+    """Owner of one recorded pf_chain_t (partition, batch size) and its CUDA graph."""
 
     def __init__(self):
         self.h = ctypes.c_void_p()
         native.call("pf_chain_create", ctypes.byref(self.h))
         self.units: list[tuple[int, bool]] = []
         self.gemm_flops: dict[int, float] = {}
+        self.seg_ends: list[int] = []
         self.timing = False
+        self.graph = False
 
     def finalize(self) -> None:
         n = ctypes.c_int(0)
@@ -107,19 +111,10 @@ class _Chain:
             native.call("pf_chain_node_info", self.h, i, ctypes.byref(u), ctypes.byref(r))
             self.units.append((u.value, bool(r.value)))
 
-    def set_timing(self, on: bool) -> None:
-        if on != self.timing:
-            native.call("pf_chain_set_timing", self.h, 1 if on else 0)
-            self.timing = on
-
-    def gemm_times(self) -> list[tuple[float, float]]:
-        """(flops, ms) of every GEMM node of the last launch."""
-        out = []
-        ms = ctypes.c_float(0)
-        for node, fl in self.gemm_flops.items():
-            native.call("pf_chain_node_elapsed", self.h, node, ctypes.byref(ms))
-            out.append((fl, ms.value))
-        return out
+    def build_graph(self, flag: Optional[int], abort: int, cursors: int, done: int) -> None:
+        ends = (ctypes.c_int * len(self.seg_ends))(*self.seg_ends)
+        native.call("pf_chain_build_graph", self.h, flag, abort, cursors, done, ends, len(self.seg_ends))
+        self.graph = True
 
     def close(self) -> None:
         if self.h:
@@ -155,6 +150,8 @@ class Executor:
         # (WorkItem, model) from the stage's Coordinator, or None
         self.work_source: Optional[Callable[[], Optional[tuple[WorkItem, FillSequential]]]] = None
         self._ctl_host = PinnedBuffer((_CTL_WORDS,), torch.int32)
+        self._desc_host = PinnedBuffer((MAX_BATCHES, 2), torch.int64)
+        self._stamps_host = PinnedBuffer((MAX_NODES, 2), torch.int64)
         self._chains: dict[tuple[int, int], _Chain] = {}
         self._staged_event: Optional[torch.cuda.Event] = None
         self._staged_part: Optional[int] = None
@@ -165,6 +162,7 @@ class Executor:
         self._store_dev: Optional[torch.Tensor] = None
         self._layout_key = None
         self._flops_frac: list[float] = []
+        self._last_flag: Optional[int] = None
 
     # ------------------------------------------------------------------ loading
 
@@ -185,6 +183,7 @@ class Executor:
         self._ids_host.tensor[:n].copy_(
             synthetic_ids(self.job_seed, item.entry.lo - 1, n, cfg.seq, cfg.vocab))
         self._stage_partition(0)
+        self.prewarm()
 
     def _layout(self, cap: int) -> None:
         """Arena: control block | weight region (largest partition) | workspace | store."""
@@ -195,6 +194,8 @@ class Executor:
         self.arena.reset()
         self._ctl = self.arena.alloc((_CTL_WORDS,), torch.int32)
         self._ctl.zero_()
+        self._desc = self.arena.alloc((MAX_BATCHES, 2), torch.int64)
+        self._stamps = self.arena.alloc((MAX_NODES, 2), torch.int64)
         max_w = max(sum(_pad256(model[i].weight_bytes()) for i in range(p.lo, p.hi))
                     for p in plan.partitions)
         self._wregion = self.arena.alloc((max_w // 2,), torch.bfloat16)
@@ -259,8 +260,8 @@ class Executor:
 
     # ------------------------------------------------------------------ chains
 
-    def _chain(self, part_idx: int, cnt: int) -> _Chain:
-        key = (part_idx, cnt)
+    def _chain(self, part_idx: int, cnt: int, flag: Optional[int] = None) -> _Chain:
+        key = (part_idx, cnt, flag)
         ch = self._chains.get(key)
         if ch is not None:
             return ch
@@ -284,6 +285,7 @@ class Executor:
             x = model[i](x, ctx)
             for node, fl in model[i].gemm_node_flops(cnt):
                 ch.gemm_flops[before + node] = fl
+            ch.seg_ends.append(ctx.node)  # one gated graph segment per module
         # last node: the batch's output slice (role 2: destination + out_off)
         if part.hi == len(model):
             # [CLS] rows of [cnt, s, h] gathered straight into the pinned results
@@ -293,6 +295,11 @@ class Executor:
             native.call("pf_chain_add_copy", ch.h, self._store_ptr(), cnt * s * h * 2, x.data_ptr(),
                         cnt * s * h * 2, cnt * s * h * 2, 1, 2)
         ch.finalize()
+        ch.seg_ends[-1] = len(ch.units)  # the output copy joins the last module's segment
+        native.call("pf_chain_set_desc", ch.h, self._desc.data_ptr())
+        native.call("pf_chain_set_stamps", ch.h, self._stamps.data_ptr())
+        base = self._ctl.data_ptr()
+        ch.build_graph(flag, base if flag else None, base + 4 * _CURSOR0 if flag else None, base + 4)
         self._chains[key] = ch
         return ch
 
@@ -301,6 +308,19 @@ class Executor:
         for ch in self._chains.values():
             ch.close()
         self._chains = {}
+
+    def prewarm(self, flag_ptr: Optional[int] = None) -> None:
+        """Record the current partition's chains and graphs for the plan's batch sizes
+        now — when the Coordinator hands over the WorkItem — instead of at the first
+        bubble, where recording would eat into the bubble."""
+        if flag_ptr is not None:
+            self._last_flag = flag_ptr or None
+        if self.item is None or self.progress.finished:
+            return
+        pidx = self.progress.part
+        for e in self.plan.partitions[pidx].per_bubble:
+            if e.num_batches:
+                self._chain(pidx, e.batch_size, self._last_flag)
 
     # ------------------------------------------------------------------ bubbles
 
@@ -342,7 +362,24 @@ class Executor:
         abort_ptr, done_ptr = base, base + 4
         cursors = base + 4 * _CURSOR0
         flag = slot.flag_ptr or None
+        self._last_flag = flag
         launches = 0
+        # device batch descriptors: batch k of this bubble reads its input / output slice
+        # offsets from desc[k] (k = the bubble's done counter when it starts)
+        dh = self._desc_host.tensor
+        for k, (first, cnt, node) in enumerate(batches):
+            if part.lo == 0:
+                dh[k, 0] = first * s * 4
+            else:
+                dh[k, 0] = first * s * h * 2
+            dh[k, 1] = first * h * 2 if part.hi == len(self.model) else first * s * h * 2
+            if node == 0:
+                self.h2d_bytes += cnt * s * 4 if part.lo == 0 else (
+                    cnt * s * h * 2 if self._store_host is not None else 0)
+            if part.hi == len(self.model):
+                self.d2h_bytes += cnt * h * 2
+            elif self._store_host is not None:
+                self.d2h_bytes += cnt * s * h * 2
         with torch.cuda.stream(st):
             if slot.start_event is not None:
                 st.wait_event(slot.start_event)
@@ -352,27 +389,18 @@ class Executor:
             if pr.resume_zero is not None:
                 self._ctl[_CURSOR0 + pr.resume_zero] = 0
                 pr.resume_zero = None
+            native.call("pf_stage_h2d", self._desc.data_ptr(), self._desc_host.ptr,
+                        16 * len(batches), st.cuda_stream)
             native.call("pf_read_globaltimer", base + 32, st.cuda_stream)
             for first, cnt, node in batches:
-                ch = self._chain(pr.part, cnt)
-                ch.set_timing(self.timing and bool(ch.gemm_flops))
-                if part.lo == 0:
-                    in_off = first * s * 4
-                    self.h2d_bytes += cnt * s * 4 if node == 0 else 0
+                ch = self._chain(pr.part, cnt, flag)
+                if node > 0:  # resume a yielded batch at its first incomplete node
+                    native.call("pf_chain_launch", ch.h, flag, abort_ptr if flag else None,
+                                cursors if flag else None, done_ptr, node, 0, 0, st.cuda_stream)
+                    launches += len(ch.units) - node + 1
                 else:
-                    in_off = first * s * h * 2
-                    if self._store_host is not None and node == 0:
-                        self.h2d_bytes += cnt * s * h * 2
-                if part.hi == len(self.model):
-                    out_off = first * h * 2
-                    self.d2h_bytes += cnt * h * 2
-                else:
-                    out_off = first * s * h * 2
-                    if self._store_host is not None:
-                        self.d2h_bytes += cnt * s * h * 2
-                native.call("pf_chain_launch", ch.h, flag, abort_ptr if flag else None,
-                            cursors if flag else None, done_ptr, node, in_off, out_off, st.cuda_stream)
-                launches += len(ch.units) - node + (1 if node == 0 else 0) + 1
+                    native.call("pf_chain_graph_launch", ch.h, st.cuda_stream)
+                    launches += len(ch.units) + len(ch.seg_ends) + 2
             native.call("pf_read_globaltimer", base + 40, st.cuda_stream)
             launches += 2
         ev = torch.cuda.Event()
@@ -401,10 +429,19 @@ class Executor:
         rec = BubbleRecord(pend.slot.index, len(pend.batches), done, 0, aborted, int(ts[0]), int(ts[1]),
                            pend.launches, pend.part, self._flops_frac[pend.part], tag=pend.slot.tag)
         if self.timing and done > 0 and not aborted:
-            last_cnt = pend.batches[min(done, len(pend.batches)) - 1][1]
-            ch = self._chains.get((pend.part, last_cnt))
-            if ch is not None and ch.timing:
-                self.gemm_samples.extend(ch.gemm_times())
+            # in-kernel stamps of the bubble's last batch: (FLOPs, ms) of every GEMM node
+            last_cnt = pend.batches[len(pend.batches) - 1][1]
+            ch = self._chains.get((pend.part, last_cnt, pend.slot.flag_ptr or None))
+            if ch is not None and ch.gemm_flops:
+                n = len(ch.units)
+                native.call("pf_stage_d2h", self._stamps_host.ptr, self._stamps.data_ptr(), 16 * n,
+                            self.stream.cuda_stream)
+                self.stream.synchronize()
+                sh = self._stamps_host.tensor
+                for node, fl in ch.gemm_flops.items():
+                    t0, t1 = int(sh[node, 0]), int(sh[node, 1])
+                    if 0 < t0 < t1:
+                        self.gemm_samples.append((fl, (t1 - t0) / 1e6))
         n_total = self.item.entry.size
         samples = 0
         for k, (first, cnt, node) in enumerate(pend.batches):
@@ -415,7 +452,7 @@ class Executor:
                 else:
                     pr.next_sample = max(pr.next_sample, first + cnt)
             elif k == done and aborted:
-                ch = self._chains[(pend.part, cnt)]
+                ch = self._chains[(pend.part, cnt, pend.slot.flag_ptr or None)]
                 cur = w[_CURSOR0:_CURSOR0 + len(ch.units)]
                 resume_node = len(ch.units)
                 for j, (u, _) in enumerate(ch.units):
@@ -445,6 +482,7 @@ class Executor:
                 pr.part += 1
                 pr.next_sample = 0
                 self._stage_partition(pr.part)
+                self.prewarm()
         self.records.append(rec)
         return rec
 

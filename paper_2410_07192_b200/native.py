@@ -125,6 +125,10 @@ _SIGNATURES: dict[str, tuple] = {
                                   c_int]),
     "pf_chain_size": (c_int, [c_void_p, POINTER(c_int)]),
     "pf_chain_set_timing": (c_int, [c_void_p, c_int]),
+    "pf_chain_set_desc": (c_int, [c_void_p, c_void_p]),
+    "pf_chain_set_stamps": (c_int, [c_void_p, c_void_p]),
+    "pf_chain_build_graph": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, POINTER(c_int), c_int]),
+    "pf_chain_graph_launch": (c_int, [c_void_p, c_void_p]),
     "pf_chain_node_elapsed": (c_int, [c_void_p, c_int, POINTER(c_float)]),
     "pf_chain_node_info": (c_int, [c_void_p, c_int, POINTER(c_uint32), POINTER(c_int)]),
     "pf_chain_launch": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int64,
