@@ -491,8 +491,13 @@ def main() -> None:
             "gpu_launches": int(tot.launches),
             "clocks": clocks.summary(),
             "result_checksum": checksum,
-            "main_job_losses": ({"fill_off": losses_off, "fill_on": losses,
-                                 "identical": losses_off == losses} if losses else None),
+            "main_job_losses": ({"fill_off": losses_off[-8:], "fill_on": losses[-8:],
+                                 "identical": losses_off == losses,
+                                 "max_rel_diff": max(abs(a - b) / max(abs(a), 1e-12)
+                                                     for a, b in zip(losses_off, losses)),
+                                 "note": "main job run with nondeterministic torch kernels (flash "
+                                         "SDPA); bitwise equality under deterministic settings is "
+                                         "tests/test_pipeline_nccl_gpu.py"} if losses else None),
         }
         text = json.dumps(line)
         print(text, flush=True)

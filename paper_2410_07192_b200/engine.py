@@ -124,24 +124,20 @@ class GPTStage(nn.Module):
         self.opt.zero_grad(set_to_none=False)
 
     def snapshot(self) -> dict:
-        """Device copies of parameters and optimizer state (to replay iterations)."""
+        """Device copies of parameters and the full optimizer state (to replay iterations)."""
+        import copy
+
         torch.cuda.synchronize()
         params = [p.detach().clone() for p in self.parameters()]
-        opt = {id(p): {k: (v.clone() if torch.is_tensor(v) else v) for k, v in st.items()}
-               for p, st in self.opt.state.items()}
-        return {"params": params, "opt": opt}
+        return {"params": params, "opt": copy.deepcopy(self.opt.state_dict())}
 
     def restore(self, snap: dict) -> None:
         torch.cuda.synchronize()
         with torch.no_grad():
             for p, q in zip(self.parameters(), snap["params"]):
                 p.copy_(q)
-            for p, st in self.opt.state.items():
-                for k, v in snap["opt"].get(id(p), {}).items():
-                    if torch.is_tensor(v):
-                        st[k].copy_(v)
-                    else:
-                        st[k] = v
+        self.opt.state.clear()
+        self.opt.load_state_dict(snap["opt"])
         self.opt.zero_grad(set_to_none=False)
         torch.cuda.synchronize()
 
