@@ -370,6 +370,19 @@ def main() -> None:
                 if rep:
                     off.setdefault(s_, []).append(t["main_end"] - t["start"])
 
+        # executables of every stage the timed steps visit are built now (arena layout,
+        # weight staging, graph recording), as the Coordinators would at admission
+        for k in range(args.warmup, n_total):
+            s_ = (rank + k * world) % P_STAGES
+            eng_ = engine_for(s_)
+            items["stage"], items["item"] = s_, None
+            nxt = next_work()
+            if nxt is not None:
+                executor.load(*nxt)
+            executor.prewarm(eng_.words.flag.value)
+        items["stage"] = None
+        torch.cuda.synchronize()
+
         # fill-on: warmup, then the timed steps
         for k in range(args.warmup):
             run_step(k, fill=True)

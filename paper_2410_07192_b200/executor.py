@@ -163,21 +163,47 @@ class Executor:
         self._layout_key = None
         self._flops_frac: list[float] = []
         self._last_flag: Optional[int] = None
+        self._dev_views: dict[int, dict] = {}
+        # executable cache: arena layouts of other (model, plan) pairs kept resident, so a
+        # worker switching between jobs or stages does not re-stage weights or re-record
+        self._layouts: dict[tuple, dict] = {}
 
     # ------------------------------------------------------------------ loading
 
+    _LAYOUT_ATTRS = ("_ctl", "_desc", "_stamps", "_wregion", "ws", "ids_dev", "_cap", "_ids_host",
+                     "_results", "_store_dev", "_store_host", "_flops_frac", "_staged_part",
+                     "_staged_event", "_chains", "model", "plan", "_dev_views")
+
+    def _save_layout(self) -> None:
+        if self._layout_key is not None:
+            self._layouts[self._layout_key] = {a: getattr(self, a) for a in self._LAYOUT_ATTRS}
+
+    def _restore_layout(self, key: tuple) -> None:
+        saved = self._layouts.pop(key)
+        for a, v in saved.items():
+            setattr(self, a, v)
+        for i, dev in self._dev_views.items():  # module weight views of this layout
+            self.model[i].dev = dev
+        self._layout_key = key
+
     def load(self, item: WorkItem, model: FillSequential) -> None:
-        """Take a new WorkItem. The arena layout and recorded chains are kept when
-        the executable is unchanged (the Coordinator's `reuse`)."""
+        """Take a new WorkItem. The arena layout, staged weights and recorded graphs are
+        kept when the executable is unchanged (the Coordinator's `reuse`)
+        and cached for executables seen before."""
         if self.pending is not None:
             self.settle()
         n = item.entry.size
         cfg = model.cfg
         key = (id(model), id(item.plan))
         if key != self._layout_key or n > self._cap:
-            self.model, self.plan = model, item.plan
-            self._layout(max(n, self._cap))
-            self._layout_key = key
+            self._save_layout()
+            if key in self._layouts and n <= self._layouts[key]["_cap"]:
+                self._restore_layout(key)
+            else:
+                self._layouts.pop(key, None)
+                self.model, self.plan = model, item.plan
+                self._layout(n)
+                self._layout_key = key
         self.item = item
         self.progress = _Progress()
         self._ids_host.tensor[:n].copy_(
@@ -186,12 +212,26 @@ class Executor:
         self.prewarm()
 
     def _layout(self, cap: int) -> None:
+        """Carve a new executable's region out of the arena; when the arena is full,
+        evict every cached executable and start over."""
+        try:
+            self._carve(cap)
+        except native.ArenaExhausted:
+            for saved in self._layouts.values():
+                for ch in saved["_chains"].values():
+                    ch.close()
+            self._layouts = {}
+            self._chains = {}
+            self.stream.synchronize()  # the arena is about to be re-carved
+            self.copy_stream.synchronize()
+            self.arena.reset()
+            self._carve(cap)
+
+    def _carve(self, cap: int) -> None:
         """Arena: control block | weight region (largest partition) | workspace | store."""
         plan, model, cfg = self.plan, self.model, self.model.cfg
-        self._drop_chains()
-        self.stream.synchronize()  # the arena is about to be re-carved
-        self.copy_stream.synchronize()
-        self.arena.reset()
+        self._chains = {}
+        self._dev_views = {}
         self._ctl = self.arena.alloc((_CTL_WORDS,), torch.int32)
         self._ctl.zero_()
         self._desc = self.arena.alloc((MAX_BATCHES, 2), torch.int64)
@@ -250,11 +290,13 @@ class Executor:
                         nel *= s_
                     mod.dev[name] = dflat[off:off + nel].view(*shape)
                     off += nel
+                self._dev_views[i] = mod.dev
                 ptr += _pad256(nbytes)
         ev = torch.cuda.Event()
         ev.record(self.copy_stream)
         self._staged_event = ev
         self._staged_part = part
+        self._dev_views = {i: self._dev_views[i] for i in range(p.lo, p.hi)}
         # recorded chains point at the previous partition's weights: drop them
         self._drop_chains()
 
@@ -494,6 +536,10 @@ class Executor:
         self.settle()
         torch.cuda.synchronize()
         self._drop_chains()
+        for saved in self._layouts.values():
+            for ch in saved["_chains"].values():
+                ch.close()
+        self._layouts = {}
         self.arena.close()
 
 
