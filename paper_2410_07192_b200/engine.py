@@ -173,6 +173,7 @@ class IterationRecord:
     anchor_off_ns: int  # nominal iteration start relative to the anchor
     end_stamp: int  # index into stamps: end of the last main-job op
     anchor_stamp: int = -1  # index into stamps holding the anchor this iteration used
+    epoch: int = 0  # stamp-buffer generation (stamp indices repeat after reset_stamps)
     bubbles: list[tuple[int, int, int]] = field(default_factory=list)  # (kind, set idx, clear idx)
 
 
@@ -228,6 +229,7 @@ class StageEngine:
         self.outputs: list[torch.Tensor] = []
         self.launches = 0  # our kernels (timer / stamp / flag) enqueued by the engine
         self._anchor_stamp = -1
+        self.epoch = 0
 
     def set_anchor(self, lead_ms: float = 5.0) -> None:
         """Anchor = device time now + lead (host enqueues ahead within the lead)."""
@@ -243,7 +245,7 @@ class StageEngine:
     def run_iteration(self, it: int, fill: bool, keep_outputs: bool = False) -> IterationRecord:
         cfg = self.cfg
         base = it * cfg.period_us * US
-        rec = IterationRecord(it, self.stage, base, -1, self._anchor_stamp)
+        rec = IterationRecord(it, self.stage, base, -1, self._anchor_stamp, self.epoch)
         prev_end_us = None
         main, comm = self.main, self.comm
         flag = self.words.flag.value
@@ -265,7 +267,7 @@ class StageEngine:
                 kind = 0 if ins.kind is BubbleKind.FWD_BWD else 1
                 rec.bubbles.append((kind, set_idx, clear_idx))
                 if fill and self.executor is not None:
-                    self.executor.fill(BubbleSlot(kind, start_ev, flag, tag=(id(self), clear_idx)))
+                    self.executor.fill(BubbleSlot(kind, start_ev, flag, tag=self._tag(clear_idx)))
                 main.wait_event(end_ev)
                 prev_end_us = end_us
                 continue
@@ -299,7 +301,7 @@ class StageEngine:
         st = self.words.stamps
         start = int(st[rec.anchor_stamp]) + rec.anchor_off_ns
         end = int(st[rec.end_stamp])
-        bubbles = [(kind, int(st[si]), int(st[ci]), (id(self), ci)) for kind, si, ci in rec.bubbles]
+        bubbles = [(kind, int(st[si]), int(st[ci]), (id(self), rec.epoch, ci)) for kind, si, ci in rec.bubbles]
         last = max([end] + [b[2] for b in bubbles])
         return {"start": start, "main_end": end, "step_end": last, "bubbles": bubbles}
 
@@ -307,6 +309,11 @@ class StageEngine:
         torch.cuda.synchronize()
         self.words.n = 0
         self.records = []
+        self.epoch += 1
+
+    def _tag(self, clear_idx: int) -> tuple:
+        """Unique id of a bubble: (engine, stamp-buffer generation, stamp index)."""
+        return (id(self), self.epoch, clear_idx)
 
 
 def measure_stage_times(model: GPTStage, reps: int = 5, warmup: int = 2) -> tuple[float, float]:
@@ -386,6 +393,7 @@ class NcclPipelineEngine:
         self._inflight: list = []  # (work, tensor) kept alive until the iteration is synced
         self._prefetched: Optional[tuple[torch.Tensor, torch.cuda.Event]] = None
         self._anchor_stamp = -1
+        self.epoch = 0
 
     # ---- P2P helpers (comm stream) ------------------------------------------------
     def _recv(self, src: int, group) -> tuple[torch.Tensor, torch.cuda.Event]:
@@ -431,7 +439,7 @@ class NcclPipelineEngine:
         k = 0 if kind is BubbleKind.FWD_BWD else 1
         rec.bubbles.append((k, set_idx, clear_idx))
         if fill and self.executor is not None:
-            self.executor.fill(BubbleSlot(k, start_ev, flag, tag=(id(self), clear_idx)))
+            self.executor.fill(BubbleSlot(k, start_ev, flag, tag=self._tag(clear_idx)))
         self.main.wait_event(end_ev)
         return got
 
@@ -445,7 +453,7 @@ class NcclPipelineEngine:
         """One training iteration of this stage; `last` = no next iteration (no
         trailing fill-drain bubble, whose end would be the next iteration's recv)."""
         s, p = self.stage, self.world
-        rec = IterationRecord(it, s, 0, -1, self._anchor_stamp)
+        rec = IterationRecord(it, s, 0, -1, self._anchor_stamp, self.epoch)
         pending_grad: dict[int, tuple[torch.Tensor, torch.cuda.Event]] = {}
         for idx, ins in enumerate(self.prog):
             if ins.op == "BUBBLE":
@@ -502,7 +510,7 @@ class NcclPipelineEngine:
         st = self.words.stamps
         start = int(st[rec.anchor_stamp])
         end = int(st[rec.end_stamp])
-        bubbles = [(kind, int(st[si]), int(st[ci]), (id(self), ci)) for kind, si, ci in rec.bubbles]
+        bubbles = [(kind, int(st[si]), int(st[ci]), (id(self), rec.epoch, ci)) for kind, si, ci in rec.bubbles]
         last = max([end] + [b[2] for b in bubbles])
         return {"start": start, "main_end": end, "step_end": last, "bubbles": bubbles,
                 "stage": self.stage}
@@ -511,3 +519,7 @@ class NcclPipelineEngine:
         self.sync()
         self.words.n = 0
         self.records = []
+        self.epoch += 1
+
+    def _tag(self, clear_idx: int) -> tuple:
+        return (id(self), self.epoch, clear_idx)
