@@ -13,7 +13,13 @@ the bubbles are real idle windows of a real main-job iteration. Step k runs one
 main-job iteration of stage (rank + k*N) mod 8, cycling through the pipeline. One
 step = one iteration with both of its bubbles filled.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c1|c2|c3]
+
+`--config` picks the BASELINE.json configuration (default c2 = configs[1], the
+headline): c1 = 4-stage 1F1B GPT-2-small main job + BERT-base bs-32 fill (configs[0]);
+c3 = 8-stage GPipe + a BERT-large fill whose weights exceed the bubble free memory
+(arena capped at 320 MB -> a multi-partition plan, weights staged host->HBM per
+partition, activations offloaded to pinned host memory between partitions).
 
 Rank 0 prints ONE JSON line. `value` is device-timed (%globaltimer stamps of the
 iterations, max over ranks); `e2e` is host wall clock around the same steps
@@ -36,9 +42,23 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "fill-job samples/s in bubbles at ≤2% main-job slowdown; % bubble time filled"
-P_STAGES = 8
-M_MICRO = 8
 FILL_BATCH_SIZES = (8, 16, 32, 64, 128)
+CONFIGS = {
+    # BASELINE.json configs[1] (headline)
+    "c2": {"stages": 8, "micro": 8, "schedule": "1f1b", "main": "gpt8b", "fill": "bert_large",
+           "batch_sizes": FILL_BATCH_SIZES, "arena_cap": 24 << 30, "chunk": 16384, "rotate": True},
+    # configs[0]: the reference's CPU-runnable case, on the GPU
+    "c1": {"stages": 4, "micro": 8, "schedule": "1f1b", "main": "gpt2small", "fill": "bert_base",
+           "batch_sizes": (32,), "arena_cap": 24 << 30, "chunk": 16384, "rotate": True},
+    # configs[2]: fill weights (0.67 GB) exceed the bubble free memory given to the fill job.
+    # A rank stays on one stage ((rank + 3) mod 8: stage 3 at N=1 has both bubble kinds)
+    # so a range progresses through the plan's partitions across iterations.
+    "c3": {"stages": 8, "micro": 8, "schedule": "gpipe", "main": "gpt8b", "fill": "bert_large",
+           "batch_sizes": FILL_BATCH_SIZES, "arena_cap": 320 << 20, "chunk": 4096, "rotate": False,
+           # Coordinator(max_batches_per_bubble=...) (coordinator.py:78-86): the reference
+           # default 16 leaves 2/3 of a 100 ms GPipe bubble idle for a 5-layer partition
+           "max_batches": 64},
+}
 FILL_FRACTION = 0.95  # reference default 0.68 (V100 context-switch slack); B200 yields in us
 
 
@@ -96,6 +116,22 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
                 "reasons": reasons, "samples": len(self.rows)}
+
+
+def measure_h2d_gbs(nbytes: int = 256 << 20, reps: int = 5) -> float:
+    """Pinned host -> HBM copy bandwidth of this box (the staging roofline)."""
+    import torch
+
+    src = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    dst = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    dst.copy_(src, non_blocking=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        dst.copy_(src, non_blocking=True)
+    e1.record()
+    e1.synchronize()
+    return nbytes * reps / e0.elapsed_time(e1) / 1e6
 
 
 def dist_env():
@@ -169,8 +205,9 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--fill", default="bert_large", choices=("bert_large", "bert_base"))
-    ap.add_argument("--main", default="gpt8b", choices=("gpt8b", "gpt2small"))
+    ap.add_argument("--config", default="c2", choices=tuple(CONFIGS))
+    ap.add_argument("--fill", default=None, choices=("bert_large", "bert_base"))
+    ap.add_argument("--main", default=None, choices=("gpt8b", "gpt2small"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pipeline", default="emulated", choices=("emulated", "nccl"),
                     help="emulated: every rank runs stages of an 8-stage pipeline against artificial "
@@ -181,6 +218,9 @@ def main() -> None:
     ap.add_argument("--fill-fraction", type=float, default=FILL_FRACTION,
                     help="share of each bubble the planner may fill (reference default 0.68)")
     args = ap.parse_args()
+    conf = CONFIGS[args.config]
+    args.fill = args.fill or conf["fill"]
+    args.main = args.main or conf["main"]
     if args.impl == "reference":
         run_reference(args)
         return
@@ -204,6 +244,8 @@ def main() -> None:
 
     native.require_device()
     peaks = load_peaks()
+    P_STAGES, M_MICRO = conf["stages"], conf["micro"]
+    sched = pf.ScheduleKind.GPIPE if conf["schedule"] == "gpipe" else pf.ScheduleKind.ONE_F_ONE_B
 
     # ---- main job and its measured stage timings
     gcfg = GPT_8B_STAGE if args.main == "gpt8b" else GPT2_SMALL_STAGE
@@ -213,24 +255,25 @@ def main() -> None:
     # ---- fill job: BERT with a B200-measured profile
     fcfg = BERT_LARGE if args.fill == "bert_large" else BERT_BASE
     fill_model = bert(fcfg, seed=0)
-    profile = measure_profile(fill_model, FILL_BATCH_SIZES)
+    profile = measure_profile(fill_model, conf["batch_sizes"])
     if args.save_profile and rank == 0:
         with open(args.save_profile, "w") as fh:
             fh.write(pf.model_to_json(profile) + "\n")
 
     # ---- bubble characterization: free memory with the main job at its peak
-    probe_cfg = pf.PipelineConfig(P_STAGES, M_MICRO, tf_ms, tb_ms, pf.ScheduleKind.ONE_F_ONE_B,
-                                  1, 1, args.fill_fraction)
-    probe = StageEngine(probe_cfg, 0, main_model, None)  # stage 0 holds the most activations
+    probe_cfg = pf.PipelineConfig(P_STAGES, M_MICRO, tf_ms, tb_ms, sched, 1, 1, args.fill_fraction)
+    _, hi_prio = torch.cuda.Stream.priority_range()
+    shared_streams = (torch.cuda.Stream(priority=hi_prio), torch.cuda.Stream(priority=hi_prio))
+    probe = StageEngine(probe_cfg, 0, main_model, None, streams=shared_streams)  # stage 0: most activations
     probe.set_anchor()
     probe.run_iteration(0, fill=False)
     torch.cuda.synchronize()
     free_b, total_b = torch.cuda.mem_get_info()
     reserved = torch.cuda.max_memory_reserved()
     free_mem = int(max(0, total_b - reserved - (4 << 30)) * 0.9)  # safety margin
-    arena_bytes = min(free_mem, 24 << 30)
-    pcfg = pf.PipelineConfig(P_STAGES, M_MICRO, tf_ms, tb_ms, pf.ScheduleKind.ONE_F_ONE_B,
-                             arena_bytes, arena_bytes, args.fill_fraction)
+    arena_bytes = min(free_mem, conf["arena_cap"])
+    pcfg = pf.PipelineConfig(P_STAGES, M_MICRO, tf_ms, tb_ms, sched, arena_bytes, arena_bytes,
+                             args.fill_fraction)
 
     executor = Executor(arena_bytes, job_seed=rank)
     coords: dict[int, pf.Coordinator] = {}
@@ -241,7 +284,9 @@ def main() -> None:
         if s not in coords:
             # the stage's Coordinator; a long-running fill job split into 16K-sample ranges
             coords[s] = pf.Coordinator(s, cycle or pf.build_bubble_cycle(cfg, s), 1,
-                                       pf.OrderingPolicy("concurrent", 16384))
+                                       pf.OrderingPolicy("concurrent", conf["chunk"]),
+                                       batch_sizes=list(conf["batch_sizes"]),
+                                       max_batches_per_bubble=conf.get("max_batches", 16))
             coords[s].admit(pf.JobSpec(f"fill-{s}", 0.0, profile, pf.JobKind.BATCH_INFERENCE, 10_000_000))
         return coords[s]
 
@@ -263,8 +308,8 @@ def main() -> None:
         tt = torch.tensor([tf_ms, tb_ms], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         tf_ms, tb_ms = tt.tolist()
-        pcfg = pf.PipelineConfig(world, M_MICRO, tf_ms, tb_ms, pf.ScheduleKind.ONE_F_ONE_B,
-                                 arena_bytes, arena_bytes, args.fill_fraction)
+        pcfg = pf.PipelineConfig(world, M_MICRO, tf_ms, tb_ms, sched, arena_bytes, arena_bytes,
+                                 args.fill_fraction)
         eng = NcclPipelineEngine(pcfg, main_model, executor)
         engines[rank] = eng
         items["stage"], items["item"] = rank, None
@@ -315,6 +360,7 @@ def main() -> None:
         executor.timing = True
         executor.gemm_samples = []
         n_rec0 = len(executor.records)
+        n_stage0 = len(executor.stagings)
         launches0 = executor.kernel_launches + eng.launches
         h2d0, d2h0 = executor.h2d_bytes, executor.d2h_bytes
         torch.cuda.synchronize()
@@ -335,12 +381,15 @@ def main() -> None:
     else:
         def engine_for(s: int) -> StageEngine:
             if s not in engines:
-                engines[s] = StageEngine(pcfg, s, main_model, executor)
+                engines[s] = StageEngine(pcfg, s, main_model, executor, streams=shared_streams)
                 coordinator_for(s, pcfg)
             return engines[s]
 
+        def stage_of(k: int) -> int:
+            return (rank + k * world) % P_STAGES if conf["rotate"] else (rank + 3) % P_STAGES
+
         def run_step(k: int, fill: bool, stage: int | None = None) -> dict:
-            s = (rank + k * world) % P_STAGES if stage is None else stage
+            s = stage_of(k) if stage is None else stage
             eng = engine_for(s)
             if fill and items.get("stage") != s:
                 if items.get("item") is not None and items.get("stage") is not None:
@@ -355,16 +404,23 @@ def main() -> None:
                 torch.cuda.synchronize()
             eng.reset_stamps()
             eng.set_anchor()
+            h0 = time.perf_counter()
             rec = eng.run_iteration(0, fill=fill)
+            h1 = time.perf_counter()
             if fill:
                 executor.settle()
             t = eng.record_timing(rec)
             t["stage"] = s
+            if args.debug:
+                ms = torch.cuda.memory_stats()
+                print(f"[dbg] stage {s} fill={fill} host enqueue {1e3 * (h1 - h0):.1f} ms, "
+                      f"alloc retries {ms.get('num_alloc_retries', 0)}, "
+                      f"reserved {torch.cuda.memory_reserved() / 2**30:.1f} GiB", file=sys.stderr)
             return t
 
         # fill-off iterations: the main job's own iteration time per stage (one
         # untimed + one timed iteration of every stage the timed fill-on steps visit)
-        for s_ in sorted({(rank + k * world) % P_STAGES for k in range(args.warmup, n_total)}):
+        for s_ in sorted({stage_of(k) for k in range(args.warmup, n_total)}):
             for rep in range(2):
                 t = run_step(s_, fill=False, stage=s_)
                 if rep:
@@ -373,7 +429,7 @@ def main() -> None:
         # executables of every stage the timed steps visit are built now (arena layout,
         # weight staging, graph recording), as the Coordinators would at admission
         for k in range(args.warmup, n_total):
-            s_ = (rank + k * world) % P_STAGES
+            s_ = stage_of(k)
             eng_ = engine_for(s_)
             items["stage"], items["item"] = s_, None
             nxt = next_work()
@@ -389,6 +445,7 @@ def main() -> None:
         executor.timing = True
         executor.gemm_samples = []
         n_rec0 = len(executor.records)
+        n_stage0 = len(executor.stagings)
         launches0 = executor.kernel_launches + sum(e.launches for e in engines.values())
         h2d0, d2h0 = executor.h2d_bytes, executor.d2h_bytes
         if world > 1:
@@ -444,6 +501,10 @@ def main() -> None:
         device_s=sum(t["step_end"] - t["start"] for t in steps) / 1e9)
     gemm_launches = len(executor.gemm_samples)
     executor.timing = False
+    staging = executor.staging_stats(n_stage0)
+    h2d_peak = measure_h2d_gbs()
+    staging["h2d_peak_gbs"] = h2d_peak
+    staging["frac"] = staging["gbs"] / h2d_peak if staging["gbs"] else None
     tot = aggregate(stats, device=torch.device("cuda", local))  # summed work, max time over ranks
     value = tot.value
     e2e = tot.sample_equivalents / tot.wall_s if tot.wall_s > 0 else 0.0
@@ -465,17 +526,21 @@ def main() -> None:
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random-init weights, synthetic token ids / activations)",
             "config": {
-                "workload": (f"{pcfg.num_stages}-stage 1F1B GPT-style main job ({gcfg.layers} layers of "
+                "name": args.config,
+                "workload": (f"{pcfg.num_stages}-stage {conf['schedule'].upper()} GPT-style main job ({gcfg.layers} layers of "
                              f"h={gcfg.hidden} per stage; "
                              + ("one stage per GPU over NCCL P2P" if args.pipeline == "nccl" else
-                                "8B model, artificial neighbours: one emulated stage per GPU-step")
+                                f"{'8B' if args.main == 'gpt8b' else 'GPT-2-small'} model, artificial "
+                                "neighbours: one emulated stage per GPU-step")
                              + f") + {fcfg.name} batch-inference fill (seq {fcfg.seq})"),
                 "pipeline": args.pipeline,
                 "main_stage": {"hidden": gcfg.hidden, "layers": gcfg.layers, "ffn": gcfg.ffn,
                                "seq": gcfg.seq, "micro_batch": gcfg.micro_batch,
                                "microbatches": M_MICRO, "stages": pcfg.num_stages,
                                "t_fwd_ms": tf_ms, "t_bwd_ms": tb_ms},
-                "fill": {"model": fcfg.name, "seq_len": fcfg.seq, "profiled_batch_sizes": list(FILL_BATCH_SIZES),
+                "fill": {"model": fcfg.name, "seq_len": fcfg.seq, "profiled_batch_sizes": list(conf["batch_sizes"]),
+                         "range_chunk_samples": conf["chunk"],
+                         "max_batches_per_bubble": conf.get("max_batches", 16),
                          "fill_fraction": args.fill_fraction, "arena_bytes": arena_bytes,
                          "plans": {str(s): pf.plan_to_dict(c.executables[f"fill-{s}"]) for s, c in coords.items()}},
                 "stages_run": [t["stage"] for t in steps],
@@ -487,6 +552,7 @@ def main() -> None:
             "per_stage_iter_ms": {str(st): {"fill_off": statistics.mean(off.get(st, [0])) / 1e6,
                                             "fill_on": statistics.mean(v) / 1e6} for st, v in on_iter.items()},
             "bubble_characterization": characterization,
+            "weight_staging": staging,
             "bubbles_preempted": sum(1 for r in recs if r.aborted),
             "bubbles_filled": len(recs),
             "fill_sample_equivalents": tot.sample_equivalents,

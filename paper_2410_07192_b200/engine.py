@@ -205,14 +205,19 @@ class StageEngine:
     the executor (if any). Emulated-neighbour (TimerLink) version for 1 GPU."""
 
     def __init__(self, config: PipelineConfig, stage_id: int, model: GPTStage,
-                 executor: Optional[Executor] = None):
+                 executor: Optional[Executor] = None,
+                 streams: Optional[tuple[torch.cuda.Stream, torch.cuda.Stream]] = None):
         self.cfg = config
         self.stage = stage_id
         self.model = model
         self.executor = executor
         lo, hi = torch.cuda.Stream.priority_range()
-        self.main = torch.cuda.Stream(priority=hi)
-        self.comm = torch.cuda.Stream(priority=hi)
+        # engines that take turns on one GPU share (main, comm): the caching allocator
+        # keeps blocks per stream, so per-engine streams would each pin a full set of
+        # main-job activations
+        if streams is None:
+            streams = (torch.cuda.Stream(priority=hi), torch.cuda.Stream(priority=hi))
+        self.main, self.comm = streams
         self.words = DeviceWords()
         self.link = TimerLink(self.words, self.comm)
         c = model.c

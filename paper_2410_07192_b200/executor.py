@@ -167,12 +167,14 @@ class Executor:
         # executable cache: arena layouts of other (model, plan) pairs kept resident, so a
         # worker switching between jobs or stages does not re-stage weights or re-record
         self._layouts: dict[tuple, dict] = {}
+        # weight-partition stagings: (bytes, start event, end event) on the copy stream
+        self.stagings: list[tuple[int, torch.cuda.Event, torch.cuda.Event]] = []
 
     # ------------------------------------------------------------------ loading
 
-    _LAYOUT_ATTRS = ("_ctl", "_desc", "_stamps", "_wregion", "ws", "ids_dev", "_cap", "_ids_host",
+    _LAYOUT_ATTRS = ("_ctl", "_desc", "_stamps", "_region", "ws", "ids_dev", "_cap", "_ids_host",
                      "_results", "_store_dev", "_store_host", "_flops_frac", "_staged_part",
-                     "_staged_event", "_chains", "model", "plan", "_dev_views")
+                     "_staged_event", "_chains", "model", "plan", "_dev_views", "_part_layouts")
 
     def _save_layout(self) -> None:
         if self._layout_key is not None:
@@ -227,8 +229,22 @@ class Executor:
             self.arena.reset()
             self._carve(cap)
 
+    def _part_need(self, part: int) -> tuple[int, dict[str, int]]:
+        """Partition `part`'s weight bytes (256-B padded) and its workspace (elements) at
+        the largest batch size the plan gives it -- the peak the planner budgeted for it
+        (Σ weights + max transient, partition.py:143-150 / profiler._module_mem)."""
+        model, p = self.model, self.plan.partitions[part]
+        w = sum(_pad256(model[i].weight_bytes()) for i in range(p.lo, p.hi))
+        b = max([e.batch_size for e in p.per_bubble] + [1])
+        need = dict(model.workspace(p.lo, p.hi, b))
+        need["hidden"] = b * model.cfg.seq * model.cfg.hidden
+        return w, need
+
     def _carve(self, cap: int) -> None:
-        """Arena: control block | weight region (largest partition) | workspace | store."""
+        """Arena: control block | partition region | ids | store. The partition region
+        holds one partition at a time -- its weights, then its workspace -- and is sized
+        for the largest partition's weights + workspace, so every partition the planner
+        fit into the bubble free memory fits the arena."""
         plan, model, cfg = self.plan, self.model, self.model.cfg
         self._chains = {}
         self._dev_views = {}
@@ -236,16 +252,14 @@ class Executor:
         self._ctl.zero_()
         self._desc = self.arena.alloc((MAX_BATCHES, 2), torch.int64)
         self._stamps = self.arena.alloc((MAX_NODES, 2), torch.int64)
-        max_w = max(sum(_pad256(model[i].weight_bytes()) for i in range(p.lo, p.hi))
-                    for p in plan.partitions)
-        self._wregion = self.arena.alloc((max_w // 2,), torch.bfloat16)
+        region = 0
+        for k in range(len(plan.partitions)):
+            w, need = self._part_need(k)
+            region = max(region, w + sum(_pad256(2 * v) for v in need.values()))
+        self._region = self.arena.alloc((region // 2,), torch.bfloat16)
+        self._part_layouts: dict[int, tuple[dict, dict]] = {}
+        self.ws = {}
         bmax = max(e.batch_size for p in plan.partitions for e in p.per_bubble)
-        need: dict[str, int] = {}
-        for p in plan.partitions:
-            for k, v in model.workspace(p.lo, p.hi, bmax).items():
-                need[k] = max(need.get(k, 0), v)
-        need["hidden"] = bmax * cfg.seq * cfg.hidden
-        self.ws = {k: self.arena.alloc((v,), torch.bfloat16) for k, v in need.items()}
         self.ids_dev = self.arena.alloc((bmax, cfg.seq), torch.int32)
         self._cap = cap
         self._ids_host = PinnedBuffer((cap, cfg.seq), torch.int32)
@@ -259,46 +273,86 @@ class Executor:
                 self._store_dev = self.arena.alloc((cap * cfg.seq * cfg.hidden,), torch.bfloat16)
             else:
                 self._store_host = PinnedBuffer((cap, cfg.seq, cfg.hidden), torch.bfloat16)
-        total = sum(model[i].flops_per_sample() for i in range(len(model))) or 1.0
-        self._flops_frac = [sum(model[i].flops_per_sample() for i in range(p.lo, p.hi)) / total
-                            for p in plan.partitions]
+        # a batch through partition [lo, hi) counts as this share of a sample: the
+        # partition's share of the model's measured execution time (profile at the
+        # largest profiled batch size) when the model carries its profile, else of FLOPs
+        prof = getattr(model, "profile", None)
+        if prof is not None and len(prof.layers) == len(model):
+            b = max(prof.batch_sizes)
+            cost = [prof.layers[i].exec_time_ms[b] for i in range(len(model))]
+        else:
+            cost = [model[i].flops_per_sample() for i in range(len(model))]
+        total = sum(cost) or 1.0
+        self._flops_frac = [sum(cost[p.lo:p.hi]) / total for p in plan.partitions]
         self._staged_part = None
 
     def _store_ptr(self) -> int:
         return self._store_dev.data_ptr() if self._store_dev is not None else self._store_host.ptr
 
+    def _part_layout(self, part: int) -> tuple[dict, dict]:
+        """Device views of partition `part` inside the region: its modules' weights from
+        the region base, then its workspace. Pure pointer arithmetic and the same every
+        time the partition is resident, so its recorded chains stay valid across
+        stagings of other partitions."""
+        lay = self._part_layouts.get(part)
+        if lay is not None:
+            return lay
+        p = self.plan.partitions[part]
+        base = self._region.data_ptr()
+        ptr = base
+        views: dict[int, dict] = {}
+        for i in range(p.lo, p.hi):
+            mod = self.model[i]
+            nbytes = mod.weight_bytes()
+            dflat = device_view(ptr, (nbytes // 2,), torch.bfloat16)
+            dev, off = {}, 0
+            for name, shape, _ in mod.param_specs():
+                nel = 1
+                for s_ in shape:
+                    nel *= s_
+                dev[name] = dflat[off:off + nel].view(*shape)
+                off += nel
+            views[i] = dev
+            ptr += _pad256(nbytes)
+        _, need = self._part_need(part)
+        off = (ptr - base) // 2
+        ws: dict[str, torch.Tensor] = {}
+        for k, v in need.items():
+            ws[k] = self._region[off:off + v]
+            off += _pad256(2 * v) // 2
+        lay = (views, ws)
+        self._part_layouts[part] = lay
+        return lay
+
     def _stage_partition(self, part: int) -> None:
-        """Stage partition `part`'s weights into the weight region on the copy stream
-        (pinned cudaMemcpyAsync), after the fill stream drained the previous partition."""
+        """Stage partition `part`'s weights into the region on the copy stream (pinned
+        cudaMemcpyAsync), after the fill stream drained the previous partition; the
+        fill stream waits on the staging event before the partition's first batch."""
         if self._staged_part == part:
             return
         p = self.plan.partitions[part]
-        ptr = self._wregion.data_ptr()
+        views, ws = self._part_layout(part)
+        e0 = torch.cuda.Event(enable_timing=True)
+        staged = 0
         with torch.cuda.stream(self.copy_stream):
             self.copy_stream.wait_stream(self.stream)
+            e0.record(self.copy_stream)
             for i in range(p.lo, p.hi):
                 mod = self.model[i]
                 nbytes = mod.weight_bytes()
-                dflat = device_view(ptr, (nbytes // 2,), torch.bfloat16)
-                native.call("pf_stage_h2d", ptr, mod.host.ptr, nbytes, self.copy_stream.cuda_stream)
+                dst = next(iter(views[i].values())).data_ptr() if views[i] else 0
+                if nbytes:
+                    native.call("pf_stage_h2d", dst, mod.host.ptr, nbytes, self.copy_stream.cuda_stream)
                 self.h2d_bytes += nbytes
-                mod.dev = {}
-                off = 0
-                for name, shape, _ in mod.param_specs():
-                    nel = 1
-                    for s_ in shape:
-                        nel *= s_
-                    mod.dev[name] = dflat[off:off + nel].view(*shape)
-                    off += nel
-                self._dev_views[i] = mod.dev
-                ptr += _pad256(nbytes)
-        ev = torch.cuda.Event()
+                staged += nbytes
+                mod.dev = views[i]
+        ev = torch.cuda.Event(enable_timing=True)
         ev.record(self.copy_stream)
         self._staged_event = ev
         self._staged_part = part
-        self._dev_views = {i: self._dev_views[i] for i in range(p.lo, p.hi)}
-        # recorded chains point at the previous partition's weights: drop them
-        self._drop_chains()
+        self.stagings.append((staged, e0, ev))
+        self.ws = ws
+        self._dev_views = dict(views)
 
     # ------------------------------------------------------------------ chains
 
@@ -310,8 +364,21 @@ class Executor:
         model, cfg = self.model, self.model.cfg
         part = self.plan.partitions[part_idx]
         s, h = cfg.seq, cfg.hidden
+        views, ws = self._part_layout(part_idx)
+        resident = {i: getattr(model[i], "dev", None) for i in views}
+        for i, dev in views.items():  # record against the partition's region layout
+            model[i].dev = dev
+        try:
+            return self._record_chain(key, part, cnt, flag, ws)
+        finally:
+            for i, dev in resident.items():
+                model[i].dev = dev
+
+    def _record_chain(self, key: tuple, part, cnt: int, flag: Optional[int], ws: dict) -> _Chain:
+        model, cfg = self.model, self.model.cfg
+        s, h = cfg.seq, cfg.hidden
         ch = _Chain()
-        ctx = ExecContext(self.stream, self.ws, chain=ch.h)
+        ctx = ExecContext(self.stream, ws, chain=ch.h)
         # node 0: the batch's input slice (role 1: source + in_off)
         if part.lo == 0:
             native.call("pf_chain_add_copy", ch.h, self.ids_dev.data_ptr(), cnt * s * 4,
@@ -359,10 +426,10 @@ class Executor:
             self._last_flag = flag_ptr or None
         if self.item is None or self.progress.finished:
             return
-        pidx = self.progress.part
-        for e in self.plan.partitions[pidx].per_bubble:
-            if e.num_batches:
-                self._chain(pidx, e.batch_size, self._last_flag)
+        for pidx, part in enumerate(self.plan.partitions):  # every partition: switches record nothing
+            for e in part.per_bubble:
+                if e.num_batches:
+                    self._chain(pidx, e.batch_size, self._last_flag)
 
     # ------------------------------------------------------------------ bubbles
 
@@ -527,6 +594,17 @@ class Executor:
                 self.prewarm()
         self.records.append(rec)
         return rec
+
+    def staging_stats(self, since: int = 0) -> dict:
+        """H2D weight staging since `self.stagings[since]`: bytes, device ms (copy-stream
+        events around each partition's pinned copies) and GB/s."""
+        nbytes, ms = 0, 0.0
+        for b, e0, e1 in self.stagings[since:]:
+            e1.synchronize()
+            nbytes += b
+            ms += e0.elapsed_time(e1)
+        return {"stagings": len(self.stagings) - since, "bytes": nbytes, "ms": ms,
+                "gbs": nbytes / ms / 1e6 if ms > 0 else None}
 
     def results(self) -> torch.Tensor:
         """[N, hidden] bf16 CLS embeddings of the current range (host, pinned)."""

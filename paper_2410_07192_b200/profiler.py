@@ -89,8 +89,10 @@ def measure_profile(model: FillSequential, batch_sizes: Sequence[int], reps: int
         layers.append(LayerProfile(exec_time_ms=exec_ms, mem_bytes=mem, weight_bytes=w,
                                    flops_per_sample=flops))
     params = sum(model[i].weight_bytes() // 2 for i in range(len(model)))
-    return ModelProfile(name=name or f"{cfg.name}-infer-b200", layers=tuple(layers), param_count=params,
+    prof = ModelProfile(name=name or f"{cfg.name}-infer-b200", layers=tuple(layers), param_count=params,
                         kind_allowed=frozenset({JobKind.BATCH_INFERENCE}))
+    model.profile = prof  # the executor weighs partitions by measured time share
+    return prof
 
 
 def _module_flops(model: FillSequential, i: int) -> float:
