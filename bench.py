@@ -58,6 +58,13 @@ CONFIGS = {
            # Coordinator(max_batches_per_bubble=...) (coordinator.py:78-86): the reference
            # default 16 leaves 2/3 of a 100 ms GPipe bubble idle for a 5-layer partition
            "max_batches": 64},
+    # configs[4]: multi-job queue -- Placer (avg-JCT routing) + per-stage SJF Coordinators,
+    # mixed BERT-base / BERT-large inference jobs, bubble free-memory cap sweep
+    "c5": {"stages": 8, "micro": 8, "schedule": "1f1b", "main": "gpt8b", "fill": "bert_large",
+           "batch_sizes": FILL_BATCH_SIZES, "caps_gb": (0.5, 1, 2, 4, 8), "max_batches": 64,
+           "jobs": (("bert_base", 8192, 0.0), ("bert_large", 4096, 0.0), ("bert_base", 2048, 0.5),
+                    ("bert_large", 8192, 1.0), ("bert_base", 4096, 1.5), ("bert_large", 2048, 2.0),
+                    ("bert_base", 16384, 3.0), ("bert_large", 1024, 4.0))},
 }
 FILL_FRACTION = 0.95  # reference default 0.68 (V100 context-switch slack); B200 yields in us
 
@@ -199,6 +206,147 @@ def run_reference(args) -> None:
 # --------------------------------------------------------------------------- our arm
 
 
+def run_service_sweep(args, conf) -> None:
+    """configs[4]: Placer + per-stage SJF Coordinators + one Executor per stage
+    (service.FillService), mixed BERT-base / BERT-large jobs, one run per bubble
+    free-memory cap. Stages of the 8-stage pipeline are time-multiplexed on this
+    GPU (artificial neighbours); each rank runs an independent replica."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2410_07192_b200 as pf
+    from paper_2410_07192_b200 import native
+    from paper_2410_07192_b200.coordinator import SJF
+    from paper_2410_07192_b200.engine import GPT2_SMALL_STAGE, GPT_8B_STAGE, GPTStage, StageEngine, measure_stage_times
+    from paper_2410_07192_b200.executor import Executor
+    from paper_2410_07192_b200.fillmodels import BERT_BASE, BERT_LARGE, bert
+    from paper_2410_07192_b200.profiler import measure_profile
+    from paper_2410_07192_b200.service import FillService, ServiceConfig, predict, write_report
+
+    native.require_device()
+    peaks = load_peaks()
+    P, M = conf["stages"], conf["micro"]
+    gcfg = GPT_8B_STAGE if args.main == "gpt8b" else GPT2_SMALL_STAGE
+    main_model = GPTStage(gcfg, seed=rank)
+    tf_ms, tb_ms = measure_stage_times(main_model)
+    registry, profiles = {}, {}
+    for name, fcfg in (("bert_base", BERT_BASE), ("bert_large", BERT_LARGE)):
+        m = bert(fcfg, seed=0)
+        prof = measure_profile(m, conf["batch_sizes"])
+        registry[prof.name], profiles[name] = m, prof
+    _, hi_prio = torch.cuda.Stream.priority_range()
+    streams = (torch.cuda.Stream(priority=hi_prio), torch.cuda.Stream(priority=hi_prio))
+    pcfg = pf.PipelineConfig(P, M, tf_ms, tb_ms, pf.ScheduleKind.ONE_F_ONE_B, 1, 1, args.fill_fraction)
+    engines = [StageEngine(pcfg, s, main_model, None, streams=streams) for s in range(P)]
+    period_s = pcfg.period_us / 1e6
+    jobs = [pf.JobSpec(f"j{i}-{name}", a * period_s, profiles[name], pf.JobKind.BATCH_INFERENCE, n)
+            for i, (name, n, a) in enumerate(conf["jobs"])]
+
+    def iterate(s: int, fill: bool) -> dict:
+        eng = engines[s]
+        eng.reset_stamps()
+        eng.set_anchor()
+        rec = eng.run_iteration(0, fill=fill)
+        if fill:
+            eng.executor.settle()
+        t = eng.record_timing(rec)
+        t["stage"] = s
+        return t
+
+    off = {}
+    for s in range(P):
+        iterate(s, False)
+        t = iterate(s, False)
+        off[s] = t["main_end"] - t["start"]
+
+    out_dir = args.report_dir or os.path.join(ROOT, "gpurun_out", "c5_report")
+    rows, launches, dev_ns, sample_eq, on_iter = [], 0, 0, 0.0, {}
+    with ClockSampler(local) as clocks:
+        w0 = time.perf_counter()
+        for cap_gb in conf["caps_gb"]:
+            cap = int(cap_gb * 2**30)
+            ccfg = pf.PipelineConfig(P, M, tf_ms, tb_ms, pf.ScheduleKind.ONE_F_ONE_B, cap, cap, args.fill_fraction)
+            scfg = ServiceConfig(ccfg, "avg_jct", SJF, tuple(conf["batch_sizes"]), conf["max_batches"])
+            executors = [Executor(cap, job_seed=s) for s in range(P)]
+            steps = []
+
+            def run_iteration(s, ex):
+                engines[s].executor = ex
+                t = iterate(s, True)
+                steps.append(t)
+                return t
+
+            svc = FillService(scfg, registry, executors, run_iteration,
+                              flag_of=lambda s: engines[s].words.flag.value)
+            rep = svc.run(jobs, max_rounds=60)
+            pred = predict(scfg, jobs)
+            for jid, res in rep.per_job.items():
+                res.predicted_completion_s = pred.get(jid)
+            recs = [r for ex in executors for r in ex.records]
+            eq = sum(r.samples_done * r.model_fraction for r in recs)
+            ns = sum(t["step_end"] - t["start"] for t in steps)
+            launches += sum(ex.kernel_launches for ex in executors) + sum(e.launches for e in engines)
+            for t in steps:
+                on_iter.setdefault(t["stage"], []).append(t["main_end"] - t["start"])
+            sc = rep.scalars()
+            row = {"free_mem_gb": cap_gb, "sample_eq_per_s": eq / (ns / 1e9) if ns else 0.0,
+                   "iterations": len(steps), **{k: sc[k] for k in (
+                       "completed", "rejected", "unfinished", "avg_jct_s", "predicted_avg_jct_s", "p99_jct_s",
+                       "makespan_s", "bubble_time_filled", "recovered_tflops_active", "mean_rel_perf",
+                       "fill_samples_per_s")},
+                   "partitions": {j: len(c.executables[j].partitions) for c in svc.coordinators
+                                  for j in c.executables}}
+            rows.append(row)
+            dev_ns += ns
+            sample_eq += eq
+            write_report(os.path.join(out_dir, f"free_mem_{cap_gb}gb"), rep,
+                         {"free_mem_gb": cap_gb, "stages": P, "microbatches": M, "routing": "avg_jct",
+                          "ordering": "sjf", "sample_eq_per_s": row["sample_eq_per_s"]})
+            for ex in executors:
+                ex.close()
+            for e in engines:
+                e.executor = None
+        torch.cuda.synchronize()
+        w1 = time.perf_counter()
+    with open(os.path.join(out_dir, "sweep.json"), "w") as fh:
+        json.dump(rows, fh, indent=2)
+    slow = [statistics.mean(v) / off[s] - 1 for s, v in on_iter.items() if off.get(s)]
+    best = rows[-1]
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": best["sample_eq_per_s"], "unit": "samples/s", "n_gpus": world,
+            "steps": sum(r["iterations"] for r in rows), "warmup": 2 * P,
+            "ms_per_step": dev_ns / 1e6 / max(1, sum(r["iterations"] for r in rows)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init weights, synthetic token ids)",
+            "config": {"name": "c5", "workload": f"{P}-stage 1F1B {gcfg.hidden}-hidden main job, "
+                       "Placer(avg_jct) + per-stage SJF Coordinators, mixed BERT-base/BERT-large jobs, "
+                       "free-memory cap sweep (stages time-multiplexed on one GPU)",
+                       "jobs": [list(j) for j in conf["jobs"]], "caps_gb": list(conf["caps_gb"]),
+                       "max_batches_per_bubble": conf["max_batches"], "fill_fraction": args.fill_fraction,
+                       "t_fwd_ms": tf_ms, "t_bwd_ms": tb_ms},
+            "sweep": rows,
+            "main_job_slowdown": statistics.mean(slow) if slow else None,
+            "value_definition": "sample-equivalents/s over device time of the filled iterations at the "
+                                "largest free-memory cap",
+            "roofline": None, "cpu_baseline": None,
+            "e2e": {"value": sample_eq / (w1 - w0), "unit": "samples/s", "h2d_bytes_per_step": None,
+                    "d2h_bytes_per_step": None},
+            "gpu_launches": launches, "clocks": clocks.summary(), "report_dir": out_dir,
+            "peaks_source": peaks["source"],
+        }
+        print(json.dumps(line), flush=True)
+        if args.out:
+            with open(args.out, "w") as fh:
+                fh.write(json.dumps(line) + "\n")
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -213,6 +361,7 @@ def main() -> None:
                     help="emulated: every rank runs stages of an 8-stage pipeline against artificial "
                          "neighbours; nccl: the N ranks ARE an N-stage pipeline (NCCL P2P over NVLink)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
+    ap.add_argument("--report-dir", default=None, help="c5: jobs.csv / summary.json per free-memory cap")
     ap.add_argument("--save-profile", default=None, help="write the measured fill ModelProfile JSON here")
     ap.add_argument("--debug", action="store_true", help="per-bubble details to stderr")
     ap.add_argument("--fill-fraction", type=float, default=FILL_FRACTION,
@@ -223,6 +372,9 @@ def main() -> None:
     args.main = args.main or conf["main"]
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.config == "c5":
+        run_service_sweep(args, conf)
         return
 
     import torch
