@@ -1,11 +1,10 @@
 """Expose this package under the reference's module names (``bubblefill.*``).
 
 ``install()`` registers ``bubblefill``, ``bubblefill.pipeline``, ``.workload``,
-``.partition``, ``.coordinator`` and ``.placer`` in ``sys.modules`` as aliases
-of this package's modules, so code (and the reference's own test-suite) written
-against ``bubblefill`` runs unchanged on the B200 build. Only the control-plane
-modules on the hot path are aliased; the reference's simulator, INI config and
-CLI are out of scope.
+``.partition``, ``.coordinator``, ``.placer`` and ``.sim`` in ``sys.modules`` as
+aliases of this package's modules, so code (and the reference's own test-suite)
+written against ``bubblefill`` runs unchanged on the B200 build. The reference's
+INI config loader and CLI are out of scope.
 """
 
 from __future__ import annotations
@@ -20,6 +19,7 @@ ALIASES = {
     "partition": "planner",
     "coordinator": "coordinator",
     "placer": "routing",
+    "sim": "sim",
 }
 
 
