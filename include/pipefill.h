@@ -122,6 +122,7 @@ int pf_copy2d(void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch, 
 #define PF_EPI_BIAS 1u     /* + bias[N]                                   */
 #define PF_EPI_GELU 2u     /* exact erf GELU (nn.GELU(approximate='none')) */
 #define PF_EPI_RESIDUAL 4u /* + residual[M,N] after the activation        */
+#define PF_EPI_RELU 8u     /* max(., 0) last (after bias and residual); not with GELU */
 
 /* Y[M,N] = epi(X[M,K] · W[N,K]^T): nn.Linear layout. tcgen05.mma (kind::f16,
  * fp32 accumulators in TMEM), TMA-fed 4-stage mbarrier pipeline, persistent CTAs,
@@ -161,6 +162,21 @@ int pf_embedding_ln(const int32_t* ids, const int32_t* type_ids, const void* wor
                     void* Y, int batch, int seq, int hidden, int vocab, float eps,
                     const pf_ctl_t* ctl, void* stream);
 
+/* ---- image kernels of convolutional fill jobs (ResNet-50), NHWC bf16 -------------
+ * A convolution = pf_im2col + pf_gemm (BatchNorm folded into the GEMM weights/bias,
+ * ReLU / residual in its epilogue). Col[B*Ho*Wo, Kp], column (ky*kw + kx)*C + c,
+ * zeros outside the image and in columns kh*kw*C..Kp; Kp % 8 == 0.
+ * Atomic work units; pf_image_units(kind 0 = im2col with out_elems = rows*Kp,
+ * kind 1 = pooling with out_elems = output pixels * C).                              */
+int pf_im2col(const void* X, void* Col, int B, int H, int W, int C, int kh, int kw, int stride,
+              int pad, int Kp, const pf_ctl_t* ctl, void* stream);
+/* k x k max pooling (padding never wins: -inf), C % 8 == 0.                           */
+int pf_maxpool(const void* X, void* Y, int B, int H, int W, int C, int k, int stride, int pad,
+               const pf_ctl_t* ctl, void* stream);
+/* Global average pooling X[B, HW, C] -> Y[B, C], fp32 sums.                            */
+int pf_avgpool(const void* X, void* Y, int B, int HW, int C, const pf_ctl_t* ctl, void* stream);
+int pf_image_units(int kind, long long out_elems, int C, uint32_t* out_units);
+
 /* ---- chain control ------------------------------------------------------------
  * Resets the per-node cursors of a chain when the chain has not been aborted
  * (a one-thread kernel: `if (!*abort) cursors[0..n) = 0`), and counts completed
@@ -198,6 +214,11 @@ int pf_chain_add_embedding_ln(pf_chain_t* chain, const int32_t* ids, const int32
                               int hidden, int vocab, float eps);
 int pf_chain_add_copy(pf_chain_t* chain, void* dst, int64_t dst_pitch, const void* src,
                       int64_t src_pitch, int64_t width, int64_t rows, int role);
+int pf_chain_add_im2col(pf_chain_t* chain, const void* X, void* Col, int B, int H, int W, int C,
+                        int kh, int kw, int stride, int pad, int Kp);
+int pf_chain_add_maxpool(pf_chain_t* chain, const void* X, void* Y, int B, int H, int W, int C,
+                         int k, int stride, int pad);
+int pf_chain_add_avgpool(pf_chain_t* chain, const void* X, void* Y, int B, int HW, int C);
 int pf_chain_size(pf_chain_t* chain, int* out_nodes);
 /* units = work units of the node; resumable = 1 for claimed-prefix nodes (GEMM tiles),
  * 0 for atomic nodes that are re-run whole (cursor must be reset to 0 first).       */

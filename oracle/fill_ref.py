@@ -11,7 +11,9 @@ is no golden vector for fill-job numerics. The semantics restated here are those
 the paper gives for the fill executor — an nn.Sequential run partition by
 partition over layer-index boundaries (partition.py:89-132) —
 with BERT's standard post-LN encoder layer (exact erf GELU, LayerNorm eps 1e-12,
-softmax attention in fp32). Tolerances (north star): bf16 path rel 2e-2 of this.
+softmax attention in fp32) and ResNet-50 v1.5 in inference form (BatchNorm folded
+into each convolution's weight and bias; torch.nn.functional.conv2d / max_pool2d /
+adaptive_avg_pool2d on NCHW fp32). Tolerances (north star): bf16 path rel 2e-2.
 
 Explicit ops only: no nn.TransformerEncoderLayer fast path, no SDPA.
 """
@@ -111,3 +113,49 @@ def run_sequential(modules: list, x, lo: int, hi: int):
     for i in range(lo, hi):
         x = modules[i](x)
     return x
+
+
+# ---------------------------------------------------------------------------- ResNet-50
+
+
+def conv_weight(w: torch.Tensor, cin: int, kh: int, kw: int) -> torch.Tensor:
+    """[Cout, Kp] GEMM weight, columns (ky*kw + kx)*Cin + c (pad columns dropped) ->
+    [Cout, Cin, kh, kw] conv2d weight."""
+    cout = w.shape[0]
+    return w[:, :kh * kw * cin].float().reshape(cout, kh, kw, cin).permute(0, 3, 1, 2).contiguous()
+
+
+def conv_bn(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor, k: int, stride: int, pad: int,
+            relu: bool, residual: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """NCHW fp32 conv with folded BN: relu(conv(x) + b [+ residual])."""
+    cin = x.shape[1]
+    y = torch.nn.functional.conv2d(x, conv_weight(w, cin, k, k), b.float(), stride=stride, padding=pad)
+    if residual is not None:
+        y = y + residual
+    return torch.relu(y) if relu else y
+
+
+def resnet_stem(img: torch.Tensor, p: dict) -> torch.Tensor:
+    """img NHWC -> NCHW fp32 after conv7x7/2 + BN + ReLU + maxpool 3x3/2."""
+    x = img.float().permute(0, 3, 1, 2)
+    y = conv_bn(x, p["w"], p["b"], 7, 2, 3, relu=True)
+    return torch.nn.functional.max_pool2d(y, 3, 2, 1)
+
+
+def bottleneck(x: torch.Tensor, p: dict, stride: int) -> torch.Tensor:
+    """NCHW fp32 bottleneck (v1.5: stride on the 3x3), projection shortcut when p has wd."""
+    t = conv_bn(x, p["w1"], p["b1"], 1, 1, 0, relu=True)
+    t = conv_bn(t, p["w2"], p["b2"], 3, stride, 1, relu=True)
+    sc = conv_bn(x, p["wd"], p["bd"], 1, stride, 0, relu=False) if "wd" in p else x
+    return conv_bn(t, p["w3"], p["b3"], 1, 1, 0, relu=True, residual=sc)
+
+
+def resnet_head(x: torch.Tensor, p: dict) -> torch.Tensor:
+    """NCHW fp32 -> logits [B, classes]: global average pool + fc."""
+    pooled = x.mean(dim=(2, 3))
+    return pooled @ p["fc_w"].float().T + p["fc_b"].float()
+
+
+def nhwc(x: torch.Tensor) -> torch.Tensor:
+    """NCHW -> NHWC (the executor's activation layout at partition boundaries)."""
+    return x.permute(0, 2, 3, 1).contiguous()

@@ -1,0 +1,293 @@
+// pf_conv.cu — HBM-bound image kernels of convolutional fill jobs (ResNet-50), NHWC bf16.
+//
+// A convolution runs as im2col -> tcgen05 GEMM (pf_gemm, bias/ReLU/residual fused in
+// its epilogue; BatchNorm folded into the GEMM's weights and bias). These kernels
+// are the data movement around it:
+//
+//   im2col    X[B,H,W,C] -> Col[B*Ho*Wo, Kp], column k = (ky*kw + kx)*C + c, zero
+//             outside the image and in the pad columns K..Kp (Kp % 8 == 0 for the
+//             GEMM's 16-B rows). C % 8 == 0: one 16-B vector per thread; the
+//             3-channel stem takes the scalar path.
+//   maxpool   k x k window, stride, zero-free padding (-inf outside), 8 channels/thread.
+//   avgpool   global mean over H*W -> [B, C], fp32 sums, 8 channels/thread.
+//
+// All three are "atomic" preemption units (gate on CTA entry, count on exit),
+// out-of-place and idempotent, like the norm kernels: an interrupted launch is
+// re-run whole. Every thread handles one 16-B output vector (or one scalar), so
+// a CTA is 256 vectors = 4 KB of output — a yield point every ~10 ns of HBM time.
+#include "pf_ops.h"
+
+namespace pf {
+namespace conv {
+
+constexpr int THREADS = 256;
+
+__global__ void __launch_bounds__(THREADS) im2col_vec_kernel(
+    const __nv_bfloat16* __restrict__ X, __nv_bfloat16* __restrict__ Col, int H, int W, int C,
+    int Ho, int Wo, int kw, int stride, int pad, int K, int Kp, long long total_vec, Ctl ctl) {
+  if (!atomic_unit_enter(ctl)) return;
+  const long long v = (long long)blockIdx.x * THREADS + threadIdx.x;
+  if (v < total_vec) {
+    const int vpr = Kp >> 3;  // vectors per Col row
+    const long long m = v / vpr;
+    const int k0 = (int)(v - m * vpr) << 3;
+    uint4 out = make_uint4(0, 0, 0, 0);
+    if (k0 < K) {
+      const int tap = k0 / C;
+      const int c0 = k0 - tap * C;
+      const int ky = tap / kw, kx = tap - (tap / kw) * kw;
+      const int ox = (int)(m % Wo);
+      const long long t = m / Wo;
+      const int oy = (int)(t % Ho);
+      const int b = (int)(t / Ho);
+      const int iy = oy * stride - pad + ky, ix = ox * stride - pad + kx;
+      if (iy >= 0 && iy < H && ix >= 0 && ix < W)
+        out = __ldg(reinterpret_cast<const uint4*>(X + (((size_t)b * H + iy) * W + ix) * C + c0));
+    }
+    *reinterpret_cast<uint4*>(Col + (size_t)m * Kp + k0) = out;
+  }
+  atomic_unit_exit(ctl);
+}
+
+__global__ void __launch_bounds__(THREADS) im2col_scalar_kernel(
+    const __nv_bfloat16* __restrict__ X, __nv_bfloat16* __restrict__ Col, int H, int W, int C,
+    int Ho, int Wo, int kw, int stride, int pad, int K, int Kp, long long total, Ctl ctl) {
+  if (!atomic_unit_enter(ctl)) return;
+  const long long e = (long long)blockIdx.x * THREADS + threadIdx.x;
+  if (e < total) {
+    const long long m = e / Kp;
+    const int k = (int)(e - m * Kp);
+    __nv_bfloat16 val = __float2bfloat16(0.f);
+    if (k < K) {
+      const int tap = k / C;
+      const int c = k - tap * C;
+      const int ky = tap / kw, kx = tap - (tap / kw) * kw;
+      const int ox = (int)(m % Wo);
+      const long long t = m / Wo;
+      const int oy = (int)(t % Ho);
+      const int b = (int)(t / Ho);
+      const int iy = oy * stride - pad + ky, ix = ox * stride - pad + kx;
+      if (iy >= 0 && iy < H && ix >= 0 && ix < W) val = X[(((size_t)b * H + iy) * W + ix) * C + c];
+    }
+    Col[e] = val;
+  }
+  atomic_unit_exit(ctl);
+}
+
+__global__ void __launch_bounds__(THREADS) maxpool_kernel(
+    const __nv_bfloat16* __restrict__ X, __nv_bfloat16* __restrict__ Y, int H, int W, int C,
+    int Ho, int Wo, int k, int stride, int pad, long long total_vec, Ctl ctl) {
+  if (!atomic_unit_enter(ctl)) return;
+  const long long v = (long long)blockIdx.x * THREADS + threadIdx.x;
+  if (v < total_vec) {
+    const int cv = C >> 3;
+    const int c0 = (int)(v % cv) << 3;
+    const long long pix = v / cv;
+    const int ox = (int)(pix % Wo);
+    const long long t = pix / Wo;
+    const int oy = (int)(t % Ho);
+    const int b = (int)(t / Ho);
+    float mx[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
+    for (int ky = 0; ky < k; ++ky) {
+      const int iy = oy * stride - pad + ky;
+      if (iy < 0 || iy >= H) continue;
+      for (int kx = 0; kx < k; ++kx) {
+        const int ix = ox * stride - pad + kx;
+        if (ix < 0 || ix >= W) continue;
+        float x[8];
+        load8(X + (((size_t)b * H + iy) * W + ix) * C + c0, x);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) mx[e] = fmaxf(mx[e], x[e]);
+      }
+    }
+    store8(Y + (size_t)pix * C + c0, mx);
+  }
+  atomic_unit_exit(ctl);
+}
+
+__global__ void __launch_bounds__(THREADS) avgpool_kernel(const __nv_bfloat16* __restrict__ X,
+                                                          __nv_bfloat16* __restrict__ Y, int HW,
+                                                          int C, long long total_vec, Ctl ctl) {
+  if (!atomic_unit_enter(ctl)) return;
+  const long long v = (long long)blockIdx.x * THREADS + threadIdx.x;
+  if (v < total_vec) {
+    const int cv = C >> 3;
+    const int c0 = (int)(v % cv) << 3;
+    const long long b = v / cv;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const __nv_bfloat16* base = X + (size_t)b * HW * C + c0;
+    for (int p = 0; p < HW; ++p) {
+      float x[8];
+      load8(base + (size_t)p * C, x);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += x[e];
+    }
+    const float inv = 1.f / (float)HW;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] *= inv;
+    store8(Y + (size_t)b * C + c0, acc);
+  }
+  atomic_unit_exit(ctl);
+}
+
+inline uint32_t blocks_for(long long n) { return (uint32_t)((n + THREADS - 1) / THREADS); }
+
+inline int out_dim(int in, int k, int stride, int pad) { return (in + 2 * pad - k) / stride + 1; }
+
+struct Im2colOp final : PreparedOp {
+  const __nv_bfloat16* x = nullptr;
+  __nv_bfloat16* col = nullptr;
+  int H = 0, W = 0, C = 0, Ho = 0, Wo = 0, kw = 0, stride = 1, pad = 0, K = 0, Kp = 0;
+  long long n = 0;  // vectors (C % 8 == 0) or elements
+  bool vec = true;
+  uint32_t units() const override { return blocks_for(n); }
+  bool resumable() const override { return false; }
+  int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
+    if (vec)
+      im2col_vec_kernel<<<units(), THREADS, 0, s>>>(x, col, H, W, C, Ho, Wo, kw, stride, pad, K, Kp, n,
+                                                   make_ctl(ctl));
+    else
+      im2col_scalar_kernel<<<units(), THREADS, 0, s>>>(x, col, H, W, C, Ho, Wo, kw, stride, pad, K, Kp,
+                                                      n, make_ctl(ctl));
+    PF_CUDA(cudaGetLastError());
+    return PF_OK;
+  }
+};
+
+struct MaxpoolOp final : PreparedOp {
+  const __nv_bfloat16* x = nullptr;
+  __nv_bfloat16* y = nullptr;
+  int H = 0, W = 0, C = 0, Ho = 0, Wo = 0, k = 0, stride = 1, pad = 0;
+  long long n = 0;
+  uint32_t units() const override { return blocks_for(n); }
+  bool resumable() const override { return false; }
+  int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
+    maxpool_kernel<<<units(), THREADS, 0, s>>>(x, y, H, W, C, Ho, Wo, k, stride, pad, n, make_ctl(ctl));
+    PF_CUDA(cudaGetLastError());
+    return PF_OK;
+  }
+};
+
+struct AvgpoolOp final : PreparedOp {
+  const __nv_bfloat16* x = nullptr;
+  __nv_bfloat16* y = nullptr;
+  int HW = 0, C = 0;
+  long long n = 0;
+  uint32_t units() const override { return blocks_for(n); }
+  bool resumable() const override { return false; }
+  int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
+    avgpool_kernel<<<units(), THREADS, 0, s>>>(x, y, HW, C, n, make_ctl(ctl));
+    PF_CUDA(cudaGetLastError());
+    return PF_OK;
+  }
+};
+
+static int check_ptrs(const void* a, const void* b, const char* who) {
+  if (!a || !b) return set_error(PF_ERR_INVALID, "%s: null pointer", who);
+  if (((uintptr_t)a | (uintptr_t)b) & 15u) return set_error(PF_ERR_INVALID, "%s: pointers must be 16-B aligned", who);
+  return PF_OK;
+}
+
+}  // namespace conv
+
+using bf = __nv_bfloat16;
+
+int make_im2col_op(OpPtr* out, const void* X, void* Col, int B, int H, int W, int C, int kh, int kw,
+                   int stride, int pad, int Kp) {
+  PF_TRY(conv::check_ptrs(X, Col, "pf_im2col"));
+  if (B <= 0 || H <= 0 || W <= 0 || C <= 0 || kh <= 0 || kw <= 0 || stride <= 0 || pad < 0)
+    return set_error(PF_ERR_INVALID, "pf_im2col: non-positive shape");
+  const int K = kh * kw * C;
+  if (Kp < K || Kp % 8 != 0) return set_error(PF_ERR_INVALID, "pf_im2col: need Kp >= kh*kw*C and Kp %% 8 == 0");
+  auto op = std::make_unique<conv::Im2colOp>();
+  op->x = reinterpret_cast<const bf*>(X);
+  op->col = reinterpret_cast<bf*>(Col);
+  op->H = H;
+  op->W = W;
+  op->C = C;
+  op->Ho = conv::out_dim(H, kh, stride, pad);
+  op->Wo = conv::out_dim(W, kw, stride, pad);
+  if (op->Ho <= 0 || op->Wo <= 0) return set_error(PF_ERR_INVALID, "pf_im2col: empty output");
+  op->kw = kw;
+  op->stride = stride;
+  op->pad = pad;
+  op->K = K;
+  op->Kp = Kp;
+  op->vec = C % 8 == 0;
+  const long long rows = (long long)B * op->Ho * op->Wo;
+  op->n = op->vec ? rows * (Kp / 8) : rows * Kp;
+  *out = std::move(op);
+  return PF_OK;
+}
+
+int make_maxpool_op(OpPtr* out, const void* X, void* Y, int B, int H, int W, int C, int k, int stride,
+                    int pad) {
+  PF_TRY(conv::check_ptrs(X, Y, "pf_maxpool"));
+  if (B <= 0 || H <= 0 || W <= 0 || C <= 0 || C % 8 != 0 || k <= 0 || stride <= 0 || pad < 0 || pad >= k)
+    return set_error(PF_ERR_INVALID, "pf_maxpool: bad shape (C %% 8 == 0, 0 <= pad < k)");
+  auto op = std::make_unique<conv::MaxpoolOp>();
+  op->x = reinterpret_cast<const bf*>(X);
+  op->y = reinterpret_cast<bf*>(Y);
+  op->H = H;
+  op->W = W;
+  op->C = C;
+  op->Ho = conv::out_dim(H, k, stride, pad);
+  op->Wo = conv::out_dim(W, k, stride, pad);
+  if (op->Ho <= 0 || op->Wo <= 0) return set_error(PF_ERR_INVALID, "pf_maxpool: empty output");
+  op->k = k;
+  op->stride = stride;
+  op->pad = pad;
+  op->n = (long long)B * op->Ho * op->Wo * (C / 8);
+  *out = std::move(op);
+  return PF_OK;
+}
+
+int make_avgpool_op(OpPtr* out, const void* X, void* Y, int B, int HW, int C) {
+  PF_TRY(conv::check_ptrs(X, Y, "pf_avgpool"));
+  if (B <= 0 || HW <= 0 || C <= 0 || C % 8 != 0)
+    return set_error(PF_ERR_INVALID, "pf_avgpool: bad shape (C %% 8 == 0)");
+  auto op = std::make_unique<conv::AvgpoolOp>();
+  op->x = reinterpret_cast<const bf*>(X);
+  op->y = reinterpret_cast<bf*>(Y);
+  op->HW = HW;
+  op->C = C;
+  op->n = (long long)B * (C / 8);
+  *out = std::move(op);
+  return PF_OK;
+}
+
+}  // namespace pf
+
+extern "C" int pf_im2col(const void* X, void* Col, int B, int H, int W, int C, int kh, int kw,
+                         int stride, int pad, int Kp, const pf_ctl_t* ctl, void* stream) {
+  PF_TRY(pf::validate_ctl(ctl));
+  pf::OpPtr op;
+  PF_TRY(pf::make_im2col_op(&op, X, Col, B, H, W, C, kh, kw, stride, pad, Kp));
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), pf::LaunchArgs{});
+}
+
+extern "C" int pf_maxpool(const void* X, void* Y, int B, int H, int W, int C, int k, int stride,
+                          int pad, const pf_ctl_t* ctl, void* stream) {
+  PF_TRY(pf::validate_ctl(ctl));
+  pf::OpPtr op;
+  PF_TRY(pf::make_maxpool_op(&op, X, Y, B, H, W, C, k, stride, pad));
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), pf::LaunchArgs{});
+}
+
+extern "C" int pf_avgpool(const void* X, void* Y, int B, int HW, int C, const pf_ctl_t* ctl,
+                          void* stream) {
+  PF_TRY(pf::validate_ctl(ctl));
+  pf::OpPtr op;
+  PF_TRY(pf::make_avgpool_op(&op, X, Y, B, HW, C));
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), pf::LaunchArgs{});
+}
+
+extern "C" int pf_image_units(int kind, long long out_elems, int C, uint32_t* out_units) {
+  // kind 0: im2col (out_elems = rows * Kp), 1: maxpool / avgpool (out_elems = pixels * C)
+  if (!out_units || out_elems <= 0 || C <= 0) return pf::set_error(PF_ERR_INVALID, "pf_image_units");
+  const bool vec = kind != 0 || C % 8 == 0;
+  *out_units = pf::conv::blocks_for(vec ? out_elems / 8 : out_elems);
+  return PF_OK;
+}

@@ -123,6 +123,7 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
   constexpr bool HAS_BIAS = (EPI & PF_EPI_BIAS) != 0;
   constexpr bool HAS_GELU = (EPI & PF_EPI_GELU) != 0;
   constexpr bool HAS_RES = (EPI & PF_EPI_RESIDUAL) != 0;
+  constexpr bool HAS_RELU = (EPI & PF_EPI_RELU) != 0;
   constexpr int COLS = CHUNKS * 32;
   const int lane = lane_id();
   const int row = row_base + lane;
@@ -211,11 +212,15 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
         }
       }
     }
-    // previous chunk's bulk store must have read the staging tile
-    if (c > 0) {
-      if (lane == 0) bulk_wait_read0();
-      __syncwarp();
+    if (HAS_RELU) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
     }
+    // the previous bulk store from this staging tile (previous chunk, or the last chunk
+    // of this warp's previous output tile: with a short K the next accumulator is ready
+    // before that store has read shared memory) must be done reading it
+    if (lane == 0) bulk_wait_read0();
+    __syncwarp();
     // row `lane` of the 32x32 tile = 4 x 16 B; TMA SWIZZLE_64B places 16-B chunk q of
     // row r at chunk q ^ ((r >> 1) & 3) (conflict-free: 8 distinct bank groups per phase)
 #pragma unroll
@@ -873,7 +878,7 @@ struct GemmPairOp final : PreparedOp {
     const int tiles = p.tiles_m * p.tiles_n;
     const int pairs = device_sm_count() / 2;
     grid = 2 * (tiles < pairs ? tiles : pairs);
-    epi = e & 7u;
+    epi = e & 15u;
     return PF_OK;
   }
   uint32_t units() const override { return (uint32_t)(p.tiles_m * p.tiles_n); }
@@ -889,7 +894,12 @@ struct GemmPairOp final : PreparedOp {
       case 4: return launch_pair_epi<BN, 4>(ta, tb, ty, p, grid, ctl, stream);
       case 5: return launch_pair_epi<BN, 5>(ta, tb, ty, p, grid, ctl, stream);
       case 6: return launch_pair_epi<BN, 6>(ta, tb, ty, p, grid, ctl, stream);
-      default: return launch_pair_epi<BN, 7>(ta, tb, ty, p, grid, ctl, stream);
+      case 7: return launch_pair_epi<BN, 7>(ta, tb, ty, p, grid, ctl, stream);
+      case 8: return launch_pair_epi<BN, 8>(ta, tb, ty, p, grid, ctl, stream);
+      case 9: return launch_pair_epi<BN, 9>(ta, tb, ty, p, grid, ctl, stream);
+      case 12: return launch_pair_epi<BN, 12>(ta, tb, ty, p, grid, ctl, stream);
+      case 13: return launch_pair_epi<BN, 13>(ta, tb, ty, p, grid, ctl, stream);
+      default: return set_error(PF_ERR_INVALID, "pf_gemm: unsupported epilogue");
     }
   }
 };
@@ -937,7 +947,7 @@ struct GemmOp final : PreparedOp {
     const int tiles = p.tiles_m * p.tiles_n;
     const int sms = device_sm_count();
     grid = tiles < sms ? tiles : sms;
-    epi = e & 7u;
+    epi = e & 15u;
     return PF_OK;
   }
   uint32_t units() const override { return (uint32_t)(p.tiles_m * p.tiles_n); }
@@ -953,7 +963,12 @@ struct GemmOp final : PreparedOp {
       case 4: return launch_epi<BN, 4>(ta, tb, ty, p, grid, ctl, stream);
       case 5: return launch_epi<BN, 5>(ta, tb, ty, p, grid, ctl, stream);
       case 6: return launch_epi<BN, 6>(ta, tb, ty, p, grid, ctl, stream);
-      default: return launch_epi<BN, 7>(ta, tb, ty, p, grid, ctl, stream);
+      case 7: return launch_epi<BN, 7>(ta, tb, ty, p, grid, ctl, stream);
+      case 8: return launch_epi<BN, 8>(ta, tb, ty, p, grid, ctl, stream);
+      case 9: return launch_epi<BN, 9>(ta, tb, ty, p, grid, ctl, stream);
+      case 12: return launch_epi<BN, 12>(ta, tb, ty, p, grid, ctl, stream);
+      case 13: return launch_epi<BN, 13>(ta, tb, ty, p, grid, ctl, stream);
+      default: return set_error(PF_ERR_INVALID, "pf_gemm: unsupported epilogue");
     }
   }
 };
@@ -969,6 +984,9 @@ int make_gemm_op(OpPtr* out, const void* X, const void* W, const void* bias, con
   if ((epilogue & PF_EPI_BIAS) && !bias) return set_error(PF_ERR_INVALID, "pf_gemm: bias is NULL");
   if ((epilogue & PF_EPI_RESIDUAL) && !residual)
     return set_error(PF_ERR_INVALID, "pf_gemm: residual is NULL");
+  if ((epilogue & PF_EPI_GELU) && (epilogue & PF_EPI_RELU))
+    return set_error(PF_ERR_INVALID, "pf_gemm: GELU and ReLU are exclusive");
+  if (epilogue & ~15u) return set_error(PF_ERR_INVALID, "pf_gemm: unknown epilogue bits");
   if (((uintptr_t)X | (uintptr_t)W | (uintptr_t)Y | (uintptr_t)bias | (uintptr_t)residual) & 15u)
     return set_error(PF_ERR_INVALID, "pf_gemm: pointers must be 16-B aligned");
   if (!device_is_sm100()) return set_error(PF_ERR_UNSUPPORTED, "pf_gemm: needs an sm_100 device");

@@ -17,50 +17,6 @@ constexpr int ROWS_PER_WARP = 2;
 constexpr int ROWS_PER_CTA = WARPS * ROWS_PER_WARP;
 constexpr int MAX_NV = 8;  // 8 vectors x 8 bf16 x 32 lanes = 2048 columns
 
-// Entry gate for atomic-unit kernels; returns false when the CTA must skip.
-__device__ __forceinline__ bool atomic_unit_enter(const Ctl& c) {
-  __shared__ int s_go;
-  if (threadIdx.x == 0) {
-    int go = 1;
-    if (chain_aborted(c)) go = 0;
-    else if (c.flag != nullptr && ld_acquire_u32(c.flag) == 0u) {
-      atomicExch(c.abort, 1u);
-      go = 0;
-    }
-    s_go = go;
-  }
-  __syncthreads();
-  return s_go != 0;
-}
-
-__device__ __forceinline__ void atomic_unit_exit(const Ctl& c) {
-  __syncthreads();
-  if (threadIdx.x == 0 && c.cursor != nullptr) {
-    __threadfence();
-    atomicAdd(c.cursor, 1u);
-  }
-}
-
-__device__ __forceinline__ void load8(const __nv_bfloat16* p, float* v) {
-  uint4 u = *reinterpret_cast<const uint4*>(p);
-  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-  for (int h = 0; h < 4; ++h) {
-    float2 f = unpack_bf16x2(w[h]);
-    v[2 * h] = f.x;
-    v[2 * h + 1] = f.y;
-  }
-}
-
-__device__ __forceinline__ void store8(__nv_bfloat16* p, const float* v) {
-  uint4 u;
-  u.x = pack_bf16x2(v[0], v[1]);
-  u.y = pack_bf16x2(v[2], v[3]);
-  u.z = pack_bf16x2(v[4], v[5]);
-  u.w = pack_bf16x2(v[6], v[7]);
-  *reinterpret_cast<uint4*>(p) = u;
-}
-
 // Normalise one row held as NV vectors of 8 per lane (vector j covers columns
 // (j*32 + lane)*8 .. +8), then write gamma/beta-scaled bf16.
 template <int NV, bool RMS>

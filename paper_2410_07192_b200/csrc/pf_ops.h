@@ -45,5 +45,10 @@ int make_attention_op(OpPtr* out, const void* QKV, const float* mask, void* O, i
 // role 2 adds out_off to dst. Any UVA addresses (HBM or mapped pinned host).
 int make_copy_op(OpPtr* out, void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch,
                  int64_t width, int64_t rows, int role);
+int make_im2col_op(OpPtr* out, const void* X, void* Col, int B, int H, int W, int C, int kh, int kw,
+                   int stride, int pad, int Kp);
+int make_maxpool_op(OpPtr* out, const void* X, void* Y, int B, int H, int W, int C, int k, int stride,
+                    int pad);
+int make_avgpool_op(OpPtr* out, const void* X, void* Y, int B, int HW, int C);
 
 }  // namespace pf

@@ -541,6 +541,26 @@ int pf_chain_add_softmax(pf_chain_t* c, const void* X, void* Y, int rows, int co
   return chain_push(c, pf::make_softmax_op(&op, X, Y, rows, cols, scale), op);
 }
 
+int pf_chain_add_im2col(pf_chain_t* c, const void* X, void* Col, int B, int H, int W, int C, int kh,
+                        int kw, int stride, int pad, int Kp) {
+  if (!c) return pf::set_error(PF_ERR_INVALID, "null chain");
+  pf::OpPtr op;
+  return chain_push(c, pf::make_im2col_op(&op, X, Col, B, H, W, C, kh, kw, stride, pad, Kp), op);
+}
+
+int pf_chain_add_maxpool(pf_chain_t* c, const void* X, void* Y, int B, int H, int W, int C, int k,
+                         int stride, int pad) {
+  if (!c) return pf::set_error(PF_ERR_INVALID, "null chain");
+  pf::OpPtr op;
+  return chain_push(c, pf::make_maxpool_op(&op, X, Y, B, H, W, C, k, stride, pad), op);
+}
+
+int pf_chain_add_avgpool(pf_chain_t* c, const void* X, void* Y, int B, int HW, int C) {
+  if (!c) return pf::set_error(PF_ERR_INVALID, "null chain");
+  pf::OpPtr op;
+  return chain_push(c, pf::make_avgpool_op(&op, X, Y, B, HW, C), op);
+}
+
 int pf_chain_add_attention(pf_chain_t* c, const void* QKV, const float* mask_add, void* O,
                            int batch, int seq, int heads, int head_dim, float scale) {
   if (!c) return pf::set_error(PF_ERR_INVALID, "null chain");

@@ -36,7 +36,7 @@ import torch
 from . import native
 from .arena import Arena, PinnedBuffer, device_view
 from .coordinator import WorkItem
-from .fillmodels import ExecContext, FillSequential, synthetic_ids
+from .fillmodels import ExecContext, FillSequential
 from .planner import ExecutionPlan
 
 _CTL_WORDS = 64 + 4096  # [0]=abort, [1]=batches done, [8..12)=timestamps (2 x u64), [64..)=cursors
@@ -156,10 +156,10 @@ class Executor:
         self._staged_event: Optional[torch.cuda.Event] = None
         self._staged_part: Optional[int] = None
         self._cap = 0  # samples the per-range buffers hold
-        self._ids_host: Optional[PinnedBuffer] = None
+        self._in_host: Optional[PinnedBuffer] = None
         self._results: Optional[PinnedBuffer] = None
-        self._store_host: Optional[PinnedBuffer] = None
-        self._store_dev: Optional[torch.Tensor] = None
+        self._store_host: Optional[list[PinnedBuffer]] = None
+        self._store_dev: Optional[list[torch.Tensor]] = None
         self._layout_key = None
         self._flops_frac: list[float] = []
         self._last_flag: Optional[int] = None
@@ -172,7 +172,7 @@ class Executor:
 
     # ------------------------------------------------------------------ loading
 
-    _LAYOUT_ATTRS = ("_ctl", "_desc", "_stamps", "_region", "ws", "ids_dev", "_cap", "_ids_host",
+    _LAYOUT_ATTRS = ("_ctl", "_desc", "_stamps", "_region", "ws", "in_dev", "_cap", "_in_host",
                      "_results", "_store_dev", "_store_host", "_flops_frac", "_staged_part",
                      "_staged_event", "_chains", "model", "plan", "_dev_views", "_part_layouts")
 
@@ -195,7 +195,6 @@ class Executor:
         if self.pending is not None:
             self.settle()
         n = item.entry.size
-        cfg = model.cfg
         key = (id(model), id(item.plan))
         if key != self._layout_key or n > self._cap:
             self._save_layout()
@@ -208,8 +207,7 @@ class Executor:
                 self._layout_key = key
         self.item = item
         self.progress = _Progress()
-        self._ids_host.tensor[:n].copy_(
-            synthetic_ids(self.job_seed, item.entry.lo - 1, n, cfg.seq, cfg.vocab))
+        self._in_host.tensor[:n].copy_(self.model.make_inputs(self.job_seed, item.entry.lo - 1, n))
         self._stage_partition(0)
         self.prewarm()
 
@@ -237,7 +235,8 @@ class Executor:
         w = sum(_pad256(model[i].weight_bytes()) for i in range(p.lo, p.hi))
         b = max([e.batch_size for e in p.per_bubble] + [1])
         need = dict(model.workspace(p.lo, p.hi, b))
-        need["hidden"] = b * model.cfg.seq * model.cfg.hidden
+        if p.lo > 0:  # the partition's input, reloaded from the activation store
+            need["in"] = b * model.boundary_elems(p.lo)
         return w, need
 
     def _carve(self, cap: int) -> None:
@@ -245,7 +244,7 @@ class Executor:
         holds one partition at a time -- its weights, then its workspace -- and is sized
         for the largest partition's weights + workspace, so every partition the planner
         fit into the bubble free memory fits the arena."""
-        plan, model, cfg = self.plan, self.model, self.model.cfg
+        plan, model = self.plan, self.model
         self._chains = {}
         self._dev_views = {}
         self._ctl = self.arena.alloc((_CTL_WORDS,), torch.int32)
@@ -259,20 +258,27 @@ class Executor:
         self._region = self.arena.alloc((region // 2,), torch.bfloat16)
         self._part_layouts: dict[int, tuple[dict, dict]] = {}
         self.ws = {}
-        bmax = max(e.batch_size for p in plan.partitions for e in p.per_bubble)
-        self.ids_dev = self.arena.alloc((bmax, cfg.seq), torch.int32)
+        bmax = max(e.batch_size for p in plan.partitions[:1] for e in p.per_bubble)
+        in_dtype, in_shape = model.input_spec()
+        self.in_dev = self.arena.alloc((max(bmax, 1), *in_shape), in_dtype)
         self._cap = cap
-        self._ids_host = PinnedBuffer((cap, cfg.seq), torch.int32)
-        self._results = PinnedBuffer((cap, cfg.hidden), torch.bfloat16)
+        self._in_host = PinnedBuffer((cap, *in_shape), in_dtype)
+        self._results = PinnedBuffer((cap, *model.result_shape()), torch.bfloat16)
         self._store_dev = None
         self._store_host = None
         if len(plan.partitions) > 1:
-            store_bytes = cap * cfg.seq * cfg.hidden * 2
+            # one sample's activation at the widest inter-partition boundary. A partition
+            # overwrites its input store in place sample by sample, which is safe only when
+            # no boundary grows (BERT); otherwise partitions ping-pong between two stores.
+            sizes = [model.boundary_elems(p.lo) for p in plan.partitions[1:]]
+            elems = max(sizes)
+            n_st = 1 if len(set(sizes)) == 1 else 2
+            store_bytes = n_st * cap * elems * 2
             free = self.arena.capacity - self.arena.stats()["used"]
             if self.activation_store == "auto" and store_bytes + (64 << 20) <= free:
-                self._store_dev = self.arena.alloc((cap * cfg.seq * cfg.hidden,), torch.bfloat16)
+                self._store_dev = [self.arena.alloc((cap * elems,), torch.bfloat16) for _ in range(n_st)]
             else:
-                self._store_host = PinnedBuffer((cap, cfg.seq, cfg.hidden), torch.bfloat16)
+                self._store_host = [PinnedBuffer((cap * elems,), torch.bfloat16) for _ in range(n_st)]
         # a batch through partition [lo, hi) counts as this share of a sample: the
         # partition's share of the model's measured execution time (profile at the
         # largest profiled batch size) when the model carries its profile, else of FLOPs
@@ -286,8 +292,11 @@ class Executor:
         self._flops_frac = [sum(cost[p.lo:p.hi]) / total for p in plan.partitions]
         self._staged_part = None
 
-    def _store_ptr(self) -> int:
-        return self._store_dev.data_ptr() if self._store_dev is not None else self._store_host.ptr
+    def _store_ptr(self, k: int) -> int:
+        """Activation store at boundary k (the output of partition k)."""
+        if self._store_dev is not None:
+            return self._store_dev[k % len(self._store_dev)].data_ptr()
+        return self._store_host[k % len(self._store_host)].ptr
 
     def _part_layout(self, part: int) -> tuple[dict, dict]:
         """Device views of partition `part` inside the region: its modules' weights from
@@ -361,9 +370,8 @@ class Executor:
         ch = self._chains.get(key)
         if ch is not None:
             return ch
-        model, cfg = self.model, self.model.cfg
+        model = self.model
         part = self.plan.partitions[part_idx]
-        s, h = cfg.seq, cfg.hidden
         views, ws = self._part_layout(part_idx)
         resident = {i: getattr(model[i], "dev", None) for i in views}
         for i, dev in views.items():  # record against the partition's region layout
@@ -375,19 +383,19 @@ class Executor:
                 model[i].dev = dev
 
     def _record_chain(self, key: tuple, part, cnt: int, flag: Optional[int], ws: dict) -> _Chain:
-        model, cfg = self.model, self.model.cfg
-        s, h = cfg.seq, cfg.hidden
+        model = self.model
         ch = _Chain()
         ctx = ExecContext(self.stream, ws, chain=ch.h)
         # node 0: the batch's input slice (role 1: source + in_off)
         if part.lo == 0:
-            native.call("pf_chain_add_copy", ch.h, self.ids_dev.data_ptr(), cnt * s * 4,
-                        self._ids_host.ptr, cnt * s * 4, cnt * s * 4, 1, 1)
-            x = self.ids_dev[:cnt]
+            nb = cnt * model.input_bytes()
+            native.call("pf_chain_add_copy", ch.h, self.in_dev.data_ptr(), nb, self._in_host.ptr, nb, nb, 1, 1)
+            x = self.in_dev[:cnt]
         else:
-            x = ctx.buf("hidden", cnt * s * h).view(cnt, s, h)
-            native.call("pf_chain_add_copy", ch.h, x.data_ptr(), cnt * s * h * 2, self._store_ptr(),
-                        cnt * s * h * 2, cnt * s * h * 2, 1, 1)
+            shape = model.boundary_shape(part.lo)
+            x = ctx.buf("in", cnt * model.boundary_elems(part.lo)).view(cnt, *shape)
+            nb = cnt * model.boundary_elems(part.lo) * 2
+            native.call("pf_chain_add_copy", ch.h, x.data_ptr(), nb, self._store_ptr(key[0] - 1), nb, nb, 1, 1)
         ctx.node = 1
         for i in range(part.lo, part.hi):
             before = ctx.node
@@ -397,12 +405,12 @@ class Executor:
             ch.seg_ends.append(ctx.node)  # one gated graph segment per module
         # last node: the batch's output slice (role 2: destination + out_off)
         if part.hi == len(model):
-            # [CLS] rows of [cnt, s, h] gathered straight into the pinned results
-            native.call("pf_chain_add_copy", ch.h, self._results.ptr, h * 2, x.data_ptr(), s * h * 2,
-                        h * 2, cnt, 2)
+            # the model's result rows (BERT: [CLS] of [cnt, s, h]) straight into pinned results
+            src, spitch, width, rows = model.result_view(x, cnt)
+            native.call("pf_chain_add_copy", ch.h, self._results.ptr, width, src, spitch, width, rows, 2)
         else:
-            native.call("pf_chain_add_copy", ch.h, self._store_ptr(), cnt * s * h * 2, x.data_ptr(),
-                        cnt * s * h * 2, cnt * s * h * 2, 1, 2)
+            nb = cnt * model.boundary_elems(part.hi) * 2
+            native.call("pf_chain_add_copy", ch.h, self._store_ptr(key[0]), nb, x.data_ptr(), nb, nb, 1, 2)
         ch.finalize()
         ch.seg_ends[-1] = len(ch.units)  # the output copy joins the last module's segment
         native.call("pf_chain_set_desc", ch.h, self._desc.data_ptr())
@@ -464,8 +472,10 @@ class Executor:
                 start += cnt
         if not batches:
             return prev
-        cfg = self.model.cfg
-        s, h = cfg.seq, cfg.hidden
+        model = self.model
+        in_b = model.input_bytes() if part.lo == 0 else model.boundary_elems(part.lo) * 2
+        res_b = 2 * _numel(model.result_shape())
+        out_b = res_b if part.hi == len(model) else model.boundary_elems(part.hi) * 2
         st = self.stream
         base = self._ctl.data_ptr()
         abort_ptr, done_ptr = base, base + 4
@@ -477,18 +487,12 @@ class Executor:
         # offsets from desc[k] (k = the bubble's done counter when it starts)
         dh = self._desc_host.tensor
         for k, (first, cnt, node) in enumerate(batches):
-            if part.lo == 0:
-                dh[k, 0] = first * s * 4
-            else:
-                dh[k, 0] = first * s * h * 2
-            dh[k, 1] = first * h * 2 if part.hi == len(self.model) else first * s * h * 2
-            if node == 0:
-                self.h2d_bytes += cnt * s * 4 if part.lo == 0 else (
-                    cnt * s * h * 2 if self._store_host is not None else 0)
-            if part.hi == len(self.model):
-                self.d2h_bytes += cnt * h * 2
-            elif self._store_host is not None:
-                self.d2h_bytes += cnt * s * h * 2
+            dh[k, 0] = first * in_b
+            dh[k, 1] = first * out_b
+            if node == 0 and (part.lo == 0 or self._store_host is not None):
+                self.h2d_bytes += cnt * in_b
+            if part.hi == len(model) or self._store_host is not None:
+                self.d2h_bytes += cnt * out_b
         with torch.cuda.stream(st):
             if slot.start_event is not None:
                 st.wait_event(slot.start_event)
@@ -607,7 +611,8 @@ class Executor:
                 "gbs": nbytes / ms / 1e6 if ms > 0 else None}
 
     def results(self) -> torch.Tensor:
-        """[N, hidden] bf16 CLS embeddings of the current range (host, pinned)."""
+        """[N, *result_shape] bf16 results of the current range (host, pinned): BERT [CLS]
+        embeddings, ResNet logits."""
         return self._results.tensor[: self.item.entry.size]
 
     def close(self) -> None:
@@ -623,3 +628,10 @@ class Executor:
 
 def _pad256(n: int) -> int:
     return (n + 255) // 256 * 256
+
+
+def _numel(shape) -> int:
+    n = 1
+    for d in shape:
+        n *= int(d)
+    return n

@@ -115,20 +115,46 @@ class ExecContext:
             self.gemm_timers.append((e0, e1, flops))
         self.launched += 1
 
-    def gemm(self, x, w, b, out, *, gelu: bool = False, residual=None) -> None:
+    def gemm(self, x, w, b, out, *, gelu: bool = False, residual=None, relu: bool = False) -> None:
         k = x.shape[-1]
         m = x.numel() // k
         n = w.shape[0]
         if self.chain is not None:
             epi = (native.PF_EPI_BIAS if b is not None else 0) | (native.PF_EPI_GELU if gelu else 0) \
-                | (native.PF_EPI_RESIDUAL if residual is not None else 0)
+                | (native.PF_EPI_RESIDUAL if residual is not None else 0) | (native.PF_EPI_RELU if relu else 0)
             native.call("pf_chain_add_gemm", self.chain, x.data_ptr(), w.data_ptr(),
                         None if b is None else b.data_ptr(),
                         None if residual is None else residual.data_ptr(), out.data_ptr(), m, n, k, epi)
             self.node += 1
             return
-        self._eager(lambda c: K.linear(x, w, b, gelu=gelu, residual=residual, out=out, ctl=c,
+        self._eager(lambda c: K.linear(x, w, b, gelu=gelu, residual=residual, relu=relu, out=out, ctl=c,
                                        stream=self.stream), flops=2.0 * m * n * k)
+
+    def im2col(self, x, kh: int, kw: int, stride: int, pad: int, kp: int, out) -> None:
+        if self.chain is not None:
+            b, h, w, c = x.shape
+            native.call("pf_chain_add_im2col", self.chain, x.data_ptr(), out.data_ptr(), b, h, w, c, kh, kw,
+                        stride, pad, kp)
+            self.node += 1
+            return
+        self._eager(lambda c_: K.im2col(x, kh, kw, stride, pad, kp, out=out, ctl=c_, stream=self.stream))
+
+    def maxpool(self, x, k: int, stride: int, pad: int, out) -> None:
+        if self.chain is not None:
+            b, h, w, c = x.shape
+            native.call("pf_chain_add_maxpool", self.chain, x.data_ptr(), out.data_ptr(), b, h, w, c, k,
+                        stride, pad)
+            self.node += 1
+            return
+        self._eager(lambda c_: K.maxpool(x, k, stride, pad, out=out, ctl=c_, stream=self.stream))
+
+    def avgpool(self, x, out) -> None:
+        if self.chain is not None:
+            b, h, w, c = x.shape
+            native.call("pf_chain_add_avgpool", self.chain, x.data_ptr(), out.data_ptr(), b, h * w, c)
+            self.node += 1
+            return
+        self._eager(lambda c_: K.avgpool(x, out=out, ctl=c_, stream=self.stream))
 
     def attention(self, qkv, heads: int, out) -> None:
         if self.chain is not None:
@@ -179,12 +205,18 @@ class FillModule(nn.Module):
     def weight_bytes(self) -> int:
         return sum(2 * _numel(shape) for _, shape, _ in self.param_specs())
 
-    def init_host(self, gen: torch.Generator, std: float = 0.02) -> None:
-        """Random init into pinned host memory: N(0, std) weights/biases, LN gamma 1, beta 0."""
+    def init_host(self, gen: torch.Generator, std: float = 0.02, pinned: bool = True) -> None:
+        """Random init into pinned host memory: N(0, std) weights/biases, LN gamma 1, beta 0.
+        pinned=False keeps the master copy in pageable memory (CPU-only oracle tests;
+        such a module cannot be staged)."""
         specs = self.param_specs()
         total = sum(_numel(s) for _, s, _ in specs)
-        self.host = PinnedBuffer((total,), torch.bfloat16)
-        flat = self.host.tensor
+        if pinned:
+            self.host = PinnedBuffer((total,), torch.bfloat16)
+            flat = self.host.tensor
+        else:
+            self.host = None
+            flat = torch.empty(total, dtype=torch.bfloat16)
         off = 0
         for name, shape, kind in specs:
             n = _numel(shape)
@@ -192,6 +224,16 @@ class FillModule(nn.Module):
                 vals = torch.ones(n)
             elif kind == "zero":
                 vals = torch.zeros(n)
+            elif isinstance(kind, tuple) and kind[0] == "conv":
+                # ("conv", fan_in, K): Kaiming-normal conv weights [Cout, Kp] in im2col
+                # column order, BatchNorm (eval) folded in; pad columns K..Kp zero
+                _, fan_in, k = kind
+                w = torch.randn(shape[0], k, generator=gen) * (2.0 / fan_in) ** 0.5
+                vals = torch.zeros(shape)
+                vals[:, :k] = w
+                vals = vals.flatten()
+            elif isinstance(kind, tuple) and kind[0] == "std":
+                vals = torch.randn(n, generator=gen) * kind[1]
             else:
                 vals = torch.randn(n, generator=gen) * std
             flat[off:off + n].copy_(vals.to(torch.bfloat16))
@@ -213,18 +255,19 @@ class FillModule(nn.Module):
         self.dev = {}
 
     # -- execution ------------------------------------------------------------
-    def workspace(self, batch: int, seq: int) -> dict[str, int]:
+    def workspace(self, batch: int) -> dict[str, int]:
+        """Workspace buffers (bf16 elements) one batch of this module needs."""
         return {}
 
     def flops_per_sample(self) -> float:
-        """Algorithmic forward FLOPs of this module for one sequence."""
+        """Algorithmic forward FLOPs of this module for one sample."""
         return 0.0
 
     def gemm_node_flops(self, batch: int) -> list[tuple[int, float]]:
         """(node index within this module, algorithmic FLOPs) of its GEMM nodes."""
         return []
 
-    def node_units(self, batch: int, seq: int) -> list[tuple[int, str]]:
+    def node_units(self, batch: int) -> list[tuple[int, str]]:
         raise NotImplementedError
 
     def forward(self, x, ctx: ExecContext):
@@ -253,12 +296,15 @@ class BertEmbeddings(FillModule):
                 ("type", (c.type_vocab, c.hidden), "w"), ("ln_g", (c.hidden,), "one"),
                 ("ln_b", (c.hidden,), "zero")]
 
-    def node_units(self, batch, seq):
-        return [(K.norm_units(batch * seq, self.cfg.hidden), ATOMIC)]
+    def workspace(self, batch):
+        return {"act": batch * self.cfg.seq * self.cfg.hidden}
+
+    def node_units(self, batch):
+        return [(K.norm_units(batch * self.cfg.seq, self.cfg.hidden), ATOMIC)]
 
     def forward(self, ids: torch.Tensor, ctx: ExecContext) -> torch.Tensor:
         b, s = ids.shape
-        out = ctx.buf("hidden", b * s * self.cfg.hidden).view(b, s, self.cfg.hidden)
+        out = ctx.buf("act", b * s * self.cfg.hidden).view(b, s, self.cfg.hidden)
         d = self.dev
         ctx.embedding(ids, d["word"], d["pos"], d["type"], d["ln_g"], d["ln_b"], self.cfg.eps, out)
         return out
@@ -284,8 +330,8 @@ class BertLayer(FillModule):
                 ("ffn2_w", (h, f), "w"), ("ffn2_b", (h,), "w"),
                 ("ln2_g", (h,), "one"), ("ln2_b", (h,), "zero")]
 
-    def workspace(self, batch, seq):
-        m, h, f = batch * seq, self.cfg.hidden, self.cfg.ffn
+    def workspace(self, batch):
+        m, h, f = batch * self.cfg.seq, self.cfg.hidden, self.cfg.ffn
         return {"qkv": m * 3 * h, "ctx": m * h, "a": m * h, "a_ln": m * h, "ffn": m * f, "o": m * h}
 
     def flops_per_sample(self) -> float:
@@ -297,7 +343,8 @@ class BertLayer(FillModule):
         return [(0, 2.0 * m * 3 * h * h), (2, 2.0 * m * h * h), (4, 2.0 * m * h * f),
                 (5, 2.0 * m * f * h)]
 
-    def node_units(self, batch, seq):
+    def node_units(self, batch):
+        seq = self.cfg.seq
         m, h, f = batch * seq, self.cfg.hidden, self.cfg.ffn
         return [(K.gemm_units(m, 3 * h, h), PREFIX),
                 (K.attention_units(batch, seq, self.cfg.heads, h // self.cfg.heads), ATOMIC),
@@ -329,16 +376,50 @@ class BertLayer(FillModule):
 
 
 class FillSequential(nn.Sequential):
-    """The fill model: an nn.Sequential whose module k is profile layer k."""
+    """The fill model: an nn.Sequential whose module k is profile layer k.
 
-    def __init__(self, cfg: BertConfig, modules: list[FillModule]):
+    Subclasses describe the model's data at its edges, which is all the Executor
+    needs to run any partition [lo, hi):
+
+    * ``input_spec()``: (dtype, per-sample shape) of the job's input samples;
+    * ``boundary_shape(i)``: per-sample bf16 activation shape entering module i
+      (what is stored between partitions at boundary i);
+    * ``result_shape()`` and ``result_view(x, cnt)``: the per-sample result and where
+      it sits in the last module's output (a 2-D copy: src, pitch, width, rows);
+    * ``make_inputs(job_seed, first, count)``: the job's synthetic samples
+      [first, first + count), identical under any split into ranges and batches."""
+
+    def __init__(self, cfg, modules: list[FillModule]):
         super().__init__(*modules)
         self.cfg = cfg
+        self.profile = None  # set by profiler.measure_profile
 
-    def init_weights(self, seed: int = 0) -> "FillSequential":
+    def input_spec(self) -> tuple[torch.dtype, tuple[int, ...]]:
+        raise NotImplementedError
+
+    def boundary_shape(self, i: int) -> tuple[int, ...]:
+        raise NotImplementedError
+
+    def result_shape(self) -> tuple[int, ...]:
+        raise NotImplementedError
+
+    def result_view(self, x: torch.Tensor, cnt: int) -> tuple[int, int, int, int]:
+        raise NotImplementedError
+
+    def make_inputs(self, job_seed: int, first: int, count: int) -> torch.Tensor:
+        raise NotImplementedError
+
+    def input_bytes(self) -> int:
+        dt, shape = self.input_spec()
+        return _numel(shape) * torch.tensor([], dtype=dt).element_size()
+
+    def boundary_elems(self, i: int) -> int:
+        return _numel(self.boundary_shape(i))
+
+    def init_weights(self, seed: int = 0, pinned: bool = True) -> "FillSequential":
         gen = torch.Generator().manual_seed(seed)
         for mod in self:
-            mod.init_host(gen)
+            mod.init_host(gen, pinned=pinned)
         return self
 
     def weight_bytes(self, lo: int, hi: int) -> int:
@@ -347,14 +428,14 @@ class FillSequential(nn.Sequential):
     def workspace(self, lo: int, hi: int, batch: int) -> dict[str, int]:
         need: dict[str, int] = {}
         for i in range(lo, hi):
-            for k, v in self[i].workspace(batch, self.cfg.seq).items():
+            for k, v in self[i].workspace(batch).items():
                 need[k] = max(need.get(k, 0), v)
         return need
 
     def node_units(self, lo: int, hi: int, batch: int) -> list[tuple[int, str]]:
         out: list[tuple[int, str]] = []
         for i in range(lo, hi):
-            out.extend(self[i].node_units(batch, self.cfg.seq))
+            out.extend(self[i].node_units(batch))
         return out
 
     def oracle_params(self, i: int) -> dict[str, torch.Tensor]:
@@ -362,13 +443,301 @@ class FillSequential(nn.Sequential):
         return {k: v.float().clone() for k, v in self[i].host_params.items()}
 
 
+class BertSequential(FillSequential):
+    """BERT: int32 token ids in, [seq, hidden] activations between modules, the
+    [CLS] row of the last hidden state out."""
+
+    def input_spec(self):
+        return torch.int32, (self.cfg.seq,)
+
+    def boundary_shape(self, i):
+        return (self.cfg.seq, self.cfg.hidden)
+
+    def result_shape(self):
+        return (self.cfg.hidden,)
+
+    def result_view(self, x, cnt):
+        s, h = self.cfg.seq, self.cfg.hidden
+        return x.data_ptr(), s * h * 2, h * 2, cnt
+
+    def make_inputs(self, job_seed, first, count):
+        return synthetic_ids(job_seed, first, count, self.cfg.seq, self.cfg.vocab)
+
+
 def bert(cfg: BertConfig = BERT_BASE, seed: Optional[int] = 0) -> FillSequential:
     """BERT encoder as the linearized fill model [embeddings, layer_0..layer_{L-1}]."""
     mods: list[FillModule] = [BertEmbeddings(cfg)] + [BertLayer(cfg) for _ in range(cfg.layers)]
-    seq = FillSequential(cfg, mods)
+    seq = BertSequential(cfg, mods)
     if seed is not None:
         seq.init_weights(seed)
     return seq
+
+
+# --------------------------------------------------------------------------- ResNet-50
+
+
+@dataclass(frozen=True)
+class ResNetConfig:
+    """ResNet-50 v1.5 (stride on the 3x3 conv), NHWC bf16, BatchNorm folded into the
+    convolutions (inference form: scale into the weights, shift into the bias)."""
+
+    name: str = "resnet50"
+    image: int = 224
+    in_ch: int = 3
+    classes: int = 1000
+    blocks: tuple[int, ...] = (3, 4, 6, 3)
+    widths: tuple[int, ...] = (64, 128, 256, 512)
+    expansion: int = 4
+    stem_ch: int = 64
+
+    @property
+    def stem_k(self) -> int:
+        return 7 * 7 * self.in_ch
+
+    @property
+    def stem_kp(self) -> int:
+        return (self.stem_k + 7) // 8 * 8  # 16-B GEMM rows
+
+    @property
+    def flops_per_sample(self) -> float:
+        return sum(m.flops_per_sample() for m in _resnet_modules(self))
+
+
+RESNET50 = ResNetConfig()
+
+
+def _act(idx: int) -> str:
+    return f"act{idx % 2}"
+
+
+class ResNetStem(FillModule):
+    """conv 7x7/2 (+BN+ReLU) as im2col + GEMM, then maxpool 3x3/2: 3 kernel nodes."""
+
+    n_nodes = 3
+
+    def __init__(self, cfg: ResNetConfig, idx: int):
+        super().__init__()
+        self.cfg, self.idx = cfg, idx
+        self.h1 = K.conv_out(cfg.image, 7, 2, 3)
+        self.h2 = K.conv_out(self.h1, 3, 2, 1)
+
+    def param_specs(self):
+        c = self.cfg
+        return [("w", (c.stem_ch, c.stem_kp), ("conv", c.stem_k, c.stem_k)),
+                ("b", (c.stem_ch,), ("std", 0.05))]
+
+    def out_shape(self):
+        return (self.h2, self.h2, self.cfg.stem_ch)
+
+    def workspace(self, batch):
+        c = self.cfg
+        return {"col": batch * self.h1 * self.h1 * c.stem_kp, "pre": batch * self.h1 * self.h1 * c.stem_ch,
+                _act(self.idx): batch * self.h2 * self.h2 * c.stem_ch}
+
+    def flops_per_sample(self):
+        return 2.0 * self.h1 * self.h1 * self.cfg.stem_ch * self.cfg.stem_k
+
+    def gemm_node_flops(self, batch):
+        return [(1, batch * self.flops_per_sample())]
+
+    def node_units(self, batch):
+        c, m = self.cfg, batch * self.h1 * self.h1
+        return [(K.image_units(0, m * c.stem_kp, c.in_ch), ATOMIC),
+                (K.gemm_units(m, c.stem_ch, c.stem_kp), PREFIX),
+                (K.image_units(1, batch * self.h2 * self.h2 * c.stem_ch, c.stem_ch), ATOMIC)]
+
+    def forward(self, x, ctx):
+        c, b = self.cfg, x.shape[0]
+        m = b * self.h1 * self.h1
+        col = ctx.buf("col", m * c.stem_kp).view(m, c.stem_kp)
+        pre = ctx.buf("pre", m * c.stem_ch).view(b, self.h1, self.h1, c.stem_ch)
+        out = ctx.buf(_act(self.idx), b * self.h2 * self.h2 * c.stem_ch).view(b, self.h2, self.h2, c.stem_ch)
+        ctx.im2col(x, 7, 7, 2, 3, c.stem_kp, col)
+        ctx.gemm(col, self.dev["w"], self.dev["b"], pre.view(m, c.stem_ch), relu=True)
+        ctx.maxpool(pre, 3, 2, 1, out)
+        return out
+
+
+class Bottleneck(FillModule):
+    """1x1 -> 3x3 (stride) -> 1x1 (x4) with identity or projection shortcut; every
+    conv is a GEMM with folded BN; ReLU, and the residual add of the last conv, run
+    in the GEMM epilogue. Nodes: gemm1, im2col, gemm2, [im2col_ds], [gemm_ds], gemm3."""
+
+    def __init__(self, cfg: ResNetConfig, idx: int, in_ch: int, width: int, stride: int, h_in: int):
+        super().__init__()
+        self.cfg, self.idx = cfg, idx
+        self.in_ch, self.width, self.stride, self.h = in_ch, width, stride, h_in
+        self.out_ch = width * cfg.expansion
+        self.ho = K.conv_out(h_in, 3, stride, 1)
+        self.ds = stride != 1 or in_ch != self.out_ch
+        self.n_nodes = 4 + (1 if self.ds else 0) + (1 if self.ds and stride != 1 else 0)
+
+    def param_specs(self):
+        ci, w, co = self.in_ch, self.width, self.out_ch
+        specs = [("w1", (w, ci), ("conv", ci, ci)), ("b1", (w,), ("std", 0.05)),
+                 ("w2", (w, 9 * w), ("conv", 9 * w, 9 * w)), ("b2", (w,), ("std", 0.05)),
+                 ("w3", (co, w), ("conv", 4 * w, w)), ("b3", (co,), ("std", 0.05))]
+        if self.ds:
+            specs += [("wd", (co, ci), ("conv", 4 * ci, ci)), ("bd", (co,), ("std", 0.05))]
+        return specs
+
+    def out_shape(self):
+        return (self.ho, self.ho, self.out_ch)
+
+    def workspace(self, batch):
+        hw, ow = self.h * self.h, self.ho * self.ho
+        need = {"t1": batch * hw * self.width, "col": batch * ow * 9 * self.width,
+                "t2": batch * ow * self.width, _act(self.idx): batch * ow * self.out_ch}
+        if self.ds:
+            need["sc"] = batch * ow * self.out_ch
+            if self.stride != 1:
+                need["colds"] = batch * ow * self.in_ch
+        return need
+
+    def flops_per_sample(self):
+        hw, ow, ci, w, co = self.h * self.h, self.ho * self.ho, self.in_ch, self.width, self.out_ch
+        f = 2.0 * (hw * ci * w + ow * 9 * w * w + ow * w * co)
+        return f + (2.0 * ow * ci * co if self.ds else 0.0)
+
+    def _gemms(self, batch):
+        """(node, M, N, K) of the GEMM nodes."""
+        hw, ow, ci, w, co = batch * self.h * self.h, batch * self.ho * self.ho, self.in_ch, self.width, self.out_ch
+        g = [(0, hw, w, ci), (2, ow, w, 9 * w)]
+        n = 3
+        if self.ds:
+            if self.stride != 1:
+                n += 1
+            g.append((n, ow, co, ci))
+            n += 1
+        g.append((n, ow, co, w))
+        return g
+
+    def gemm_node_flops(self, batch):
+        return [(node, 2.0 * m * n * k) for node, m, n, k in self._gemms(batch)]
+
+    def node_units(self, batch):
+        ow = batch * self.ho * self.ho
+        units = {node: (K.gemm_units(m, n, k), PREFIX) for node, m, n, k in self._gemms(batch)}
+        units[1] = (K.image_units(0, ow * 9 * self.width, self.width), ATOMIC)
+        if self.ds and self.stride != 1:
+            units[3] = (K.image_units(0, ow * self.in_ch, self.in_ch), ATOMIC)
+        return [units[i] for i in range(self.n_nodes)]
+
+    def forward(self, x, ctx):
+        b = x.shape[0]
+        d = self.dev
+        hw, ow, ci, w, co = b * self.h * self.h, b * self.ho * self.ho, self.in_ch, self.width, self.out_ch
+        x2 = x.reshape(hw, ci)
+        t1 = ctx.buf("t1", hw * w).view(b, self.h, self.h, w)
+        col = ctx.buf("col", ow * 9 * w).view(ow, 9 * w)
+        t2 = ctx.buf("t2", ow * w).view(ow, w)
+        out = ctx.buf(_act(self.idx), ow * co).view(b, self.ho, self.ho, co)
+        ctx.gemm(x2, d["w1"], d["b1"], t1.view(hw, w), relu=True)
+        ctx.im2col(t1, 3, 3, self.stride, 1, 9 * w, col)
+        ctx.gemm(col, d["w2"], d["b2"], t2, relu=True)
+        if self.ds:
+            src = x2
+            if self.stride != 1:
+                src = ctx.buf("colds", ow * ci).view(ow, ci)
+                ctx.im2col(x, 1, 1, self.stride, 0, ci, src)
+            sc = ctx.buf("sc", ow * co).view(ow, co)
+            ctx.gemm(src, d["wd"], d["bd"], sc)
+        else:
+            sc = x2
+        ctx.gemm(t2, d["w3"], d["b3"], out.view(ow, co), residual=sc, relu=True)
+        return out
+
+
+class ResNetHead(FillModule):
+    """Global average pool + fully connected classifier: 2 kernel nodes."""
+
+    n_nodes = 2
+
+    def __init__(self, cfg: ResNetConfig, idx: int, in_ch: int, h_in: int):
+        super().__init__()
+        self.cfg, self.idx, self.in_ch, self.h = cfg, idx, in_ch, h_in
+
+    def param_specs(self):
+        return [("fc_w", (self.cfg.classes, self.in_ch), ("std", self.in_ch ** -0.5)),
+                ("fc_b", (self.cfg.classes,), ("std", 0.01))]
+
+    def out_shape(self):
+        return (self.cfg.classes,)
+
+    def workspace(self, batch):
+        return {"pooled": batch * self.in_ch, _act(self.idx): batch * self.cfg.classes}
+
+    def flops_per_sample(self):
+        return 2.0 * self.in_ch * self.cfg.classes
+
+    def gemm_node_flops(self, batch):
+        return [(1, batch * self.flops_per_sample())]
+
+    def node_units(self, batch):
+        return [(K.image_units(1, batch * self.in_ch, self.in_ch), ATOMIC),
+                (K.gemm_units(batch, self.cfg.classes, self.in_ch), PREFIX)]
+
+    def forward(self, x, ctx):
+        b = x.shape[0]
+        pooled = ctx.buf("pooled", b * self.in_ch).view(b, self.in_ch)
+        logits = ctx.buf(_act(self.idx), b * self.cfg.classes).view(b, self.cfg.classes)
+        ctx.avgpool(x, pooled)
+        ctx.gemm(pooled, self.dev["fc_w"], self.dev["fc_b"], logits)
+        return logits
+
+
+def _resnet_modules(cfg: ResNetConfig) -> list[FillModule]:
+    mods: list[FillModule] = [ResNetStem(cfg, 0)]
+    ch, h = cfg.stem_ch, mods[0].out_shape()[0]
+    for stage, (n, w) in enumerate(zip(cfg.blocks, cfg.widths)):
+        for j in range(n):
+            stride = 2 if (j == 0 and stage > 0) else 1
+            blk = Bottleneck(cfg, len(mods), ch, w, stride, h)
+            mods.append(blk)
+            ch, h = blk.out_ch, blk.ho
+    mods.append(ResNetHead(cfg, len(mods), ch, h))
+    return mods
+
+
+class ResNetSequential(FillSequential):
+    """ResNet: bf16 NHWC images in, NHWC activations between modules, logits out."""
+
+    def input_spec(self):
+        c = self.cfg
+        return torch.bfloat16, (c.image, c.image, c.in_ch)
+
+    def boundary_shape(self, i):
+        if i == 0:
+            return self.input_spec()[1]
+        return self[i - 1].out_shape()
+
+    def result_shape(self):
+        return (self.cfg.classes,)
+
+    def result_view(self, x, cnt):
+        n = cnt * self.cfg.classes * 2
+        return x.data_ptr(), n, n, 1
+
+    def make_inputs(self, job_seed, first, count):
+        return synthetic_images(job_seed, first, count, self.cfg.image, self.cfg.in_ch)
+
+
+def resnet50(cfg: ResNetConfig = RESNET50, seed: Optional[int] = 0, pinned: bool = True) -> FillSequential:
+    """ResNet-50 as the linearized fill model [stem, 16 bottlenecks, head]."""
+    seq = ResNetSequential(cfg, _resnet_modules(cfg))
+    if seed is not None:
+        seq.init_weights(seed, pinned=pinned)
+    return seq
+
+
+def synthetic_images(job_seed: int, first_sample: int, count: int, size: int, ch: int) -> torch.Tensor:
+    """N(0, 1) NHWC bf16 images; sample i depends only on (job_seed, i)."""
+    out = torch.empty(count, size, size, ch, dtype=torch.bfloat16)
+    g = torch.Generator()
+    for j in range(count):
+        g.manual_seed((job_seed * 1_000_003 + first_sample + j) * 2_654_435_761 % (2 ** 63 - 1))
+        out[j] = torch.randn(size, size, ch, generator=g).to(torch.bfloat16)
+    return out
 
 
 def synthetic_ids(job_seed: int, first_sample: int, count: int, seq: int, vocab: int) -> torch.Tensor:
@@ -383,6 +752,8 @@ def synthetic_ids(job_seed: int, first_sample: int, count: int, seq: int, vocab:
 
 
 __all__ = ["BertConfig", "BERT_BASE", "BERT_LARGE", "ExecContext", "FillModule", "BertEmbeddings",
-           "BertLayer", "FillSequential", "bert", "synthetic_ids", "PREFIX", "ATOMIC"]
+           "BertLayer", "FillSequential", "BertSequential", "bert", "synthetic_ids", "PREFIX", "ATOMIC",
+           "ResNetConfig", "RESNET50", "ResNetStem", "Bottleneck", "ResNetHead", "ResNetSequential",
+           "resnet50", "synthetic_images"]
 
 _ = ctypes  # ctypes is used by arena/native through this module's imports

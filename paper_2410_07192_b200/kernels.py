@@ -15,7 +15,7 @@ from typing import Optional
 import torch
 
 from . import native
-from .native import PF_EPI_BIAS, PF_EPI_GELU, PF_EPI_RESIDUAL, PfCtl
+from .native import PF_EPI_BIAS, PF_EPI_GELU, PF_EPI_RELU, PF_EPI_RESIDUAL, PfCtl
 
 
 @dataclass
@@ -73,11 +73,12 @@ def linear(
     *,
     gelu: bool = False,
     residual: Optional[torch.Tensor] = None,
+    relu: bool = False,
     out: Optional[torch.Tensor] = None,
     ctl: Optional[KernelCtl] = None,
     stream: Optional[torch.cuda.Stream] = None,
 ) -> torch.Tensor:
-    """out = [GELU](x @ weight.T + bias) [+ residual] — tcgen05 GEMM (pf_gemm)."""
+    """out = [ReLU]([GELU](x @ weight.T + bias) [+ residual]) — tcgen05 GEMM (pf_gemm)."""
     _check_bf16_cuda("x", x)
     _check_bf16_cuda("weight", weight)
     k = x.shape[-1]
@@ -94,6 +95,8 @@ def linear(
     if residual is not None:
         _check_bf16_cuda("residual", residual)
         epi |= PF_EPI_RESIDUAL
+    if relu:
+        epi |= PF_EPI_RELU
     if out is None:
         out = torch.empty(*x.shape[:-1], n, dtype=torch.bfloat16, device=x.device)
     native.call(
@@ -227,4 +230,76 @@ def embedding_ln(
         type_emb.data_ptr(), gamma.data_ptr(), beta.data_ptr(), out.data_ptr(), batch, seq, hidden,
         word.shape[0], float(eps), _ctl_ref(ctl), _stream(stream),
     )
+    return out
+
+
+def conv_out(size: int, k: int, stride: int, pad: int) -> int:
+    return (size + 2 * pad - k) // stride + 1
+
+
+def image_units(kind: int, out_elems: int, channels: int) -> int:
+    out = ctypes.c_uint32(0)
+    native.call("pf_image_units", kind, out_elems, channels, ctypes.byref(out))
+    return out.value
+
+
+def im2col(
+    x: torch.Tensor,
+    kh: int,
+    kw: int,
+    stride: int,
+    pad: int,
+    kp: Optional[int] = None,
+    *,
+    out: Optional[torch.Tensor] = None,
+    ctl: Optional[KernelCtl] = None,
+    stream: Optional[torch.cuda.Stream] = None,
+) -> torch.Tensor:
+    """NHWC x[B,H,W,C] -> col[B*Ho*Wo, Kp], column (ky*kw + kx)*C + c (pf_im2col)."""
+    _check_bf16_cuda("x", x)
+    b, h, w, c = x.shape
+    k = kh * kw * c
+    kp = kp or (k + 7) // 8 * 8
+    ho, wo = conv_out(h, kh, stride, pad), conv_out(w, kw, stride, pad)
+    if out is None:
+        out = torch.empty(b * ho * wo, kp, dtype=torch.bfloat16, device=x.device)
+    native.call("pf_im2col", x.data_ptr(), out.data_ptr(), b, h, w, c, kh, kw, stride, pad, kp,
+                _ctl_ref(ctl), _stream(stream))
+    return out
+
+
+def maxpool(
+    x: torch.Tensor,
+    k: int = 3,
+    stride: int = 2,
+    pad: int = 1,
+    *,
+    out: Optional[torch.Tensor] = None,
+    ctl: Optional[KernelCtl] = None,
+    stream: Optional[torch.cuda.Stream] = None,
+) -> torch.Tensor:
+    """NHWC max pooling (pf_maxpool)."""
+    _check_bf16_cuda("x", x)
+    b, h, w, c = x.shape
+    ho, wo = conv_out(h, k, stride, pad), conv_out(w, k, stride, pad)
+    if out is None:
+        out = torch.empty(b, ho, wo, c, dtype=torch.bfloat16, device=x.device)
+    native.call("pf_maxpool", x.data_ptr(), out.data_ptr(), b, h, w, c, k, stride, pad, _ctl_ref(ctl),
+                _stream(stream))
+    return out
+
+
+def avgpool(
+    x: torch.Tensor,
+    *,
+    out: Optional[torch.Tensor] = None,
+    ctl: Optional[KernelCtl] = None,
+    stream: Optional[torch.cuda.Stream] = None,
+) -> torch.Tensor:
+    """Global average pool NHWC x[B,H,W,C] -> [B, C] (pf_avgpool)."""
+    _check_bf16_cuda("x", x)
+    b, h, w, c = x.shape
+    if out is None:
+        out = torch.empty(b, c, dtype=torch.bfloat16, device=x.device)
+    native.call("pf_avgpool", x.data_ptr(), out.data_ptr(), b, h * w, c, _ctl_ref(ctl), _stream(stream))
     return out

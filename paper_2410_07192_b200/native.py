@@ -27,6 +27,7 @@ PF_ERR_OOM = -4
 PF_EPI_BIAS = 1
 PF_EPI_GELU = 2
 PF_EPI_RESIDUAL = 4
+PF_EPI_RELU = 8
 
 
 class NativeUnavailable(RuntimeError):
@@ -107,6 +108,17 @@ _SIGNATURES: dict[str, tuple] = {
     "pf_copy_units": (c_int, [c_uint64, POINTER(c_uint32)]),
     "pf_copy2d": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, POINTER(PfCtl),
                           c_void_p]),
+    "pf_im2col": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                          c_int, POINTER(PfCtl), c_void_p]),
+    "pf_maxpool": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                           POINTER(PfCtl), c_void_p]),
+    "pf_avgpool": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, POINTER(PfCtl), c_void_p]),
+    "pf_image_units": (c_int, [c_int, ctypes.c_longlong, c_int, POINTER(c_uint32)]),
+    "pf_chain_add_im2col": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int,
+                                    c_int, c_int, c_int]),
+    "pf_chain_add_maxpool": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int,
+                                     c_int, c_int]),
+    "pf_chain_add_avgpool": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int]),
     "pf_chain_create": (c_int, [POINTER(c_void_p)]),
     "pf_chain_destroy": (c_int, [c_void_p]),
     "pf_chain_add_gemm": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int,

@@ -18,17 +18,22 @@ from typing import Sequence
 import torch
 
 from .arena import Arena
-from .fillmodels import ExecContext, FillSequential, synthetic_ids
+from .fillmodels import ExecContext, FillSequential
 from .profiles import JobKind, LayerProfile, ModelProfile
 
 FIXED_TRANSIENT_BYTES = 1 << 20  # control block, cursors, alignment slack
 
 
 def _module_mem(model: FillSequential, i: int, b: int) -> tuple[int, int]:
-    cfg = model.cfg
+    """(weight bytes, transient bytes at batch b) of module i as the executor lays it
+    out: its workspace, the partition-input buffer (if a partition starts here), the
+    batch's inputs and results, and the control block."""
     w = model[i].weight_bytes()
-    ws = sum(2 * v for v in model[i].workspace(b, cfg.seq).values())
-    act = 2 * b * cfg.seq * cfg.hidden + 2 * b * cfg.hidden + 4 * b * cfg.seq
+    ws = sum(2 * v for v in model[i].workspace(b).values())
+    res = 2 * b
+    for d in model.result_shape():
+        res *= d
+    act = 2 * b * model.boundary_elems(i) + res + b * model.input_bytes()
     return w, ws + act + FIXED_TRANSIENT_BYTES
 
 
@@ -38,23 +43,23 @@ def measure_profile(model: FillSequential, batch_sizes: Sequence[int], reps: int
     bmax = max(batch_sizes)
     weights = sum((model[i].weight_bytes() + 255) // 256 * 256 for i in range(len(model)))
     need = model.workspace(0, len(model), bmax)
-    need["hidden"] = bmax * cfg.seq * cfg.hidden
-    arena = Arena(weights + 2 * sum(need.values()) + 4 * bmax * cfg.seq + (64 << 20))
+    in_dtype, in_shape = model.input_spec()
+    arena = Arena(weights + 2 * sum(need.values()) + bmax * model.input_bytes() + (64 << 20))
     stream = torch.cuda.Stream()
     try:
         for mod in model:
             mod.stage(arena, stream)
         ws = {k: arena.alloc((v,), torch.bfloat16) for k, v in need.items()}
-        ids_dev = arena.alloc((bmax, cfg.seq), torch.int32)
+        in_dev = arena.alloc((bmax, *in_shape), in_dtype)
         times: dict[int, list[float]] = {}
         for b in sorted(batch_sizes):
-            ids_dev[:b].copy_(synthetic_ids(0, 0, b, cfg.seq, cfg.vocab))
+            in_dev[:b].copy_(model.make_inputs(0, 0, b))
             per_rep = []
             for r in range(warmup + reps):
                 evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(model) + 1)]
                 with torch.cuda.stream(stream):
                     ctx = ExecContext(stream, ws)
-                    x = ids_dev[:b]
+                    x = in_dev[:b]
                     evs[0].record(stream)
                     for i, mod in enumerate(model):
                         x = mod(x, ctx)
@@ -96,8 +101,6 @@ def measure_profile(model: FillSequential, batch_sizes: Sequence[int], reps: int
 
 
 def _module_flops(model: FillSequential, i: int) -> float:
-    cfg = model.cfg
-    if i == 0:
-        return 0.0
-    s, h, f = cfg.seq, cfg.hidden, cfg.ffn
-    return 2.0 * s * (4 * h * h + 2 * h * f) + 4.0 * s * s * h
+    """Algorithmic forward FLOPs of module i per sample (BERT: 24*s*h^2 + 4*s^2*h per
+    layer; ResNet: 2 * MACs of its convolutions and classifier)."""
+    return model[i].flops_per_sample()

@@ -38,6 +38,7 @@ def _bf16(*shape, scale=1.0, gen=None):
         (4096, 4096, 1024, True, True, False),  # BERT-large FFN1
         (128, 128, 64, False, False, False),
         (200, 264, 136, True, True, True),      # ragged M/N/K tails
+        (65536, 64, 152, True, False, False),   # short K, ~4 tiles per CTA: epilogue staging reuse
         (1, 8, 8, False, False, False),
     ],
 )
