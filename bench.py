@@ -59,12 +59,13 @@ CONFIGS = {
            # default 16 leaves 2/3 of a 100 ms GPipe bubble idle for a 5-layer partition
            "max_batches": 64},
     # configs[4]: multi-job queue -- Placer (avg-JCT routing) + per-stage SJF Coordinators,
-    # mixed BERT-base / BERT-large inference jobs, bubble free-memory cap sweep
+    # mixed BERT-base / BERT-large / ResNet-50 inference jobs, bubble free-memory cap sweep
     "c5": {"stages": 8, "micro": 8, "schedule": "1f1b", "main": "gpt8b", "fill": "bert_large",
            "batch_sizes": FILL_BATCH_SIZES, "caps_gb": (0.5, 1, 2, 4, 8), "max_batches": 64,
-           "jobs": (("bert_base", 8192, 0.0), ("bert_large", 4096, 0.0), ("bert_base", 2048, 0.5),
-                    ("bert_large", 8192, 1.0), ("bert_base", 4096, 1.5), ("bert_large", 2048, 2.0),
-                    ("bert_base", 16384, 3.0), ("bert_large", 1024, 4.0))},
+           "jobs": (("bert_base", 8192, 0.0), ("bert_large", 4096, 0.0), ("resnet50", 2048, 0.25),
+                    ("bert_base", 2048, 0.5), ("bert_large", 8192, 1.0), ("resnet50", 1024, 1.25),
+                    ("bert_base", 4096, 1.5), ("bert_large", 2048, 2.0), ("bert_base", 16384, 3.0),
+                    ("resnet50", 4096, 3.5), ("bert_large", 1024, 4.0))},
 }
 FILL_FRACTION = 0.95  # reference default 0.68 (V100 context-switch slack); B200 yields in us
 
@@ -223,7 +224,7 @@ def run_service_sweep(args, conf) -> None:
     from paper_2410_07192_b200.coordinator import SJF
     from paper_2410_07192_b200.engine import GPT2_SMALL_STAGE, GPT_8B_STAGE, GPTStage, StageEngine, measure_stage_times
     from paper_2410_07192_b200.executor import Executor
-    from paper_2410_07192_b200.fillmodels import BERT_BASE, BERT_LARGE, bert
+    from paper_2410_07192_b200.fillmodels import BERT_BASE, BERT_LARGE, bert, resnet50
     from paper_2410_07192_b200.profiler import measure_profile
     from paper_2410_07192_b200.service import FillService, ServiceConfig, predict, write_report
 
@@ -234,8 +235,9 @@ def run_service_sweep(args, conf) -> None:
     main_model = GPTStage(gcfg, seed=rank)
     tf_ms, tb_ms = measure_stage_times(main_model)
     registry, profiles = {}, {}
-    for name, fcfg in (("bert_base", BERT_BASE), ("bert_large", BERT_LARGE)):
-        m = bert(fcfg, seed=0)
+    for name, make in (("bert_base", lambda: bert(BERT_BASE, seed=0)),
+                       ("bert_large", lambda: bert(BERT_LARGE, seed=0)), ("resnet50", lambda: resnet50(seed=0))):
+        m = make()
         prof = measure_profile(m, conf["batch_sizes"])
         registry[prof.name], profiles[name] = m, prof
     _, hi_prio = torch.cuda.Stream.priority_range()
@@ -324,7 +326,8 @@ def run_service_sweep(args, conf) -> None:
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random-init weights, synthetic token ids)",
             "config": {"name": "c5", "workload": f"{P}-stage 1F1B {gcfg.hidden}-hidden main job, "
-                       "Placer(avg_jct) + per-stage SJF Coordinators, mixed BERT-base/BERT-large jobs, "
+                       "Placer(avg_jct) + per-stage SJF Coordinators, mixed BERT-base/BERT-large/ResNet-50 "
+                       "inference jobs, "
                        "free-memory cap sweep (stages time-multiplexed on one GPU)",
                        "jobs": [list(j) for j in conf["jobs"]], "caps_gb": list(conf["caps_gb"]),
                        "max_batches_per_bubble": conf["max_batches"], "fill_fraction": args.fill_fraction,

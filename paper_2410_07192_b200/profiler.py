@@ -26,10 +26,13 @@ FIXED_TRANSIENT_BYTES = 1 << 20  # control block, cursors, alignment slack
 
 def _module_mem(model: FillSequential, i: int, b: int) -> tuple[int, int]:
     """(weight bytes, transient bytes at batch b) of module i as the executor lays it
-    out: its workspace, the partition-input buffer (if a partition starts here), the
-    batch's inputs and results, and the control block."""
+    out. A partition's workspace is the union (per buffer name, the largest size) of
+    its modules' buffers, so every module is charged the union over the whole model:
+    then "weights + max transient" of any partition -- the planner's peak
+    (partition.py:143-150) -- bounds the executor's partition region. Plus the
+    partition-input buffer, the batch's inputs and results, and the control block."""
     w = model[i].weight_bytes()
-    ws = sum(2 * v for v in model[i].workspace(b).values())
+    ws = sum(2 * v for v in model.workspace(0, len(model), b).values())
     res = 2 * b
     for d in model.result_shape():
         res *= d
