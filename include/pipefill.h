@@ -131,6 +131,13 @@ int pf_copy2d(void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch, 
 int pf_gemm(const void* X, const void* W, const void* bias, const void* residual, void* Y,
             int M, int N, int K, uint32_t epilogue, const pf_ctl_t* ctl, void* stream);
 int pf_gemm_units(int M, int N, int K, uint32_t* out_units);
+/* Split-K GEMM (weight gradients: K = batch x pixels is long, M x N is small):
+ * Y[z] = X[:, Kz] · W[:, Kz]^T for the z-th of `splits` K slices (each >= 1 K-block of
+ * 64), Y a [splits, M, N] bf16 stack the consumer sums in fp32 (pf_sgd_update).
+ * pf_gemm_splitk_splits gives the effective slice count for a request.               */
+int pf_gemm_splitk(const void* X, const void* W, void* Y, int M, int N, int K, int splits,
+                   const pf_ctl_t* ctl, void* stream);
+int pf_gemm_splitk_splits(int K, int requested, int* out_splits);
 
 /* Y = LayerNorm(X + residual) * gamma + beta, per row of `cols` (residual may be
  * NULL). fp32 statistics, two-pass variance. Work units = ceil(rows/rows_per_unit). */
@@ -177,6 +184,59 @@ int pf_maxpool(const void* X, void* Y, int B, int H, int W, int C, int k, int st
 int pf_avgpool(const void* X, void* Y, int B, int HW, int C, const pf_ctl_t* ctl, void* stream);
 int pf_image_units(int kind, long long out_elems, int C, uint32_t* out_units);
 
+/* ---- training fill jobs (ResNet-50 fwd + bwd + SGD), NHWC bf16 as [M, C] --------
+ * BatchNorm batch statistics: pf_colstats writes per-CTA partials (sum x, sum x^2) of
+ * X[M, C] (or, with G given, (sum dA, sum dA*xhat), dA = G*[Ymask > 0]) to
+ * partial[P, 2C] fp32 and reports P (<= 512); pf_bn_finalize turns them into mean,
+ * invstd and scale = gamma*invstd, shift = beta - mean*scale; pf_bn_bwd_finalize into
+ * dbeta (= column sums) and dgamma (may be NULL). pf_bn_apply: Y = act(X*scale + shift
+ * [+ R]). pf_bn_bwd_apply: dX = gamma*invstd*(dA - dbeta/M - xhat*dgamma/M), dA
+ * optionally written too. C % 8 == 0, C <= 2048.                                     */
+int pf_colstats(const void* X, const void* G, const void* Ymask, const float* mean, const float* invstd,
+                float* partial, int M, int C, int* out_partials, const pf_ctl_t* ctl, void* stream);
+int pf_bn_finalize(const float* partial, int P, int M, int C, const float* gamma, const float* beta,
+                   float eps, float* mean, float* invstd, float* scale, float* shift, const pf_ctl_t* ctl,
+                   void* stream);
+int pf_bn_bwd_finalize(const float* partial, int P, int C, float* dgamma, float* dbeta,
+                       const pf_ctl_t* ctl, void* stream);
+int pf_bn_apply(const void* X, const float* scale, const float* shift, const void* R, void* Y, long long M,
+                int C, int relu, const pf_ctl_t* ctl, void* stream);
+int pf_bn_bwd_apply(const void* X, const void* G, const void* Ymask, const float* mean, const float* invstd,
+                    const float* gamma, const float* dgamma, const float* dbeta, void* dX, void* dA, int M,
+                    int C, const pf_ctl_t* ctl, void* stream);
+/* Y[C, R] = X[R, C]^T (bf16), the operand layout of dgrad / wgrad GEMMs.              */
+int pf_transpose(const void* X, void* Y, int R, int C, const pf_ctl_t* ctl, void* stream);
+/* Inverse of pf_im2col as a gather: dX = sum of the dCol entries that read each input
+ * element [+ R] (deterministic, no atomics).                                           */
+int pf_col2im(const void* dCol, const void* R, void* dX, int B, int H, int W, int C, int kh, int kw,
+              int stride, int pad, int Kp, const pf_ctl_t* ctl, void* stream);
+/* Max-pool backward: the gradient goes to the first maximum of each window.          */
+int pf_maxpool_bwd(const void* X, const void* dY, void* dX, int B, int H, int W, int C, int k, int stride,
+                   int pad, const pf_ctl_t* ctl, void* stream);
+int pf_avgpool_bwd(const void* dY, void* dX, int B, int HW, int C, const pf_ctl_t* ctl, void* stream);
+/* Softmax cross-entropy, warp per row: loss[4*b] = logsumexp(Z_b) - Z_b[label_b],
+ * dZ = (softmax(Z) - onehot) * grad_scale. labels int32, 4-word stride per sample.   */
+int pf_softmax_xent(const void* Z, const int32_t* labels, float* loss, void* dZ, int B, int N,
+                    float grad_scale, const pf_ctl_t* ctl, void* stream);
+/* SGD with momentum over parameter segments in one launch: g = sum of `splits` bf16
+ * partials (grad_kind 0, split_stride elements apart) or fp32 (grad_kind 1);
+ * g += weight_decay*w; v = momentum*v + g; w -= lr*v on the fp32 master; the bf16
+ * working copy (may be NULL) is rewritten. Claims 4096-element units through the
+ * cursor (resumable prefix: never applies an update twice).                         */
+typedef struct {
+  float* master;
+  float* momentum;
+  void* work;
+  const void* grad;
+  long long n;
+  long long split_stride;
+  int splits;
+  int grad_kind;
+  float weight_decay;
+} pf_sgd_segment_t;
+int pf_sgd_update(const pf_sgd_segment_t* segs, int nseg, float lr, float momentum, const pf_ctl_t* ctl,
+                  void* stream);
+
 /* ---- chain control ------------------------------------------------------------
  * Resets the per-node cursors of a chain when the chain has not been aborted
  * (a one-thread kernel: `if (!*abort) cursors[0..n) = 0`), and counts completed
@@ -213,7 +273,31 @@ int pf_chain_add_embedding_ln(pf_chain_t* chain, const int32_t* ids, const int32
                               const void* gamma, const void* beta, void* Y, int batch, int seq,
                               int hidden, int vocab, float eps);
 int pf_chain_add_copy(pf_chain_t* chain, void* dst, int64_t dst_pitch, const void* src,
-                      int64_t src_pitch, int64_t width, int64_t rows, int role);
+                      int64_t src_pitch, int64_t width, int64_t rows, int role);  /* role 0..3 */
+int pf_chain_add_gemm_splitk(pf_chain_t* chain, const void* X, const void* W, void* Y, int M, int N,
+                             int K, int splits);
+int pf_chain_add_colstats(pf_chain_t* chain, const void* X, const void* G, const void* Ymask,
+                          const float* mean, const float* invstd, float* partial, int M, int C,
+                          int* out_partials);
+int pf_chain_add_bn_finalize(pf_chain_t* chain, const float* partial, int P, int M, int C, const float* gamma,
+                             const float* beta, float eps, float* mean, float* invstd, float* scale,
+                             float* shift);
+int pf_chain_add_bn_bwd_finalize(pf_chain_t* chain, const float* partial, int P, int C, float* dgamma,
+                                 float* dbeta);
+int pf_chain_add_bn_apply(pf_chain_t* chain, const void* X, const float* scale, const float* shift,
+                          const void* R, void* Y, long long M, int C, int relu);
+int pf_chain_add_bn_bwd_apply(pf_chain_t* chain, const void* X, const void* G, const void* Ymask,
+                              const float* mean, const float* invstd, const float* gamma, const float* dgamma,
+                              const float* dbeta, void* dX, void* dA, int M, int C);
+int pf_chain_add_transpose(pf_chain_t* chain, const void* X, void* Y, int R, int C);
+int pf_chain_add_col2im(pf_chain_t* chain, const void* dCol, const void* R, void* dX, int B, int H, int W,
+                        int C, int kh, int kw, int stride, int pad, int Kp);
+int pf_chain_add_maxpool_bwd(pf_chain_t* chain, const void* X, const void* dY, void* dX, int B, int H, int W,
+                             int C, int k, int stride, int pad);
+int pf_chain_add_avgpool_bwd(pf_chain_t* chain, const void* dY, void* dX, int B, int HW, int C);
+int pf_chain_add_softmax_xent(pf_chain_t* chain, const void* Z, const int32_t* labels, float* loss, void* dZ,
+                              int B, int N, float grad_scale);
+int pf_chain_add_sgd(pf_chain_t* chain, const pf_sgd_segment_t* segs, int nseg, float lr, float momentum);
 int pf_chain_add_im2col(pf_chain_t* chain, const void* X, void* Col, int B, int H, int W, int C,
                         int kh, int kw, int stride, int pad, int Kp);
 int pf_chain_add_maxpool(pf_chain_t* chain, const void* X, void* Y, int B, int H, int W, int C,
@@ -223,9 +307,12 @@ int pf_chain_size(pf_chain_t* chain, int* out_nodes);
 /* units = work units of the node; resumable = 1 for claimed-prefix nodes (GEMM tiles),
  * 0 for atomic nodes that are re-run whole (cursor must be reset to 0 first).       */
 int pf_chain_node_info(pf_chain_t* chain, int node, uint32_t* out_units, int* out_resumable);
-/* Device-side batch descriptors: with desc set, copy nodes of role 1/2 take their
- * batch-slice offsets from desc[2 * (*done) + role - 1] (int64 pairs in device memory),
- * so one recorded graph serves every batch of a bubble.                            */
+/* Device-side batch descriptors: with desc set, copy nodes of role r in 1..3 take
+ * their batch-slice offset from desc[PF_DESC_WORDS * (*done) + r - 1] (int64 words in
+ * device memory), so one recorded graph serves every batch of a bubble. Role 1 adds
+ * it to the source (the batch's inputs), role 2 to the destination (its results),
+ * role 3 to the source (a second input stream, e.g. a training job's labels).      */
+#define PF_DESC_WORDS 4
 int pf_chain_set_desc(pf_chain_t* chain, const int64_t* desc);
 /* In-kernel timing: node i of a launch writes [earliest CTA start, latest CTA end]
  * (%globaltimer ns) to stamps[2i], stamps[2i+1] (GEMM nodes; reset at chain begin).   */

@@ -68,6 +68,10 @@ struct Params {
   int M, N, K;
   int tiles_m, tiles_n;
   unsigned long long* stamp;  // optional [first CTA start, last CTA end] in ns
+  // split-K (single-CTA kernel only): k_splits slices of kb_per_split K-blocks each;
+  // slice z of output tile (tm, tn) is stored to Y[z] of a [k_splits, M, N] stack
+  int k_splits;
+  int kb_per_split;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -100,7 +104,10 @@ __shared__ unsigned long long s_gemm_diag[16];
 #define DIAG_FLUSH()
 #endif
 
-__device__ __forceinline__ void tile_coords(int tile, const Params& p, int& tm, int& tn) {
+__device__ __forceinline__ void tile_coords(int tile, const Params& p, int& tm, int& tn, int& ks) {
+  const int per_split = p.tiles_m * p.tiles_n;
+  ks = tile / per_split;
+  tile -= ks * per_split;
   const int per_group = GROUP_M * p.tiles_n;
   const int g = tile / per_group;
   const int first_m = g * GROUP_M;
@@ -119,7 +126,7 @@ template <int CHUNKS, uint32_t EPI, bool PAIR>
 __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap* tmY,
                                               uint8_t* stg, uint32_t taddr0, uint64_t* tfull,
                                               uint32_t aphase, int row_base, int col_base,
-                                              __nv_bfloat16* my_bias) {
+                                              __nv_bfloat16* my_bias, int ks) {
   constexpr bool HAS_BIAS = (EPI & PF_EPI_BIAS) != 0;
   constexpr bool HAS_GELU = (EPI & PF_EPI_GELU) != 0;
   constexpr bool HAS_RES = (EPI & PF_EPI_RESIDUAL) != 0;
@@ -240,7 +247,8 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
     fence_async_smem();
     __syncwarp();
     if (lane == 0 && col0 < p.N) {
-      tma_store_2d(tmY, stg, col0, row_base);
+      if (p.k_splits > 1) tma_store_3d(tmY, stg, col0, row_base, ks);
+      else tma_store_2d(tmY, stg, col0, row_base);
       bulk_commit();
     }
   }
@@ -303,7 +311,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
 
-  const int num_tiles = p.tiles_m * p.tiles_n;
+  const int num_tiles = p.tiles_m * p.tiles_n * p.k_splits;
   const int num_kb = (p.K + BK - 1) / BK;
 
   if (warp == PRODUCER_WARP) {
@@ -326,9 +334,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         sphase ^= 1u;
       }
       if (tile < 0) break;
-      int tm, tn;
-      tile_coords(tile, p, tm, tn);
-      for (int kb = 0; kb < num_kb; ++kb) {
+      int tm, tn, ks;
+      tile_coords(tile, p, tm, tn, ks);
+      const int kb0 = ks * p.kb_per_split;
+      const int kb1 = min(num_kb, kb0 + p.kb_per_split);
+      for (int kb = kb0; kb < kb1; ++kb) {
         {
           DIAG_T0();
           mbar_wait(&empty_bar[stage], phase ^ 1u);
@@ -379,7 +389,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const long long _tm0 = clock64();
 #endif
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-      for (int kb = 0; kb < num_kb; ++kb) {
+      const int kb0 = (tile / (p.tiles_m * p.tiles_n)) * p.kb_per_split;
+      const int kb1 = min(num_kb, kb0 + p.kb_per_split);
+      for (int kb = kb0; kb < kb1; ++kb) {
         {
           DIAG_T0();
           mbar_wait(&full_bar[stage], phase);
@@ -394,7 +406,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // K advance inside the 128-B swizzle atom: +32 B per UMMA_K step
             const uint64_t ad = umma_desc_sw128_kmajor(a_addr + k * UMMA_K * 2);
             const uint64_t bd = umma_desc_sw128_kmajor(b_addr + k * UMMA_K * 2);
-            umma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            umma_bf16_ss(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           }
           umma_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs retire
         }
@@ -442,14 +454,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         sphase ^= 1u;
       }
       if (tile < 0) break;
-      int tm, tn;
-      tile_coords(tile, p, tm, tn);
+      int tm, tn, ks;
+      tile_coords(tile, p, tm, tn, ks);
       const int row_base = tm * BM + lane_grp * 32;
       const int col_base = tn * BN + col_half * C::COLS_PER_EPI_WARP;
       const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) +
                              (uint32_t)(acc * BN + col_half * C::COLS_PER_EPI_WARP);
       epilogue_tile<C::CHUNKS, EPI, false>(p, &tmY, my_stg, taddr, &tfull_bar[acc], aphase, row_base,
-                                           col_base, my_bias);
+                                           col_base, my_bias, ks);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
@@ -602,8 +614,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         sphase ^= 1u;
       }
       if (tile < 0) break;
-      int tm, tn;
-      tile_coords(tile, p, tm, tn);
+      int tm, tn, ks;
+      tile_coords(tile, p, tm, tn, ks);
       for (int kb = 0; kb < num_kb; ++kb) {
         {
           DIAG_T0();
@@ -725,14 +737,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         sphase ^= 1u;
       }
       if (tile < 0) break;
-      int tm, tn;
-      tile_coords(tile, p, tm, tn);
+      int tm, tn, ks;
+      tile_coords(tile, p, tm, tn, ks);
       const int row_base = tm * PM + (int)rank * BM + lane_grp * 32;
       const int col_base = tn * BN + col_half * C::COLS_PER_EPI_WARP;
       const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) +
                              (uint32_t)(acc * BN + col_half * C::COLS_PER_EPI_WARP);
       epilogue_tile<C::CHUNKS, EPI, true>(p, &tmY, my_stg, taddr, &tfull_bar[acc], aphase, row_base,
-                                          col_base, my_bias);
+                                          col_base, my_bias, 0);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader0 + (uint32_t)(acc * 8));
@@ -801,6 +813,30 @@ static int make_tmap_store(CUtensorMap* map, const void* base, int rows, int col
                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(PF_ERR_CUDA, "output tensor map failed (%d)", (int)r);
   return PF_OK;
+}
+
+// Split-K output map: a [splits, rows, cols] stack, box 32 x 32 x 1, 64-B swizzle
+// (clipped per slice, so a ragged last m-tile never spills into the next slice).
+static int make_tmap_store_3d(CUtensorMap* map, const void* base, int splits, int rows, int cols) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return set_error(PF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)splits};
+  cuuint64_t strides[2] = {(cuuint64_t)cols * 2, (cuuint64_t)rows * cols * 2};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(PF_ERR_CUDA, "split-K output tensor map failed (%d)", (int)r);
+  return PF_OK;
+}
+
+// Effective split count: every slice gets >= 1 K-block.
+static int effective_splits(int K, int requested) {
+  const int kb = (K + BK - 1) / BK;
+  int s = requested < 1 ? 1 : (requested > kb ? kb : requested);
+  const int per = (kb + s - 1) / s;
+  return (kb + per - 1) / per;
 }
 
 // BN choice: minimise (waves x BN), the per-SM tensor-pipe time, on 148 SMs.
@@ -875,6 +911,8 @@ struct GemmPairOp final : PreparedOp {
     p.tiles_m = (M + 2 * BM - 1) / (2 * BM);
     p.tiles_n = (N + BN - 1) / BN;
     p.stamp = nullptr;
+    p.k_splits = 1;
+    p.kb_per_split = (K + BK - 1) / BK;
     const int tiles = p.tiles_m * p.tiles_n;
     const int pairs = device_sm_count() / 2;
     grid = 2 * (tiles < pairs ? tiles : pairs);
@@ -944,13 +982,27 @@ struct GemmOp final : PreparedOp {
     p.tiles_m = (M + BM - 1) / BM;
     p.tiles_n = (N + BN - 1) / BN;
     p.stamp = nullptr;
+    p.k_splits = 1;
+    p.kb_per_split = (K + BK - 1) / BK;
     const int tiles = p.tiles_m * p.tiles_n;
     const int sms = device_sm_count();
     grid = tiles < sms ? tiles : sms;
     epi = e & 15u;
     return PF_OK;
   }
-  uint32_t units() const override { return (uint32_t)(p.tiles_m * p.tiles_n); }
+  // Split-K: Y is a [splits, M, N] stack of partial products over K slices (no epilogue).
+  int prepare_splitk(const void* X, const void* W, void* Y, int M, int N, int K, int splits) {
+    PF_TRY(prepare(X, W, nullptr, nullptr, Y, M, N, K, 0u));
+    const int kb = (K + BK - 1) / BK;
+    p.k_splits = effective_splits(K, splits);
+    p.kb_per_split = (kb + p.k_splits - 1) / p.k_splits;
+    if (p.k_splits > 1) PF_TRY(make_tmap_store_3d(&ty, Y, p.k_splits, M, N));
+    const int tiles = p.tiles_m * p.tiles_n * p.k_splits;
+    const int sms = device_sm_count();
+    grid = tiles < sms ? tiles : sms;
+    return PF_OK;
+  }
+  uint32_t units() const override { return (uint32_t)(p.tiles_m * p.tiles_n * p.k_splits); }
   bool resumable() const override { return true; }
   int run(const pf_ctl_t* ctl, cudaStream_t stream, const LaunchArgs& a) override {
     Params p = this->p;
@@ -1026,6 +1078,56 @@ int make_gemm_op(OpPtr* out, const void* X, const void* W, const void* bias, con
 }
 
 }  // namespace pf
+
+namespace pf {
+
+int make_gemm_splitk_op(OpPtr* out, const void* X, const void* W, void* Y, int M, int N, int K,
+                        int splits) {
+  if (!X || !W || !Y || M <= 0 || N <= 0 || K <= 0 || splits < 1)
+    return set_error(PF_ERR_INVALID, "pf_gemm_splitk: null pointer or non-positive shape");
+  if (K % 8 != 0 || N % 8 != 0)
+    return set_error(PF_ERR_INVALID, "pf_gemm_splitk: K and N must be multiples of 8 (16-B rows)");
+  if (((uintptr_t)X | (uintptr_t)W | (uintptr_t)Y) & 15u)
+    return set_error(PF_ERR_INVALID, "pf_gemm_splitk: pointers must be 16-B aligned");
+  if (!device_is_sm100()) return set_error(PF_ERR_UNSUPPORTED, "pf_gemm_splitk: needs an sm_100 device");
+  switch (gemm::pick_bn(M, N)) {
+    case 256: {
+      auto op = std::make_unique<gemm::GemmOp<256>>();
+      PF_TRY(op->prepare_splitk(X, W, Y, M, N, K, splits));
+      *out = std::move(op);
+      return PF_OK;
+    }
+    case 192: {
+      auto op = std::make_unique<gemm::GemmOp<192>>();
+      PF_TRY(op->prepare_splitk(X, W, Y, M, N, K, splits));
+      *out = std::move(op);
+      return PF_OK;
+    }
+    default: {
+      auto op = std::make_unique<gemm::GemmOp<128>>();
+      PF_TRY(op->prepare_splitk(X, W, Y, M, N, K, splits));
+      *out = std::move(op);
+      return PF_OK;
+    }
+  }
+}
+
+}  // namespace pf
+
+extern "C" int pf_gemm_splitk(const void* X, const void* W, void* Y, int M, int N, int K, int splits,
+                              const pf_ctl_t* ctl, void* stream) {
+  using namespace pf;
+  PF_TRY(validate_ctl(ctl));
+  OpPtr op;
+  PF_TRY(make_gemm_splitk_op(&op, X, W, Y, M, N, K, splits));
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), pf::LaunchArgs{});
+}
+
+extern "C" int pf_gemm_splitk_splits(int K, int requested, int* out_splits) {
+  if (!out_splits || K <= 0) return pf::set_error(PF_ERR_INVALID, "pf_gemm_splitk_splits");
+  *out_splits = pf::gemm::effective_splits(K, requested);
+  return PF_OK;
+}
 
 extern "C" int pf_gemm_diag(unsigned long long* out8, int reset) {
 #ifdef PF_GEMM_DIAG

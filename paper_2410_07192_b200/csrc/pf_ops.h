@@ -33,6 +33,27 @@ using OpPtr = std::unique_ptr<PreparedOp>;
 
 int make_gemm_op(OpPtr* out, const void* X, const void* W, const void* bias, const void* residual,
                  void* Y, int M, int N, int K, uint32_t epi);
+int make_gemm_splitk_op(OpPtr* out, const void* X, const void* W, void* Y, int M, int N, int K,
+                        int splits);
+int make_transpose_op(OpPtr* out, const void* X, void* Y, int R, int C);
+int make_colstats_op(OpPtr* out, const void* X, const void* G, const void* Ymask, const float* mean,
+                     const float* invstd, float* partial, int M, int C, int* out_partials);
+int make_bn_finalize_op(OpPtr* out, const float* partial, int P, int M, int C, const float* gamma,
+                        const float* beta, float eps, float* mean, float* invstd, float* scale, float* shift);
+int make_bn_bwd_finalize_op(OpPtr* out, const float* partial, int P, int C, float* dgamma, float* dbeta);
+int make_bn_apply_op(OpPtr* out, const void* X, const float* scale, const float* shift, const void* R, void* Y,
+                     long long M, int C, int relu);
+int make_bn_bwd_apply_op(OpPtr* out, const void* X, const void* G, const void* Ymask, const float* mean,
+                         const float* invstd, const float* gamma, const float* dgamma, const float* dbeta,
+                         void* dX, void* dA, int M, int C);
+int make_col2im_op(OpPtr* out, const void* dCol, const void* R, void* dX, int B, int H, int W, int C, int kh,
+                   int kw, int stride, int pad, int Kp);
+int make_maxpool_bwd_op(OpPtr* out, const void* X, const void* dY, void* dX, int B, int H, int W, int C, int k,
+                        int stride, int pad);
+int make_avgpool_bwd_op(OpPtr* out, const void* dY, void* dX, int B, int HW, int C);
+int make_xent_op(OpPtr* out, const void* Z, const int32_t* labels, float* loss, void* dZ, int B, int N,
+                 float grad_scale);
+int make_sgd_op(OpPtr* out, const pf_sgd_segment_t* segs, int nseg, float lr, float momentum);
 int make_norm_op(OpPtr* out, bool rms, const void* X, const void* residual, const void* gamma,
                  const void* beta, void* Y, int rows, int cols, float eps);
 int make_softmax_op(OpPtr* out, const void* X, void* Y, int rows, int cols, float scale);

@@ -133,8 +133,8 @@ __global__ void __launch_bounds__(COPY_THREADS) copy_kernel(uint4* __restrict__ 
   __syncthreads();
   if (!s_go) return;
   if (desc != nullptr && role != 0) {  // batch slice offset chosen on the device
-    const int64_t off = desc[2 * (int64_t)ld_volatile_u32(idx) + role - 1];
-    if (role == 1) src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(src) + off);
+    const int64_t off = desc[PF_DESC_WORDS * (int64_t)ld_volatile_u32(idx) + role - 1];
+    if (role != 2) src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(src) + off);
     else dst = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(dst) + off);
   }
   const uint64_t per = COPY_BYTES_PER_CTA / 16;
@@ -189,7 +189,8 @@ struct CopyOp final : PreparedOp {
 
 int make_copy_op(OpPtr* out, void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch,
                  int64_t width, int64_t rows, int role) {
-  if (!dst || !src || width < 0 || rows < 0) return set_error(PF_ERR_INVALID, "pf_copy: bad arguments");
+  if (!dst || !src || width < 0 || rows < 0 || role < 0 || role > 3)
+    return set_error(PF_ERR_INVALID, "pf_copy: bad arguments");
   if ((width | dst_pitch | src_pitch) & 15 || (((uintptr_t)dst | (uintptr_t)src) & 15u))
     return set_error(PF_ERR_INVALID, "pf_copy: sizes, pitches and pointers must be 16-B aligned");
   auto op = std::make_unique<CopyOp>();
@@ -539,6 +540,64 @@ int pf_chain_add_softmax(pf_chain_t* c, const void* X, void* Y, int rows, int co
   if (!c) return pf::set_error(PF_ERR_INVALID, "null chain");
   pf::OpPtr op;
   return chain_push(c, pf::make_softmax_op(&op, X, Y, rows, cols, scale), op);
+}
+
+int pf_chain_add_gemm_splitk(pf_chain_t* c, const void* X, const void* W, void* Y, int M, int N, int K,
+                             int splits) {
+  if (!c) return pf::set_error(PF_ERR_INVALID, "null chain");
+  pf::OpPtr op;
+  return chain_push(c, pf::make_gemm_splitk_op(&op, X, W, Y, M, N, K, splits), op);
+}
+
+#define PF_CHAIN_ADD(MAKE)                          \
+  do {                                              \
+    if (!c) return pf::set_error(PF_ERR_INVALID, "null chain"); \
+    pf::OpPtr op;                                   \
+    return chain_push(c, MAKE, op);                 \
+  } while (0)
+
+int pf_chain_add_colstats(pf_chain_t* c, const void* X, const void* G, const void* Ymask, const float* mean,
+                          const float* invstd, float* partial, int M, int C, int* out_partials) {
+  PF_CHAIN_ADD(pf::make_colstats_op(&op, X, G, Ymask, mean, invstd, partial, M, C, out_partials));
+}
+int pf_chain_add_bn_finalize(pf_chain_t* c, const float* partial, int P, int M, int C, const float* gamma,
+                             const float* beta, float eps, float* mean, float* invstd, float* scale,
+                             float* shift) {
+  PF_CHAIN_ADD(pf::make_bn_finalize_op(&op, partial, P, M, C, gamma, beta, eps, mean, invstd, scale, shift));
+}
+int pf_chain_add_bn_bwd_finalize(pf_chain_t* c, const float* partial, int P, int C, float* dgamma,
+                                 float* dbeta) {
+  PF_CHAIN_ADD(pf::make_bn_bwd_finalize_op(&op, partial, P, C, dgamma, dbeta));
+}
+int pf_chain_add_bn_apply(pf_chain_t* c, const void* X, const float* scale, const float* shift, const void* R,
+                          void* Y, long long M, int C, int relu) {
+  PF_CHAIN_ADD(pf::make_bn_apply_op(&op, X, scale, shift, R, Y, M, C, relu));
+}
+int pf_chain_add_bn_bwd_apply(pf_chain_t* c, const void* X, const void* G, const void* Ymask, const float* mean,
+                              const float* invstd, const float* gamma, const float* dgamma, const float* dbeta,
+                              void* dX, void* dA, int M, int C) {
+  PF_CHAIN_ADD(pf::make_bn_bwd_apply_op(&op, X, G, Ymask, mean, invstd, gamma, dgamma, dbeta, dX, dA, M, C));
+}
+int pf_chain_add_transpose(pf_chain_t* c, const void* X, void* Y, int R, int C) {
+  PF_CHAIN_ADD(pf::make_transpose_op(&op, X, Y, R, C));
+}
+int pf_chain_add_col2im(pf_chain_t* c, const void* dCol, const void* R, void* dX, int B, int H, int W, int C,
+                        int kh, int kw, int stride, int pad, int Kp) {
+  PF_CHAIN_ADD(pf::make_col2im_op(&op, dCol, R, dX, B, H, W, C, kh, kw, stride, pad, Kp));
+}
+int pf_chain_add_maxpool_bwd(pf_chain_t* c, const void* X, const void* dY, void* dX, int B, int H, int W, int C,
+                             int k, int stride, int pad) {
+  PF_CHAIN_ADD(pf::make_maxpool_bwd_op(&op, X, dY, dX, B, H, W, C, k, stride, pad));
+}
+int pf_chain_add_avgpool_bwd(pf_chain_t* c, const void* dY, void* dX, int B, int HW, int C) {
+  PF_CHAIN_ADD(pf::make_avgpool_bwd_op(&op, dY, dX, B, HW, C));
+}
+int pf_chain_add_softmax_xent(pf_chain_t* c, const void* Z, const int32_t* labels, float* loss, void* dZ, int B,
+                              int N, float grad_scale) {
+  PF_CHAIN_ADD(pf::make_xent_op(&op, Z, labels, loss, dZ, B, N, grad_scale));
+}
+int pf_chain_add_sgd(pf_chain_t* c, const pf_sgd_segment_t* segs, int nseg, float lr, float momentum) {
+  PF_CHAIN_ADD(pf::make_sgd_op(&op, segs, nseg, lr, momentum));
 }
 
 int pf_chain_add_im2col(pf_chain_t* c, const void* X, void* Col, int B, int H, int W, int C, int kh,

@@ -43,6 +43,7 @@ _CTL_WORDS = 64 + 4096  # [0]=abort, [1]=batches done, [8..12)=timestamps (2 x u
 _CURSOR0 = 64
 MAX_BATCHES = 64  # per bubble (device batch descriptors)
 MAX_NODES = 4096
+DESC_WORDS = 4  # PF_DESC_WORDS: (input, result, aux input, -) byte offsets per batch
 
 
 @dataclass
@@ -150,7 +151,7 @@ class Executor:
         # (WorkItem, model) from the stage's Coordinator, or None
         self.work_source: Optional[Callable[[], Optional[tuple[WorkItem, FillSequential]]]] = None
         self._ctl_host = PinnedBuffer((_CTL_WORDS,), torch.int32)
-        self._desc_host = PinnedBuffer((MAX_BATCHES, 2), torch.int64)
+        self._desc_host = PinnedBuffer((MAX_BATCHES, DESC_WORDS), torch.int64)
         self._stamps_host = PinnedBuffer((MAX_NODES, 2), torch.int64)
         self._chains: dict[tuple[int, int], _Chain] = {}
         self._staged_event: Optional[torch.cuda.Event] = None
@@ -249,7 +250,7 @@ class Executor:
         self._dev_views = {}
         self._ctl = self.arena.alloc((_CTL_WORDS,), torch.int32)
         self._ctl.zero_()
-        self._desc = self.arena.alloc((MAX_BATCHES, 2), torch.int64)
+        self._desc = self.arena.alloc((MAX_BATCHES, DESC_WORDS), torch.int64)
         self._stamps = self.arena.alloc((MAX_NODES, 2), torch.int64)
         region = 0
         for k in range(len(plan.partitions)):
@@ -503,7 +504,7 @@ class Executor:
                 self._ctl[_CURSOR0 + pr.resume_zero] = 0
                 pr.resume_zero = None
             native.call("pf_stage_h2d", self._desc.data_ptr(), self._desc_host.ptr,
-                        16 * len(batches), st.cuda_stream)
+                        8 * DESC_WORDS * len(batches), st.cuda_stream)
             native.call("pf_read_globaltimer", base + 32, st.cuda_stream)
             for first, cnt, node in batches:
                 ch = self._chain(pr.part, cnt, flag)

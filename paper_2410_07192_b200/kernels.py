@@ -303,3 +303,124 @@ def avgpool(
         out = torch.empty(b, c, dtype=torch.bfloat16, device=x.device)
     native.call("pf_avgpool", x.data_ptr(), out.data_ptr(), b, h * w, c, _ctl_ref(ctl), _stream(stream))
     return out
+
+
+# ---------------------------------------------------------------------------- training
+
+
+def gemm_splitk_splits(k: int, requested: int) -> int:
+    out = ctypes.c_int(0)
+    native.call("pf_gemm_splitk_splits", k, requested, ctypes.byref(out))
+    return out.value
+
+
+def gemm_splitk(x: torch.Tensor, weight: torch.Tensor, splits: int, *, out: Optional[torch.Tensor] = None,
+                ctl: Optional[KernelCtl] = None, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """[S, M, N] partial products of x[M, K] @ weight[N, K].T over S K-slices (pf_gemm_splitk)."""
+    _check_bf16_cuda("x", x)
+    _check_bf16_cuda("weight", weight)
+    m, k = x.shape
+    n = weight.shape[0]
+    s = gemm_splitk_splits(k, splits)
+    if out is None:
+        out = torch.empty(s, m, n, dtype=torch.bfloat16, device=x.device)
+    native.call("pf_gemm_splitk", x.data_ptr(), weight.data_ptr(), out.data_ptr(), m, n, k, splits,
+                _ctl_ref(ctl), _stream(stream))
+    return out
+
+
+def transpose(x: torch.Tensor, *, out=None, ctl=None, stream=None) -> torch.Tensor:
+    r, c = x.shape
+    if out is None:
+        out = torch.empty(c, r, dtype=torch.bfloat16, device=x.device)
+    native.call("pf_transpose", x.data_ptr(), out.data_ptr(), r, c, _ctl_ref(ctl), _stream(stream))
+    return out
+
+
+def colstats(x: torch.Tensor, partial: torch.Tensor, *, g=None, ymask=None, mean=None, invstd=None,
+             ctl=None, stream=None) -> int:
+    """Per-CTA column partials of x[M, C] into partial[P, 2C]; returns P (pf_colstats)."""
+    m, c = x.shape
+    p = ctypes.c_int(0)
+    native.call("pf_colstats", x.data_ptr(), _ptr(g), _ptr(ymask), _ptr(mean), _ptr(invstd),
+                partial.data_ptr(), m, c, ctypes.byref(p), _ctl_ref(ctl), _stream(stream))
+    return p.value
+
+
+def bn_finalize(partial, p, m, gamma, beta, eps, mean, invstd, scale, shift, *, ctl=None, stream=None):
+    c = gamma.numel()
+    native.call("pf_bn_finalize", partial.data_ptr(), p, m, c, gamma.data_ptr(), beta.data_ptr(), float(eps),
+                mean.data_ptr(), invstd.data_ptr(), scale.data_ptr(), shift.data_ptr(), _ctl_ref(ctl),
+                _stream(stream))
+
+
+def bn_bwd_finalize(partial, p, c, dgamma, dbeta, *, ctl=None, stream=None):
+    native.call("pf_bn_bwd_finalize", partial.data_ptr(), p, c, _ptr(dgamma), dbeta.data_ptr(),
+                _ctl_ref(ctl), _stream(stream))
+
+
+def bn_apply(x, scale, shift, out, *, residual=None, relu=False, ctl=None, stream=None):
+    m, c = x.shape
+    native.call("pf_bn_apply", x.data_ptr(), scale.data_ptr(), shift.data_ptr(), _ptr(residual),
+                out.data_ptr(), m, c, int(relu), _ctl_ref(ctl), _stream(stream))
+    return out
+
+
+def bn_bwd_apply(x, g, mean, invstd, gamma, dgamma, dbeta, dx, *, ymask=None, da=None, ctl=None, stream=None):
+    m, c = x.shape
+    native.call("pf_bn_bwd_apply", x.data_ptr(), g.data_ptr(), _ptr(ymask), mean.data_ptr(),
+                invstd.data_ptr(), gamma.data_ptr(), dgamma.data_ptr(), dbeta.data_ptr(), dx.data_ptr(),
+                _ptr(da), m, c, _ctl_ref(ctl), _stream(stream))
+    return dx
+
+
+def col2im(dcol, b, h, w, c, kh, kw, stride, pad, *, residual=None, out=None, ctl=None, stream=None):
+    kp = dcol.shape[-1]
+    if out is None:
+        out = torch.empty(b, h, w, c, dtype=torch.bfloat16, device=dcol.device)
+    native.call("pf_col2im", dcol.data_ptr(), _ptr(residual), out.data_ptr(), b, h, w, c, kh, kw, stride, pad,
+                kp, _ctl_ref(ctl), _stream(stream))
+    return out
+
+
+def maxpool_bwd(x, dy, k=3, stride=2, pad=1, *, out=None, ctl=None, stream=None):
+    b, h, w, c = x.shape
+    if out is None:
+        out = torch.empty_like(x)
+    native.call("pf_maxpool_bwd", x.data_ptr(), dy.data_ptr(), out.data_ptr(), b, h, w, c, k, stride, pad,
+                _ctl_ref(ctl), _stream(stream))
+    return out
+
+
+def avgpool_bwd(dy, hw, *, out=None, ctl=None, stream=None):
+    b, c = dy.shape
+    if out is None:
+        out = torch.empty(b, hw, c, dtype=torch.bfloat16, device=dy.device)
+    native.call("pf_avgpool_bwd", dy.data_ptr(), out.data_ptr(), b, hw, c, _ctl_ref(ctl), _stream(stream))
+    return out
+
+
+def softmax_xent(z, labels4, loss4, dz, grad_scale, *, ctl=None, stream=None):
+    b, n = z.shape
+    native.call("pf_softmax_xent", z.data_ptr(), labels4.data_ptr(), loss4.data_ptr(), dz.data_ptr(), b, n,
+                float(grad_scale), _ctl_ref(ctl), _stream(stream))
+
+
+def sgd_segments(segs: list[dict]):
+    arr = (native.SgdSegment * len(segs))()
+    for i, s in enumerate(segs):
+        arr[i].master = s["master"]
+        arr[i].momentum = s["momentum"]
+        arr[i].work = s.get("work")
+        arr[i].grad = s["grad"]
+        arr[i].n = s["n"]
+        arr[i].split_stride = s.get("split_stride", 0)
+        arr[i].splits = s.get("splits", 1)
+        arr[i].grad_kind = s.get("grad_kind", 0)
+        arr[i].weight_decay = s.get("weight_decay", 0.0)
+    return arr
+
+
+def sgd_update(segs: list[dict], lr: float, momentum: float, *, ctl=None, stream=None):
+    arr = sgd_segments(segs)
+    native.call("pf_sgd_update", arr, len(segs), float(lr), float(momentum), _ctl_ref(ctl), _stream(stream))

@@ -53,6 +53,14 @@ class PfCtl(ctypes.Structure):
     _fields_ = [("flag", c_void_p), ("abort", c_void_p), ("cursor", c_void_p)]
 
 
+class SgdSegment(ctypes.Structure):
+    """Mirror of pf_sgd_segment_t."""
+
+    _fields_ = [("master", c_void_p), ("momentum", c_void_p), ("work", c_void_p), ("grad", c_void_p),
+                ("n", ctypes.c_longlong), ("split_stride", ctypes.c_longlong), ("splits", c_int),
+                ("grad_kind", c_int), ("weight_decay", c_float)]
+
+
 _SIGNATURES: dict[str, tuple] = {
     "pf_abi_version": (c_int, []),
     "pf_last_error": (c_char_p, []),
@@ -119,6 +127,46 @@ _SIGNATURES: dict[str, tuple] = {
     "pf_chain_add_maxpool": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int,
                                      c_int, c_int]),
     "pf_chain_add_avgpool": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int]),
+    "pf_gemm_splitk": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, POINTER(PfCtl),
+                               c_void_p]),
+    "pf_gemm_splitk_splits": (c_int, [c_int, c_int, POINTER(c_int)]),
+    "pf_colstats": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int,
+                            POINTER(c_int), POINTER(PfCtl), c_void_p]),
+    "pf_bn_finalize": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_float, c_void_p,
+                               c_void_p, c_void_p, c_void_p, POINTER(PfCtl), c_void_p]),
+    "pf_bn_bwd_finalize": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, POINTER(PfCtl), c_void_p]),
+    "pf_bn_apply": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, ctypes.c_longlong, c_int, c_int,
+                            POINTER(PfCtl), c_void_p]),
+    "pf_bn_bwd_apply": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                c_void_p, c_void_p, c_void_p, c_int, c_int, POINTER(PfCtl), c_void_p]),
+    "pf_transpose": (c_int, [c_void_p, c_void_p, c_int, c_int, POINTER(PfCtl), c_void_p]),
+    "pf_col2im": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                          c_int, c_int, POINTER(PfCtl), c_void_p]),
+    "pf_maxpool_bwd": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                               POINTER(PfCtl), c_void_p]),
+    "pf_avgpool_bwd": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, POINTER(PfCtl), c_void_p]),
+    "pf_softmax_xent": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_float, POINTER(PfCtl),
+                                c_void_p]),
+    "pf_sgd_update": (c_int, [POINTER(SgdSegment), c_int, c_float, c_float, POINTER(PfCtl), c_void_p]),
+    "pf_chain_add_gemm_splitk": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int]),
+    "pf_chain_add_colstats": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                      c_int, c_int, POINTER(c_int)]),
+    "pf_chain_add_bn_finalize": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_float,
+                                         c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pf_chain_add_bn_bwd_finalize": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]),
+    "pf_chain_add_bn_apply": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                      ctypes.c_longlong, c_int, c_int]),
+    "pf_chain_add_bn_bwd_apply": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                          c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int]),
+    "pf_chain_add_transpose": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int]),
+    "pf_chain_add_col2im": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int,
+                                    c_int, c_int, c_int, c_int]),
+    "pf_chain_add_maxpool_bwd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int,
+                                         c_int, c_int, c_int]),
+    "pf_chain_add_avgpool_bwd": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int]),
+    "pf_chain_add_softmax_xent": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int,
+                                          c_float]),
+    "pf_chain_add_sgd": (c_int, [c_void_p, POINTER(SgdSegment), c_int, c_float, c_float]),
     "pf_chain_create": (c_int, [POINTER(c_void_p)]),
     "pf_chain_destroy": (c_int, [c_void_p]),
     "pf_chain_add_gemm": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
