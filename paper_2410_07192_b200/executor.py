@@ -173,7 +173,8 @@ class Executor:
 
     # ------------------------------------------------------------------ loading
 
-    _LAYOUT_ATTRS = ("_ctl", "_desc", "_stamps", "_region", "ws", "in_dev", "_cap", "_in_host",
+    _LAYOUT_ATTRS = ("_ctl", "_desc", "_stamps", "_region", "ws", "in_dev", "_cap", "_in_host", "_aux_host",
+                     "aux_dev",
                      "_results", "_store_dev", "_store_host", "_flops_frac", "_staged_part",
                      "_staged_event", "_chains", "model", "plan", "_dev_views", "_part_layouts")
 
@@ -209,6 +210,8 @@ class Executor:
         self.item = item
         self.progress = _Progress()
         self._in_host.tensor[:n].copy_(self.model.make_inputs(self.job_seed, item.entry.lo - 1, n))
+        if self._aux_host is not None:
+            self._aux_host.tensor[:n].copy_(self.model.make_aux(self.job_seed, item.entry.lo - 1, n))
         self._stage_partition(0)
         self.prewarm()
 
@@ -264,7 +267,10 @@ class Executor:
         self.in_dev = self.arena.alloc((max(bmax, 1), *in_shape), in_dtype)
         self._cap = cap
         self._in_host = PinnedBuffer((cap, *in_shape), in_dtype)
-        self._results = PinnedBuffer((cap, *model.result_shape()), torch.bfloat16)
+        self._results = PinnedBuffer((cap, *model.result_shape()), model.result_dtype())
+        aux = model.aux_spec()
+        self._aux_host = PinnedBuffer((cap, *aux[1]), aux[0]) if aux else None
+        self.aux_dev = self.arena.alloc((max(bmax, 1), *aux[1]), aux[0]) if aux else None
         self._store_dev = None
         self._store_host = None
         if len(plan.partitions) > 1:
@@ -313,17 +319,8 @@ class Executor:
         views: dict[int, dict] = {}
         for i in range(p.lo, p.hi):
             mod = self.model[i]
-            nbytes = mod.weight_bytes()
-            dflat = device_view(ptr, (nbytes // 2,), torch.bfloat16)
-            dev, off = {}, 0
-            for name, shape, _ in mod.param_specs():
-                nel = 1
-                for s_ in shape:
-                    nel *= s_
-                dev[name] = dflat[off:off + nel].view(*shape)
-                off += nel
-            views[i] = dev
-            ptr += _pad256(nbytes)
+            views[i] = mod.make_views(ptr)
+            ptr += _pad256(mod.weight_bytes())
         _, need = self._part_need(part)
         off = (ptr - base) // 2
         ws: dict[str, torch.Tensor] = {}
@@ -333,6 +330,14 @@ class Executor:
         lay = (views, ws)
         self._part_layouts[part] = lay
         return lay
+
+    def _module_ptr(self, part: int, i: int) -> int:
+        """Device address of module i's staged state inside the region."""
+        p = self.plan.partitions[part]
+        ptr = self._region.data_ptr()
+        for j in range(p.lo, i):
+            ptr += _pad256(self.model[j].weight_bytes())
+        return ptr
 
     def _stage_partition(self, part: int) -> None:
         """Stage partition `part`'s weights into the region on the copy stream (pinned
@@ -350,7 +355,7 @@ class Executor:
             for i in range(p.lo, p.hi):
                 mod = self.model[i]
                 nbytes = mod.weight_bytes()
-                dst = next(iter(views[i].values())).data_ptr() if views[i] else 0
+                dst = self._module_ptr(part, i)
                 if nbytes:
                     native.call("pf_stage_h2d", dst, mod.host.ptr, nbytes, self.copy_stream.cuda_stream)
                 self.h2d_bytes += nbytes
@@ -387,6 +392,8 @@ class Executor:
         model = self.model
         ch = _Chain()
         ctx = ExecContext(self.stream, ws, chain=ch.h)
+        if model.is_training:
+            return self._record_train_chain(key, ch, ctx, part, cnt, flag)
         # node 0: the batch's input slice (role 1: source + in_off)
         if part.lo == 0:
             nb = cnt * model.input_bytes()
@@ -420,6 +427,48 @@ class Executor:
         ch.build_graph(flag, base if flag else None, base + 4 * _CURSOR0 if flag else None, base + 4)
         self._chains[key] = ch
         return ch
+
+    def _record_train_chain(self, key: tuple, ch: _Chain, ctx: ExecContext, part, cnt: int,
+                            flag: Optional[int]) -> _Chain:
+        """One training step on one batch: inputs and labels in, forward, loss, backward,
+        optimizer step, per-sample losses out. Training plans run whole (one partition)."""
+        model = self.model
+        if part.lo != 0 or part.hi != len(model):
+            raise NotImplementedError("training fill jobs run single-partition plans")
+        nb = cnt * model.input_bytes()
+        native.call("pf_chain_add_copy", ch.h, self.in_dev.data_ptr(), nb, self._in_host.ptr, nb, nb, 1, 1)
+        ab = cnt * self._aux_host.tensor[0].numel() * self._aux_host.tensor.element_size()
+        native.call("pf_chain_add_copy", ch.h, self.aux_dev.data_ptr(), ab, self._aux_host.ptr, ab, ab, 1, 3)
+        ctx.node = 2
+        loss = ctx.fbuf("loss", cnt * 4).view(cnt, 4)
+        seg_ends, gemm_flops = model.record_step(self.in_dev[:cnt], self.aux_dev[:cnt], loss, ctx)
+        ch.seg_ends = seg_ends
+        ch.gemm_flops = gemm_flops
+        rb = cnt * 16
+        native.call("pf_chain_add_copy", ch.h, self._results.ptr, rb, loss.data_ptr(), rb, rb, 1, 2)
+        ch.finalize()
+        ch.seg_ends[-1] = len(ch.units)
+        native.call("pf_chain_set_desc", ch.h, self._desc.data_ptr())
+        native.call("pf_chain_set_stamps", ch.h, self._stamps.data_ptr())
+        base = self._ctl.data_ptr()
+        ch.build_graph(flag, base if flag else None, base + 4 * _CURSOR0 if flag else None, base + 4)
+        self._chains[key] = ch
+        return ch
+
+    def _write_back(self) -> None:
+        """Training jobs: copy the trained state of every module back to its pinned host
+        blob (copy stream, after the fill stream), so the next range -- or a restage after
+        an eviction -- continues from it."""
+        part = 0
+        with torch.cuda.stream(self.copy_stream):
+            self.copy_stream.wait_stream(self.stream)
+            for i in range(len(self.model)):
+                mod = self.model[i]
+                if mod.host is not None and mod.weight_bytes():
+                    native.call("pf_stage_d2h", mod.host.ptr, self._module_ptr(part, i), mod.weight_bytes(),
+                                self.copy_stream.cuda_stream)
+                    self.d2h_bytes += mod.weight_bytes()
+        self.copy_stream.synchronize()
 
     def _drop_chains(self) -> None:
         # safe with launches in flight: kernel parameters are copied at launch time
@@ -475,7 +524,8 @@ class Executor:
             return prev
         model = self.model
         in_b = model.input_bytes() if part.lo == 0 else model.boundary_elems(part.lo) * 2
-        res_b = 2 * _numel(model.result_shape())
+        res_b = self._results.tensor.element_size() * _numel(model.result_shape())
+        aux_b = 0 if self._aux_host is None else self._aux_host.tensor[0].numel() * self._aux_host.tensor.element_size()
         out_b = res_b if part.hi == len(model) else model.boundary_elems(part.hi) * 2
         st = self.stream
         base = self._ctl.data_ptr()
@@ -490,6 +540,9 @@ class Executor:
         for k, (first, cnt, node) in enumerate(batches):
             dh[k, 0] = first * in_b
             dh[k, 1] = first * out_b
+            dh[k, 2] = first * aux_b
+            if node == 0 and aux_b:
+                self.h2d_bytes += cnt * aux_b
             if node == 0 and (part.lo == 0 or self._store_host is not None):
                 self.h2d_bytes += cnt * in_b
             if part.hi == len(model) or self._store_host is not None:
@@ -592,6 +645,8 @@ class Executor:
         if pr.resume is None and pr.next_sample >= n_total:
             if pr.part == len(self.plan.partitions) - 1:
                 pr.finished = True
+                if self.model.is_training:
+                    self._write_back()
             else:
                 pr.part += 1
                 pr.next_sample = 0

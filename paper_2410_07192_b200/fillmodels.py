@@ -100,6 +100,10 @@ class ExecContext:
     def buf(self, name: str, numel: int) -> torch.Tensor:
         return self.ws[name].view(-1)[:numel]
 
+    def fbuf(self, name: str, numel: int) -> torch.Tensor:
+        """fp32 view of a workspace buffer (its size is counted in bf16 elements: 2 per float)."""
+        return self.ws[name].view(-1)[:2 * numel].view(torch.float32)
+
     # -- nodes -----------------------------------------------------------------
     def _eager(self, fn, flops: float = 0.0) -> None:
         if not self.active():
@@ -254,6 +258,19 @@ class FillModule(nn.Module):
     def unstage(self) -> None:
         self.dev = {}
 
+    def make_views(self, ptr: int) -> dict[str, torch.Tensor]:
+        """Device tensors of this module's staged state starting at `ptr` (the layout of
+        its host blob: bf16 parameters in param_specs order)."""
+        nbytes = self.weight_bytes()
+        from .arena import device_view
+        dflat = device_view(ptr, (max(nbytes // 2, 1),), torch.bfloat16)
+        dev, off = {}, 0
+        for name, shape, _ in self.param_specs():
+            n = _numel(shape)
+            dev[name] = dflat[off:off + n].view(*shape)
+            off += n
+        return dev
+
     # -- execution ------------------------------------------------------------
     def workspace(self, batch: int) -> dict[str, int]:
         """Workspace buffers (bf16 elements) one batch of this module needs."""
@@ -389,10 +406,22 @@ class FillSequential(nn.Sequential):
     * ``make_inputs(job_seed, first, count)``: the job's synthetic samples
       [first, first + count), identical under any split into ranges and batches."""
 
+    is_training = False  # a training job: one chain = forward, loss, backward, optimizer step
+
     def __init__(self, cfg, modules: list[FillModule]):
         super().__init__(*modules)
         self.cfg = cfg
         self.profile = None  # set by profiler.measure_profile
+
+    def result_dtype(self) -> torch.dtype:
+        return torch.bfloat16
+
+    def aux_spec(self) -> Optional[tuple[torch.dtype, tuple[int, ...]]]:
+        """(dtype, per-sample shape) of a second per-sample input (labels), or None."""
+        return None
+
+    def make_aux(self, job_seed: int, first: int, count: int) -> torch.Tensor:
+        raise NotImplementedError
 
     def input_spec(self) -> tuple[torch.dtype, tuple[int, ...]]:
         raise NotImplementedError
