@@ -58,6 +58,10 @@ CONFIGS = {
            # Coordinator(max_batches_per_bubble=...) (coordinator.py:78-86): the reference
            # default 16 leaves 2/3 of a 100 ms GPipe bubble idle for a 5-layer partition
            "max_batches": 64},
+    # configs[3]: ResNet-50 fill-job TRAINING (fwd + bwd + SGD per batch) under 1F1B at 2/4/8 stages
+    "c4": {"stages": 8, "micro": 8, "schedule": "1f1b", "main": "gpt8b", "fill": "resnet50_train",
+           "batch_sizes": (32, 64), "arena_cap": 80 << 30, "chunk": 4096, "depths": (2, 4, 8),
+           "max_batches": 64},
     # configs[4]: multi-job queue -- Placer (avg-JCT routing) + per-stage SJF Coordinators,
     # mixed BERT-base / BERT-large / ResNet-50 inference jobs, bubble free-memory cap sweep
     "c5": {"stages": 8, "micro": 8, "schedule": "1f1b", "main": "gpt8b", "fill": "bert_large",
@@ -350,6 +354,178 @@ def run_service_sweep(args, conf) -> None:
         dist.destroy_process_group()
 
 
+def run_training_depths(args, conf) -> None:
+    """configs[3]: ResNet-50 training as the fill job of the 8B main job's 1F1B pipeline at
+    each depth p in conf["depths"]. At N=1 the p stages are emulated (artificial
+    neighbours) and visited round-robin, one iteration per step, like configs[1]; each
+    stage trains its own ResNet-50 job planned by the DP from a B200-measured training
+    profile. value = images trained per second of device time at the deepest pipeline."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2410_07192_b200 as pf
+    from paper_2410_07192_b200 import native
+    from paper_2410_07192_b200.engine import GPT2_SMALL_STAGE, GPT_8B_STAGE, GPTStage, StageEngine, measure_stage_times
+    from paper_2410_07192_b200.executor import Executor
+    from paper_2410_07192_b200.metrics import FillStats, aggregate, busy_in_bubbles, mean_slowdown
+    from paper_2410_07192_b200.profiler import measure_train_profile
+    from paper_2410_07192_b200.training import resnet50_train
+
+    native.require_device()
+    peaks = load_peaks()
+    gcfg = GPT_8B_STAGE if args.main == "gpt8b" else GPT2_SMALL_STAGE
+    main_model = GPTStage(gcfg, seed=rank)
+    tf_ms, tb_ms = measure_stage_times(main_model)
+    _, hi_prio = torch.cuda.Stream.priority_range()
+    streams = (torch.cuda.Stream(priority=hi_prio), torch.cuda.Stream(priority=hi_prio))
+    free_b, total_b = torch.cuda.mem_get_info()
+    probe_model = resnet50_train(seed=0)
+    profile = measure_train_profile(probe_model, conf["batch_sizes"])
+    torch.cuda.synchronize()
+    # the main job's peak with 8 microbatches in flight (stage 0 of the deepest pipeline)
+    probe = StageEngine(pf.PipelineConfig(max(conf["depths"]), conf["micro"], tf_ms, tb_ms,
+                                          pf.ScheduleKind.ONE_F_ONE_B, 1, 1, args.fill_fraction),
+                        0, main_model, None, streams=streams)
+    probe.set_anchor()
+    probe.run_iteration(0, fill=False)
+    torch.cuda.synchronize()
+    free_b, total_b = torch.cuda.mem_get_info()
+    reserved = torch.cuda.max_memory_reserved()
+    arena_bytes = int(min(max(0, total_b - reserved - (4 << 30)) * 0.9, conf["arena_cap"]))
+    executor = Executor(arena_bytes, job_seed=rank)
+    n_total = args.warmup + args.steps
+    results, stats_all = {}, []
+    with ClockSampler(local) as clocks:
+        for P in conf["depths"]:
+            pcfg = pf.PipelineConfig(P, conf["micro"], tf_ms, tb_ms, pf.ScheduleKind.ONE_F_ONE_B, arena_bytes,
+                                     arena_bytes, args.fill_fraction)
+            engines = {s_: StageEngine(pcfg, s_, main_model, executor, streams=streams) for s_ in range(P)}
+            models = {s_: resnet50_train(seed=s_) for s_ in range(P)}
+            for m_ in models.values():
+                m_.profile = profile
+            coords, items = {}, {}
+            for s_ in range(P):
+                coords[s_] = pf.Coordinator(s_, pf.build_bubble_cycle(pcfg, s_), 1,
+                                            pf.OrderingPolicy("concurrent", conf["chunk"]),
+                                            batch_sizes=list(conf["batch_sizes"]),
+                                            max_batches_per_bubble=conf["max_batches"])
+                coords[s_].admit(pf.JobSpec(f"train-{s_}", 0.0, profile, pf.JobKind.TRAINING, 1 << 22))
+
+            def next_work(s_):
+                prev = items.get(s_)
+                if prev is not None and not executor.busy:
+                    coords[s_].on_range_done(0, prev, 0.0)
+                item = coords[s_].request_work(0, 0.0)
+                items[s_] = item
+                return None if item is None else (item, models[s_])
+
+            def iterate(s_, fill):
+                eng = engines[s_]
+                eng.reset_stamps()
+                eng.set_anchor()
+                rec = eng.run_iteration(0, fill=fill)
+                if fill:
+                    executor.settle()
+                t = eng.record_timing(rec)
+                t["stage"] = s_
+                return t
+
+            off = {}
+            for s_ in range(P):
+                iterate(s_, False)
+                t = iterate(s_, False)
+                off[s_] = [t["main_end"] - t["start"]]
+            current = {"stage": None}
+
+            def step(k):
+                s_ = (rank + k * world) % P
+                if current["stage"] != s_:
+                    nxt = next_work(s_) if items.get(s_) is None else (items[s_], models[s_])
+                    if nxt is not None:
+                        executor.load(*nxt)
+                    executor.prewarm(engines[s_].words.flag.value)
+                    executor.work_source = lambda s__=s_: next_work(s__)
+                    current["stage"] = s_
+                    torch.cuda.synchronize()
+                return iterate(s_, True)
+
+            for k in range(args.warmup):
+                step(k)
+            executor.timing = True
+            executor.gemm_samples = []
+            n_rec0 = len(executor.records)
+            launches0 = executor.kernel_launches + sum(e.launches for e in engines.values())
+            steps = [step(k) for k in range(args.warmup, n_total)]
+            executor.timing = False
+            recs = executor.records[n_rec0:]
+            by_tag = {r_.tag: r_ for r_ in recs}
+            bubbles, fills, on_iter = [], [], {}
+            for t in steps:
+                on_iter.setdefault(t["stage"], []).append(t["main_end"] - t["start"])
+                for kind, t_set, t_clr, tag in t["bubbles"]:
+                    r_ = by_tag.get(tag)
+                    bubbles.append((t_set, t_clr))
+                    fills.append((r_.fill_start_ns, r_.fill_end_ns) if r_ is not None else (0, 0))
+            st = FillStats(
+                sample_equivalents=sum(r_.samples_done * r_.model_fraction for r_ in recs),
+                samples_completed=sum(r_.samples_completed for r_ in recs),
+                fill_busy_ns=busy_in_bubbles(bubbles, fills), bubble_ns=sum(b1 - b0 for b0, b1 in bubbles),
+                idle_ns=sum(pf.build_bubble_cycle(pcfg, t["stage"]).total_idle_us * 1000 for t in steps),
+                gemm_flops=sum(f for f, _ in executor.gemm_samples), gemm_ms=sum(ms for _, ms in executor.gemm_samples),
+                launches=executor.kernel_launches + sum(e.launches for e in engines.values()) - launches0,
+                device_s=sum(t["step_end"] - t["start"] for t in steps) / 1e9)
+            tot = aggregate(st, device=torch.device("cuda", local))
+            stats_all.append(tot)
+            results[str(P)] = {
+                "images_per_s": tot.value, "bubble_time_filled": tot.bubble_filled,
+                "bubble_time_filled_of_total_idle": tot.idle_filled,
+                "main_job_slowdown": mean_slowdown(on_iter, off),
+                "gemm_tflops_in_situ": tot.gemm_tflops, "sgd_steps": int(sum(r_.batches_done for r_ in recs)),
+                "plan_stage0": pf.plan_to_dict(coords[0].executables["train-0"]),
+                "ms_per_step": 1000 * tot.device_s / max(1, len(steps))}
+            executor.work_source = None
+            for m_ in models.values():
+                _ = m_
+    deepest = results[str(max(conf["depths"]))]
+    peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": deepest["images_per_s"], "unit": "images/s (training)", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": deepest["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init ResNet-50, N(0,1) 224x224 images, uniform labels)",
+            "config": {"name": "c4", "workload": "ResNet-50 training fill (fwd+bwd+SGD per batch, train-mode BN) in "
+                       "the bubbles of a 1F1B GPT-style 8B main job at 2/4/8 stages (artificial neighbours)",
+                       "depths": list(conf["depths"]), "batch_sizes": list(conf["batch_sizes"]),
+                       "fill_fraction": args.fill_fraction, "arena_bytes": arena_bytes,
+                       "t_fwd_ms": tf_ms, "t_bwd_ms": tb_ms,
+                       "train_step_ms": {str(b): profile_step_ms(profile, b) for b in conf["batch_sizes"]}},
+            "per_pipeline_depth": results,
+            "bubble_time_filled": deepest["bubble_time_filled"],
+            "main_job_slowdown": deepest["main_job_slowdown"],
+            "roofline": {"bound": "tensor", "achieved": deepest["gemm_tflops_in_situ"], "peak": peak,
+                         "unit": "TFLOP/s", "frac": deepest["gemm_tflops_in_situ"] / peak, "traffic": None,
+                         "kernel": "pf_gemm + pf_gemm_splitk (tcgen05)"},
+            "cpu_baseline": None,
+            "e2e": None, "gpu_launches": int(sum(t.launches for t in stats_all)), "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+        if args.out:
+            with open(args.out, "w") as fh:
+                fh.write(json.dumps(line) + "\n")
+    executor.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def profile_step_ms(profile, b: int) -> float:
+    return sum(layer.exec_time_ms[b] for layer in profile.layers)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -378,6 +554,9 @@ def main() -> None:
         return
     if args.config == "c5":
         run_service_sweep(args, conf)
+        return
+    if args.config == "c4":
+        run_training_depths(args, conf)
         return
 
     import torch

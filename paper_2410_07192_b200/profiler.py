@@ -107,3 +107,71 @@ def _module_flops(model: FillSequential, i: int) -> float:
     """Algorithmic forward FLOPs of module i per sample (BERT: 24*s*h^2 + 4*s^2*h per
     layer; ResNet: 2 * MACs of its convolutions and classifier)."""
     return model[i].flops_per_sample()
+
+
+def measure_train_profile(model: FillSequential, batch_sizes: Sequence[int], reps: int = 4,
+                          warmup: int = 2, name: str | None = None) -> ModelProfile:
+    """Profile of a training fill job (forward + loss + backward + SGD per batch).
+
+    A training step is one recorded chain over the whole model, so it is timed whole:
+    the executor runs `warmup + reps` steps at each batch size, one per (unbounded)
+    bubble, and the step time is the median of the in-kernel %globaltimer span of the
+    bubble's work. Module k is charged the step time x its share of the step's FLOPs
+    (the planner only sums layers for a training plan). Memory: module k's optimizer
+    state (fp32 master + momentum + bf16 working copy) plus, as transient, the step's
+    whole workspace (saved activations, gradients, scratch) and its inputs/results --
+    a training step keeps every module's activations alive until its backward."""
+    from fractions import Fraction  # noqa: F401  (plan types below use exact rationals)
+
+    from . import schedule as S
+    from .coordinator import Coordinator
+    from .executor import BubbleSlot, Executor
+    from .profiles import JobSpec
+
+    flops = [model[i].flops_per_sample() for i in range(len(model))]
+    total_f = sum(flops) or 1.0
+    sizes = sorted(batch_sizes)
+    step_ms: dict[int, float] = {}
+    for b in sizes:
+        layers = tuple(LayerProfile({b: 0.001}, {b: model[i].weight_bytes() + 1}, model[i].weight_bytes(), 1.0)
+                       for i in range(len(model)))
+        prof = ModelProfile("probe", layers, 1, frozenset({JobKind.TRAINING}))
+        cyc = S.BubbleCycle((S.BubbleSpec(10**6, 10**6, 10**12, S.BubbleKind.FWD_BWD),
+                             S.BubbleSpec(0, 0, 10**12, S.BubbleKind.FILL_DRAIN)), 2 * 10**6, 0)
+        coord = Coordinator(0, cyc, 1, batch_sizes=[b], max_batches_per_bubble=1)
+        coord.admit(JobSpec("probe", 0.0, prof, JobKind.TRAINING, b * (warmup + reps)))
+        item = coord.request_work(0, 0.0)
+        need = model.workspace(0, len(model), b)
+        arena_bytes = sum((model[i].weight_bytes() + 255) // 256 * 256 for i in range(len(model))) \
+            + 2 * sum((2 * v + 255) // 256 * 256 for v in need.values()) + b * model.input_bytes() + (256 << 20)
+        ex = Executor(arena_bytes)
+        try:
+            ex.load(item, model)
+            spans = []
+            for k in range(warmup + reps):
+                ex.fill(BubbleSlot(0, None, 0))
+                rec = ex.settle()
+                if k >= warmup and rec is not None and rec.fill_end_ns > rec.fill_start_ns:
+                    spans.append((rec.fill_end_ns - rec.fill_start_ns) / 1e6)
+            spans.sort()
+            step_ms[b] = spans[len(spans) // 2]
+        finally:
+            ex.close()
+    layers = []
+    for i in range(len(model)):
+        w = model[i].weight_bytes()
+        exec_ms, mem = {}, {}
+        prev_t = 0.0
+        for b in sizes:
+            need = model.workspace(0, len(model), b)
+            transient = sum(2 * v for v in need.values()) + b * model.input_bytes() + FIXED_TRANSIENT_BYTES
+            t = max(step_ms[b] * flops[i] / total_f, prev_t, 1e-3)
+            exec_ms[b], mem[b] = t, w + transient
+            prev_t = t
+        layers.append(LayerProfile(exec_time_ms=exec_ms, mem_bytes=mem, weight_bytes=w,
+                                   flops_per_sample=flops[i]))
+    params = sum(model[i].weight_bytes() // 10 for i in range(len(model)))
+    prof = ModelProfile(name=name or f"{model.cfg.name}-train-b200", layers=tuple(layers), param_count=params,
+                        kind_allowed=frozenset({JobKind.TRAINING}))
+    model.profile = prof
+    return prof

@@ -100,10 +100,13 @@ class TrainModule(FillModule):
     def param_specs(self):  # bf16 GEMM operands (reference / eager views)
         return [(p.name, p.shape, p.init) for p in self.tparams() if p.work]
 
-    def init_host(self, gen: torch.Generator, std: float = 0.02, pinned: bool = True) -> None:
+    def init_host(self, gen: torch.Generator, std: float = 0.02, pinned: bool = True,
+                  raw: Optional[torch.Tensor] = None) -> None:
+        """Random init of the state blob (`raw`: a slice of the whole step's blob)."""
         lay, total = self._layout()
-        self.host = PinnedBuffer((total,), torch.uint8) if pinned else None
-        raw = self.host.tensor if pinned else torch.zeros(total, dtype=torch.uint8)
+        if raw is None:
+            self.host = PinnedBuffer((total,), torch.uint8) if pinned else None
+            raw = self.host.tensor if pinned else torch.zeros(total, dtype=torch.uint8)
         raw.zero_()
         self.host_params = {}
         for p in self.tparams():
@@ -150,7 +153,8 @@ class TrainModule(FillModule):
         n = _numel(p.shape)
         if p.grad == "f32":
             return 2 * n
-        return self.splits(p.name, batch) * n
+        # chains of any batch up to `batch` (multiples of 8) share this buffer
+        return max(self.splits(p.name, b) for b in range(8, max(batch, 8) + 1, 8)) * n
 
     def splits(self, name: str, batch: int) -> int:
         """Split-K slice count of the weight gradient of parameter `name` at this batch."""
@@ -249,7 +253,7 @@ class _Rec:
         k = x.shape[-1]
         dzt = self.transpose(dz, ctx.buf("tA", n * m).view(n, m))
         xt = self.transpose(x.reshape(m, k), ctx.buf("tB", k * m).view(k, m))
-        self.gemm_splitk(dzt, xt, gbuf.view(splits, n, k), splits)
+        self.gemm_splitk(dzt, xt, gbuf.view(-1)[:splits * n * k].view(splits, n, k), splits)
 
     def dgrad(self, dz, w, out, residual=None):
         """out[M, K] = dz[M, N] w[N, K] (+ residual): GEMM against w^T."""
@@ -545,18 +549,93 @@ class TrainHead(TrainModule):
         return dx
 
 
+class ResNetTrainStep(FillModule):
+    """The whole training step as ONE node of the linearized model. A training step needs
+    every module's saved activations for its backward, so it cannot be split into
+    partitions that run in different bubbles; presenting it as a single profile layer
+    makes every plan the DP produces for it single-partition (partition.py:247-297).
+    The 18 modules' states are slices of one pinned blob: one staging copy, one
+    write-back."""
+
+    def __init__(self, mods: list["TrainModule"]):
+        super().__init__()
+        self.mods = torch.nn.ModuleList(mods)
+
+    def _offsets(self):
+        offs, off = [], 0
+        for m in self.mods:
+            offs.append(off)
+            off += _pad(m.weight_bytes(), 256)
+        return offs, off
+
+    def weight_bytes(self) -> int:
+        return self._offsets()[1]
+
+    def param_specs(self):
+        return []
+
+    def init_host(self, gen: torch.Generator, std: float = 0.02, pinned: bool = True,
+                  raw: Optional[torch.Tensor] = None) -> None:
+        offs, total = self._offsets()
+        self.host = PinnedBuffer((total,), torch.uint8) if pinned else None
+        blob = self.host.tensor if pinned else torch.zeros(total, dtype=torch.uint8)
+        for m, o in zip(self.mods, offs):
+            m.init_host(gen, pinned=pinned, raw=blob[o:o + m.weight_bytes()])
+        self.host_params = {}
+
+    def make_views(self, ptr: int) -> dict:
+        offs, _ = self._offsets()
+        return {"mods": [m.make_views(ptr + o) for m, o in zip(self.mods, offs)]}
+
+    @property
+    def dev(self):
+        return {"mods": [m.dev for m in self.mods]} if hasattr(self, "mods") else {}
+
+    @dev.setter
+    def dev(self, value):
+        if value and hasattr(self, "mods"):
+            for m, d in zip(self.mods, value["mods"]):
+                m.dev = d
+
+    def workspace(self, batch: int) -> dict[str, int]:
+        need: dict[str, int] = {}
+        for m in self.mods:
+            for k, v in m.workspace(batch).items():
+                need[k] = max(need.get(k, 0), v)
+        for j in (0, 1):  # gradient ping-pong between modules
+            need[f"grad{j}"] = max(batch * _numel(m.out_shape()) for m in list(self.mods)[:-1])
+        need["partial"] = max(need.get("partial", 0), 2 * MAX_PARTIALS * 2 * 2048)
+        need["scale"] = need["shift"] = 2 * 2048
+        return need
+
+    def flops_per_sample(self) -> float:
+        return sum(m.flops_per_sample() for m in self.mods)
+
+    def node_units(self, batch):
+        return []
+
+    def forward(self, x, ctx):
+        raise RuntimeError("a training step is recorded through ResNetTrainSequential.record_step")
+
+
 class ResNetTrainSequential(FillSequential):
-    """ResNet-50 training job: [stem, 16 bottlenecks, head]; one batch = one SGD step."""
+    """ResNet-50 training job: one node (the step) wrapping [stem, 16 bottlenecks, head];
+    one batch = one SGD step."""
 
     is_training = True
     capture_grads = False  # tests: keep a copy of the gradient entering every module's backward
+
+    @property
+    def blocks(self) -> list["TrainModule"]:
+        """The 18 modules of the step: stem, bottlenecks, head."""
+        return list(self[0].mods)
 
     def input_spec(self):
         c = self.cfg
         return torch.bfloat16, (c.image, c.image, c.in_ch)
 
     def boundary_shape(self, i):
-        return self.input_spec()[1] if i == 0 else self[i - 1].out_shape()
+        return self.input_spec()[1] if i == 0 else (4,)
 
     def result_shape(self):
         return (4,)  # per-sample loss at [0] (16-B rows)
@@ -577,17 +656,10 @@ class ResNetTrainSequential(FillSequential):
         return synthetic_labels(job_seed, first, count, self.cfg.classes)
 
     def workspace(self, lo: int, hi: int, batch: int) -> dict[str, int]:
-        need: dict[str, int] = {}
-        for i in range(len(self)):  # a training step always spans the whole model
-            for k, v in self[i].workspace(batch).items():
-                need[k] = max(need.get(k, 0), v)
-        for j in (0, 1):  # gradient ping-pong between modules
-            need[f"grad{j}"] = max(batch * _numel(self[i].out_shape()) for i in range(len(self) - 1))
-        need["partial"] = max(need.get("partial", 0), 2 * MAX_PARTIALS * 2 * 2048)
-        need["scale"] = need["shift"] = 2 * 2048
+        need = dict(self[0].workspace(batch))
         if self.capture_grads:
-            for i in range(len(self) - 1):
-                need[f"cap{i}"] = batch * _numel(self[i].out_shape())
+            for m in self.blocks[:-1]:
+                need[f"cap{m.idx}"] = batch * _numel(m.out_shape())
         return need
 
     def record_step(self, x, labels, loss, ctx: ExecContext) -> tuple[list[int], dict]:
@@ -598,16 +670,17 @@ class ResNetTrainSequential(FillSequential):
         b = x.shape[0]
         if b % 8:
             raise ValueError("training batches must be a multiple of 8 samples")
+        mods = self.blocks
         ends = []
         y = x
-        for mod in list(self)[:-1]:
+        for mod in mods[:-1]:
             y = mod.record_forward(r, y)
             ends.append(ctx.node)
-        self[-1].record_forward(r, y, labels, loss)
+        mods[-1].record_forward(r, y, labels, loss)
         ends.append(ctx.node)
-        dy = self[-1].record_backward(r)
+        dy = mods[-1].record_backward(r)
         ends.append(ctx.node)
-        for mod in reversed(list(self)[:-1]):
+        for mod in reversed(mods[:-1]):
             if self.capture_grads:
                 nb = dy.numel() * 2
                 cap = ctx.buf(f"cap{mod.idx}", dy.numel())
@@ -615,7 +688,7 @@ class ResNetTrainSequential(FillSequential):
             dy = mod.record_backward(r, dy)
             ends.append(ctx.node)
         segs = []
-        for mod in self:
+        for mod in mods:
             segs.extend(mod.sgd_segments(ctx, b))
         arr = K.sgd_segments(segs)
         native.call("pf_chain_add_sgd", ctx.chain, arr, len(segs), LR, MOMENTUM)
@@ -648,12 +721,12 @@ def resnet50_train(cfg: ResNetConfig = RESNET50, seed: Optional[int] = 0, pinned
             ch, h = blk.out_ch, blk.ho
     mods.append(TrainHead(cfg, len(mods), ch, h))
     _ = _InferBlock
-    seq = ResNetTrainSequential(cfg, mods)
+    seq = ResNetTrainSequential(cfg, [ResNetTrainStep(mods)])
     if seed is not None:
         seq.init_weights(seed, pinned=pinned)
     return seq
 
 
-__all__ = ["ResNetTrainSequential", "resnet50_train", "synthetic_labels", "TrainStem", "TrainBottleneck",
+__all__ = ["ResNetTrainSequential", "ResNetTrainStep", "resnet50_train", "synthetic_labels", "TrainStem", "TrainBottleneck",
            "TrainHead", "LR", "MOMENTUM", "WEIGHT_DECAY"]
 _ = (ATOMIC, PREFIX, dataclass)

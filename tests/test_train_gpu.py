@@ -32,7 +32,7 @@ def _torchvision_from(model):
     import torchvision
 
     tv = torchvision.models.resnet50(weights=None)
-    st = [model[i].state_host() for i in range(len(model))]
+    st = [m.state_host() for m in model.blocks]
 
     def load(conv, bn, w, g, b):
         k = conv.kernel_size[0]
@@ -58,7 +58,8 @@ def _torchvision_from(model):
 
 def _checked(model, tv, blocks):
     """(name, ours fp32 master -> torchvision layout, torchvision tensor)."""
-    st0, st5, sth = model[0].state_host(), model[5].state_host(), model[-1].state_host()
+    mb = model.blocks
+    st0, st5, sth = mb[0].state_host(), mb[5].state_host(), mb[-1].state_host()
     b5 = blocks[4]
     return [("stem conv", fill_ref.conv_weight(st0["w"], 3, 7, 7), tv.conv1.weight),
             ("stem bn gamma", st0["g"], tv.bn1.weight),
@@ -103,7 +104,7 @@ def test_resnet50_training_step_matches_torchvision_module_by_module():
     batch, seed = 8, 3
     tv, blocks = _torchvision_from(model)
     tv.train()
-    w0_stem = model[0].state_host()["w"].clone()
+    w0_stem = model.blocks[0].state_host()["w"].clone()
     item = _plan_item(pf, model, batch, batch)
     ex = Executor(8 << 30, job_seed=seed)
     ex.load(item, model)
@@ -112,14 +113,15 @@ def test_resnet50_training_step_matches_torchvision_module_by_module():
     torch.cuda.synchronize()
     assert not ex.busy
     ws = ex.ws
-    L = len(model)
+    mb = model.blocks
+    L = len(mb)
 
     def gpu_out(i):
-        b, (h, w, c) = batch, model[i].out_shape()
+        b, (h, w, c) = batch, mb[i].out_shape()
         return ws[f"out{i}"].view(-1)[:b * h * w * c].view(b, h, w, c)
 
     def gpu_cap(i):
-        b, (h, w, c) = batch, model[i].out_shape()
+        b, (h, w, c) = batch, mb[i].out_shape()
         return ws[f"cap{i}"].view(-1)[:b * h * w * c].view(b, h, w, c)
 
     def gpu_grad(i, name, shape, kind="gemm"):
@@ -129,7 +131,7 @@ def test_resnet50_training_step_matches_torchvision_module_by_module():
         g = ws[f"g{i}.{name}"].view(-1)
         if kind == "f32":
             return g[:2 * n].view(torch.float32).float().cpu().view(*shape)
-        s = model[i].splits(name, batch)
+        s = mb[i].splits(name, batch)
         return g[:s * n].view(s, n).float().sum(0).cpu().view(*shape)
 
     report = {}
@@ -144,7 +146,7 @@ def test_resnet50_training_step_matches_torchvision_module_by_module():
     stem_dbeta = _rel(gpu_grad(0, "b", (c,), "f32"), tv.bn1.bias.grad)
     # bottlenecks: identity (2), projection stride 1 (1) and stride 2 (4, 8, 14), deep (16)
     for i in (1, 2, 4, 8, 14, 16):
-        blk, mod = blocks[i - 1], model[i]
+        blk, mod = blocks[i - 1], mb[i]
         x = _nchw(mod.saved["x"]).requires_grad_(True)
         for p_ in blk.parameters():
             p_.grad = None
@@ -160,7 +162,6 @@ def test_resnet50_training_step_matches_torchvision_module_by_module():
             report[f"block{i} dWd"] = _rel(gpu_grad(i, "wd", (mod.out_ch, mod.in_ch)).view(mod.out_ch, mod.in_ch, 1, 1),
                                            blk.downsample[0].weight.grad)
     # head: loss and classifier gradients
-    x = _nchw(model[L - 1].saved["pooled"].view(batch, -1)[:, :, None, None].expand(-1, -1, 1, 1).permute(0, 2, 3, 1))
     xin = _nchw(gpu_out(L - 2)).requires_grad_(True)
     logits = tv.fc(torch.flatten(tv.avgpool(xin), 1))
     lab = synthetic_labels(seed, 0, batch, cfg.classes)[:, 0].long()
@@ -173,9 +174,8 @@ def test_resnet50_training_step_matches_torchvision_module_by_module():
     # SGD (first step: v = g + wd * w): the stem weight's written-back master
     g = gpu_grad(0, "w", (c, cfg.stem_kp))
     want = w0_stem - LR * (g + WEIGHT_DECAY * w0_stem)
-    report["sgd update"] = _rel(model[0].state_host()["w"] - w0_stem, want - w0_stem)
+    report["sgd update"] = _rel(mb[0].state_host()["w"] - w0_stem, want - w0_stem)
     ex.close()
-    _ = x
     print("REPORT", {k: round(v, 5) for k, v in report.items()}, "stem dbeta", stem_dbeta)
     for k, v in report.items():
         tol = 1e-5 if k == "sgd update" else (2e-2 if ("fwd" in k or k == "loss") else 1.5e-1)
