@@ -187,7 +187,7 @@ int pf_image_units(int kind, long long out_elems, int C, uint32_t* out_units);
 /* ---- training fill jobs (ResNet-50 fwd + bwd + SGD), NHWC bf16 as [M, C] --------
  * BatchNorm batch statistics: pf_colstats writes per-CTA partials (sum x, sum x^2) of
  * X[M, C] (or, with G given, (sum dA, sum dA*xhat), dA = G*[Ymask > 0]) to
- * partial[P, 2C] fp32 and reports P (<= 512); pf_bn_finalize turns them into mean,
+ * partial[P, 2C] fp32 and reports P (<= 1024); pf_bn_finalize turns them into mean,
  * invstd and scale = gamma*invstd, shift = beta - mean*scale; pf_bn_bwd_finalize into
  * dbeta (= column sums) and dgamma (may be NULL). pf_bn_apply: Y = act(X*scale + shift
  * [+ R]). pf_bn_bwd_apply: dX = gamma*invstd*(dA - dbeta/M - xhat*dgamma/M), dA

@@ -174,6 +174,55 @@ __device__ __forceinline__ void atomic_unit_exit(const Ctl& c) {
   }
 }
 
+// Mid-kernel re-check for persistent (grid-stride) atomic units: thread 0 re-reads the
+// flag; on a closed bubble the CTA stops WITHOUT counting itself (the node stays
+// incomplete and is re-run whole on resume). Call uniformly across the CTA.
+__device__ __forceinline__ bool atomic_unit_poll(const Ctl& c) {
+  __shared__ int s_live;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int live = 1;
+    if (c.flag != nullptr && ld_acquire_u32(c.flag) == 0u) {
+      atomicExch(c.abort, 1u);
+      live = 0;
+    }
+    s_live = live;
+  }
+  __syncthreads();
+  return s_live != 0;
+}
+
+// Grid of a persistent atomic-unit kernel: enough CTAs of `threads` to cover `items`
+// items once, capped at one full wave (2048 threads per SM); every CTA strides over the rest. Entry and exit
+// are paid once per CTA instead of once per 256 items (the gate's flag load and barrier
+// cost ~1 us per CTA, which dominated the element-wise training kernels).
+inline unsigned persistent_grid(long long items, int threads) {
+  const long long need = (items + threads - 1) / threads;
+  const long long cap = (2048LL / threads) * device_sm_count();  // one full wave of resident threads
+  return (unsigned)(need < cap ? (need > 0 ? need : 1) : cap);
+}
+
+// Poll the flag every PF_POLL_STRIDES grid strides (~64 x 592 CTAs x 256 items).
+#define PF_POLL_STRIDES 64
+
+// Body of a persistent atomic-unit kernel over item index `v` in [0, N):
+//   PF_ITEMS_BEGIN(N) { ... uses v ... } PF_ITEMS_END
+#define PF_ITEMS_BEGIN(N)                                                                  \
+  if (!atomic_unit_enter(ctl)) return;                                                    \
+  {                                                                                       \
+    const long long pf_n_ = (N);                                                          \
+    const long long pf_stride_ = (long long)gridDim.x * blockDim.x;                       \
+    int pf_it_ = 0;                                                                       \
+    for (long long pf_base_ = (long long)blockIdx.x * blockDim.x; pf_base_ < pf_n_;        \
+         pf_base_ += pf_stride_, ++pf_it_) {                                              \
+      if (pf_it_ && (pf_it_ % PF_POLL_STRIDES) == 0 && !atomic_unit_poll(ctl)) return;    \
+      const long long v = pf_base_ + threadIdx.x;                                         \
+      if (v < pf_n_)
+#define PF_ITEMS_END \
+    }                \
+  }                  \
+  atomic_unit_exit(ctl);
+
 __device__ __forceinline__ void load8(const __nv_bfloat16* p, float* v) {
   uint4 u = *reinterpret_cast<const uint4*>(p);
   const uint32_t w[4] = {u.x, u.y, u.z, u.w};

@@ -25,9 +25,7 @@ constexpr int THREADS = 256;
 __global__ void __launch_bounds__(THREADS) im2col_vec_kernel(
     const __nv_bfloat16* __restrict__ X, __nv_bfloat16* __restrict__ Col, int H, int W, int C,
     int Ho, int Wo, int kw, int stride, int pad, int K, int Kp, long long total_vec, Ctl ctl) {
-  if (!atomic_unit_enter(ctl)) return;
-  const long long v = (long long)blockIdx.x * THREADS + threadIdx.x;
-  if (v < total_vec) {
+  PF_ITEMS_BEGIN(total_vec) {
     const int vpr = Kp >> 3;  // vectors per Col row
     const long long m = v / vpr;
     const int k0 = (int)(v - m * vpr) << 3;
@@ -46,15 +44,14 @@ __global__ void __launch_bounds__(THREADS) im2col_vec_kernel(
     }
     *reinterpret_cast<uint4*>(Col + (size_t)m * Kp + k0) = out;
   }
-  atomic_unit_exit(ctl);
+  PF_ITEMS_END
 }
 
 __global__ void __launch_bounds__(THREADS) im2col_scalar_kernel(
     const __nv_bfloat16* __restrict__ X, __nv_bfloat16* __restrict__ Col, int H, int W, int C,
     int Ho, int Wo, int kw, int stride, int pad, int K, int Kp, long long total, Ctl ctl) {
-  if (!atomic_unit_enter(ctl)) return;
-  const long long e = (long long)blockIdx.x * THREADS + threadIdx.x;
-  if (e < total) {
+  PF_ITEMS_BEGIN(total) {
+    const long long e = v;
     const long long m = e / Kp;
     const int k = (int)(e - m * Kp);
     __nv_bfloat16 val = __float2bfloat16(0.f);
@@ -71,15 +68,13 @@ __global__ void __launch_bounds__(THREADS) im2col_scalar_kernel(
     }
     Col[e] = val;
   }
-  atomic_unit_exit(ctl);
+  PF_ITEMS_END
 }
 
 __global__ void __launch_bounds__(THREADS) maxpool_kernel(
     const __nv_bfloat16* __restrict__ X, __nv_bfloat16* __restrict__ Y, int H, int W, int C,
     int Ho, int Wo, int k, int stride, int pad, long long total_vec, Ctl ctl) {
-  if (!atomic_unit_enter(ctl)) return;
-  const long long v = (long long)blockIdx.x * THREADS + threadIdx.x;
-  if (v < total_vec) {
+  PF_ITEMS_BEGIN(total_vec) {
     const int cv = C >> 3;
     const int c0 = (int)(v % cv) << 3;
     const long long pix = v / cv;
@@ -104,15 +99,13 @@ __global__ void __launch_bounds__(THREADS) maxpool_kernel(
     }
     store8(Y + (size_t)pix * C + c0, mx);
   }
-  atomic_unit_exit(ctl);
+  PF_ITEMS_END
 }
 
 __global__ void __launch_bounds__(THREADS) avgpool_kernel(const __nv_bfloat16* __restrict__ X,
                                                           __nv_bfloat16* __restrict__ Y, int HW,
                                                           int C, long long total_vec, Ctl ctl) {
-  if (!atomic_unit_enter(ctl)) return;
-  const long long v = (long long)blockIdx.x * THREADS + threadIdx.x;
-  if (v < total_vec) {
+  PF_ITEMS_BEGIN(total_vec) {
     const int cv = C >> 3;
     const int c0 = (int)(v % cv) << 3;
     const long long b = v / cv;
@@ -129,10 +122,10 @@ __global__ void __launch_bounds__(THREADS) avgpool_kernel(const __nv_bfloat16* _
     for (int e = 0; e < 8; ++e) acc[e] *= inv;
     store8(Y + (size_t)b * C + c0, acc);
   }
-  atomic_unit_exit(ctl);
+  PF_ITEMS_END
 }
 
-inline uint32_t blocks_for(long long n) { return (uint32_t)((n + THREADS - 1) / THREADS); }
+inline uint32_t blocks_for(long long n) { return persistent_grid(n, THREADS); }
 
 inline int out_dim(int in, int k, int stride, int pad) { return (in + 2 * pad - k) / stride + 1; }
 

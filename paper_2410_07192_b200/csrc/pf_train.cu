@@ -33,32 +33,63 @@ namespace pf {
 namespace train {
 
 constexpr int T = 256;
-constexpr int MAX_PARTIALS = 512;
+constexpr int MAX_PARTIALS = 1024;
+constexpr int FT = 1024;  // finalize threads: 32 warps split the partial rows
 constexpr int SGD_CHUNK = 4096;  // elements per claimed unit
 
 using bf = __nv_bfloat16;
 
-inline uint32_t blocks_for(long long n) { return (uint32_t)((n + T - 1) / T); }
+inline uint32_t blocks_for(long long n) { return persistent_grid(n, T); }
+
+__device__ __forceinline__ void ld8f(const float* p, float* v) {  // 8 floats, 32-B aligned
+  const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
 
 // ---------------------------------------------------------------------------- transpose
 
+// 64 x 64 tiles: each thread loads 16 B (8 bf16) of a row and stores 16 B of a column
+// segment; the CTA strides over tiles (persistent atomic unit).
 __global__ void __launch_bounds__(T) transpose_kernel(const bf* __restrict__ X, bf* __restrict__ Y,
-                                                      int R, int C, int tiles_c, Ctl ctl) {
+                                                      int R, int C, int tiles_c, int ntiles, Ctl ctl) {
   if (!atomic_unit_enter(ctl)) return;
-  __shared__ bf tile[32][34];
-  const int tr = blockIdx.x / tiles_c, tc = blockIdx.x % tiles_c;
-  const int r0 = tr * 32, c0 = tc * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  __shared__ bf tile[64][72];  // 144-B rows: 16-B aligned, staggered banks
+  const int t = threadIdx.x;
+  const int lr = t >> 3, lc = (t & 7) * 8;  // 32 rows x 8 vectors per pass
+  int it = 0;
+  for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++it) {
+    if (it && (it % PF_POLL_STRIDES) == 0 && !atomic_unit_poll(ctl)) return;
+    const int r0 = (tl / tiles_c) * 64, c0 = (tl % tiles_c) * 64;
+    const bool full = r0 + 64 <= R && c0 + 64 <= C && (C % 8) == 0 && (R % 8) == 0;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int r = r0 + ty + 8 * k, c = c0 + tx;
-    if (r < R && c < C) tile[ty + 8 * k][tx] = X[(size_t)r * C + c];
-  }
-  __syncthreads();
+    for (int k = 0; k < 2; ++k) {
+      const int rr = lr + 32 * k, r = r0 + rr;
+      if (full) {
+        *reinterpret_cast<uint4*>(&tile[rr][lc]) = *reinterpret_cast<const uint4*>(X + (size_t)r * C + c0 + lc);
+      } else {
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int c = c0 + ty + 8 * k, r = r0 + tx;
-    if (r < R && c < C) Y[(size_t)c * R + r] = tile[tx][ty + 8 * k];
+        for (int e = 0; e < 8; ++e) {
+          const int c = c0 + lc + e;
+          tile[rr][lc + e] = (r < R && c < C) ? X[(size_t)r * C + c] : __float2bfloat16(0.f);
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int cc = lr + 32 * k, c = c0 + cc;  // output row = input column
+      __align__(16) bf o[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = tile[lc + e][cc];
+      if (full) {
+        *reinterpret_cast<uint4*>(Y + (size_t)c * R + r0 + lc) = *reinterpret_cast<const uint4*>(o);
+      } else if (c < C) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (r0 + lc + e < R) Y[(size_t)c * R + r0 + lc + e] = o[e];
+      }
+    }
+    __syncthreads();
   }
   atomic_unit_exit(ctl);
 }
@@ -93,6 +124,7 @@ __global__ void __launch_bounds__(T) colstats_kernel(const bf* __restrict__ X, c
   const int r0 = blockIdx.x * rows_per_cta;
   const int r1 = min(M, r0 + rows_per_cta);
   if (rsub < rsub_n) {
+#pragma unroll 4
     for (int r = r0 + rsub; r < r1; r += rsub_n) {
       float x[8];
       load8(X + (size_t)r * C + c0, x);
@@ -140,19 +172,39 @@ __global__ void __launch_bounds__(T) colstats_kernel(const bf* __restrict__ X, c
 }
 
 // partials -> mean, invstd, scale = gamma * invstd, shift = beta - mean * scale
-__global__ void __launch_bounds__(T) bn_finalize_kernel(const float* __restrict__ partial, int P, int M,
+// Sums the P partial rows of 32 channels per CTA: lane = channel, the 8 warps split
+// the partial rows (8 independent load chains instead of one chain of P loads), then a
+// fixed-order shared-memory combine (deterministic).
+__device__ __forceinline__ void sum_partials(const float* __restrict__ partial, int P, int C, int c, double& s,
+                                             double& ss) {
+  __shared__ double red[2][FT / 32][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double a = 0.0, b = 0.0;
+  if (c < C)
+    for (int p = w; p < P; p += FT / 32) {
+      a += partial[(size_t)p * 2 * C + c];
+      b += partial[(size_t)p * 2 * C + C + c];
+    }
+  red[0][w][lane] = a;
+  red[1][w][lane] = b;
+  __syncthreads();
+  s = ss = 0.0;
+  for (int k = 0; k < FT / 32; ++k) {
+    s += red[0][k][lane];
+    ss += red[1][k][lane];
+  }
+}
+
+__global__ void __launch_bounds__(FT) bn_finalize_kernel(const float* __restrict__ partial, int P, int M,
                                                         int C, const float* __restrict__ gamma,
                                                         const float* __restrict__ beta, float eps,
                                                         float* mean, float* invstd, float* scale,
                                                         float* shift, Ctl ctl) {
   if (!atomic_unit_enter(ctl)) return;
-  const int c = blockIdx.x * T + threadIdx.x;
-  if (c < C) {
-    double s = 0.0, ss = 0.0;
-    for (int p = 0; p < P; ++p) {
-      s += partial[(size_t)p * 2 * C + c];
-      ss += partial[(size_t)p * 2 * C + C + c];
-    }
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  double s, ss;
+  sum_partials(partial, P, C, c, s, ss);
+  if (c < C && threadIdx.x < 32) {
     const double m = s / M;
     const double var = fmax(ss / M - m * m, 0.0);
     const float is = (float)(1.0 / sqrt(var + (double)eps));
@@ -167,18 +219,15 @@ __global__ void __launch_bounds__(T) bn_finalize_kernel(const float* __restrict_
 
 // partials -> dbeta = sum dA, dgamma = sum dA * xhat (also a plain column sum when
 // called on mode-0 partials: dsum = sum x goes to `dbeta`, dgamma may be null)
-__global__ void __launch_bounds__(T) bn_bwd_finalize_kernel(const float* __restrict__ partial, int P,
+__global__ void __launch_bounds__(FT) bn_bwd_finalize_kernel(const float* __restrict__ partial, int P,
                                                             int C, float* dgamma, float* dbeta, Ctl ctl) {
   if (!atomic_unit_enter(ctl)) return;
-  const int c = blockIdx.x * T + threadIdx.x;
-  if (c < C) {
-    float s = 0.f, sx = 0.f;
-    for (int p = 0; p < P; ++p) {
-      s += partial[(size_t)p * 2 * C + c];
-      sx += partial[(size_t)p * 2 * C + C + c];
-    }
-    dbeta[c] = s;
-    if (dgamma) dgamma[c] = sx;
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  double s, sx;
+  sum_partials(partial, P, C, c, s, sx);
+  if (c < C && threadIdx.x < 32) {
+    dbeta[c] = (float)s;
+    if (dgamma) dgamma[c] = (float)sx;
   }
   atomic_unit_exit(ctl);
 }
@@ -189,14 +238,14 @@ __global__ void __launch_bounds__(T) bn_apply_kernel(const bf* __restrict__ X, c
                                                      const float* __restrict__ shift, const bf* __restrict__ R,
                                                      bf* __restrict__ Y, int C, long long nvec, int relu,
                                                      Ctl ctl) {
-  if (!atomic_unit_enter(ctl)) return;
-  const long long v = (long long)blockIdx.x * T + threadIdx.x;
-  if (v < nvec) {
+  PF_ITEMS_BEGIN(nvec) {
     const int c0 = (int)(v % (C >> 3)) << 3;
-    float x[8];
+    float x[8], sc[8], sh[8];
     load8(X + v * 8, x);
+    ld8f(scale + c0, sc);
+    ld8f(shift + c0, sh);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) x[e] = x[e] * scale[c0 + e] + shift[c0 + e];
+    for (int e = 0; e < 8; ++e) x[e] = x[e] * sc[e] + sh[e];
     if (R) {
       float r[8];
       load8(R + v * 8, r);
@@ -209,7 +258,7 @@ __global__ void __launch_bounds__(T) bn_apply_kernel(const bf* __restrict__ X, c
     }
     store8(Y + v * 8, x);
   }
-  atomic_unit_exit(ctl);
+  PF_ITEMS_END
 }
 
 // dA = G * [Ymask > 0]; dX = gamma * invstd * (dA - dbeta / M - xhat * dgamma / M).
@@ -219,9 +268,7 @@ __global__ void __launch_bounds__(T) bn_bwd_apply_kernel(
     const float* __restrict__ mean, const float* __restrict__ invstd, const float* __restrict__ gamma,
     const float* __restrict__ dgamma, const float* __restrict__ dbeta, bf* __restrict__ dX,
     bf* __restrict__ dA_out, int M, int C, long long nvec, Ctl ctl) {
-  if (!atomic_unit_enter(ctl)) return;
-  const long long v = (long long)blockIdx.x * T + threadIdx.x;
-  if (v < nvec) {
+  PF_ITEMS_BEGIN(nvec) {
     const int c0 = (int)(v % (C >> 3)) << 3;
     float x[8], g[8];
     load8(X + v * 8, x);
@@ -234,16 +281,20 @@ __global__ void __launch_bounds__(T) bn_bwd_apply_kernel(
     }
     if (dA_out) store8(dA_out + v * 8, g);
     const float inv_m = 1.f / (float)M;
-    float o[8];
+    float o[8], mu[8], is[8], ga[8], dg[8], db[8];
+    ld8f(mean + c0, mu);
+    ld8f(invstd + c0, is);
+    ld8f(gamma + c0, ga);
+    ld8f(dgamma + c0, dg);
+    ld8f(dbeta + c0, db);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const int c = c0 + e;
-      const float xh = (x[e] - mean[c]) * invstd[c];
-      o[e] = gamma[c] * invstd[c] * (g[e] - dbeta[c] * inv_m - xh * dgamma[c] * inv_m);
+      const float xh = (x[e] - mu[e]) * is[e];
+      o[e] = ga[e] * is[e] * (g[e] - db[e] * inv_m - xh * dg[e] * inv_m);
     }
     store8(dX + v * 8, o);
   }
-  atomic_unit_exit(ctl);
+  PF_ITEMS_END
 }
 
 // ---------------------------------------------------------------------------- image backward
@@ -252,9 +303,7 @@ __global__ void __launch_bounds__(T) col2im_kernel(const bf* __restrict__ dCol, 
                                                    bf* __restrict__ dX, int H, int W, int C, int Ho, int Wo,
                                                    int kh, int kw, int stride, int pad, int Kp,
                                                    long long nvec, Ctl ctl) {
-  if (!atomic_unit_enter(ctl)) return;
-  const long long v = (long long)blockIdx.x * T + threadIdx.x;
-  if (v < nvec) {
+  PF_ITEMS_BEGIN(nvec) {
     const int cv = C >> 3;
     const int c0 = (int)(v % cv) << 3;
     const long long pix = v / cv;
@@ -289,16 +338,14 @@ __global__ void __launch_bounds__(T) col2im_kernel(const bf* __restrict__ dCol, 
     }
     store8(dX + pix * C + c0, acc);
   }
-  atomic_unit_exit(ctl);
+  PF_ITEMS_END
 }
 
 __global__ void __launch_bounds__(T) maxpool_bwd_kernel(const bf* __restrict__ X, const bf* __restrict__ dY,
                                                         bf* __restrict__ dX, int H, int W, int C, int Ho,
                                                         int Wo, int k, int stride, int pad, long long nvec,
                                                         Ctl ctl) {
-  if (!atomic_unit_enter(ctl)) return;
-  const long long v = (long long)blockIdx.x * T + threadIdx.x;
-  if (v < nvec) {
+  PF_ITEMS_BEGIN(nvec) {
     const int cv = C >> 3;
     const int c0 = (int)(v % cv) << 3;
     const long long pix = v / cv;
@@ -352,14 +399,12 @@ __global__ void __launch_bounds__(T) maxpool_bwd_kernel(const bf* __restrict__ X
     }
     store8(dX + pix * C + c0, acc);
   }
-  atomic_unit_exit(ctl);
+  PF_ITEMS_END
 }
 
 __global__ void __launch_bounds__(T) avgpool_bwd_kernel(const bf* __restrict__ dY, bf* __restrict__ dX,
                                                         int HW, int C, long long nvec, Ctl ctl) {
-  if (!atomic_unit_enter(ctl)) return;
-  const long long v = (long long)blockIdx.x * T + threadIdx.x;
-  if (v < nvec) {
+  PF_ITEMS_BEGIN(nvec) {
     const int cv = C >> 3;
     const int c0 = (int)(v % cv) << 3;
     const long long b = v / ((long long)HW * cv);
@@ -370,7 +415,7 @@ __global__ void __launch_bounds__(T) avgpool_bwd_kernel(const bf* __restrict__ d
     for (int e = 0; e < 8; ++e) g[e] *= inv;
     store8(dX + v * 8, g);
   }
-  atomic_unit_exit(ctl);
+  PF_ITEMS_END
 }
 
 // ---------------------------------------------------------------------------- loss
@@ -439,21 +484,31 @@ struct SgdSeg {
   int first_unit;      // prefix sum of units before this segment
 };
 
+constexpr int MAX_SGD_SEGS = 256;
+
 __global__ void __launch_bounds__(T) sgd_kernel(const SgdSeg* __restrict__ segs, int nseg, int units,
                                                 float lr, float mu, Ctl ctl) {
   if (chain_aborted(ctl)) return;
   __shared__ int s_unit;
+  __shared__ int s_first[MAX_SGD_SEGS];  // first unit of every segment: binary-searched in smem
+  for (int i = threadIdx.x; i < nseg; i += T) s_first[i] = segs[i].first_unit;
+  __syncthreads();
   for (int it = 0;; ++it) {
     if (threadIdx.x == 0) s_unit = claim_unit(ctl, units, it);
     __syncthreads();
     const int u = s_unit;
     __syncthreads();
     if (u < 0) break;
-    int si = 0;
-    while (si + 1 < nseg && segs[si + 1].first_unit <= u) ++si;
-    const SgdSeg sg = segs[si];
+    int sl = 0, sh = nseg - 1;  // last segment with first_unit <= u
+    while (sl < sh) {
+      const int mid = (sl + sh + 1) >> 1;
+      if (s_first[mid] <= u) sl = mid;
+      else sh = mid - 1;
+    }
+    const SgdSeg sg = segs[sl];
     const long long lo = (long long)(u - sg.first_unit) * SGD_CHUNK;
     const long long hi = min(sg.n, lo + SGD_CHUNK);
+#pragma unroll 4
     for (long long i = lo + threadIdx.x; i < hi; i += T) {
       float g = 0.f;
       if (sg.kind == 0) {
@@ -479,10 +534,14 @@ struct TransposeOp final : PreparedOp {
   const bf* x = nullptr;
   bf* y = nullptr;
   int R = 0, C = 0;
-  uint32_t units() const override { return (uint32_t)(((R + 31) / 32) * ((C + 31) / 32)); }
+  int ntiles() const { return ((R + 63) / 64) * ((C + 63) / 64); }
+  uint32_t units() const override {
+    const int cap = 8 * device_sm_count();
+    return (uint32_t)(ntiles() < cap ? ntiles() : cap);
+  }
   bool resumable() const override { return false; }
   int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
-    transpose_kernel<<<units(), T, 0, s>>>(x, y, R, C, (C + 31) / 32, make_ctl(ctl));
+    transpose_kernel<<<units(), T, 0, s>>>(x, y, R, C, (C + 63) / 64, ntiles(), make_ctl(ctl));
     PF_CUDA(cudaGetLastError());
     return PF_OK;
   }
@@ -509,14 +568,14 @@ struct BnFinalizeOp final : PreparedOp {
   int P = 0, M = 0, C = 0;
   float eps = 0.f;
   bool bwd = false;
-  uint32_t units() const override { return blocks_for(C); }
+  uint32_t units() const override { return (uint32_t)((C + 31) / 32); }
   bool resumable() const override { return false; }
   int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
     if (bwd)
-      bn_bwd_finalize_kernel<<<units(), T, 0, s>>>(partial, P, C, dgamma, dbeta, make_ctl(ctl));
+      bn_bwd_finalize_kernel<<<units(), FT, 0, s>>>(partial, P, C, dgamma, dbeta, make_ctl(ctl));
     else
-      bn_finalize_kernel<<<units(), T, 0, s>>>(partial, P, M, C, gamma, beta, eps, mean, invstd, scale,
-                                               shift, make_ctl(ctl));
+      bn_finalize_kernel<<<units(), FT, 0, s>>>(partial, P, M, C, gamma, beta, eps, mean, invstd, scale,
+                                                shift, make_ctl(ctl));
     PF_CUDA(cudaGetLastError());
     return PF_OK;
   }
@@ -655,7 +714,7 @@ int make_colstats_op(OpPtr* out, const void* X, const void* G, const void* Ymask
   op->M = M;
   op->C = C;
   op->mode = G ? 1 : 0;
-  const int target = 2 * device_sm_count();
+  const int target = 4 * device_sm_count();
   int rows = (M + target - 1) / target;
   if (rows < 32) rows = 32;
   op->P = (M + rows - 1) / rows;
@@ -820,7 +879,8 @@ int make_xent_op(OpPtr* out, const void* Z, const int32_t* labels, float* loss, 
 }
 
 int make_sgd_op(OpPtr* out, const pf_sgd_segment_t* segs, int nseg, float lr, float momentum) {
-  if (!segs || nseg <= 0) return set_error(PF_ERR_INVALID, "pf_sgd_update: no segments");
+  if (!segs || nseg <= 0 || nseg > train::MAX_SGD_SEGS)
+    return set_error(PF_ERR_INVALID, "pf_sgd_update: need 1..256 segments");
   std::vector<train::SgdSeg> hs(nseg);
   int units = 0;
   for (int i = 0; i < nseg; ++i) {
@@ -847,8 +907,8 @@ int make_sgd_op(OpPtr* out, const pf_sgd_segment_t* segs, int nseg, float lr, fl
   op->total_units = units;
   op->lr = lr;
   op->mu = momentum;
-  const int sms = device_sm_count();
-  op->grid = units < sms ? units : sms;
+  const int cap = 8 * device_sm_count();
+  op->grid = units < cap ? units : cap;
   *out = std::move(op);
   return PF_OK;
 }

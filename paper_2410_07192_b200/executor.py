@@ -43,6 +43,9 @@ _CTL_WORDS = 64 + 4096  # [0]=abort, [1]=batches done, [8..12)=timestamps (2 x u
 _CURSOR0 = 64
 MAX_BATCHES = 64  # per bubble (device batch descriptors)
 MAX_NODES = 4096
+# PF_EXEC_GRAPHS=0 replays chains node by node (pf_chain_launch) instead of as gated CUDA
+# graphs: for profilers that do not see kernels inside conditional graph nodes (ncu)
+_USE_GRAPHS = __import__("os").environ.get("PF_EXEC_GRAPHS", "1") != "0"
 DESC_WORDS = 4  # PF_DESC_WORDS: (input, result, aux input, -) byte offsets per batch
 
 
@@ -561,7 +564,7 @@ class Executor:
             native.call("pf_read_globaltimer", base + 32, st.cuda_stream)
             for first, cnt, node in batches:
                 ch = self._chain(pr.part, cnt, flag)
-                if node > 0:  # resume a yielded batch at its first incomplete node
+                if node > 0 or not _USE_GRAPHS:  # resume a yielded batch at its first incomplete node
                     native.call("pf_chain_launch", ch.h, flag, abort_ptr if flag else None,
                                 cursors if flag else None, done_ptr, node, 0, 0, st.cuda_stream)
                     launches += len(ch.units) - node + 1

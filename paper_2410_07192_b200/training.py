@@ -42,7 +42,7 @@ LR = 0.01  # ~ the linear-scaling rule (0.1 per 256 images) at fill batch sizes 
 MOMENTUM = 0.9
 WEIGHT_DECAY = 1e-4
 BN_EPS = 1e-5
-MAX_PARTIALS = 512
+MAX_PARTIALS = 1024  # pf_colstats partial rows (4 per SM)
 
 
 def _pad(n: int, a: int = 128) -> int:

@@ -48,7 +48,7 @@ def test_transpose_exact(K):
 def _bn_forward(K, z, gamma, beta, eps=1e-5, residual=None, relu=True):
     m, c = z.shape
     dev = z.device
-    partial = torch.empty(512, 2 * c, device=dev)
+    partial = torch.empty(1024, 2 * c, device=dev)
     p = K.colstats(z, partial)
     mean, invstd, scale, shift = (torch.empty(c, device=dev) for _ in range(4))
     K.bn_finalize(partial, p, m, gamma, beta, eps, mean, invstd, scale, shift)
@@ -78,7 +78,7 @@ def test_batchnorm_forward_backward(K):
     yt.backward(dy.float())
     # backward: stats partials of (dA, dA*xhat), dA = dy*[y>0]
     dev = zc.device
-    partial = torch.empty(512, 2 * c, device=dev)
+    partial = torch.empty(1024, 2 * c, device=dev)
     p = K.colstats(zc, partial, g=dy.cuda(), ymask=y, mean=mean, invstd=invstd)
     dgamma, dbeta = torch.empty(c, device=dev), torch.empty(c, device=dev)
     K.bn_bwd_finalize(partial, p, c, dgamma, dbeta)
