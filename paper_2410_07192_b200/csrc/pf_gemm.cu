@@ -839,8 +839,14 @@ static int effective_splits(int K, int requested) {
   return (kb + per - 1) / per;
 }
 
-// BN choice: minimise (waves x BN), the per-SM tensor-pipe time, on 148 SMs.
+// BN choice: minimise waves x per-tile time on 148 SMs.
 static int pick_bn(int M, int N) {
+  static int forced = -1;  // PF_GEMM_BN=128|192|256 pins the tile width (experiments)
+  if (forced < 0) {
+    const char* e = getenv("PF_GEMM_BN");
+    forced = e ? atoi(e) : 0;
+  }
+  if (forced == 128 || forced == 192 || forced == 256) return forced;
   const int sms = device_sm_count();
   const int cands[3] = {256, 192, 128};
   int best = 256;
@@ -848,7 +854,11 @@ static int pick_bn(int M, int N) {
   for (int bn : cands) {
     long tiles = (long)((M + BM - 1) / BM) * ((N + bn - 1) / bn);
     long waves = (tiles + sms - 1) / sms;
-    long cost = waves * bn;
+    // a tile costs ~ (BN + 200) column-units: a K-block carries a fixed ~200-unit floor
+    // (operand staging, barriers, per-MMA overhead) on top of the BN-proportional MMA
+    // time (fit to 16384 x {1024, 3072, 4096} x {1024, 4096} sweeps: BN 256 beat 128 by
+    // 1.2-1.4x although it runs half the tiles per wave; scripts/gemm_bn_sweep.py)
+    long cost = waves * (bn + 200);
     if (best_cost < 0 || cost < best_cost) {
       best_cost = cost;
       best = bn;
