@@ -13,7 +13,8 @@ import re
 from ctypes import POINTER, c_char_p, c_float, c_int, c_int64, c_uint32, c_uint64, c_void_p
 
 LIB_NAME = "libpipefill.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# PF_LIB_PATH points at another build of the same ABI (diagnostic / A-B builds)
+LIB_PATH = os.environ.get("PF_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 HEADER_PATH = os.path.join(
     os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "pipefill.h"
 )
