@@ -835,6 +835,13 @@ def main() -> None:
         device_s=sum(t["step_end"] - t["start"] for t in steps) / 1e9)
     gemm_launches = len(executor.gemm_samples)
     executor.timing = False
+    traffic, traffic_src = None, None
+    try:  # DRAM bytes per GEMM launch from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")) as fh:
+            tdoc = json.load(fh)
+        traffic, traffic_src = tdoc["per_launch_dram_bytes"], tdoc["source"]
+    except (OSError, KeyError, ValueError):
+        pass
     staging = executor.staging_stats(n_stage0)
     h2d_peak = measure_h2d_gbs()
     staging["h2d_peak_gbs"] = h2d_peak
@@ -894,7 +901,8 @@ def main() -> None:
             "value_definition": "sample-equivalents/s: completed batches x share of the model's FLOPs in "
                                 "the batch's partition, over device time of the timed iterations",
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak if peak else None, "traffic": None,
+                         "frac": achieved / peak if peak else None, "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "kernel": "pf_gemm (tcgen05)", "launches_timed": gemm_launches,
                          "peak_source": peaks["source"] + " bf16_tflops_sustained"},
             "cpu_baseline": cpu,
