@@ -169,6 +169,21 @@ int pf_embedding_ln(const int32_t* ids, const int32_t* type_ids, const void* wor
                     void* Y, int batch, int seq, int hidden, int vocab, float eps,
                     const pf_ctl_t* ctl, void* stream);
 
+/* ---- fp32 fill path (north star: "fp32 path rel 1e-4") -------------------------
+ * fp32 storage and math on the SIMT pipes (TF32 tensor cores cannot meet 1e-4):
+ * pf_gemm_f32 (epilogue bits BIAS | GELU | RESIDUAL as for pf_gemm; 128x128 tiles claimed
+ * through the cursor: resumable), pf_layernorm_f32, pf_embedding_ln_f32 and
+ * pf_attention_f32 (seq <= 128, head_dim 64; packed QKV layout as pf_attention).     */
+int pf_gemm_f32(const float* X, const float* W, const float* bias, const float* residual, float* Y, int M, int N,
+                int K, uint32_t epilogue, const pf_ctl_t* ctl, void* stream);
+int pf_layernorm_f32(const float* X, const float* residual, const float* gamma, const float* beta, float* Y,
+                     int rows, int cols, float eps, const pf_ctl_t* ctl, void* stream);
+int pf_embedding_ln_f32(const int32_t* ids, const float* word, const float* pos, const float* type,
+                        const float* gamma, const float* beta, float* Y, int batch, int seq, int hidden, int vocab,
+                        float eps, const pf_ctl_t* ctl, void* stream);
+int pf_attention_f32(const float* QKV, float* O, int batch, int seq, int heads, int head_dim, float scale,
+                     const pf_ctl_t* ctl, void* stream);
+
 /* ---- image kernels of convolutional fill jobs (ResNet-50), NHWC bf16 -------------
  * A convolution = pf_im2col + pf_gemm (BatchNorm folded into the GEMM weights/bias,
  * ReLU / residual in its epilogue). Col[B*Ho*Wo, Kp], column (ky*kw + kx)*C + c,
@@ -298,6 +313,15 @@ int pf_chain_add_avgpool_bwd(pf_chain_t* chain, const void* dY, void* dX, int B,
 int pf_chain_add_softmax_xent(pf_chain_t* chain, const void* Z, const int32_t* labels, float* loss, void* dZ,
                               int B, int N, float grad_scale);
 int pf_chain_add_sgd(pf_chain_t* chain, const pf_sgd_segment_t* segs, int nseg, float lr, float momentum);
+int pf_chain_add_gemm_f32(pf_chain_t* chain, const float* X, const float* W, const float* bias,
+                          const float* residual, float* Y, int M, int N, int K, uint32_t epilogue);
+int pf_chain_add_layernorm_f32(pf_chain_t* chain, const float* X, const float* residual, const float* gamma,
+                               const float* beta, float* Y, int rows, int cols, float eps);
+int pf_chain_add_embedding_ln_f32(pf_chain_t* chain, const int32_t* ids, const float* word, const float* pos,
+                                  const float* type, const float* gamma, const float* beta, float* Y, int batch,
+                                  int seq, int hidden, int vocab, float eps);
+int pf_chain_add_attention_f32(pf_chain_t* chain, const float* QKV, float* O, int batch, int seq, int heads,
+                               int head_dim, float scale);
 int pf_chain_add_im2col(pf_chain_t* chain, const void* X, void* Col, int B, int H, int W, int C,
                         int kh, int kw, int stride, int pad, int Kp);
 int pf_chain_add_maxpool(pf_chain_t* chain, const void* X, void* Y, int B, int H, int W, int C,

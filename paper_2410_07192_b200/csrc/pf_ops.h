@@ -54,6 +54,15 @@ int make_avgpool_bwd_op(OpPtr* out, const void* dY, void* dX, int B, int HW, int
 int make_xent_op(OpPtr* out, const void* Z, const int32_t* labels, float* loss, void* dZ, int B, int N,
                  float grad_scale);
 int make_sgd_op(OpPtr* out, const pf_sgd_segment_t* segs, int nseg, float lr, float momentum);
+int make_sgemm_op(OpPtr* out, const float* X, const float* W, const float* bias, const float* residual, float* Y,
+                  int M, int N, int K, uint32_t epi);
+int make_layernorm_f32_op(OpPtr* out, const float* X, const float* residual, const float* gamma, const float* beta,
+                          float* Y, int rows, int cols, float eps);
+int make_embedding_ln_f32_op(OpPtr* out, const int32_t* ids, const float* word, const float* pos, const float* type,
+                             const float* gamma, const float* beta, float* Y, int batch, int seq, int hidden,
+                             int vocab, float eps);
+int make_attention_f32_op(OpPtr* out, const float* QKV, float* O, int batch, int seq, int heads, int head_dim,
+                          float scale);
 int make_norm_op(OpPtr* out, bool rms, const void* X, const void* residual, const void* gamma,
                  const void* beta, void* Y, int rows, int cols, float eps);
 int make_softmax_op(OpPtr* out, const void* X, void* Y, int rows, int cols, float scale);

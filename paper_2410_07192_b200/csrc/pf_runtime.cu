@@ -556,6 +556,24 @@ int pf_chain_add_gemm_splitk(pf_chain_t* c, const void* X, const void* W, void* 
     return chain_push(c, MAKE, op);                 \
   } while (0)
 
+int pf_chain_add_gemm_f32(pf_chain_t* c, const float* X, const float* W, const float* bias, const float* residual,
+                          float* Y, int M, int N, int K, uint32_t epilogue) {
+  PF_CHAIN_ADD(pf::make_sgemm_op(&op, X, W, bias, residual, Y, M, N, K, epilogue));
+}
+int pf_chain_add_layernorm_f32(pf_chain_t* c, const float* X, const float* residual, const float* gamma,
+                               const float* beta, float* Y, int rows, int cols, float eps) {
+  PF_CHAIN_ADD(pf::make_layernorm_f32_op(&op, X, residual, gamma, beta, Y, rows, cols, eps));
+}
+int pf_chain_add_embedding_ln_f32(pf_chain_t* c, const int32_t* ids, const float* word, const float* pos,
+                                  const float* type, const float* gamma, const float* beta, float* Y, int batch,
+                                  int seq, int hidden, int vocab, float eps) {
+  PF_CHAIN_ADD(pf::make_embedding_ln_f32_op(&op, ids, word, pos, type, gamma, beta, Y, batch, seq, hidden, vocab, eps));
+}
+int pf_chain_add_attention_f32(pf_chain_t* c, const float* QKV, float* O, int batch, int seq, int heads,
+                               int head_dim, float scale) {
+  PF_CHAIN_ADD(pf::make_attention_f32_op(&op, QKV, O, batch, seq, heads, head_dim, scale));
+}
+
 int pf_chain_add_colstats(pf_chain_t* c, const void* X, const void* G, const void* Ymask, const float* mean,
                           const float* invstd, float* partial, int M, int C, int* out_partials) {
   PF_CHAIN_ADD(pf::make_colstats_op(&op, X, G, Ymask, mean, invstd, partial, M, C, out_partials));

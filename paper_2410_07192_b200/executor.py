@@ -242,8 +242,8 @@ class Executor:
         w = sum(_pad256(model[i].weight_bytes()) for i in range(p.lo, p.hi))
         b = max([e.batch_size for e in p.per_bubble] + [1])
         need = dict(model.workspace(p.lo, p.hi, b))
-        if p.lo > 0:  # the partition's input, reloaded from the activation store
-            need["in"] = b * model.boundary_elems(p.lo)
+        if p.lo > 0:  # the partition's input, reloaded from the activation store (bf16 units)
+            need["in"] = b * model.boundary_elems(p.lo) * model.act_bytes() // 2
         return w, need
 
     def _carve(self, cap: int) -> None:
@@ -283,12 +283,13 @@ class Executor:
             sizes = [model.boundary_elems(p.lo) for p in plan.partitions[1:]]
             elems = max(sizes)
             n_st = 1 if len(set(sizes)) == 1 else 2
-            store_bytes = n_st * cap * elems * 2
+            adt = model.act_dtype()
+            store_bytes = n_st * cap * elems * model.act_bytes()
             free = self.arena.capacity - self.arena.stats()["used"]
             if self.activation_store == "auto" and store_bytes + (64 << 20) <= free:
-                self._store_dev = [self.arena.alloc((cap * elems,), torch.bfloat16) for _ in range(n_st)]
+                self._store_dev = [self.arena.alloc((cap * elems,), adt) for _ in range(n_st)]
             else:
-                self._store_host = [PinnedBuffer((cap * elems,), torch.bfloat16) for _ in range(n_st)]
+                self._store_host = [PinnedBuffer((cap * elems,), adt) for _ in range(n_st)]
         # a batch through partition [lo, hi) counts as this share of a sample: the
         # partition's share of the model's measured execution time (profile at the
         # largest profiled batch size) when the model carries its profile, else of FLOPs
@@ -404,8 +405,8 @@ class Executor:
             x = self.in_dev[:cnt]
         else:
             shape = model.boundary_shape(part.lo)
-            x = ctx.buf("in", cnt * model.boundary_elems(part.lo)).view(cnt, *shape)
-            nb = cnt * model.boundary_elems(part.lo) * 2
+            x = ctx.buf("in", cnt * model.boundary_elems(part.lo), model.act_dtype()).view(cnt, *shape)
+            nb = cnt * model.boundary_elems(part.lo) * model.act_bytes()
             native.call("pf_chain_add_copy", ch.h, x.data_ptr(), nb, self._store_ptr(key[0] - 1), nb, nb, 1, 1)
         ctx.node = 1
         for i in range(part.lo, part.hi):
@@ -420,7 +421,7 @@ class Executor:
             src, spitch, width, rows = model.result_view(x, cnt)
             native.call("pf_chain_add_copy", ch.h, self._results.ptr, width, src, spitch, width, rows, 2)
         else:
-            nb = cnt * model.boundary_elems(part.hi) * 2
+            nb = cnt * model.boundary_elems(part.hi) * model.act_bytes()
             native.call("pf_chain_add_copy", ch.h, self._store_ptr(key[0]), nb, x.data_ptr(), nb, nb, 1, 2)
         ch.finalize()
         ch.seg_ends[-1] = len(ch.units)  # the output copy joins the last module's segment
@@ -526,10 +527,10 @@ class Executor:
         if not batches:
             return prev
         model = self.model
-        in_b = model.input_bytes() if part.lo == 0 else model.boundary_elems(part.lo) * 2
+        in_b = model.input_bytes() if part.lo == 0 else model.boundary_elems(part.lo) * model.act_bytes()
         res_b = self._results.tensor.element_size() * _numel(model.result_shape())
         aux_b = 0 if self._aux_host is None else self._aux_host.tensor[0].numel() * self._aux_host.tensor.element_size()
-        out_b = res_b if part.hi == len(model) else model.boundary_elems(part.hi) * 2
+        out_b = res_b if part.hi == len(model) else model.boundary_elems(part.hi) * model.act_bytes()
         st = self.stream
         base = self._ctl.data_ptr()
         abort_ptr, done_ptr = base, base + 4

@@ -42,6 +42,7 @@ class BertConfig:
     type_vocab: int = 2
     eps: float = 1e-12
     seq: int = 128
+    precision: str = "bf16"  # "fp32": fp32 weights, activations and math (the rel-1e-4 path)
 
     @property
     def params_per_layer(self) -> int:
@@ -97,8 +98,13 @@ class ExecContext:
     def skip(self) -> None:
         self.node += 1
 
-    def buf(self, name: str, numel: int) -> torch.Tensor:
-        return self.ws[name].view(-1)[:numel]
+    def buf(self, name: str, numel: int, dtype: torch.dtype = torch.bfloat16) -> torch.Tensor:
+        """`numel` elements of `dtype` at the start of workspace buffer `name` (buffers are
+        allocated in bf16 units)."""
+        if dtype == torch.bfloat16:
+            return self.ws[name].view(-1)[:numel]
+        esize = torch.tensor([], dtype=dtype).element_size()
+        return self.ws[name].view(-1)[:numel * esize // 2].view(dtype)
 
     def fbuf(self, name: str, numel: int) -> torch.Tensor:
         """fp32 view of a workspace buffer (its size is counted in bf16 elements: 2 per float)."""
@@ -126,7 +132,8 @@ class ExecContext:
         if self.chain is not None:
             epi = (native.PF_EPI_BIAS if b is not None else 0) | (native.PF_EPI_GELU if gelu else 0) \
                 | (native.PF_EPI_RESIDUAL if residual is not None else 0) | (native.PF_EPI_RELU if relu else 0)
-            native.call("pf_chain_add_gemm", self.chain, x.data_ptr(), w.data_ptr(),
+            fn = "pf_chain_add_gemm_f32" if x.dtype == torch.float32 else "pf_chain_add_gemm"
+            native.call(fn, self.chain, x.data_ptr(), w.data_ptr(),
                         None if b is None else b.data_ptr(),
                         None if residual is None else residual.data_ptr(), out.data_ptr(), m, n, k, epi)
             self.node += 1
@@ -164,8 +171,12 @@ class ExecContext:
         if self.chain is not None:
             b, s, three_h = qkv.shape
             hd = three_h // 3 // heads
-            native.call("pf_chain_add_attention", self.chain, qkv.data_ptr(), None, out.data_ptr(), b, s,
-                        heads, hd, float(hd ** -0.5))
+            if qkv.dtype == torch.float32:
+                native.call("pf_chain_add_attention_f32", self.chain, qkv.data_ptr(), out.data_ptr(), b, s, heads,
+                            hd, float(hd ** -0.5))
+            else:
+                native.call("pf_chain_add_attention", self.chain, qkv.data_ptr(), None, out.data_ptr(), b, s,
+                            heads, hd, float(hd ** -0.5))
             self.node += 1
             return
         self._eager(lambda c: K.attention(qkv, heads, out=out, ctl=c, stream=self.stream))
@@ -173,7 +184,8 @@ class ExecContext:
     def layernorm(self, x, g, b, eps: float, out) -> None:
         if self.chain is not None:
             cols = x.shape[-1]
-            native.call("pf_chain_add_layernorm", self.chain, x.data_ptr(), None, g.data_ptr(),
+            fn = "pf_chain_add_layernorm_f32" if x.dtype == torch.float32 else "pf_chain_add_layernorm"
+            native.call(fn, self.chain, x.data_ptr(), None, g.data_ptr(),
                         b.data_ptr(), out.data_ptr(), x.numel() // cols, cols, float(eps))
             self.node += 1
             return
@@ -182,9 +194,14 @@ class ExecContext:
     def embedding(self, ids, word, pos, typ, g, b, eps: float, out) -> None:
         if self.chain is not None:
             bsz, s = ids.shape
-            native.call("pf_chain_add_embedding_ln", self.chain, ids.data_ptr(), None, word.data_ptr(),
-                        pos.data_ptr(), typ.data_ptr(), g.data_ptr(), b.data_ptr(), out.data_ptr(), bsz, s,
-                        word.shape[1], word.shape[0], float(eps))
+            if word.dtype == torch.float32:
+                native.call("pf_chain_add_embedding_ln_f32", self.chain, ids.data_ptr(), word.data_ptr(),
+                            pos.data_ptr(), typ.data_ptr(), g.data_ptr(), b.data_ptr(), out.data_ptr(), bsz, s,
+                            word.shape[1], word.shape[0], float(eps))
+            else:
+                native.call("pf_chain_add_embedding_ln", self.chain, ids.data_ptr(), None, word.data_ptr(),
+                            pos.data_ptr(), typ.data_ptr(), g.data_ptr(), b.data_ptr(), out.data_ptr(), bsz, s,
+                            word.shape[1], word.shape[0], float(eps))
             self.node += 1
             return
         self._eager(lambda c: K.embedding_ln(ids, word, pos, typ, g, b, eps, out=out, ctl=c,
@@ -195,6 +212,7 @@ class FillModule(nn.Module):
     """One node of the linearized fill model."""
 
     n_nodes = 0
+    dtype = torch.bfloat16  # parameter dtype (fp32 modules of the fp32 path override it)
 
     def __init__(self):
         super().__init__()
@@ -207,7 +225,8 @@ class FillModule(nn.Module):
         raise NotImplementedError
 
     def weight_bytes(self) -> int:
-        return sum(2 * _numel(shape) for _, shape, _ in self.param_specs())
+        esize = torch.tensor([], dtype=self.dtype).element_size()
+        return sum(esize * _numel(shape) for _, shape, _ in self.param_specs())
 
     def init_host(self, gen: torch.Generator, std: float = 0.02, pinned: bool = True) -> None:
         """Random init into pinned host memory: N(0, std) weights/biases, LN gamma 1, beta 0.
@@ -216,11 +235,11 @@ class FillModule(nn.Module):
         specs = self.param_specs()
         total = sum(_numel(s) for _, s, _ in specs)
         if pinned:
-            self.host = PinnedBuffer((total,), torch.bfloat16)
+            self.host = PinnedBuffer((total,), self.dtype)
             flat = self.host.tensor
         else:
             self.host = None
-            flat = torch.empty(total, dtype=torch.bfloat16)
+            flat = torch.empty(total, dtype=self.dtype)
         off = 0
         for name, shape, kind in specs:
             n = _numel(shape)
@@ -240,15 +259,16 @@ class FillModule(nn.Module):
                 vals = torch.randn(n, generator=gen) * kind[1]
             else:
                 vals = torch.randn(n, generator=gen) * std
-            flat[off:off + n].copy_(vals.to(torch.bfloat16))
+            flat[off:off + n].copy_(vals.to(self.dtype))
             self.host_params[name] = flat[off:off + n].view(*shape)
             off += n
 
     def stage(self, arena: Arena, stream: torch.cuda.Stream) -> None:
         """H2D copy of this module's weights into the arena (pinned cudaMemcpyAsync)."""
         total = self.host.tensor.numel()
-        dflat = arena.alloc((total,), torch.bfloat16)
-        native.call("pf_stage_h2d", dflat.data_ptr(), self.host.ptr, 2 * total, stream.cuda_stream)
+        dflat = arena.alloc((total,), self.dtype)
+        native.call("pf_stage_h2d", dflat.data_ptr(), self.host.ptr, self.host.tensor.element_size() * total,
+                    stream.cuda_stream)
         off = 0
         for name, shape, _ in self.param_specs():
             n = _numel(shape)
@@ -263,7 +283,8 @@ class FillModule(nn.Module):
         its host blob: bf16 parameters in param_specs order)."""
         nbytes = self.weight_bytes()
         from .arena import device_view
-        dflat = device_view(ptr, (max(nbytes // 2, 1),), torch.bfloat16)
+        esize = torch.tensor([], dtype=self.dtype).element_size()
+        dflat = device_view(ptr, (max(nbytes // esize, 1),), self.dtype)
         dev, off = {}, 0
         for name, shape, _ in self.param_specs():
             n = _numel(shape)
@@ -306,6 +327,7 @@ class BertEmbeddings(FillModule):
     def __init__(self, cfg: BertConfig):
         super().__init__()
         self.cfg = cfg
+        self.dtype = torch.float32 if cfg.precision == "fp32" else torch.bfloat16
 
     def param_specs(self):
         c = self.cfg
@@ -313,15 +335,16 @@ class BertEmbeddings(FillModule):
                 ("type", (c.type_vocab, c.hidden), "w"), ("ln_g", (c.hidden,), "one"),
                 ("ln_b", (c.hidden,), "zero")]
 
-    def workspace(self, batch):
-        return {"act": batch * self.cfg.seq * self.cfg.hidden}
+    def workspace(self, batch):  # bf16 units
+        u = 2 if self.cfg.precision == "fp32" else 1
+        return {"act": u * batch * self.cfg.seq * self.cfg.hidden}
 
     def node_units(self, batch):
         return [(K.norm_units(batch * self.cfg.seq, self.cfg.hidden), ATOMIC)]
 
     def forward(self, ids: torch.Tensor, ctx: ExecContext) -> torch.Tensor:
         b, s = ids.shape
-        out = ctx.buf("act", b * s * self.cfg.hidden).view(b, s, self.cfg.hidden)
+        out = ctx.buf("act", b * s * self.cfg.hidden, self.dtype).view(b, s, self.cfg.hidden)
         d = self.dev
         ctx.embedding(ids, d["word"], d["pos"], d["type"], d["ln_g"], d["ln_b"], self.cfg.eps, out)
         return out
@@ -337,6 +360,7 @@ class BertLayer(FillModule):
     def __init__(self, cfg: BertConfig):
         super().__init__()
         self.cfg = cfg
+        self.dtype = torch.float32 if cfg.precision == "fp32" else torch.bfloat16
 
     def param_specs(self):
         h, f = self.cfg.hidden, self.cfg.ffn
@@ -347,9 +371,11 @@ class BertLayer(FillModule):
                 ("ffn2_w", (h, f), "w"), ("ffn2_b", (h,), "w"),
                 ("ln2_g", (h,), "one"), ("ln2_b", (h,), "zero")]
 
-    def workspace(self, batch):
+    def workspace(self, batch):  # bf16 units
         m, h, f = batch * self.cfg.seq, self.cfg.hidden, self.cfg.ffn
-        return {"qkv": m * 3 * h, "ctx": m * h, "a": m * h, "a_ln": m * h, "ffn": m * f, "o": m * h}
+        u = 2 if self.cfg.precision == "fp32" else 1
+        return {"qkv": u * m * 3 * h, "ctx": u * m * h, "a": u * m * h, "a_ln": u * m * h, "ffn": u * m * f,
+                "o": u * m * h}
 
     def flops_per_sample(self) -> float:
         s, h, f = self.cfg.seq, self.cfg.hidden, self.cfg.ffn
@@ -376,12 +402,13 @@ class BertLayer(FillModule):
         m, f = b * s, self.cfg.ffn
         d = self.dev
         x2 = x.view(m, h)
-        qkv = ctx.buf("qkv", m * 3 * h).view(b, s, 3 * h)
-        cx = ctx.buf("ctx", m * h).view(m, h)
-        a = ctx.buf("a", m * h).view(m, h)
-        a_ln = ctx.buf("a_ln", m * h).view(m, h)
-        hf = ctx.buf("ffn", m * f).view(m, f)
-        o = ctx.buf("o", m * h).view(m, h)
+        dt = self.dtype
+        qkv = ctx.buf("qkv", m * 3 * h, dt).view(b, s, 3 * h)
+        cx = ctx.buf("ctx", m * h, dt).view(m, h)
+        a = ctx.buf("a", m * h, dt).view(m, h)
+        a_ln = ctx.buf("a_ln", m * h, dt).view(m, h)
+        hf = ctx.buf("ffn", m * f, dt).view(m, f)
+        o = ctx.buf("o", m * h, dt).view(m, h)
         ctx.gemm(x2, d["qkv_w"], d["qkv_b"], qkv.view(m, 3 * h))
         ctx.attention(qkv, self.cfg.heads, cx.view(b, s, h))
         ctx.gemm(cx, d["out_w"], d["out_b"], a, residual=x2)
@@ -415,6 +442,13 @@ class FillSequential(nn.Sequential):
 
     def result_dtype(self) -> torch.dtype:
         return torch.bfloat16
+
+    def act_dtype(self) -> torch.dtype:
+        """dtype of the activations stored between partitions."""
+        return torch.bfloat16
+
+    def act_bytes(self) -> int:
+        return torch.tensor([], dtype=self.act_dtype()).element_size()
 
     def aux_spec(self) -> Optional[tuple[torch.dtype, tuple[int, ...]]]:
         """(dtype, per-sample shape) of a second per-sample input (labels), or None."""
@@ -485,9 +519,15 @@ class BertSequential(FillSequential):
     def result_shape(self):
         return (self.cfg.hidden,)
 
+    def act_dtype(self):
+        return torch.float32 if self.cfg.precision == "fp32" else torch.bfloat16
+
+    def result_dtype(self):
+        return self.act_dtype()
+
     def result_view(self, x, cnt):
-        s, h = self.cfg.seq, self.cfg.hidden
-        return x.data_ptr(), s * h * 2, h * 2, cnt
+        s, h, e = self.cfg.seq, self.cfg.hidden, self.act_bytes()
+        return x.data_ptr(), s * h * e, h * e, cnt
 
     def make_inputs(self, job_seed, first, count):
         return synthetic_ids(job_seed, first, count, self.cfg.seq, self.cfg.vocab)

@@ -78,7 +78,10 @@ def linear(
     ctl: Optional[KernelCtl] = None,
     stream: Optional[torch.cuda.Stream] = None,
 ) -> torch.Tensor:
-    """out = [ReLU]([GELU](x @ weight.T + bias) [+ residual]) — tcgen05 GEMM (pf_gemm)."""
+    """out = [ReLU]([GELU](x @ weight.T + bias) [+ residual]) — tcgen05 GEMM (pf_gemm); fp32
+    tensors take the fp32 path (pf_gemm_f32)."""
+    if x.dtype == torch.float32:
+        return _linear_f32(x, weight, bias, gelu=gelu, residual=residual, out=out, ctl=ctl, stream=stream)
     _check_bf16_cuda("x", x)
     _check_bf16_cuda("weight", weight)
     k = x.shape[-1]
@@ -117,7 +120,14 @@ def layernorm(
     ctl: Optional[KernelCtl] = None,
     stream: Optional[torch.cuda.Stream] = None,
 ) -> torch.Tensor:
-    """out = LayerNorm(x [+ residual]) (pf_layernorm)."""
+    """out = LayerNorm(x [+ residual]) (pf_layernorm; fp32 tensors: pf_layernorm_f32)."""
+    if x.dtype == torch.float32:
+        cols = x.shape[-1]
+        if out is None:
+            out = torch.empty_like(x)
+        native.call("pf_layernorm_f32", x.data_ptr(), _ptr(residual), gamma.data_ptr(), beta.data_ptr(),
+                    out.data_ptr(), x.numel() // cols, cols, float(eps), _ctl_ref(ctl), _stream(stream))
+        return out
     _check_bf16_cuda("x", x)
     cols = x.shape[-1]
     rows = x.numel() // cols
@@ -184,13 +194,22 @@ def attention(
     ctl: Optional[KernelCtl] = None,
     stream: Optional[torch.cuda.Stream] = None,
 ) -> torch.Tensor:
-    """Multi-head attention over packed qkv [batch, seq, 3*hidden] -> [batch, seq, hidden]."""
-    _check_bf16_cuda("qkv", qkv)
+    """Multi-head attention over packed qkv [batch, seq, 3*hidden] -> [batch, seq, hidden]
+    (pf_attention; fp32 tensors: pf_attention_f32, no mask)."""
     batch, seq, three_h = qkv.shape
     hidden = three_h // 3
     head_dim = hidden // heads
     if scale is None:
         scale = head_dim ** -0.5
+    if qkv.dtype == torch.float32:
+        if mask_add is not None:
+            raise ValueError("the fp32 attention path takes no mask")
+        if out is None:
+            out = torch.empty(batch, seq, hidden, dtype=torch.float32, device=qkv.device)
+        native.call("pf_attention_f32", qkv.data_ptr(), out.data_ptr(), batch, seq, heads, head_dim, float(scale),
+                    _ctl_ref(ctl), _stream(stream))
+        return out
+    _check_bf16_cuda("qkv", qkv)
     if mask_add is not None:
         if mask_add.dtype != torch.float32 or mask_add.shape != (batch, seq):
             raise ValueError("mask_add must be fp32 [batch, seq]")
@@ -223,6 +242,13 @@ def embedding_ln(
         raise ValueError("ids must be int32 on CUDA")
     batch, seq = ids.shape
     hidden = word.shape[1]
+    if word.dtype == torch.float32:
+        if out is None:
+            out = torch.empty(batch, seq, hidden, dtype=torch.float32, device=ids.device)
+        native.call("pf_embedding_ln_f32", ids.data_ptr(), word.data_ptr(), pos.data_ptr(), type_emb.data_ptr(),
+                    gamma.data_ptr(), beta.data_ptr(), out.data_ptr(), batch, seq, hidden, word.shape[0], float(eps),
+                    _ctl_ref(ctl), _stream(stream))
+        return out
     if out is None:
         out = torch.empty(batch, seq, hidden, dtype=torch.bfloat16, device=ids.device)
     native.call(
@@ -424,3 +450,16 @@ def sgd_segments(segs: list[dict]):
 def sgd_update(segs: list[dict], lr: float, momentum: float, *, ctl=None, stream=None):
     arr = sgd_segments(segs)
     native.call("pf_sgd_update", arr, len(segs), float(lr), float(momentum), _ctl_ref(ctl), _stream(stream))
+
+
+def _linear_f32(x, weight, bias=None, *, gelu=False, residual=None, out=None, ctl=None, stream=None):
+    k = x.shape[-1]
+    m = x.numel() // k
+    n = weight.shape[0]
+    epi = (PF_EPI_BIAS if bias is not None else 0) | (PF_EPI_GELU if gelu else 0) \
+        | (PF_EPI_RESIDUAL if residual is not None else 0)
+    if out is None:
+        out = torch.empty(*x.shape[:-1], n, dtype=torch.float32, device=x.device)
+    native.call("pf_gemm_f32", x.data_ptr(), weight.data_ptr(), _ptr(bias), _ptr(residual), out.data_ptr(),
+                m, n, k, epi, _ctl_ref(ctl), _stream(stream))
+    return out

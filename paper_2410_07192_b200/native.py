@@ -168,6 +168,21 @@ _SIGNATURES: dict[str, tuple] = {
     "pf_chain_add_softmax_xent": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int,
                                           c_float]),
     "pf_chain_add_sgd": (c_int, [c_void_p, POINTER(SgdSegment), c_int, c_float, c_float]),
+    "pf_gemm_f32": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_uint32,
+                            POINTER(PfCtl), c_void_p]),
+    "pf_layernorm_f32": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_float,
+                                 POINTER(PfCtl), c_void_p]),
+    "pf_embedding_ln_f32": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
+                                    c_int, c_int, c_int, c_float, POINTER(PfCtl), c_void_p]),
+    "pf_attention_f32": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_float, POINTER(PfCtl),
+                                 c_void_p]),
+    "pf_chain_add_gemm_f32": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int,
+                                      c_int, c_uint32]),
+    "pf_chain_add_layernorm_f32": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
+                                           c_int, c_float]),
+    "pf_chain_add_embedding_ln_f32": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                              c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_float]),
+    "pf_chain_add_attention_f32": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_float]),
     "pf_chain_create": (c_int, [POINTER(c_void_p)]),
     "pf_chain_destroy": (c_int, [c_void_p]),
     "pf_chain_add_gemm": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int,

@@ -33,10 +33,10 @@ def _module_mem(model: FillSequential, i: int, b: int) -> tuple[int, int]:
     partition-input buffer, the batch's inputs and results, and the control block."""
     w = model[i].weight_bytes()
     ws = sum(2 * v for v in model.workspace(0, len(model), b).values())
-    res = 2 * b
+    res = b * torch.tensor([], dtype=model.result_dtype()).element_size()
     for d in model.result_shape():
         res *= d
-    act = 2 * b * model.boundary_elems(i) + res + b * model.input_bytes()
+    act = model.act_bytes() * b * model.boundary_elems(i) + res + b * model.input_bytes()
     return w, ws + act + FIXED_TRANSIENT_BYTES
 
 

@@ -11,7 +11,9 @@ from test_train_gpu import _plan_item
 native.require_device()
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 4
-model = bert(BERT_LARGE, seed=0)
+import dataclasses
+cfg = dataclasses.replace(BERT_LARGE, precision=os.environ.get("PRECISION", "bf16"))
+model = bert(cfg, seed=0)
 item = _plan_item(pf, model, B * n, B)
 ex = Executor(8 << 30)
 ex.load(item, model)
@@ -20,7 +22,7 @@ for k in range(n):
     ex.fill(BubbleSlot(0, None, 0))
     rec = ex.settle()
     times.append((rec.fill_end_ns - rec.fill_start_ns) / 1e6)
-fl = BERT_LARGE.flops_per_sample * B
+fl = cfg.flops_per_sample * B
 print("batch ms", [round(t, 3) for t in times], "samples/s", B / (min(times) / 1e3),
       "TFLOP/s", fl / (min(times) / 1e3) / 1e12)
 ex.close()
