@@ -175,6 +175,7 @@ class IterationRecord:
     anchor_stamp: int = -1  # index into stamps holding the anchor this iteration used
     epoch: int = 0  # stamp-buffer generation (stamp indices repeat after reset_stamps)
     bubbles: list[tuple[int, int, int]] = field(default_factory=list)  # (kind, set idx, clear idx)
+    bubble_mem: list[tuple[int, int]] = field(default_factory=list)  # (kind, main-job bytes allocated)
 
 
 # --------------------------------------------------------------------------- links
@@ -271,6 +272,9 @@ class StageEngine:
                 self.launches += 3
                 kind = 0 if ins.kind is BubbleKind.FWD_BWD else 1
                 rec.bubbles.append((kind, set_idx, clear_idx))
+                # the main job's allocated bytes while the bubble is open (the allocator
+                # tracks tensors in enqueue order, which is the order they live on the device)
+                rec.bubble_mem.append((kind, torch.cuda.memory_allocated()))
                 if fill and self.executor is not None:
                     self.executor.fill(BubbleSlot(kind, start_ev, flag, tag=self._tag(clear_idx)))
                 main.wait_event(end_ev)
@@ -443,6 +447,7 @@ class NcclPipelineEngine:
         self.launches += 2
         k = 0 if kind is BubbleKind.FWD_BWD else 1
         rec.bubbles.append((k, set_idx, clear_idx))
+        rec.bubble_mem.append((k, torch.cuda.memory_allocated()))
         if fill and self.executor is not None:
             self.executor.fill(BubbleSlot(k, start_ev, flag, tag=self._tag(clear_idx)))
         self.main.wait_event(end_ev)
@@ -528,3 +533,67 @@ class NcclPipelineEngine:
 
     def _tag(self, clear_idx: int) -> tuple:
         return (id(self), self.epoch, clear_idx)
+
+
+# --------------------------------------------------------------------------- characterization
+
+
+def characterize_bubbles(stage_id: int, timings: list[dict], records: list[IterationRecord],
+                         fill_fraction: float, total_bytes: int, reserve_bytes: int = 2 << 30,
+                         analytic=None):
+    """Bubble characterization from measured iterations: the paper
+    probes each bubble's duration with a doubling wait and reads memory_allocated();
+    here every BUBBLE instruction already stamps its start (flag set) and its end (recv
+    completion, flag cleared) on the device, so the durations are read directly, and the
+    main job's allocated bytes at each BUBBLE instruction give its free memory.
+
+    `timings` are engine.record_timing dicts of fill-off iterations and `records` the
+    matching IterationRecords. Returns (BubbleCycle, report) -- the cycle uses the
+    reference's usable-time rule (schedule.cycle_from_measurements)."""
+    import statistics
+
+    from .schedule import cycle_from_measurements
+
+    durs = {0: [], 1: []}
+    for t in timings:
+        for kind, t_set, t_clr, _ in t["bubbles"]:
+            durs[kind].append((t_clr - t_set) // 1000)
+    mem = {0: [], 1: []}
+    for r in records:
+        for kind, alloc in r.bubble_mem:
+            mem[kind].append(alloc)
+    periods = [t["main_end"] - t["start"] for t in timings]
+    period_us = int(statistics.median(periods) // 1000) if periods else 0
+    d = [int(statistics.median(durs[k])) if durs[k] else 0 for k in (0, 1)]
+    free = [max(0, total_bytes - (max(mem[k]) if mem[k] else 0) - reserve_bytes) for k in (0, 1)]
+    unfill = 0
+    if analytic is not None:
+        unfill = max(0, min(analytic.unfillable_us, period_us - sum(d)))
+    cycle = cycle_from_measurements(stage_id, max(period_us, sum(d)), d, free, fill_fraction, unfillable_us=unfill)
+    report = {"measured_bubbles_us": d, "measured_period_us": period_us,
+              "bubble_samples": {str(k): len(durs[k]) for k in (0, 1)},
+              "main_job_allocated_bytes": [max(mem[k]) if mem[k] else 0 for k in (0, 1)],
+              "free_mem_bytes": free}
+    if analytic is not None:
+        report.update({"analytic_bubbles_us": [b.duration_us for b in analytic.bubbles],
+                       "analytic_period_us": analytic.period_us})
+    return cycle, report
+
+
+def characterize_stage(engine: "StageEngine", iterations: int = 3, fill_fraction: float = 0.68,
+                       reserve_bytes: int = 2 << 30):
+    """Run `iterations` fill-off iterations of an emulated stage and characterize its bubbles."""
+    from .schedule import build_bubble_cycle
+
+    timings, records = [], []
+    for k in range(iterations + 1):  # the first iteration warms the main job up (discarded)
+        engine.reset_stamps()
+        engine.set_anchor()
+        rec = engine.run_iteration(0, fill=False)
+        t = engine.record_timing(rec)
+        if k:
+            timings.append(t)
+            records.append(rec)
+    _, total = torch.cuda.mem_get_info()
+    return characterize_bubbles(engine.stage, timings, records, fill_fraction, total, reserve_bytes,
+                                analytic=build_bubble_cycle(engine.cfg, engine.stage))

@@ -147,3 +147,25 @@ def test_executor_preemption_resume_is_exact(pf):
     assert torch.equal(ex.results(), ref), (n, aborted)
     ex.close()
     native.call("pf_flag_destroy", flag)
+
+
+def test_bubble_characterization_matches_the_emulated_timeline(pf):
+    """Measured characterization (flag stamps + allocated bytes at each BUBBLE) of an
+    emulated stage reproduces the analytic bubble durations its artificial neighbours
+    follow (PAPER.md:424-425; schedule.build_bubble_cycle)."""
+    from paper_2410_07192_b200.engine import (GPT2_SMALL_STAGE, GPTStage, StageEngine, characterize_stage,
+                                              measure_stage_times)
+
+    model = GPTStage(GPT2_SMALL_STAGE, seed=0)
+    tf, tb = measure_stage_times(model)
+    for stage in (0, 2):
+        cfg = pf.PipelineConfig(4, 8, tf, tb, pf.ScheduleKind.ONE_F_ONE_B, 1, 1, 0.68)
+        eng = StageEngine(cfg, stage, model, None)
+        cycle, rep = characterize_stage(eng, iterations=2)
+        for got, want in zip(rep["measured_bubbles_us"], rep["analytic_bubbles_us"]):
+            if want == 0:
+                continue
+            # the neighbours follow the analytic timeline; the stage's own compute is real
+            assert abs(got - want) <= 0.1 * want + 200, rep
+        assert all(f > 0 for f in rep["free_mem_bytes"]), rep
+        assert cycle.bubbles[0].duration_us == rep["measured_bubbles_us"][0]
