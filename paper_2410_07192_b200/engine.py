@@ -137,7 +137,12 @@ class GPTStage(nn.Module):
             for p, q in zip(self.parameters(), snap["params"]):
                 p.copy_(q)
         self.opt.state.clear()
-        self.opt.load_state_dict(snap["opt"])
+        # load a copy: load_state_dict keeps (does not copy) state tensors that already have
+        # the parameter's dtype and device, so the optimizer would otherwise update the
+        # snapshot in place and a second restore would replay a corrupted state
+        import copy
+
+        self.opt.load_state_dict(copy.deepcopy(snap["opt"]))
         self.opt.zero_grad(set_to_none=False)
         torch.cuda.synchronize()
 
@@ -406,9 +411,11 @@ class NcclPipelineEngine:
 
     # ---- P2P helpers (comm stream) ------------------------------------------------
     def _recv(self, src: int, group) -> tuple[torch.Tensor, torch.cuda.Event]:
-        buf = torch.empty(self.shape, dtype=torch.bfloat16, device="cuda")
         with torch.cuda.stream(self.comm):
-            buf.record_stream(self.comm)
+            # allocated on the comm stream, so anything the allocator does to the block
+            # (deterministic mode fills new memory) is ordered before NCCL's recv into it
+            buf = torch.empty(self.shape, dtype=torch.bfloat16, device="cuda")
+            buf.record_stream(self.main)  # consumed on the main stream after `ev`
             work = self.dist.irecv(buf, src, group=group)
             work.wait()  # comm stream waits for the NCCL recv
             ev = torch.cuda.Event()
