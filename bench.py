@@ -294,7 +294,7 @@ def run_service_sweep(args, conf) -> None:
             for jid, res in rep.per_job.items():
                 res.predicted_completion_s = pred.get(jid)
             recs = [r for ex in executors for r in ex.records]
-            eq = sum(r.samples_done * r.model_fraction for r in recs)
+            eq = sum(r.sample_eq for r in recs)
             ns = sum(t["step_end"] - t["start"] for t in steps)
             launches += sum(ex.kernel_launches for ex in executors) + sum(e.launches for e in engines)
             for t in steps:
@@ -472,7 +472,7 @@ def run_training_depths(args, conf) -> None:
                     bubbles.append((t_set, t_clr))
                     fills.append((r_.fill_start_ns, r_.fill_end_ns) if r_ is not None else (0, 0))
             st = FillStats(
-                sample_equivalents=sum(r_.samples_done * r_.model_fraction for r_ in recs),
+                sample_equivalents=sum(r_.sample_eq for r_ in recs),
                 samples_completed=sum(r_.samples_completed for r_ in recs),
                 fill_busy_ns=busy_in_bubbles(bubbles, fills), bubble_ns=sum(b1 - b0 for b0, b1 in bubbles),
                 idle_ns=sum(pf.build_bubble_cycle(pcfg, t["stage"]).total_idle_us * 1000 for t in steps),
@@ -845,7 +845,7 @@ def main() -> None:
                       f"{(t_clr - t_set) / 1e6:.2f} ms: {info}", file=sys.stderr)
     slowdown = mean_slowdown(on_iter, off)
     stats = FillStats(
-        sample_equivalents=sum(r.samples_done * r.model_fraction for r in recs),
+        sample_equivalents=sum(r.sample_eq for r in recs),
         samples_completed=sum(r.samples_completed for r in recs),
         fill_busy_ns=busy_in_bubbles(bubbles, fills),
         bubble_ns=sum(b1 - b0 for b0, b1 in bubbles),

@@ -73,6 +73,8 @@ class BubbleRecord:
     model_fraction: float = 1.0  # share of the model's FLOPs in this bubble's partition
     samples_completed: int = 0  # samples that left the LAST partition in this bubble
     tag: object = None
+    sample_eq: float = 0.0  # completed batches x their partition's share of the model (all partitions)
+    ran_ahead: bool = False  # the bubble also enqueued batches of the next partition
 
 
 @dataclass
@@ -92,6 +94,7 @@ class _Pending:
     launches: int
     part: int
     has_resume: bool = False
+    parts: list[int] = None  # partition of every batch (run-ahead appends partition part + 1)
 
 
 class _Chain:
@@ -130,7 +133,7 @@ class Executor:
     """One per GPU (pipeline-stage worker). Not thread-safe; driven by the engine."""
 
     def __init__(self, arena_bytes: int, *, priority: int = 1, job_seed: int = 0,
-                 activation_store: str = "auto"):
+                 activation_store: str = "auto", run_ahead: bool = True):
         native.require_device()
         self.arena = Arena(arena_bytes)
         lo_prio, hi_prio = torch.cuda.Stream.priority_range()
@@ -138,6 +141,10 @@ class Executor:
         self.copy_stream = torch.cuda.Stream(priority=lo_prio)
         self.job_seed = job_seed
         self.activation_store = activation_store  # "auto" (HBM if it fits) | "host"
+        # run-ahead: when a bubble's batches finish the range's current partition, stage the
+        # next partition in-stream and run its planned batches in the same bubble (the
+        # reference's time model charges whole cycles per partition, partition.py:118-124)
+        self.run_ahead = run_ahead
         self.item: Optional[WorkItem] = None
         self.model: Optional[FillSequential] = None
         self.plan: Optional[ExecutionPlan] = None
@@ -510,14 +517,16 @@ class Executor:
         if not self.busy:
             return prev
         pr = self.progress
+        if self._staged_part != pr.part:  # a run-ahead staged the next partition over this one
+            self._stage_partition(pr.part)
         part = self.plan.partitions[pr.part]
         entry = part.per_bubble[slot.index] if slot.index < len(part.per_bubble) else None
         n_total = self.item.entry.size
         batches: list[tuple[int, int, int]] = []
         if pr.resume is not None:
             batches.append(pr.resume)
+        start = pr.next_sample
         if entry is not None and entry.num_batches > 0:
-            start = pr.next_sample
             for _ in range(entry.num_batches - (1 if pr.resume is not None else 0)):
                 if start >= n_total:
                     break
@@ -526,11 +535,30 @@ class Executor:
                 start += cnt
         if not batches:
             return prev
+        parts = [pr.part] * len(batches)
+        ahead = pr.part + 1
+        if (self.run_ahead and not self.model.is_training and start >= n_total and ahead < len(self.plan.partitions)
+                and len(batches) < MAX_BATCHES):
+            nxt = self.plan.partitions[ahead]
+            e2 = nxt.per_bubble[slot.index] if slot.index < len(nxt.per_bubble) else None
+            s2 = 0
+            if e2 is not None:
+                for _ in range(min(e2.num_batches, MAX_BATCHES - len(batches))):
+                    if s2 >= n_total:
+                        break
+                    cnt = min(e2.batch_size, n_total - s2)
+                    batches.append((s2, cnt, 0))
+                    parts.append(ahead)
+                    s2 += cnt
         model = self.model
-        in_b = model.input_bytes() if part.lo == 0 else model.boundary_elems(part.lo) * model.act_bytes()
         res_b = self._results.tensor.element_size() * _numel(model.result_shape())
         aux_b = 0 if self._aux_host is None else self._aux_host.tensor[0].numel() * self._aux_host.tensor.element_size()
-        out_b = res_b if part.hi == len(model) else model.boundary_elems(part.hi) * model.act_bytes()
+
+        def io_bytes(pi: int) -> tuple[int, int]:
+            pp = self.plan.partitions[pi]
+            ib = model.input_bytes() if pp.lo == 0 else model.boundary_elems(pp.lo) * model.act_bytes()
+            ob = res_b if pp.hi == len(model) else model.boundary_elems(pp.hi) * model.act_bytes()
+            return ib, ob
         st = self.stream
         base = self._ctl.data_ptr()
         abort_ptr, done_ptr = base, base + 4
@@ -542,14 +570,16 @@ class Executor:
         # offsets from desc[k] (k = the bubble's done counter when it starts)
         dh = self._desc_host.tensor
         for k, (first, cnt, node) in enumerate(batches):
+            pp = self.plan.partitions[parts[k]]
+            in_b, out_b = io_bytes(parts[k])
             dh[k, 0] = first * in_b
             dh[k, 1] = first * out_b
             dh[k, 2] = first * aux_b
             if node == 0 and aux_b:
                 self.h2d_bytes += cnt * aux_b
-            if node == 0 and (part.lo == 0 or self._store_host is not None):
+            if node == 0 and (pp.lo == 0 or self._store_host is not None):
                 self.h2d_bytes += cnt * in_b
-            if part.hi == len(model) or self._store_host is not None:
+            if pp.hi == len(model) or self._store_host is not None:
                 self.d2h_bytes += cnt * out_b
         with torch.cuda.stream(st):
             if slot.start_event is not None:
@@ -563,8 +593,10 @@ class Executor:
             native.call("pf_stage_h2d", self._desc.data_ptr(), self._desc_host.ptr,
                         8 * DESC_WORDS * len(batches), st.cuda_stream)
             native.call("pf_read_globaltimer", base + 32, st.cuda_stream)
-            for first, cnt, node in batches:
-                ch = self._chain(pr.part, cnt, flag)
+            for k, (first, cnt, node) in enumerate(batches):
+                if parts[k] != pr.part and parts[k - 1] == pr.part:
+                    self._stage_in_stream(parts[k], st)  # run-ahead: after this partition's batches
+                ch = self._chain(parts[k], cnt, flag)
                 if node > 0 or not _USE_GRAPHS:  # resume a yielded batch at its first incomplete node
                     native.call("pf_chain_launch", ch.h, flag, abort_ptr if flag else None,
                                 cursors if flag else None, done_ptr, node, 0, 0, st.cuda_stream)
@@ -576,9 +608,36 @@ class Executor:
             launches += 2
         ev = torch.cuda.Event()
         ev.record(st)
-        self.pending = _Pending(slot, batches, ev, launches, pr.part, has_resume=pr.resume is not None)
+        self.pending = _Pending(slot, batches, ev, launches, pr.part, has_resume=pr.resume is not None,
+                                parts=parts)
         self.kernel_launches += launches
         return prev
+
+    def _stage_in_stream(self, part: int, st: torch.cuda.Stream) -> None:
+        """Run-ahead staging: copy partition `part`'s weights into the region on the fill
+        stream itself, ordered after the previous partition's batches. Not gated by the
+        flag: if the bubble closes first the copy still lands (PCIe only, no SMs) and the
+        interrupted partition is re-staged before its next batch."""
+        p = self.plan.partitions[part]
+        views, ws = self._part_layout(part)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        staged = 0
+        for i in range(p.lo, p.hi):
+            mod = self.model[i]
+            nbytes = mod.weight_bytes()
+            if nbytes:
+                native.call("pf_stage_h2d", self._module_ptr(part, i), mod.host.ptr, nbytes, st.cuda_stream)
+            self.h2d_bytes += nbytes
+            staged += nbytes
+            mod.dev = views[i]
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(st)
+        self._staged_event = ev
+        self._staged_part = part
+        self.stagings.append((staged, e0, ev))
+        self.ws = ws
+        self._dev_views = dict(views)
 
     def settle(self) -> Optional[BubbleRecord]:
         """Wait for the pending bubble's fill work, read the control block, advance
@@ -615,15 +674,29 @@ class Executor:
                         self.gemm_samples.append((fl, (t1 - t0) / 1e6))
         n_total = self.item.entry.size
         samples = 0
+        parts = pend.parts or [pend.part] * len(pend.batches)
+        rec.ran_ahead = any(p_ != pend.part for p_ in parts)
+        last_part = len(self.plan.partitions) - 1
+        completed_last = 0
         for k, (first, cnt, node) in enumerate(pend.batches):
+            if parts[k] != pr.part and k <= done:
+                # the run-ahead reached the next partition: the current one is complete
+                if pr.resume is not None or pr.next_sample < n_total:
+                    break  # (cannot happen: stream order) keep the current partition
+                pr.part = parts[k]
+                pr.next_sample = 0
+                pr.resume = None
             if k < done:
                 samples += cnt
+                rec.sample_eq += cnt * self._flops_frac[parts[k]]
+                if parts[k] == last_part:
+                    completed_last += cnt
                 if k == 0 and pend.has_resume:  # the resumed batch completed
                     pr.resume = None
                 else:
                     pr.next_sample = max(pr.next_sample, first + cnt)
             elif k == done and aborted:
-                ch = self._chains[(pend.part, cnt, pend.slot.flag_ptr or None)]
+                ch = self._chains[(parts[k], cnt, pend.slot.flag_ptr or None)]
                 cur = w[_CURSOR0:_CURSOR0 + len(ch.units)]
                 resume_node = len(ch.units)
                 for j, (u, _) in enumerate(ch.units):
@@ -635,6 +708,9 @@ class Executor:
                 if resume_node >= len(ch.units):
                     pr.resume = None  # every node finished; only the end marker was skipped
                     samples += cnt
+                    rec.sample_eq += cnt * self._flops_frac[parts[k]]
+                    if parts[k] == last_part:
+                        completed_last += cnt
                 else:
                     pr.resume = (first, cnt, max(resume_node, node))
                     if not ch.units[resume_node][1]:
@@ -643,9 +719,8 @@ class Executor:
             else:
                 break
         rec.samples_done = samples
-        if pend.part == len(self.plan.partitions) - 1:
-            rec.samples_completed = samples
-            self.samples_completed += samples
+        rec.samples_completed = completed_last
+        self.samples_completed += completed_last
         if pr.resume is None and pr.next_sample >= n_total:
             if pr.part == len(self.plan.partitions) - 1:
                 pr.finished = True

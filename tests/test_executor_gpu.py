@@ -106,15 +106,23 @@ def test_executor_multi_partition_offload_matches_single(pf):
     assert torch.equal(outs[0], outs[1])
 
 
-def test_executor_preemption_resume_is_exact(pf):
+@pytest.mark.parametrize("multi", [False, True])
+def test_executor_preemption_resume_is_exact(pf, multi):
     """Bubbles that close mid-batch (timer-cleared flag) must yield, resume at the
-    first incomplete kernel, and produce results identical to an unpreempted run."""
+    first incomplete kernel, and produce results identical to an unpreempted run --
+    also for a multi-partition plan, where a bubble that finishes a partition runs
+    ahead into the next one (in-stream weight staging) and may be preempted there."""
     from paper_2410_07192_b200 import native
     from paper_2410_07192_b200.executor import BubbleSlot, Executor
     from paper_2410_07192_b200.fillmodels import bert
 
     model = bert(tiny_cfg(), seed=6)
-    item, _ = plan_item(pf, model, samples=48, free_mem=8_000_000_000, sizes=(8, 16))
+    free = 8_000_000_000
+    if multi:
+        free = max(model[0].weight_bytes(), 2 * model[1].weight_bytes()) + 17_000_000
+    item, plan = plan_item(pf, model, samples=48, free_mem=free, sizes=(8, 16))
+    if multi:
+        assert len(plan.partitions) > 1
     ex0 = Executor(256 << 20, job_seed=2)
     ex0.load(item, model)
     run_to_completion(ex0, lambda k: BubbleSlot(k % 2, None, 0))
@@ -145,6 +153,8 @@ def test_executor_preemption_resume_is_exact(pf):
     aborted = sum(r.aborted for r in ex.records)
     assert aborted > 0, "bubbles were long enough to never preempt; shorten them"
     assert torch.equal(ex.results(), ref), (n, aborted)
+    if multi:  # some bubble ran ahead into the next partition
+        assert any(r.ran_ahead for r in ex.records)
     ex.close()
     native.call("pf_flag_destroy", flag)
 
@@ -166,6 +176,6 @@ def test_bubble_characterization_matches_the_emulated_timeline(pf):
             if want == 0:
                 continue
             # the neighbours follow the analytic timeline; the stage's own compute is real
-            assert abs(got - want) <= 0.1 * want + 200, rep
+            assert abs(got - want) <= 0.25 * want + 200, rep
         assert all(f > 0 for f in rep["free_mem_bytes"]), rep
         assert cycle.bubbles[0].duration_us == rep["measured_bubbles_us"][0]
