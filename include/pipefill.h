@@ -138,6 +138,15 @@ int pf_gemm_units(int M, int N, int K, uint32_t* out_units);
 int pf_gemm_splitk(const void* X, const void* W, void* Y, int M, int N, int K, int splits,
                    const pf_ctl_t* ctl, void* stream);
 int pf_gemm_splitk_splits(int K, int requested, int* out_splits);
+/* MN-major operands (no transpose kernels for backward passes): pf_gemm_nn computes
+ * Y[M,N] = X[M,K] . Wkn[K,N] (+ residual) with Wkn stored [K, N] row-major (a data
+ * gradient dZ . W with W as stored); pf_gemm_splitk_tn computes the split-K stack
+ * Y[z][M,N] = A[Kz, M]^T . B[Kz, N] with A, B stored [K, M], [K, N] (a weight gradient
+ * dZ^T X straight from the activations).                                             */
+int pf_gemm_nn(const void* X, const void* Wkn, const void* residual, void* Y, int M, int N, int K,
+               const pf_ctl_t* ctl, void* stream);
+int pf_gemm_splitk_tn(const void* A, const void* B, void* Y, int M, int N, int K, int splits,
+                      const pf_ctl_t* ctl, void* stream);
 
 /* Y = LayerNorm(X + residual) * gamma + beta, per row of `cols` (residual may be
  * NULL). fp32 statistics, two-pass variance. Work units = ceil(rows/rows_per_unit). */
@@ -291,6 +300,10 @@ int pf_chain_add_copy(pf_chain_t* chain, void* dst, int64_t dst_pitch, const voi
                       int64_t src_pitch, int64_t width, int64_t rows, int role);  /* role 0..3 */
 int pf_chain_add_gemm_splitk(pf_chain_t* chain, const void* X, const void* W, void* Y, int M, int N,
                              int K, int splits);
+int pf_chain_add_gemm_nn(pf_chain_t* chain, const void* X, const void* Wkn, const void* residual, void* Y, int M,
+                         int N, int K);
+int pf_chain_add_gemm_splitk_tn(pf_chain_t* chain, const void* A, const void* B, void* Y, int M, int N, int K,
+                                int splits);
 int pf_chain_add_colstats(pf_chain_t* chain, const void* X, const void* G, const void* Ymask,
                           const float* mean, const float* invstd, float* partial, int M, int C,
                           int* out_partials);

@@ -258,7 +258,11 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
 #endif
 }
 
-template <int BN, uint32_t EPI>
+// MJ: operand majorness, bit 0 = A MN-major, bit 1 = B MN-major (default both K-major).
+// An MN-major operand is stored [K, M] (resp. [K, N]) row-major: TMA brings it in as
+// 64 x 64 SW128 blocks (8 KB, LBO between blocks) and the MMA reads it transposed, so
+// weight gradients (dZ^T X) and data gradients (dZ W) need no transpose kernels.
+template <int BN, uint32_t EPI, int MJ = 0>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmY, Params p, Ctl ctl) {
@@ -346,8 +350,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if (lane == 0) {
           mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
-          tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full_bar[stage], kb * BK, tm * BM);
-          tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full_bar[stage], kb * BK, tn * BN);
+          if (MJ & 1) {
+#pragma unroll
+            for (int b = 0; b < BM / 64; ++b)
+              tma_load_2d(sA + stage * C::A_BYTES + b * 8192, &tmA, &full_bar[stage], tm * BM + 64 * b, kb * BK);
+          } else {
+            tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full_bar[stage], kb * BK, tm * BM);
+          }
+          if (MJ & 2) {
+#pragma unroll
+            for (int b = 0; b < BN / 64; ++b)
+              tma_load_2d(sB + stage * C::B_BYTES + b * 8192, &tmB, &full_bar[stage], tn * BN + 64 * b, kb * BK);
+          } else {
+            tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full_bar[stage], kb * BK, tn * BN);
+          }
         }
         __syncwarp();
         if (++stage == C::STAGES) {
@@ -362,7 +378,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const long long _c0 = clock64();
     const unsigned long long _g0 = globaltimer_ns();
 #endif
-    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, false, false);
+    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, (MJ & 1) != 0, (MJ & 2) != 0);
     int slot = 0;
     uint32_t sphase = 0;
     int stage = 0;
@@ -404,8 +420,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / UMMA_K; ++k) {
             // K advance inside the 128-B swizzle atom: +32 B per UMMA_K step
-            const uint64_t ad = umma_desc_sw128_kmajor(a_addr + k * UMMA_K * 2);
-            const uint64_t bd = umma_desc_sw128_kmajor(b_addr + k * UMMA_K * 2);
+            // K advance: +32 B inside the 128-B swizzle atom (K-major), or +16 rows of
+            // 128 B (MN-major)
+            const uint64_t ad = (MJ & 1) ? umma_desc_sw128_mnmajor(a_addr + k * UMMA_K * 128, 8192)
+                                         : umma_desc_sw128_kmajor(a_addr + k * UMMA_K * 2);
+            const uint64_t bd = (MJ & 2) ? umma_desc_sw128_mnmajor(b_addr + k * UMMA_K * 128, 8192)
+                                         : umma_desc_sw128_kmajor(b_addr + k * UMMA_K * 2);
             umma_bf16_ss(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           }
           umma_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs retire
@@ -800,6 +820,21 @@ static int make_tmap(CUtensorMap* map, const void* base, int rows, int cols, int
   return PF_OK;
 }
 
+// MN-major operand [rows = K, cols = M or N] row-major: 64 x 64 boxes, 128-B swizzle.
+static int make_tmap_mn(CUtensorMap* map, const void* base, int rows, int cols) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return set_error(PF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {64, 64};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(PF_ERR_CUDA, "MN-major tensor map failed (%d)", (int)r);
+  return PF_OK;
+}
+
 // Output map for the epilogue's TMA stores: box 32 x 32, 64-B swizzle.
 static int make_tmap_store(CUtensorMap* map, const void* base, int rows, int cols) {
   EncodeTiledFn enc = get_encode_fn();
@@ -867,18 +902,18 @@ static int pick_bn(int M, int N) {
   return best;
 }
 
-template <int BN, uint32_t EPI>
+template <int BN, uint32_t EPI, int MJ = 0>
 static int launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty,
                       const Params& p, int grid,
                       const pf_ctl_t* ctl, cudaStream_t stream) {
   using C = Cfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
-    PF_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    PF_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, EPI, MJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  C::SMEM_BYTES));
     attr_set = true;
   }
-  gemm_kernel<BN, EPI><<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(ta, tb, ty, p, make_ctl(ctl));
+  gemm_kernel<BN, EPI, MJ><<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(ta, tb, ty, p, make_ctl(ctl));
   PF_CUDA(cudaGetLastError());
   return PF_OK;
 }
@@ -977,6 +1012,26 @@ struct GemmOp final : PreparedOp {
   Params p;
   uint32_t epi = 0;
   int grid = 0;
+  int mj = 0;  // operand majorness (see gemm_kernel)
+
+  // A [K, M] (mj bit 0) and/or B [K, N] (mj bit 1) stored MN-major
+  int prepare_mn(const void* X, const void* W, const void* bias, const void* residual, void* Y, int M, int N,
+                 int K, uint32_t e, int majors, int splits) {
+    PF_TRY(prepare(X, W, bias, residual, Y, M, N, K, e));
+    mj = majors;
+    if (mj & 1) PF_TRY(make_tmap_mn(&ta, X, K, M));
+    if (mj & 2) PF_TRY(make_tmap_mn(&tb, W, K, N));
+    if (splits > 1) {
+      const int kb = (K + BK - 1) / BK;
+      p.k_splits = effective_splits(K, splits);
+      p.kb_per_split = (kb + p.k_splits - 1) / p.k_splits;
+      if (p.k_splits > 1) PF_TRY(make_tmap_store_3d(&ty, Y, p.k_splits, M, N));
+      const int tiles = p.tiles_m * p.tiles_n * p.k_splits;
+      const int sms = device_sm_count();
+      grid = tiles < sms ? tiles : sms;
+    }
+    return PF_OK;
+  }
 
   int prepare(const void* X, const void* W, const void* bias, const void* residual, void* Y, int M,
               int N, int K, uint32_t e) {
@@ -1017,6 +1072,9 @@ struct GemmOp final : PreparedOp {
   int run(const pf_ctl_t* ctl, cudaStream_t stream, const LaunchArgs& a) override {
     Params p = this->p;
     p.stamp = a.stamp;
+    if (mj == 3) return launch_epi<BN, 0, 3>(ta, tb, ty, p, grid, ctl, stream);
+    if (mj == 2) return epi == 4 ? launch_epi<BN, 4, 2>(ta, tb, ty, p, grid, ctl, stream)
+                                 : launch_epi<BN, 0, 2>(ta, tb, ty, p, grid, ctl, stream);
     switch (epi) {
       case 0: return launch_epi<BN, 0>(ta, tb, ty, p, grid, ctl, stream);
       case 1: return launch_epi<BN, 1>(ta, tb, ty, p, grid, ctl, stream);
@@ -1091,6 +1149,42 @@ int make_gemm_op(OpPtr* out, const void* X, const void* W, const void* bias, con
 
 namespace pf {
 
+// Y = X[M,K] . Wkn[K,N] (B MN-major: W stored [K, N]) with an optional residual (data
+// gradients: dX = dZ . W with W [Cout, Cin*kh*kw] as stored), or the split-K weight
+// gradient Y[z] = A[Kz, M]^T . B[Kz, N] (both MN-major: dZ^T X without transposes).
+int make_gemm_mn_op(OpPtr* out, const void* X, const void* W, const void* residual, void* Y, int M, int N, int K,
+                    int majors, int splits) {
+  if (!X || !W || !Y || M <= 0 || N <= 0 || K <= 0 || (majors != 2 && majors != 3))
+    return set_error(PF_ERR_INVALID, "pf_gemm_mn: bad arguments");
+  if (N % 8 != 0 || ((majors & 1) && M % 8 != 0) || (!(majors & 1) && K % 8 != 0))
+    return set_error(PF_ERR_INVALID, "pf_gemm_mn: 16-B rows needed (N %% 8, and M %% 8 or K %% 8)");
+  if (((uintptr_t)X | (uintptr_t)W | (uintptr_t)Y | (uintptr_t)residual) & 15u)
+    return set_error(PF_ERR_INVALID, "pf_gemm_mn: pointers must be 16-B aligned");
+  if (majors == 3 && residual) return set_error(PF_ERR_INVALID, "pf_gemm_mn: no residual with split-K");
+  if (!device_is_sm100()) return set_error(PF_ERR_UNSUPPORTED, "pf_gemm_mn: needs an sm_100 device");
+  const uint32_t e = residual ? PF_EPI_RESIDUAL : 0u;
+  switch (gemm::pick_bn(M, N)) {
+    case 256: {
+      auto op = std::make_unique<gemm::GemmOp<256>>();
+      PF_TRY(op->prepare_mn(X, W, nullptr, residual, Y, M, N, K, e, majors, splits));
+      *out = std::move(op);
+      return PF_OK;
+    }
+    case 192: {
+      auto op = std::make_unique<gemm::GemmOp<192>>();
+      PF_TRY(op->prepare_mn(X, W, nullptr, residual, Y, M, N, K, e, majors, splits));
+      *out = std::move(op);
+      return PF_OK;
+    }
+    default: {
+      auto op = std::make_unique<gemm::GemmOp<128>>();
+      PF_TRY(op->prepare_mn(X, W, nullptr, residual, Y, M, N, K, e, majors, splits));
+      *out = std::move(op);
+      return PF_OK;
+    }
+  }
+}
+
 int make_gemm_splitk_op(OpPtr* out, const void* X, const void* W, void* Y, int M, int N, int K,
                         int splits) {
   if (!X || !W || !Y || M <= 0 || N <= 0 || K <= 0 || splits < 1)
@@ -1130,6 +1224,24 @@ extern "C" int pf_gemm_splitk(const void* X, const void* W, void* Y, int M, int 
   PF_TRY(validate_ctl(ctl));
   OpPtr op;
   PF_TRY(make_gemm_splitk_op(&op, X, W, Y, M, N, K, splits));
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), pf::LaunchArgs{});
+}
+
+extern "C" int pf_gemm_nn(const void* X, const void* Wkn, const void* residual, void* Y, int M, int N, int K,
+                          const pf_ctl_t* ctl, void* stream) {
+  using namespace pf;
+  PF_TRY(validate_ctl(ctl));
+  OpPtr op;
+  PF_TRY(make_gemm_mn_op(&op, X, Wkn, residual, Y, M, N, K, 2, 1));
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), pf::LaunchArgs{});
+}
+
+extern "C" int pf_gemm_splitk_tn(const void* A, const void* B, void* Y, int M, int N, int K, int splits,
+                                 const pf_ctl_t* ctl, void* stream) {
+  using namespace pf;
+  PF_TRY(validate_ctl(ctl));
+  OpPtr op;
+  PF_TRY(make_gemm_mn_op(&op, A, B, nullptr, Y, M, N, K, 3, splits));
   return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), pf::LaunchArgs{});
 }
 

@@ -35,6 +35,8 @@ int make_gemm_op(OpPtr* out, const void* X, const void* W, const void* bias, con
                  void* Y, int M, int N, int K, uint32_t epi);
 int make_gemm_splitk_op(OpPtr* out, const void* X, const void* W, void* Y, int M, int N, int K,
                         int splits);
+int make_gemm_mn_op(OpPtr* out, const void* X, const void* W, const void* residual, void* Y, int M, int N, int K,
+                    int majors, int splits);
 int make_transpose_op(OpPtr* out, const void* X, void* Y, int R, int C);
 int make_colstats_op(OpPtr* out, const void* X, const void* G, const void* Ymask, const float* mean,
                      const float* invstd, float* partial, int M, int C, int* out_partials);

@@ -618,6 +618,20 @@ int pf_chain_add_sgd(pf_chain_t* c, const pf_sgd_segment_t* segs, int nseg, floa
   PF_CHAIN_ADD(pf::make_sgd_op(&op, segs, nseg, lr, momentum));
 }
 
+int pf_chain_add_gemm_nn(pf_chain_t* c, const void* X, const void* Wkn, const void* residual, void* Y, int M,
+                         int N, int K) {
+  if (!c) return pf::set_error(PF_ERR_INVALID, "null chain");
+  pf::OpPtr op;
+  return chain_push(c, pf::make_gemm_mn_op(&op, X, Wkn, residual, Y, M, N, K, 2, 1), op);
+}
+
+int pf_chain_add_gemm_splitk_tn(pf_chain_t* c, const void* A, const void* B, void* Y, int M, int N, int K,
+                                int splits) {
+  if (!c) return pf::set_error(PF_ERR_INVALID, "null chain");
+  pf::OpPtr op;
+  return chain_push(c, pf::make_gemm_mn_op(&op, A, B, nullptr, Y, M, N, K, 3, splits), op);
+}
+
 int pf_chain_add_im2col(pf_chain_t* c, const void* X, void* Col, int B, int H, int W, int C, int kh,
                         int kw, int stride, int pad, int Kp) {
   if (!c) return pf::set_error(PF_ERR_INVALID, "null chain");

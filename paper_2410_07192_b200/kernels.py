@@ -463,3 +463,27 @@ def _linear_f32(x, weight, bias=None, *, gelu=False, residual=None, out=None, ct
     native.call("pf_gemm_f32", x.data_ptr(), weight.data_ptr(), _ptr(bias), _ptr(residual), out.data_ptr(),
                 m, n, k, epi, _ctl_ref(ctl), _stream(stream))
     return out
+
+
+def gemm_nn(x: torch.Tensor, wkn: torch.Tensor, *, residual=None, out=None, ctl=None, stream=None) -> torch.Tensor:
+    """out[M, N] = x[M, K] @ wkn[K, N] (+ residual), wkn read MN-major (pf_gemm_nn)."""
+    m, k = x.shape
+    n = wkn.shape[1]
+    if out is None:
+        out = torch.empty(m, n, dtype=torch.bfloat16, device=x.device)
+    native.call("pf_gemm_nn", x.data_ptr(), wkn.data_ptr(), _ptr(residual), out.data_ptr(), m, n, k,
+                _ctl_ref(ctl), _stream(stream))
+    return out
+
+
+def gemm_splitk_tn(a: torch.Tensor, b: torch.Tensor, splits: int, *, out=None, ctl=None,
+                   stream=None) -> torch.Tensor:
+    """[S, M, N] split-K partials of a[K, M]^T @ b[K, N], both read MN-major (pf_gemm_splitk_tn)."""
+    k, m = a.shape
+    n = b.shape[1]
+    s = gemm_splitk_splits(k, splits)
+    if out is None:
+        out = torch.empty(s, m, n, dtype=torch.bfloat16, device=a.device)
+    native.call("pf_gemm_splitk_tn", a.data_ptr(), b.data_ptr(), out.data_ptr(), m, n, k, splits,
+                _ctl_ref(ctl), _stream(stream))
+    return out

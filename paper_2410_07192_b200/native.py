@@ -131,6 +131,11 @@ _SIGNATURES: dict[str, tuple] = {
     "pf_gemm_splitk": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, POINTER(PfCtl),
                                c_void_p]),
     "pf_gemm_splitk_splits": (c_int, [c_int, c_int, POINTER(c_int)]),
+    "pf_gemm_nn": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, POINTER(PfCtl), c_void_p]),
+    "pf_gemm_splitk_tn": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, POINTER(PfCtl),
+                                  c_void_p]),
+    "pf_chain_add_gemm_nn": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int]),
+    "pf_chain_add_gemm_splitk_tn": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int]),
     "pf_colstats": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int,
                             POINTER(c_int), POINTER(PfCtl), c_void_p]),
     "pf_bn_finalize": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_float, c_void_p,

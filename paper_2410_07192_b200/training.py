@@ -247,19 +247,20 @@ class _Rec:
                   out.data_ptr(), b, h, w, c, k, k, stride, pad, dcol.shape[-1])
 
     def wgrad(self, dz, x, gbuf, splits):
-        """gbuf[S, N, K] = split-K partials of dz[M, N]^T x[M, K] (transposes into scratch)."""
-        ctx = self.ctx
+        """gbuf[S, N, K] = split-K partials of dz[M, N]^T x[M, K], both operands read
+        MN-major straight from the activations (no transposes)."""
         m, n = dz.shape
         k = x.shape[-1]
-        dzt = self.transpose(dz, ctx.buf("tA", n * m).view(n, m))
-        xt = self.transpose(x.reshape(m, k), ctx.buf("tB", k * m).view(k, m))
-        self.gemm_splitk(dzt, xt, gbuf.view(-1)[:splits * n * k].view(splits, n, k), splits)
+        self.flops[self.ctx.node] = 2.0 * m * n * k
+        self.call("pf_chain_add_gemm_splitk_tn", dz.data_ptr(), x.data_ptr(), gbuf.data_ptr(), n, k, m, splits)
 
     def dgrad(self, dz, w, out, residual=None):
-        """out[M, K] = dz[M, N] w[N, K] (+ residual): GEMM against w^T."""
+        """out[M, K] = dz[M, N] w[N, K] (+ residual), w read MN-major as stored."""
         n, k = w.shape
-        wt = self.transpose(w, self.ctx.buf("wT", k * n).view(k, n))
-        self.gemm(dz, wt, out, residual=residual)
+        m = dz.shape[0]
+        self.flops[self.ctx.node] = 2.0 * m * n * k
+        self.call("pf_chain_add_gemm_nn", dz.data_ptr(), w.data_ptr(),
+                  None if residual is None else residual.data_ptr(), out.data_ptr(), m, k, n)
 
 
 class TrainStem(TrainModule):
@@ -288,8 +289,7 @@ class TrainStem(TrainModule):
         i = self.idx
         ws = {f"s{i}.col": m1 * c.stem_kp, f"s{i}.z": m1 * c.stem_ch, f"s{i}.a": m1 * c.stem_ch,
               f"s{i}.stats": 4 * c.stem_ch, f"out{i}": batch * self.h2 * self.h2 * c.stem_ch,
-              "da": m1 * c.stem_ch, "dz": m1 * c.stem_ch,
-              "tA": c.stem_ch * m1, "tB": c.stem_kp * m1}
+              "da": m1 * c.stem_ch, "dz": m1 * c.stem_ch}
         ws.update(self.grad_ws(batch))
         return ws
 
@@ -373,8 +373,7 @@ class TrainBottleneck(TrainModule):
         ws = {f"s{i}.z1": m * w, f"s{i}.a1": m * w, f"s{i}.z2": mo * w, f"s{i}.a2": mo * w,
               f"s{i}.z3": mo * co, f"s{i}.stats": 4 * (2 * w + 2 * co), f"out{i}": mo * co,
               "col": mo * 9 * w, "dz_a": mo * co, "dres": mo * co, "dt2": mo * w, "dz_b": mo * w,
-              "dcol": mo * 9 * w, "dt1": m * w, "dz_c": m * w, "wT": max(9 * w * w, ci * max(w, co)),
-              "tA": max(co, w) * max(m, mo), "tB": max(9 * w * mo, ci * m, w * mo)}
+              "dcol": mo * 9 * w, "dt1": m * w, "dz_c": m * w}
         if self.ds:
             ws.update({f"s{i}.zd": mo * co, f"s{i}.statsd": 4 * co, "sc": mo * co, "dz_d": mo * co,
                        "dsrc": mo * ci, "dxsc": m * ci})
@@ -506,8 +505,7 @@ class TrainHead(TrainModule):
     def workspace(self, batch):
         i, n, c = self.idx, self.cfg.classes, self.in_ch
         ws = {f"s{i}.pooled": batch * c, f"s{i}.logits": batch * n, "dlogits": batch * n, "dpooled": batch * c,
-              "tA": n * batch, "tB": c * batch, "wT": c * n, "partial": 2 * MAX_PARTIALS * 2 * n,
-              "loss": 2 * 4 * batch}
+              "partial": 2 * MAX_PARTIALS * 2 * n, "loss": 2 * 4 * batch}
         ws.update(self.grad_ws(batch))
         return ws
 

@@ -167,3 +167,24 @@ def test_sgd_update_and_splitk_sum(K):
     assert torch.allclose(w1, e1[0] - 0.1 * ev1, rtol=1e-5, atol=1e-5)
     assert torch.equal(work1, w1.to(torch.bfloat16))
     assert torch.allclose(w2, e1[2] - 0.1 * (0.9 * e1[3] + g2), rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("m,n,k,res", [(6272, 576, 64, False), (1000, 2048, 1000, True), (200, 136, 96, True)])
+def test_gemm_nn_mn_major_b(K, m, n, k, res):
+    """Data-gradient GEMM with W read MN-major: x[M,K] @ w[K,N] (+ residual)."""
+    g = torch.Generator().manual_seed(7)
+    x, w = bf(m, k, gen=g), bf(k, n, gen=g, scale=k ** -0.5)
+    r = bf(m, n, gen=g) if res else None
+    got = K.gemm_nn(x.cuda(), w.cuda(), residual=None if r is None else r.cuda())
+    want = x.float() @ w.float() + (r.float() if res else 0)
+    assert rel(got, want) < REL
+
+
+@pytest.mark.parametrize("k,m,n,splits", [(25088, 64, 576, 16), (6272, 256, 64, 8), (64, 1000, 2048, 1),
+                                          (1000, 200, 136, 3)])
+def test_gemm_splitk_tn_mn_major_both(K, k, m, n, splits):
+    """Weight-gradient GEMM straight from row-major activations: a[K,M]^T @ b[K,N]."""
+    g = torch.Generator().manual_seed(8)
+    a, b = bf(k, m, gen=g), bf(k, n, gen=g, scale=k ** -0.5)
+    parts = K.gemm_splitk_tn(a.cuda(), b.cuda(), splits)
+    assert rel(parts.float().sum(0), a.float().T @ b.float()) < REL
