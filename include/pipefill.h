@@ -369,6 +369,21 @@ int pf_chain_node_elapsed(pf_chain_t* chain, int node, float* out_ms);
 int pf_chain_launch(pf_chain_t* chain, const uint32_t* flag, uint32_t* abort, uint32_t* cursors,
                     uint32_t* done, int start_node, int64_t in_off, int64_t out_off, void* stream);
 
+/* ---- gated weight staging (run-ahead into the next partition) -------------------
+ * One partition's weights as a CUDA graph: a one-thread gate kernel, then a
+ * conditional IF node whose body is one host->device memcpy node per (dst, pinned src,
+ * bytes). The gate lets the copies run only when the chain-abort word is 0 -- i.e.
+ * every batch enqueued before it on the stream completed -- and writes the decision
+ * to *staged_out (1 = staged). A run-ahead staging behind a batch that yielded is
+ * therefore skipped and cannot overwrite the yielded batch's weights or workspace
+ * (the region holds one partition at a time). No reference counterpart:
+ * the reference charges partitions whole cycles (partition.py:118-124).              */
+typedef struct pf_staging pf_staging_t;
+int pf_staging_create(pf_staging_t** out, void* const* dst, const void* const* src,
+                      const uint64_t* bytes, int n, const uint32_t* abort, uint32_t* staged_out);
+int pf_staging_launch(pf_staging_t* staging, void* stream);
+int pf_staging_destroy(pf_staging_t* staging);
+
 #ifdef __cplusplus
 }
 #endif

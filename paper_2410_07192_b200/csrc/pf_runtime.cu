@@ -494,9 +494,91 @@ __global__ void chain_gate_kernel(cudaGraphConditionalHandle h, const uint32_t* 
   }
   cudaGraphSetConditional(h, go);
 }
+// Gate of a run-ahead staging: copy only when no earlier batch on the stream yielded.
+__global__ void staging_gate_kernel(cudaGraphConditionalHandle h, const uint32_t* abort,
+                                    uint32_t* staged_out) {
+  const unsigned go = ld_volatile_u32(abort) == 0u ? 1u : 0u;
+  *staged_out = go;
+  cudaGraphSetConditional(h, go);
+}
 }  // namespace pf
 
+struct pf_staging {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
 extern "C" {
+
+int pf_staging_create(pf_staging_t** out, void* const* dst, const void* const* src,
+                      const uint64_t* bytes, int n, const uint32_t* abort, uint32_t* staged_out) {
+  using namespace pf;
+  if (!out || n < 0 || (n > 0 && (!dst || !src || !bytes)) || !abort || !staged_out)
+    return set_error(PF_ERR_INVALID, "pf_staging_create: bad arguments");
+  cudaGraph_t g;
+  PF_CUDA(cudaGraphCreate(&g, 0));
+  int rc = PF_OK;
+  do {
+    cudaGraphConditionalHandle h;
+    if ((rc = check_cuda(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault),
+                         "cudaGraphConditionalHandleCreate")) != PF_OK)
+      break;
+    const uint32_t* ab = abort;
+    uint32_t* so = staged_out;
+    void* args[] = {&h, &ab, &so};
+    cudaKernelNodeParams kp = {};
+    kp.func = (void*)staging_gate_kernel;
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(1);
+    kp.kernelParams = args;
+    cudaGraphNode_t gate;
+    if ((rc = check_cuda(cudaGraphAddKernelNode(&gate, g, nullptr, 0, &kp), "gate node")) != PF_OK) break;
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeIf;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cn;
+    if ((rc = check_cuda(cudaGraphAddNode(&cn, g, &gate, 1, &cp), "cudaGraphAddNode(cond)")) != PF_OK)
+      break;
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    cudaGraphNode_t prev = nullptr;
+    for (int i = 0; i < n && rc == PF_OK; ++i) {
+      if (bytes[i] == 0) continue;
+      cudaGraphNode_t nd;
+      rc = check_cuda(cudaGraphAddMemcpyNode1D(&nd, body, prev ? &prev : nullptr, prev ? 1 : 0, dst[i],
+                                               src[i], (size_t)bytes[i], cudaMemcpyHostToDevice),
+                      "cudaGraphAddMemcpyNode1D (conditional body)");
+      prev = nd;
+    }
+    if (rc != PF_OK) break;
+    auto* st = new pf_staging();
+    st->graph = g;
+    if ((rc = check_cuda(cudaGraphInstantiate(&st->exec, g, 0), "cudaGraphInstantiate(staging)")) != PF_OK) {
+      delete st;
+      break;
+    }
+    *out = st;
+    return PF_OK;
+  } while (false);
+  cudaGraphDestroy(g);
+  return rc;
+}
+
+int pf_staging_launch(pf_staging_t* st, void* stream) {
+  using namespace pf;
+  if (!st || !st->exec) return set_error(PF_ERR_INVALID, "pf_staging_launch: null staging");
+  PF_CUDA(cudaGraphLaunch(st->exec, reinterpret_cast<cudaStream_t>(stream)));
+  return PF_OK;
+}
+
+int pf_staging_destroy(pf_staging_t* st) {
+  if (!st) return PF_OK;
+  if (st->exec) cudaGraphExecDestroy(st->exec);
+  if (st->graph) cudaGraphDestroy(st->graph);
+  delete st;
+  return PF_OK;
+}
 
 int pf_chain_create(pf_chain_t** out) {
   if (!out) return pf::set_error(PF_ERR_INVALID, "pf_chain_create: null out");

@@ -39,7 +39,8 @@ from .coordinator import WorkItem
 from .fillmodels import ExecContext, FillSequential
 from .planner import ExecutionPlan
 
-_CTL_WORDS = 64 + 4096  # [0]=abort, [1]=batches done, [8..12)=timestamps (2 x u64), [64..)=cursors
+_CTL_WORDS = 64 + 4096  # [0]=abort, [1]=batches done, [2]=run-ahead staged, [8..12)=timestamps (2 x u64),
+#                        [64..)=cursors
 _CURSOR0 = 64
 MAX_BATCHES = 64  # per bubble (device batch descriptors)
 MAX_NODES = 4096
@@ -162,6 +163,8 @@ class Executor:
         self.work_source: Optional[Callable[[], Optional[tuple[WorkItem, FillSequential]]]] = None
         self._ctl_host = PinnedBuffer((_CTL_WORDS,), torch.int32)
         self._desc_host = PinnedBuffer((MAX_BATCHES, DESC_WORDS), torch.int64)
+        self._gated: dict[int, ctypes.c_void_p] = {}
+        self._ahead_staging: Optional[int] = None  # index in self.stagings of the last run-ahead copy
         self._stamps_host = PinnedBuffer((MAX_NODES, 2), torch.int64)
         self._chains: dict[tuple[int, int], _Chain] = {}
         self._staged_event: Optional[torch.cuda.Event] = None
@@ -186,7 +189,7 @@ class Executor:
     _LAYOUT_ATTRS = ("_ctl", "_desc", "_stamps", "_region", "ws", "in_dev", "_cap", "_in_host", "_aux_host",
                      "aux_dev",
                      "_results", "_store_dev", "_store_host", "_flops_frac", "_staged_part",
-                     "_staged_event", "_chains", "model", "plan", "_dev_views", "_part_layouts")
+                     "_staged_event", "_chains", "model", "plan", "_dev_views", "_part_layouts", "_gated")
 
     def _save_layout(self) -> None:
         if self._layout_key is not None:
@@ -232,8 +235,7 @@ class Executor:
             self._carve(cap)
         except native.ArenaExhausted:
             for saved in self._layouts.values():
-                for ch in saved["_chains"].values():
-                    ch.close()
+                _close_layout(saved)
             self._layouts = {}
             self._chains = {}
             self.stream.synchronize()  # the arena is about to be re-carved
@@ -271,6 +273,7 @@ class Executor:
             region = max(region, w + sum(_pad256(2 * v) for v in need.values()))
         self._region = self.arena.alloc((region // 2,), torch.bfloat16)
         self._part_layouts: dict[int, tuple[dict, dict]] = {}
+        self._gated: dict[int, ctypes.c_void_p] = {}  # partition -> gated run-ahead staging graph
         self.ws = {}
         bmax = max(e.batch_size for p in plan.partitions[:1] for e in p.per_bubble)
         in_dtype, in_shape = model.input_spec()
@@ -586,7 +589,7 @@ class Executor:
                 st.wait_event(slot.start_event)
             if self._staged_event is not None:
                 st.wait_event(self._staged_event)
-            self._ctl[:2].zero_()  # fresh bubble: abort word and done counter
+            self._ctl[:3].zero_()  # fresh bubble: abort word, done counter, run-ahead staged
             if pr.resume_zero is not None:
                 self._ctl[_CURSOR0 + pr.resume_zero] = 0
                 pr.resume_zero = None
@@ -615,29 +618,55 @@ class Executor:
 
     def _stage_in_stream(self, part: int, st: torch.cuda.Stream) -> None:
         """Run-ahead staging: copy partition `part`'s weights into the region on the fill
-        stream itself, ordered after the previous partition's batches. Not gated by the
-        flag: if the bubble closes first the copy still lands (PCIe only, no SMs) and the
-        interrupted partition is re-staged before its next batch."""
+        stream itself, ordered after the previous partition's batches, as a gated graph
+        (pf_staging_*): the copies run only if none of those batches yielded (abort word
+        0), else the region keeps the current partition's weights and the yielded batch's
+        workspace, and settle() rolls the host-side layout back. Not gated by the flag:
+        a copy that outlives the bubble only uses PCIe."""
         p = self.plan.partitions[part]
         views, ws = self._part_layout(part)
+        g = self._gated.get(part)
+        if g is None:
+            mods = [i for i in range(p.lo, p.hi) if self.model[i].weight_bytes()]
+            n = len(mods)
+            dst = (ctypes.c_void_p * max(n, 1))(*[self._module_ptr(part, i) for i in mods])
+            src = (ctypes.c_void_p * max(n, 1))(*[self.model[i].host.ptr for i in mods])
+            nb = (ctypes.c_uint64 * max(n, 1))(*[self.model[i].weight_bytes() for i in mods])
+            g = ctypes.c_void_p()
+            base = self._ctl.data_ptr()
+            native.call("pf_staging_create", ctypes.byref(g), dst, src, nb, n, base, base + 8)
+            self._gated[part] = g
         e0 = torch.cuda.Event(enable_timing=True)
         e0.record(st)
-        staged = 0
+        native.call("pf_staging_launch", g, st.cuda_stream)
+        staged = sum(self.model[i].weight_bytes() for i in range(p.lo, p.hi))
+        self.h2d_bytes += staged
         for i in range(p.lo, p.hi):
-            mod = self.model[i]
-            nbytes = mod.weight_bytes()
-            if nbytes:
-                native.call("pf_stage_h2d", self._module_ptr(part, i), mod.host.ptr, nbytes, st.cuda_stream)
-            self.h2d_bytes += nbytes
-            staged += nbytes
-            mod.dev = views[i]
+            self.model[i].dev = views[i]
         ev = torch.cuda.Event(enable_timing=True)
         ev.record(st)
         self._staged_event = ev
         self._staged_part = part
         self.stagings.append((staged, e0, ev))
+        self._ahead_staging = len(self.stagings) - 1
         self.ws = ws
         self._dev_views = dict(views)
+
+    def _rollback_ahead_staging(self, part: int) -> None:
+        """The gated run-ahead staging was skipped on the device: partition `part` is still
+        resident; restore its host-side views and uncount the copy."""
+        views, ws = self._part_layout(part)
+        for i in range(self.plan.partitions[part].lo, self.plan.partitions[part].hi):
+            self.model[i].dev = views[i]
+        self.ws = ws
+        self._dev_views = dict(views)
+        self._staged_part = part
+        k = self._ahead_staging
+        if k is not None and k < len(self.stagings):
+            b, e0, e1 = self.stagings[k]
+            self.h2d_bytes -= b
+            self.stagings[k] = (0, e0, e1)
+        self._ahead_staging = None
 
     def settle(self) -> Optional[BubbleRecord]:
         """Wait for the pending bubble's fill work, read the control block, advance
@@ -676,6 +705,8 @@ class Executor:
         samples = 0
         parts = pend.parts or [pend.part] * len(pend.batches)
         rec.ran_ahead = any(p_ != pend.part for p_ in parts)
+        if rec.ran_ahead and int(w[2]) == 0:  # a batch of this partition yielded: staging skipped
+            self._rollback_ahead_staging(pend.part)
         last_part = len(self.plan.partitions) - 1
         completed_last = 0
         for k, (first, cnt, node) in enumerate(pend.batches):
@@ -754,11 +785,20 @@ class Executor:
         self.settle()
         torch.cuda.synchronize()
         self._drop_chains()
+        for g in getattr(self, "_gated", {}).values():
+            native.call("pf_staging_destroy", g)
+        self._gated = {}
         for saved in self._layouts.values():
-            for ch in saved["_chains"].values():
-                ch.close()
+            _close_layout(saved)
         self._layouts = {}
         self.arena.close()
+
+
+def _close_layout(saved: dict) -> None:
+    for ch in saved["_chains"].values():
+        ch.close()
+    for g in saved.get("_gated", {}).values():
+        native.call("pf_staging_destroy", g)
 
 
 def _pad256(n: int) -> int:

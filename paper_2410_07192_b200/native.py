@@ -216,6 +216,10 @@ _SIGNATURES: dict[str, tuple] = {
                                 c_int64, c_void_p]),
     "pf_chain_begin": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
     "pf_chain_end": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "pf_staging_create": (c_int, [POINTER(c_void_p), POINTER(c_void_p), POINTER(c_void_p), POINTER(c_uint64),
+                                  c_int, c_void_p, c_void_p]),
+    "pf_staging_launch": (c_int, [c_void_p, c_void_p]),
+    "pf_staging_destroy": (c_int, [c_void_p]),
 }
 
 _lib: ctypes.CDLL | None = None
