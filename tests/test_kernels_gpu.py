@@ -89,7 +89,9 @@ def test_softmax(K, rows, cols):
     assert rel_err(got, ref) < REL_TOL_BF16
 
 
-@pytest.mark.parametrize("batch,seq,heads,masked", [(32, 128, 12, False), (4, 128, 16, True), (3, 77, 2, False), (2, 1, 1, False)])
+@pytest.mark.parametrize("batch,seq,heads,masked", [(32, 128, 12, False), (4, 128, 16, True), (3, 77, 2, False),
+                                                     (2, 1, 1, False), (128, 128, 16, False), (40, 128, 16, True),
+                                                     (37, 100, 12, False)])
 def test_attention(K, batch, seq, heads, masked):
     g = torch.Generator().manual_seed(batch * seq + heads)
     hidden = heads * 64
@@ -143,3 +145,26 @@ def test_gemm_preemption_protocol(K):
     assert cursor.item() >= K.gemm_units(m, n, k) and abort.item() == 0
     ref = x.float() @ w.float().T
     assert rel_err(y, ref) < REL_TOL_BF16
+
+
+def test_attention_preemption_protocol(K):
+    """Persistent attention: flag 0 -> no CTA counts itself, abort set, output untouched;
+    flag 1 -> every CTA counts itself (units = CTAs launched) and the result is correct."""
+    batch, seq, heads = 64, 128, 16  # 1024 units over <= 296 CTAs: several units per CTA
+    g = torch.Generator().manual_seed(5)
+    qkv = _bf16(batch, seq, 3 * heads * 64, gen=g).cuda()
+    words = torch.zeros(8, dtype=torch.int32, device="cuda")
+    flag, abort, cursor = (words[i:i + 1] for i in range(3))
+    ctl = K.KernelCtl(flag.data_ptr(), abort.data_ptr(), cursor.data_ptr())
+    out = torch.zeros(batch, seq, heads * 64, dtype=torch.bfloat16, device="cuda")
+    K.attention(qkv, heads, out=out, ctl=ctl)
+    torch.cuda.synchronize()
+    assert abort.item() == 1 and cursor.item() == 0 and out.abs().max().item() == 0
+    abort.zero_()
+    flag.fill_(1)
+    K.attention(qkv, heads, out=out, ctl=ctl)
+    torch.cuda.synchronize()
+    units = K.attention_units(batch, seq, heads, 64)
+    assert abort.item() == 0 and cursor.item() == units and units <= batch * heads
+    ref = fill_ref.attention(qkv.float().cpu(), heads, None)
+    assert rel_err(out, ref) < REL_TOL_BF16
