@@ -79,20 +79,6 @@ __device__ uint32_t g_att_diag[296][8][8];
 #define ATT_STAMP(i, ev) do {} while (0)
 #endif
 
-// mbarrier wait that parks the thread in hardware until the phase completes (or the
-// hint expires) instead of spinning: the producer / MMA / epilogue warps spend most of a
-// unit waiting, and spinning warps steal issue slots from the softmax warps.
-__device__ __forceinline__ void mbar_wait_park(uint64_t* bar, uint32_t parity) {
-  const uint32_t addr = smem_u32(bar);
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
-      "r"(parity), "r"(1000000u)
-      : "memory");
-}
-
 __device__ __forceinline__ void tma_qkv(const CUtensorMap* tm, uint8_t* dst, uint64_t* bar, int slot,
                                         int row0) {
   asm volatile(

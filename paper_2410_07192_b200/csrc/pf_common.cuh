@@ -285,6 +285,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Waits that park the thread in hardware (try_wait with a suspend-time hint) until the
+// phase completes instead of spinning: warps that wait most of the time (epilogue warps
+// on the accumulator, the TMA producer on a free stage) then stop stealing issue slots
+// from the warps sharing their SM sub-partition (the single-thread MMA issuer).
+__device__ __forceinline__ void mbar_wait_park(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITP_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAITP_%=;\n\t}" ::"r"(addr),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // device: TMA
 
@@ -467,6 +482,17 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAITC_%=;\n\t}" ::"r"(addr),
       "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_cluster_park(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITCP_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAITCP_%=;\n\t}" ::"r"(addr),
+      "r"(parity), "r"(1000000u)
       : "memory");
 }
 

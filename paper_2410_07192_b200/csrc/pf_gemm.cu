@@ -151,10 +151,28 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
     __syncwarp();
   }
   const __nv_bfloat16* rrow = HAS_RES ? p.residual + (size_t)row * p.N : nullptr;
+  // The residual does not depend on the accumulator: chunk 0's slice is fetched before the
+  // wait for it, and chunk c+1's while chunk c is processed, so the global-load latency
+  // (32 rows per warp instruction) is hidden instead of exposed once per chunk.
+  auto load_res = [&](int col0, uint4 (&dst)[4]) {
+    if (row_ok && col0 + 32 <= p.N) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dst[q] = __ldg(reinterpret_cast<const uint4*>(rrow + col0) + q);
+    } else {
+      __nv_bfloat16 tmp[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        tmp[j] = (row_ok && col0 + j < p.N) ? rrow[col0 + j] : __float2bfloat16(0.f);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dst[q] = reinterpret_cast<const uint4*>(tmp)[q];
+    }
+  };
+  uint4 res_nxt[4];
+  if (HAS_RES) load_res(col_base, res_nxt);
   {
     DIAG_T0();
-    if (PAIR) mbar_wait_cluster(tfull, aphase);
-    else mbar_wait(tfull, aphase);
+    if (PAIR) mbar_wait_cluster_park(tfull, aphase);
+    else mbar_wait_park(tfull, aphase);
     if (lane == 0) DIAG_ADD(3);
   }
   tc_fence_after();
@@ -169,18 +187,9 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
     const int col0 = col_base + c * 32;
     uint4 res_cur[4];
     if (HAS_RES) {
-      // the residual slice of this chunk is fetched while the TMEM load completes
-      if (row_ok && col0 + 32 <= p.N) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) res_cur[q] = reinterpret_cast<const uint4*>(rrow + col0)[q];
-      } else {
-        __nv_bfloat16 tmp[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          tmp[j] = (row_ok && col0 + j < p.N) ? rrow[col0 + j] : __float2bfloat16(0.f);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) res_cur[q] = reinterpret_cast<const uint4*>(tmp)[q];
-      }
+      for (int q = 0; q < 4; ++q) res_cur[q] = res_nxt[q];
+      if (c + 1 < CHUNKS) load_res(col0 + 32, res_nxt);
     }
     __syncwarp();
     tmem_ld_wait();  // chunk c landed
@@ -345,7 +354,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int kb = kb0; kb < kb1; ++kb) {
         {
           DIAG_T0();
-          mbar_wait(&empty_bar[stage], phase ^ 1u);
+          mbar_wait_park(&empty_bar[stage], phase ^ 1u);
           if (lane == 0) DIAG_ADD(2);
         }
         if (lane == 0) {
@@ -639,7 +648,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       for (int kb = 0; kb < num_kb; ++kb) {
         {
           DIAG_T0();
-          mbar_wait(&empty_bar[stage], phase ^ 1u);
+          mbar_wait_park(&empty_bar[stage], phase ^ 1u);
           if (lane == 0 && leader) DIAG_ADD(2);
         }
         if (lane == 0) {

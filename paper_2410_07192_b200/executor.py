@@ -47,6 +47,8 @@ MAX_NODES = 4096
 # PF_EXEC_GRAPHS=0 replays chains node by node (pf_chain_launch) instead of as gated CUDA
 # graphs: for profilers that do not see kernels inside conditional graph nodes (ncu)
 _USE_GRAPHS = __import__("os").environ.get("PF_EXEC_GRAPHS", "1") != "0"
+# modules per gated graph segment (gate kernel + conditional IF node); see DESIGN.md §3
+_SEG_MODULES = int(__import__("os").environ.get("PF_SEG_MODULES", "2"))
 DESC_WORDS = 4  # PF_DESC_WORDS: (input, result, aux input, -) byte offsets per batch
 
 
@@ -424,7 +426,8 @@ class Executor:
             x = model[i](x, ctx)
             for node, fl in model[i].gemm_node_flops(cnt):
                 ch.gemm_flops[before + node] = fl
-            ch.seg_ends.append(ctx.node)  # one gated graph segment per module
+            if (i - part.lo + 1) % _SEG_MODULES == 0 or i == part.hi - 1:
+                ch.seg_ends.append(ctx.node)  # one gated graph segment per _SEG_MODULES modules
         # last node: the batch's output slice (role 2: destination + out_off)
         if part.hi == len(model):
             # the model's result rows (BERT: [CLS] of [cnt, s, h]) straight into pinned results

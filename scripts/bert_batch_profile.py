@@ -26,3 +26,34 @@ fl = cfg.flops_per_sample * B
 print("batch ms", [round(t, 3) for t in times], "samples/s", B / (min(times) / 1e3),
       "TFLOP/s", fl / (min(times) / 1e3) / 1e12)
 ex.close()
+
+# in-situ per-GEMM-node durations (in-kernel %globaltimer stamps) of one more batch
+ex = Executor(8 << 30)
+ex.load(_plan_item(pf, model, B * 2, B), model)
+ex.timing = True
+for k in range(2):
+    ex.fill(BubbleSlot(0, None, 0))
+    rec = ex.settle()
+tot = (rec.fill_end_ns - rec.fill_start_ns) / 1e6
+g = ex.gemm_samples[-4 * cfg.layers:]
+names = ["QKV", "out+res", "FFN1+gelu", "FFN2+res"]
+gsum = 0.0
+for j, nm in enumerate(names):
+    v = g[j::4]
+    ms = sum(t for _, t in v) / len(v)
+    gsum += sum(t for _, t in v)
+    print(f"{nm:10s} {ms * 1e3:7.1f} us  {v[0][0] / ms / 1e9:7.0f} TFLOP/s")
+print(f"batch {tot:.3f} ms: GEMMs {gsum:.3f} ms ({gsum / tot * 100:.1f}%), rest {tot - gsum:.3f} ms "
+      f"({(tot - gsum) / cfg.layers * 1e3:.1f} us per layer: attention + 2 LN + gates)")
+# gaps between GEMM nodes from the raw in-kernel stamps (t0 = first CTA start, t1 = last CTA end)
+ch = next(iter(ex._chains.values()))
+nodes = sorted(ch.gemm_flops)
+st = ex._stamps_host.tensor
+ts = [(int(st[n, 0]), int(st[n, 1])) for n in nodes]
+gaps = {"QKV->out (attention)": [], "out->FFN1 (LN)": [], "FFN1->FFN2 (adjacent)": [], "FFN2->QKV (LN, gate, next layer)": []}
+keys = list(gaps)
+for i in range(len(ts) - 1):
+    gaps[keys[i % 4]].append((ts[i + 1][0] - ts[i][1]) / 1e3)
+for k, v in gaps.items():
+    print(f"{k:34s} mean {sum(v) / len(v):7.1f} us  min {min(v):6.1f}")
+ex.close()
