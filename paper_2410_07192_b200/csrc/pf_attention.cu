@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
   const int units = batch * heads;
   const int n_mine = (int)blockIdx.x < units ? (units - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
+  pdl_enter();
   if (tid == 0) {
     int go = 1;
     if (chain_aborted(ctl)) go = 0;
@@ -423,12 +424,9 @@ struct AttentionOp final : PreparedOp {
   uint32_t units() const override { return attention_grid(batch, heads); }
   bool resumable() const override { return false; }
   int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
-    if (mask == nullptr && seq == S_MAX)
-      attention_kernel<true><<<units(), THREADS, SMEM_REQUEST, s>>>(tm, mask, out, batch, seq, heads,
-                                                                    scale_log2, make_ctl(ctl));
-    else
-      attention_kernel<false><<<units(), THREADS, SMEM_REQUEST, s>>>(tm, mask, out, batch, seq, heads,
-                                                                     scale_log2, make_ctl(ctl));
+    auto k = (mask == nullptr && seq == S_MAX) ? attention_kernel<true> : attention_kernel<false>;
+    PF_CUDA(launch_pdl(k, dim3(units()), dim3(THREADS), SMEM_REQUEST, s, tm, mask, out, batch, seq,
+                       heads, scale_log2, make_ctl(ctl)));
     PF_CUDA(cudaGetLastError());
     return PF_OK;
   }

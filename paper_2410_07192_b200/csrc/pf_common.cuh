@@ -18,6 +18,28 @@ int set_error(int code, const char* fmt, ...);
 int check_cuda(cudaError_t err, const char* what);
 int device_sm_count();
 bool device_is_sm100();
+bool pdl_enabled();  // programmatic dependent launch for chain kernels (PF_PDL=0 disables)
+
+// Launch with programmatic stream serialization (PDL): the kernel may be launched while
+// the previous kernel on the stream is still running; it calls pdl_wait() before touching
+// anything the previous kernel writes, and pdl_trigger() so the next one can launch early.
+// Captured into the chains' CUDA graphs as programmatic edges: the launch latency and the
+// CTA ramp of every kernel boundary overlap the previous kernel's tail.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 #define PF_TRY(expr)              \
   do {                            \
@@ -64,6 +86,15 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+// PDL: wait until the previous kernel on the stream completed and its writes are visible
+// (a no-op for a normal launch), then let the next kernel launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_enter() {
+  pdl_wait();
+  pdl_trigger();
 }
 
 // True when this launch must not start any work at all (chain already aborted).
@@ -152,6 +183,7 @@ __device__ __forceinline__ float2 unpack_bf16x2(uint32_t u) {
 
 // Entry gate for atomic-unit kernels; returns false when the CTA must skip.
 __device__ __forceinline__ bool atomic_unit_enter(const Ctl& c) {
+  pdl_enter();
   __shared__ int s_go;
   if (threadIdx.x == 0) {
     int go = 1;

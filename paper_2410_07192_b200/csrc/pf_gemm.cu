@@ -296,6 +296,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int warp = warp_id();
   const int lane = lane_id();
 
+  pdl_enter();
   if (chain_aborted(ctl)) return;  // uniform across the CTA: nothing allocated yet
   DIAG_INIT();
   if (threadIdx.x == 0 && p.stamp) atomicMin(&p.stamp[0], globaltimer_ns());
@@ -922,7 +923,8 @@ static int launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const CUtens
                                  C::SMEM_BYTES));
     attr_set = true;
   }
-  gemm_kernel<BN, EPI, MJ><<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(ta, tb, ty, p, make_ctl(ctl));
+  PF_CUDA(launch_pdl(gemm_kernel<BN, EPI, MJ>, dim3(grid), dim3(NUM_THREADS), C::SMEM_BYTES, stream, ta, tb,
+                     ty, p, make_ctl(ctl)));
   PF_CUDA(cudaGetLastError());
   return PF_OK;
 }

@@ -216,11 +216,13 @@ struct NormOp final : PreparedOp {
   bool resumable() const override { return false; }
   int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
     if (rms) {
-      PF_NV_DISPATCH(nv_for(cols), (norm_kernel<NV, true><<<grid_for(rows), WARPS * 32, 0, s>>>(
-                                       x, r, g, nullptr, y, rows, cols, eps, make_ctl(ctl))));
+      PF_NV_DISPATCH(nv_for(cols), PF_CUDA(launch_pdl(norm_kernel<NV, true>, dim3(grid_for(rows)),
+                                                      dim3(WARPS * 32), 0, s, x, r, g, nullptr, y,
+                                                      rows, cols, eps, make_ctl(ctl))));
     } else {
-      PF_NV_DISPATCH(nv_for(cols), (norm_kernel<NV, false><<<grid_for(rows), WARPS * 32, 0, s>>>(
-                                       x, r, g, b, y, rows, cols, eps, make_ctl(ctl))));
+      PF_NV_DISPATCH(nv_for(cols), PF_CUDA(launch_pdl(norm_kernel<NV, false>, dim3(grid_for(rows)),
+                                                      dim3(WARPS * 32), 0, s, x, r, g, b, y, rows,
+                                                      cols, eps, make_ctl(ctl))));
     }
     PF_CUDA(cudaGetLastError());
     return PF_OK;

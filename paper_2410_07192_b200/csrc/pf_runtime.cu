@@ -59,6 +59,14 @@ int device_sm_count() {
   return n > 0 ? n : 148;
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("PF_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool device_is_sm100() {
   const DevInfo& d = dev_info();
   return d.major == 10 && d.minor == 0;
@@ -120,6 +128,7 @@ __global__ void __launch_bounds__(COPY_THREADS) copy_kernel(uint4* __restrict__ 
                                                             uint64_t n16, Ctl ctl,
                                                             const int64_t* desc,
                                                             const uint32_t* idx, int role) {
+  pdl_enter();
   __shared__ int s_go;
   if (threadIdx.x == 0) {
     int go = 1;
@@ -179,10 +188,10 @@ struct CopyOp final : PreparedOp {
     const uint8_t* sp = src + (role == 1 && !dev ? a.in_off : 0);
     uint8_t* dp = dst + (role == 2 && !dev ? a.out_off : 0);
     if (n16() == 0) return PF_OK;
-    copy_kernel<<<units(), COPY_THREADS, 0, s>>>(
-        reinterpret_cast<uint4*>(dp), dpitch / 16, reinterpret_cast<const uint4*>(sp), spitch / 16,
-        width / 16, n16(), make_ctl(ctl), dev ? a.desc : nullptr, a.idx, role);
-    PF_CUDA(cudaGetLastError());
+    PF_CUDA(launch_pdl(copy_kernel, dim3(units()), dim3(COPY_THREADS), 0, s,
+                       reinterpret_cast<uint4*>(dp), dpitch / 16, reinterpret_cast<const uint4*>(sp),
+                       spitch / 16, width / 16, n16(), make_ctl(ctl), dev ? a.desc : nullptr, a.idx,
+                       role));
     return PF_OK;
   }
 };
