@@ -231,7 +231,8 @@ def run_service_sweep(args, conf) -> None:
     from paper_2410_07192_b200.executor import Executor
     from paper_2410_07192_b200.fillmodels import BERT_BASE, BERT_LARGE, bert, resnet50
     from paper_2410_07192_b200.profiler import measure_profile
-    from paper_2410_07192_b200.service import FillService, ServiceConfig, predict, write_report
+    from paper_2410_07192_b200.service import (FillService, ServiceConfig, predict, write_plan, write_report,
+                                               write_sweep)
 
     native.require_device()
     peaks = load_peaks()
@@ -271,7 +272,7 @@ def run_service_sweep(args, conf) -> None:
         off[s] = t["main_end"] - t["start"]
 
     out_dir = args.report_dir or os.path.join(ROOT, "gpurun_out", "c5_report")
-    rows, launches, dev_ns, sample_eq, on_iter = [], 0, 0, 0.0, {}
+    rows, launches, dev_ns, sample_eq, on_iter, sweep_rows = [], 0, 0, 0.0, {}, []
     with ClockSampler(local) as clocks:
         w0 = time.perf_counter()
         for cap_gb in conf["caps_gb"]:
@@ -297,8 +298,12 @@ def run_service_sweep(args, conf) -> None:
             eq = sum(r.sample_eq for r in recs)
             ns = sum(t["step_end"] - t["start"] for t in steps)
             launches += sum(ex.kernel_launches for ex in executors) + sum(e.launches for e in engines)
+            cap_iter = {}
             for t in steps:
                 on_iter.setdefault(t["stage"], []).append(t["main_end"] - t["start"])
+                cap_iter.setdefault(t["stage"], []).append(t["main_end"] - t["start"])
+            rep.scalars_extra["main_job_slowdown"] = statistics.mean(
+                statistics.mean(v) / off[s_] - 1 for s_, v in cap_iter.items() if off.get(s_))
             sc = rep.scalars()
             row = {"free_mem_gb": cap_gb, "sample_eq_per_s": eq / (ns / 1e9) if ns else 0.0,
                    "iterations": len(steps), **{k: sc[k] for k in (
@@ -310,9 +315,13 @@ def run_service_sweep(args, conf) -> None:
             rows.append(row)
             dev_ns += ns
             sample_eq += eq
-            write_report(os.path.join(out_dir, f"free_mem_{cap_gb}gb"), rep,
-                         {"free_mem_gb": cap_gb, "stages": P, "microbatches": M, "routing": "avg_jct",
-                          "ordering": "sjf", "sample_eq_per_s": row["sample_eq_per_s"]})
+            vdir = os.path.join(out_dir, f"free_mem_{cap_gb}gb")
+            write_report(vdir, rep, {"free_mem_gb": cap_gb, "stages": P, "microbatches": M, "routing": "avg_jct",
+                                     "ordering": "sjf", "sample_eq_per_s": row["sample_eq_per_s"]}, seed=0)
+            for c in svc.coordinators:  # the executed plans, as the reference's `partition` writes them
+                for jid, plan in c.executables.items():
+                    write_plan(os.path.join(vdir, "plans", f"stage{c.stage_id}", jid), plan, jid, c.stage_id)
+            sweep_rows.append((f"free_mem_{cap_gb}gb", {"free_mem_gb": cap_gb}, sc))
             for ex in executors:
                 ex.close()
             for e in engines:
@@ -321,6 +330,7 @@ def run_service_sweep(args, conf) -> None:
         w1 = time.perf_counter()
     with open(os.path.join(out_dir, "sweep.json"), "w") as fh:
         json.dump(rows, fh, indent=2)
+    write_sweep(out_dir, sweep_rows, seed=0)
     slow = [statistics.mean(v) / off[s] - 1 for s, v in on_iter.items() if off.get(s)]
     best = rows[-1]
     if rank == 0:

@@ -91,6 +91,7 @@ class ServiceReport:
     fill_busy_ns: int = 0
     samples_completed: int = 0
     scalars_extra: dict = field(default_factory=dict)
+    gpus: int = 1  # pipeline stages served (one worker each)
 
     def scalars(self) -> dict:
         done = sorted(self.per_job.values(), key=lambda r: r.job_id)
@@ -115,6 +116,18 @@ class ServiceReport:
             "rounds": self.rounds,
             "period_s": self.period_s,
         }
+        # the reference's SimReport.scalars keys (sim.py:139-153), from measured quantities:
+        # bubble_ratio = measured bubble time / stage time, wall-clock TFLOP/s over all GPUs,
+        # GPU-hours = measured busy time (sim.py:119-120), gpus_saved (sim.py:156-159)
+        stage_ns = self.rounds * self.period_s * 1e9 * max(1, self.gpus)
+        ratio = self.bubble_ns / stage_ns if stage_ns > 0 else 0.0
+        out.update({
+            "bubble_ratio": ratio,
+            "recovered_tflops_wallclock": flops / (span * max(1, self.gpus)) / 1e12 if span > 0 else 0.0,
+            "mean_fill_gpu_hours": busy / 3600.0 / len(done) if done else 0.0,
+            "gpus_saved": max(1, self.gpus) * ratio * out["mean_rel_perf"],
+            "main_job_slowdown": None,
+        })
         out.update(self.scalars_extra)
         return out
 
@@ -237,7 +250,8 @@ class FillService:
                                      assigned[jid], job.samples * job.model.flops_per_sample, busy, rel)
         unfinished = [j.id for j in jobs if j.id not in completion and j.id not in rejected]
         samples = sum(r.samples for r in per_job.values())
-        return ServiceReport(per_job, rejected, unfinished, rounds, self.period_s, bubble_ns, fill_ns, samples)
+        return ServiceReport(per_job, rejected, unfinished, rounds, self.period_s, bubble_ns, fill_ns, samples,
+                             gpus=len(self.coordinators))
 
 
 def predict(config: ServiceConfig, jobs: Sequence[JobSpec],
@@ -295,9 +309,29 @@ def predict(config: ServiceConfig, jobs: Sequence[JobSpec],
     return done
 
 
-def write_report(out_dir: str | Path, report: ServiceReport, extra: Optional[dict] = None) -> None:
+TOOL_VERSION = "b200-0.1.0"
+# sweep.csv columns after the variant and its axes (cli.py:137-151)
+SWEEP_CSV_FIXED = ["bubble_ratio", "avg_jct_s", "p99_jct_s", "makespan_s", "completed", "rejected",
+                   "recovered_tflops_wallclock", "recovered_tflops_active", "mean_rel_perf",
+                   "mean_fill_gpu_hours", "gpus_saved", "main_job_slowdown"]
+
+
+def write_manifest(out_dir: str | Path, subcommand: str, seed: int, config: Optional[dict] = None) -> None:
+    """manifest.json with the reference's keys (cli.py:62-74); the run is configured in code,
+    so the config is recorded inline (config_path / trace_path are None)."""
+    doc = {"tool_version": TOOL_VERSION, "subcommand": subcommand, "seed": seed, "config_path": None,
+           "config_sha256": None, "trace_path": None, "trace_sha256": None}
+    if config is not None:
+        doc["config"] = config
+    Path(out_dir).mkdir(parents=True, exist_ok=True)
+    (Path(out_dir) / "manifest.json").write_text(json.dumps(doc, indent=2, sort_keys=True) + "\n")
+
+
+def write_report(out_dir: str | Path, report: ServiceReport, extra: Optional[dict] = None,
+                 seed: Optional[int] = None) -> None:
     """jobs.csv (the reference's columns + model, samples, measured busy, JCT and the
-    time model's predicted completion) and summary.json (cli.py:80-99)."""
+    time model's predicted completion), summary.json (cli.py:80-99) and, with a seed,
+    manifest.json (cli.py:62-74)."""
     out = Path(out_dir)
     out.mkdir(parents=True, exist_ok=True)
     with open(out / "jobs.csv", "w", newline="") as fh:
@@ -309,8 +343,40 @@ def write_report(out_dir: str | Path, report: ServiceReport, extra: Optional[dic
                         rec.coordinator, repr(rec.fill_flops), rec.model, rec.samples, repr(rec.busy_s),
                         repr(rec.jct_s), repr(rec.predicted_completion_s)])
     summary = dict(report.scalars())
+    summary["tool_version"] = TOOL_VERSION
     summary["rejected_ids"] = sorted(report.rejected)
     summary["unfinished_ids"] = sorted(report.unfinished)
     if extra:
         summary.update(extra)
     (out / "summary.json").write_text(json.dumps(summary, indent=2, sort_keys=True) + "\n")
+    if seed is not None:
+        write_manifest(out, "serve", seed, extra)
+
+
+def write_sweep(out_dir: str | Path, rows: Sequence[tuple[str, dict, dict]], seed: int = 0) -> None:
+    """sweep.csv in the reference's layout (cli.py:153-185): one row per variant, its axes,
+    then SWEEP_CSV_FIXED from that variant's scalars (floats as repr); plus manifest.json.
+    `rows` = (variant name, {axis: value}, scalars)."""
+    out = Path(out_dir)
+    out.mkdir(parents=True, exist_ok=True)
+    axis_names = list(rows[0][1]) if rows else []
+    with open(out / "sweep.csv", "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(["variant", *axis_names, *SWEEP_CSV_FIXED])
+        for name, axes, sc in rows:
+            w.writerow([name, *[axes[a] for a in axis_names]]
+                       + [repr(sc[k]) if isinstance(sc[k], float) else sc[k] for k in SWEEP_CSV_FIXED])
+    write_manifest(out, "sweep", seed)
+
+
+def write_plan(out_dir: str | Path, plan, model_name: str, stage: int, algo: str = "dp") -> None:
+    """plan.json as the reference's `partition` subcommand writes it (cli.py:214-236):
+    {algo, model, stage, plan_to_dict(plan)..., tool_version}."""
+    from .planner import plan_to_dict
+
+    doc: dict = {"algo": algo, "model": model_name, "stage": stage}
+    doc.update(plan_to_dict(plan))
+    doc["tool_version"] = TOOL_VERSION
+    out = Path(out_dir)
+    out.mkdir(parents=True, exist_ok=True)
+    (out / "plan.json").write_text(json.dumps(doc, indent=2, sort_keys=True) + "\n")

@@ -136,3 +136,47 @@ def test_service_measured_completions_equal_prediction(tmp_path):
     assert summary["completed"] == len(jobs)
     header = (tmp_path / "jobs.csv").read_text().splitlines()[0].split(",")
     assert header[:6] == ["id", "arrival_s", "start_s", "completion_s", "coordinator", "flops"]
+    # the reference's SimReport.scalars keys are all reported (sim.py:139-153)
+    for k in ("bubble_ratio", "recovered_tflops_wallclock", "recovered_tflops_active", "mean_rel_perf",
+              "mean_fill_gpu_hours", "gpus_saved", "main_job_slowdown", "avg_jct_s", "p99_jct_s", "makespan_s"):
+        assert k in summary, k
+
+
+def test_report_files_follow_reference_layout(tmp_path):
+    """manifest.json / sweep.csv / plan.json carry the reference CLI's keys and columns
+    (cli.py:62-74, 137-185, 214-236); plan.json's body is plan_to_dict of the executed plan."""
+    from paper_2410_07192_b200.planner import dp_optimal_plan, plan_to_dict
+    from paper_2410_07192_b200.service import SWEEP_CSV_FIXED, write_manifest, write_plan, write_sweep
+
+    cfg = _pipeline()
+    jobs = _jobs(cfg)
+    scfg = ServiceConfig(cfg, routing="avg_jct", ordering=SJF)
+    exs = [_StandIn(cfg.period_us / 1e6) for _ in range(cfg.num_stages)]
+
+    def run_iteration(stage, ex):
+        ex.left -= 1
+        ex.records.append(BubbleRecord(0, 1, 1, 1, False, 100, 900, tag=(stage,)))
+        return {"start": 0, "main_end": 1000, "step_end": 1000, "bubbles": [(0, 0, 1000, (stage,))]}
+
+    rep = FillService(scfg, {j.model.name: j.model.name for j in jobs}, exs, run_iteration).run(jobs, 10_000)
+    write_report(tmp_path / "v0", rep, {"free_mem_gb": 4.5}, seed=7)
+    man = json.loads((tmp_path / "v0" / "manifest.json").read_text())
+    assert set(man) >= {"tool_version", "subcommand", "seed", "config_path", "config_sha256", "trace_path",
+                        "trace_sha256"} and man["seed"] == 7
+    sc = rep.scalars()
+    assert 0.0 < sc["bubble_ratio"] <= 1.0 and sc["gpus_saved"] >= 0.0
+    write_sweep(tmp_path, [("v0", {"free_mem_gb": 4.5}, sc), ("v1", {"free_mem_gb": 8.0}, sc)])
+    lines = (tmp_path / "sweep.csv").read_text().splitlines()
+    assert lines[0].split(",") == ["variant", "free_mem_gb", *SWEEP_CSV_FIXED] and len(lines) == 3
+    if os.path.isdir(REF_SRC):  # same fixed columns as the reference CLI's sweep.csv
+        out = subprocess.run([sys.executable, "-c", f"import sys; sys.path.insert(0, {REF_SRC!r}); "
+                              "from bubblefill import cli; print(','.join(cli.SWEEP_CSV_FIXED[1:]))"],
+                             capture_output=True, text=True, check=True).stdout.strip()
+        assert out.split(",") == SWEEP_CSV_FIXED
+    plan = dp_optimal_plan(jobs[0].model, pf.build_bubble_cycle(cfg, 3))
+    write_plan(tmp_path / "plan", plan, jobs[0].model.name, 3)
+    doc = json.loads((tmp_path / "plan" / "plan.json").read_text())
+    assert doc["algo"] == "dp" and doc["stage"] == 3 and doc["model"] == jobs[0].model.name
+    assert {k: doc[k] for k in plan_to_dict(plan)} == json.loads(json.dumps(plan_to_dict(plan)))
+    write_manifest(tmp_path / "m", "serve", 0, {"x": 1})
+    assert json.loads((tmp_path / "m" / "manifest.json").read_text())["config"] == {"x": 1}
