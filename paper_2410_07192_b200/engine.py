@@ -241,6 +241,9 @@ class StageEngine:
         self.launches = 0  # our kernels (timer / stamp / flag) enqueued by the engine
         self._anchor_stamp = -1
         self.epoch = 0
+        # bubble probe (probe_bubbles): {bubble kind: ns} the main stream stays busy from the
+        # bubble's start before its next instruction (PAPER.md:424's "wait" at the BUBBLE)
+        self.probe_ns: dict[int, int] = {}
 
     def set_anchor(self, lead_ms: float = 5.0) -> None:
         """Anchor = device time now + lead (host enqueues ahead within the lead)."""
@@ -282,6 +285,11 @@ class StageEngine:
                 rec.bubble_mem.append((kind, torch.cuda.memory_allocated()))
                 if fill and self.executor is not None:
                     self.executor.fill(BubbleSlot(kind, start_ev, flag, tag=self._tag(clear_idx)))
+                if kind in self.probe_ns:  # probe: the main job "waits" w ns into the bubble
+                    main.wait_event(start_ev)
+                    native.call("pf_wait_until", self.words.stamps.data_ptr() + 8 * set_idx,
+                                int(self.probe_ns[kind]), None, main.cuda_stream)
+                    self.launches += 1
                 main.wait_event(end_ev)
                 prev_end_us = end_us
                 continue
@@ -585,6 +593,56 @@ def characterize_bubbles(stage_id: int, timings: list[dict], records: list[Itera
         report.update({"analytic_bubbles_us": [b.duration_us for b in analytic.bubbles],
                        "analytic_period_us": analytic.period_us})
     return cycle, report
+
+
+def probe_bubbles(engine: "StageEngine", start_ms: float = 1.0, tol_ms: float = 0.5, refine: int = 6,
+                  iterations: int = 2) -> dict:
+    """The paper's bubble-duration probe: at every BUBBLE instruction of one
+    kind the main job waits w before proceeding; while its iteration time is unaffected the
+    wait doubles, then the largest unaffected w is refined by bisection. Returns
+    {"probed_us": [fwd_bwd, fill_drain], "base_iteration_us": ..., "probes": n}.
+
+    "Unaffected" = the main-job time of `iterations` back-to-back iterations from one anchor
+    grows by at most tol_ms (the fill-drain bubble wraps into the next iteration, so one
+    iteration alone would not see it). The direct measurement (flag stamps,
+    characterize_bubbles) is what the bench uses; this probe is the paper's method, kept to
+    cross-check it (tests/test_executor_gpu.py)."""
+    calls = [0]
+
+    def run(probe: dict) -> int:
+        engine.probe_ns = dict(probe)
+        engine.reset_stamps()
+        engine.set_anchor()
+        recs = [engine.run_iteration(i, fill=False) for i in range(iterations)]
+        t0 = engine.record_timing(recs[0])
+        t1 = engine.record_timing(recs[-1])
+        engine.probe_ns = {}
+        calls[0] += 1
+        return t1["main_end"] - t0["start"]
+
+    run({})  # warm-up
+    base = min(run({}) for _ in range(2))
+    tol = int(tol_ms * 1e6)
+    kinds_present = {ins.kind for ins, s, e in engine.timeline if ins.op == "BUBBLE" and e > s}
+    period_ns = engine.cfg.period_us * US
+    out = []
+    for kind in (BubbleKind.FWD_BWD, BubbleKind.FILL_DRAIN):
+        k = 0 if kind is BubbleKind.FWD_BWD else 1
+        if kind not in kinds_present:
+            out.append(0)
+            continue
+        ok, w = 0, int(start_ms * 1e6)
+        while w <= period_ns and run({k: w}) <= base + tol:
+            ok, w = w, 2 * w
+        lo, hi = ok, w
+        for _ in range(refine):
+            mid = (lo + hi) // 2
+            if run({k: mid}) <= base + tol:
+                lo = mid
+            else:
+                hi = mid
+        out.append(lo // 1000)
+    return {"probed_us": out, "base_iteration_us": base // 1000, "probes": calls[0]}
 
 
 def characterize_stage(engine: "StageEngine", iterations: int = 3, fill_fraction: float = 0.68,

@@ -179,3 +179,20 @@ def test_bubble_characterization_matches_the_emulated_timeline(pf):
             assert abs(got - want) <= 0.25 * want + 200, rep
         assert all(f > 0 for f in rep["free_mem_bytes"]), rep
         assert cycle.bubbles[0].duration_us == rep["measured_bubbles_us"][0]
+
+
+def test_doubling_probe_matches_measured_bubbles(pf):
+    """The paper's doubling-wait probe and the direct flag-stamp measurement
+    agree on every bubble's duration of an emulated stage."""
+    from paper_2410_07192_b200.engine import (GPT2_SMALL_STAGE, GPTStage, StageEngine, characterize_stage,
+                                              measure_stage_times, probe_bubbles)
+
+    model = GPTStage(GPT2_SMALL_STAGE, seed=0)
+    tf, tb = measure_stage_times(model)
+    cfg = pf.PipelineConfig(4, 8, tf, tb, pf.ScheduleKind.ONE_F_ONE_B, 1, 1, 0.68)
+    eng = StageEngine(cfg, 1, model, None)
+    _, rep = characterize_stage(eng, iterations=2)
+    probe = probe_bubbles(eng, start_ms=0.25, tol_ms=0.2, refine=6)
+    for got, want in zip(probe["probed_us"], rep["measured_bubbles_us"]):
+        # resolution: the bisection step plus the slowdown tolerance
+        assert abs(got - want) <= 0.1 * want + 400, (probe, rep)
