@@ -56,7 +56,8 @@ def test_gemm(K, m, n, k, bias, gelu, res):
     assert rel_err(got, ref) < REL_TOL_BF16
 
 
-@pytest.mark.parametrize("rows,cols,res", [(4096, 768, True), (4096, 1024, False), (33, 2048, True), (5, 8, False)])
+@pytest.mark.parametrize("rows,cols,res", [(4096, 768, True), (4096, 1024, False), (33, 2048, True), (5, 8, False),
+                                           (16384, 1024, True), (7001, 1024, False)])
 def test_layernorm(K, rows, cols, res):
     g = torch.Generator().manual_seed(rows + cols)
     x = _bf16(rows, cols, gen=g)
@@ -168,3 +169,26 @@ def test_attention_preemption_protocol(K):
     assert abort.item() == 0 and cursor.item() == units and units <= batch * heads
     ref = fill_ref.attention(qkv.float().cpu(), heads, None)
     assert rel_err(out, ref) < REL_TOL_BF16
+
+
+def test_layernorm_preemption_protocol(K):
+    """Persistent LayerNorm: flag 0 -> nothing written, abort set, cursor 0; flag 1 -> every
+    CTA counts itself (units = CTAs launched) and the rows are exact re-runs."""
+    rows, cols = 9000, 1024
+    g = torch.Generator().manual_seed(3)
+    x = _bf16(rows, cols, gen=g).cuda()
+    gamma = torch.ones(cols, dtype=torch.bfloat16, device="cuda")
+    beta = torch.zeros(cols, dtype=torch.bfloat16, device="cuda")
+    words = torch.zeros(8, dtype=torch.int32, device="cuda")
+    flag, abort, cursor = (words[i:i + 1] for i in range(3))
+    ctl = K.KernelCtl(flag.data_ptr(), abort.data_ptr(), cursor.data_ptr())
+    out = torch.zeros_like(x)
+    K.layernorm(x, gamma, beta, 1e-12, out=out, ctl=ctl)
+    torch.cuda.synchronize()
+    assert abort.item() == 1 and cursor.item() == 0 and out.abs().max().item() == 0
+    abort.zero_()
+    flag.fill_(1)
+    K.layernorm(x, gamma, beta, 1e-12, out=out, ctl=ctl)
+    torch.cuda.synchronize()
+    assert abort.item() == 0 and cursor.item() == K.norm_units(rows, cols)
+    assert torch.equal(out, K.layernorm(x, gamma, beta, 1e-12))
