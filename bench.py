@@ -223,7 +223,8 @@ def run_service_sweep(args, conf) -> None:
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                timeout=__import__("datetime").timedelta(seconds=240))
     import paper_2410_07192_b200 as pf
     from paper_2410_07192_b200 import native
     from paper_2410_07192_b200.coordinator import SJF
@@ -377,7 +378,8 @@ def run_training_depths(args, conf) -> None:
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                timeout=__import__("datetime").timedelta(seconds=240))
     import paper_2410_07192_b200 as pf
     from paper_2410_07192_b200 import native
     from paper_2410_07192_b200.engine import GPT2_SMALL_STAGE, GPT_8B_STAGE, GPTStage, StageEngine, measure_stage_times
@@ -578,7 +580,8 @@ def main() -> None:
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                timeout=__import__("datetime").timedelta(seconds=240))
     if args.pipeline == "nccl":
         # main job with deterministic kernels (math SDPA): fill-on and fill-off losses are then
         # comparable bit for bit, so any effect of the fill job on the main job would show

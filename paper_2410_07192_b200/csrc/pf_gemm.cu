@@ -72,6 +72,12 @@ struct Params {
   // slice z of output tile (tm, tn) is stored to Y[z] of a [k_splits, M, N] stack
   int k_splits;
   int kb_per_split;
+  // Tail wave in half tiles: units [0, n_full) are full BM x BN tiles; when tail_halves is
+  // set, each of the remaining tiles is split into two BM x BN/2 units (n_full + 2 x rem
+  // units in all), so a last wave of rem <= grid/2 tiles takes ~(BN/2 + 200)/(BN + 200) of a
+  // full wave instead of a whole one (see pick_bn's cost model).
+  int n_full;
+  int tail_halves;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -115,6 +121,17 @@ __device__ __forceinline__ void tile_coords(int tile, const Params& p, int& tm, 
   const int r = tile - g * per_group;
   tm = first_m + r % rows;
   tn = r / rows;
+}
+
+// Unit u -> output tile (tm, tn), K slice ks and half (-1 = the whole BN-wide tile).
+__device__ __forceinline__ void unit_info(int u, const Params& p, int& tm, int& tn, int& ks, int& half) {
+  half = -1;
+  if (p.tail_halves && u >= p.n_full) {
+    const int v = u - p.n_full;
+    half = v & 1;
+    u = p.n_full + (v >> 1);
+  }
+  tile_coords(u, p, tm, tn, ks);
 }
 
 // One epilogue warp's share of an output tile: 32 rows (its TMEM lane group) x
@@ -325,7 +342,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
 
-  const int num_tiles = p.tiles_m * p.tiles_n * p.k_splits;
+  const int num_tiles = p.tail_halves ? 2 * p.tiles_m * p.tiles_n - p.n_full : p.tiles_m * p.tiles_n * p.k_splits;
   const int num_kb = (p.K + BK - 1) / BK;
 
   if (warp == PRODUCER_WARP) {
@@ -348,8 +365,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         sphase ^= 1u;
       }
       if (tile < 0) break;
-      int tm, tn, ks;
-      tile_coords(tile, p, tm, tn, ks);
+      int tm, tn, ks, half;  // a half unit loads the whole BN rows of W (L2-resident) and uses half
+      unit_info(tile, p, tm, tn, ks, half);
       const int kb0 = ks * p.kb_per_split;
       const int kb1 = min(num_kb, kb0 + p.kb_per_split);
       for (int kb = kb0; kb < kb1; ++kb) {
@@ -389,6 +406,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const unsigned long long _g0 = globaltimer_ns();
 #endif
     constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, (MJ & 1) != 0, (MJ & 2) != 0);
+    constexpr uint32_t idesc_half = umma_idesc_bf16(BM, BN / 2, (MJ & 1) != 0, (MJ & 2) != 0);
     int slot = 0;
     uint32_t sphase = 0;
     int stage = 0;
@@ -415,8 +433,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const long long _tm0 = clock64();
 #endif
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-      const int kb0 = (tile / (p.tiles_m * p.tiles_n)) * p.kb_per_split;
+      int utm, utn, uks, uhalf;
+      unit_info(tile, p, utm, utn, uks, uhalf);
+      const int kb0 = uks * p.kb_per_split;
       const int kb1 = min(num_kb, kb0 + p.kb_per_split);
+      // a half unit: N = BN/2 from rows [half * BN/2, +BN/2) of the staged W tile
+      const uint32_t idesc_u = uhalf < 0 ? idesc : idesc_half;
+      const uint32_t b_off = uhalf < 0 ? 0u : (uint32_t)(uhalf * (BN / 2) * 128);
       for (int kb = kb0; kb < kb1; ++kb) {
         {
           DIAG_T0();
@@ -426,7 +449,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc_fence_after();
         if (lane == 0) {
           const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
-          const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES) + b_off;
 #pragma unroll
           for (int k = 0; k < BK / UMMA_K; ++k) {
             // K advance inside the 128-B swizzle atom: +32 B per UMMA_K step
@@ -436,7 +459,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                          : umma_desc_sw128_kmajor(a_addr + k * UMMA_K * 2);
             const uint64_t bd = (MJ & 2) ? umma_desc_sw128_mnmajor(b_addr + k * UMMA_K * 128, 8192)
                                          : umma_desc_sw128_kmajor(b_addr + k * UMMA_K * 2);
-            umma_bf16_ss(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            umma_bf16_ss(d_tmem, ad, bd, idesc_u, (kb != kb0 || k != 0) ? 1u : 0u);
           }
           umma_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs retire
         }
@@ -484,14 +507,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         sphase ^= 1u;
       }
       if (tile < 0) break;
-      int tm, tn, ks;
-      tile_coords(tile, p, tm, tn, ks);
+      int tm, tn, ks, half;
+      unit_info(tile, p, tm, tn, ks, half);
       const int row_base = tm * BM + lane_grp * 32;
-      const int col_base = tn * BN + col_half * C::COLS_PER_EPI_WARP;
-      const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) +
-                             (uint32_t)(acc * BN + col_half * C::COLS_PER_EPI_WARP);
-      epilogue_tile<C::CHUNKS, EPI, false>(p, &tmY, my_stg, taddr, &tfull_bar[acc], aphase, row_base,
-                                           col_base, my_bias, ks);
+      if (half < 0) {
+        const int col_base = tn * BN + col_half * C::COLS_PER_EPI_WARP;
+        const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) +
+                               (uint32_t)(acc * BN + col_half * C::COLS_PER_EPI_WARP);
+        epilogue_tile<C::CHUNKS, EPI, false>(p, &tmY, my_stg, taddr, &tfull_bar[acc], aphase, row_base,
+                                             col_base, my_bias, ks);
+      } else if constexpr (C::CHUNKS % 2 == 0) {
+        constexpr int HC = C::COLS_PER_EPI_WARP / 2;
+        const int col_base = tn * BN + half * (BN / 2) + col_half * HC;
+        const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(acc * BN + col_half * HC);
+        epilogue_tile<C::CHUNKS / 2, EPI, false>(p, &tmY, my_stg, taddr, &tfull_bar[acc], aphase, row_base,
+                                                 col_base, my_bias, ks);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
@@ -884,6 +915,21 @@ static int effective_splits(int K, int requested) {
   return (kb + per - 1) / per;
 }
 
+// Tail wave in half tiles (Params::tail_halves): a last wave of rem <= grid/2 tiles is run
+// as 2 x rem half-width units. BN 128 / 256 only (the halves keep whole 32-column
+// epilogue chunks per warp). PF_GEMM_TAIL=0 disables it.
+static int tail_n_full(int tiles, int bn) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("PF_GEMM_TAIL");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  const int sms = device_sm_count();
+  if (!on || (bn != 128 && bn != 256) || tiles <= sms) return tiles;
+  const int rem = tiles % sms;
+  return (rem > 0 && 2 * rem <= sms) ? tiles - rem : tiles;
+}
+
 // BN choice: minimise waves x per-tile time on 148 SMs.
 static int pick_bn(int M, int N) {
   static int forced = -1;  // PF_GEMM_BN=128|192|256 pins the tile width (experiments)
@@ -972,6 +1018,8 @@ struct GemmPairOp final : PreparedOp {
     const int tiles = p.tiles_m * p.tiles_n;
     const int pairs = device_sm_count() / 2;
     grid = 2 * (tiles < pairs ? tiles : pairs);
+    p.n_full = tiles;
+    p.tail_halves = 0;
     epi = e & 15u;
     return PF_OK;
   }
@@ -1030,6 +1078,10 @@ struct GemmOp final : PreparedOp {
                  int K, uint32_t e, int majors, int splits) {
     PF_TRY(prepare(X, W, bias, residual, Y, M, N, K, e));
     mj = majors;
+    if (mj != 0 || splits > 1) {  // the tail halves are for the forward (K-major, unsplit) GEMMs
+      p.tail_halves = 0;
+      p.n_full = p.tiles_m * p.tiles_n;
+    }
     if (mj & 1) PF_TRY(make_tmap_mn(&ta, X, K, M));
     if (mj & 2) PF_TRY(make_tmap_mn(&tb, W, K, N));
     if (splits > 1) {
@@ -1063,12 +1115,16 @@ struct GemmOp final : PreparedOp {
     const int tiles = p.tiles_m * p.tiles_n;
     const int sms = device_sm_count();
     grid = tiles < sms ? tiles : sms;
+    p.n_full = tail_n_full(tiles, BN);
+    p.tail_halves = p.n_full < tiles ? 1 : 0;
     epi = e & 15u;
     return PF_OK;
   }
   // Split-K: Y is a [splits, M, N] stack of partial products over K slices (no epilogue).
   int prepare_splitk(const void* X, const void* W, void* Y, int M, int N, int K, int splits) {
     PF_TRY(prepare(X, W, nullptr, nullptr, Y, M, N, K, 0u));
+    p.tail_halves = 0;
+    p.n_full = p.tiles_m * p.tiles_n;
     const int kb = (K + BK - 1) / BK;
     p.k_splits = effective_splits(K, splits);
     p.kb_per_split = (kb + p.k_splits - 1) / p.k_splits;
@@ -1078,7 +1134,10 @@ struct GemmOp final : PreparedOp {
     grid = tiles < sms ? tiles : sms;
     return PF_OK;
   }
-  uint32_t units() const override { return (uint32_t)(p.tiles_m * p.tiles_n * p.k_splits); }
+  uint32_t units() const override {
+    return p.tail_halves ? (uint32_t)(2 * p.tiles_m * p.tiles_n - p.n_full)
+                         : (uint32_t)(p.tiles_m * p.tiles_n * p.k_splits);
+  }
   bool resumable() const override { return true; }
   int run(const pf_ctl_t* ctl, cudaStream_t stream, const LaunchArgs& a) override {
     Params p = this->p;
@@ -1287,7 +1346,8 @@ extern "C" int pf_gemm_units(int M, int N, int K, uint32_t* out_units) {
     return PF_OK;
   }
   const int bn = gemm::pick_bn(M, N);
-  *out_units = (uint32_t)(((M + gemm::BM - 1) / gemm::BM) * ((N + bn - 1) / bn));
+  const int tiles = ((M + gemm::BM - 1) / gemm::BM) * ((N + bn - 1) / bn);
+  *out_units = (uint32_t)(2 * tiles - gemm::tail_n_full(tiles, bn));
   return PF_OK;
 }
 

@@ -58,13 +58,6 @@ __device__ __forceinline__ void norm_row_store(float (&x)[NV][8], int cols, floa
   }
 }
 
-// Persistent: a few CTAs per SM, every warp strides over rows (stride = all warps of the
-// grid) and prefetches its next row (raw bf16 in registers) while it reduces and writes the
-// current one, so each warp keeps two rows in flight. The entry gate is paid once per CTA;
-// a warp re-polls the flag every 8 rows and, on a closed bubble, marks the CTA dead (it
-// then stops without counting itself: the node is re-run whole on resume).
-constexpr int NORM_CTAS_PER_SM = 4;
-
 template <int NV, bool RMS>
 __global__ void __launch_bounds__(WARPS * 32) norm_kernel(const __nv_bfloat16* __restrict__ X,
                                                           const __nv_bfloat16* __restrict__ R,
@@ -73,60 +66,30 @@ __global__ void __launch_bounds__(WARPS * 32) norm_kernel(const __nv_bfloat16* _
                                                           __nv_bfloat16* __restrict__ Y, int rows,
                                                           int cols, float eps, Ctl ctl) {
   if (!atomic_unit_enter(ctl)) return;
-  __shared__ int s_dead;
-  if (threadIdx.x == 0) s_dead = 0;
-  __syncthreads();
   const int lane = lane_id();
-  const int nw = (int)gridDim.x * WARPS;
-  uint4 xa[NV], ra[NV];
-  auto fetch = [&](int row) {
+  const int row0 = blockIdx.x * ROWS_PER_CTA + warp_id() * ROWS_PER_WARP;
+#pragma unroll
+  for (int rr = 0; rr < ROWS_PER_WARP; ++rr) {
+    const int row = row0 + rr;
+    if (row >= rows) break;
+    float x[NV][8];
     const size_t off = (size_t)row * cols;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const int c = (j * 32 + lane) * 8;
       if (c < cols) {
-        xa[j] = __ldg(reinterpret_cast<const uint4*>(X + off + c));
-        if (R) ra[j] = __ldg(reinterpret_cast<const uint4*>(R + off + c));
-      }
-    }
-  };
-  int row = (int)blockIdx.x * WARPS + warp_id();
-  if (row < rows) fetch(row);
-  for (int it = 1; row < rows; row += nw, ++it) {
-    float x[NV][8];
-#pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      const uint32_t w[4] = {xa[j].x, xa[j].y, xa[j].z, xa[j].w};
-      const uint32_t v[4] = {ra[j].x, ra[j].y, ra[j].z, ra[j].w};
-#pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const float2 f = unpack_bf16x2(w[h]);
-        x[j][2 * h] = f.x;
-        x[j][2 * h + 1] = f.y;
+        load8(X + off + c, x[j]);
         if (R) {
-          const float2 g = unpack_bf16x2(v[h]);
-          x[j][2 * h] += g.x;
-          x[j][2 * h + 1] += g.y;
+          float r[8];
+          load8(R + off + c, r);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[j][e] += r[e];
         }
       }
     }
-    if (row + nw < rows) fetch(row + nw);  // the next row streams in under this row's math
-    norm_row_store<NV, RMS>(x, cols, eps, gamma, beta, Y + (size_t)row * cols);
-    if ((it & 7) == 0 && ctl.flag != nullptr) {
-      unsigned closed = 0;
-      if (lane == 0 && ld_acquire_u32(ctl.flag) == 0u) {
-        atomicExch(ctl.abort, 1u);
-        s_dead = 1;
-        closed = 1;
-      }
-      if (__shfl_sync(0xffffffffu, closed, 0)) break;
-    }
+    norm_row_store<NV, RMS>(x, cols, eps, gamma, beta, Y + off);
   }
-  __syncthreads();
-  if (threadIdx.x == 0 && ctl.cursor != nullptr && !s_dead) {
-    __threadfence();
-    atomicAdd(ctl.cursor, 1u);
-  }
+  atomic_unit_exit(ctl);
 }
 
 template <int NV>
@@ -221,11 +184,6 @@ __global__ void __launch_bounds__(WARPS * 32) softmax_kernel(const __nv_bfloat16
 
 inline int nv_for(int cols) { return (cols + 255) / 256; }
 inline int grid_for(int rows) { return (rows + ROWS_PER_CTA - 1) / ROWS_PER_CTA; }
-inline int norm_grid(int rows) {
-  const int cap = NORM_CTAS_PER_SM * device_sm_count();
-  const int g = grid_for(rows);
-  return g < cap ? g : cap;
-}
 
 #define PF_NV_DISPATCH(NVVAL, ...)                                         \
   switch (NVVAL) {                                                         \
@@ -254,15 +212,15 @@ struct NormOp final : PreparedOp {
   __nv_bfloat16* y = nullptr;
   int rows = 0, cols = 0;
   float eps = 0.f;
-  uint32_t units() const override { return (uint32_t)norm_grid(rows); }
+  uint32_t units() const override { return (uint32_t)grid_for(rows); }
   bool resumable() const override { return false; }
   int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
     if (rms) {
-      PF_NV_DISPATCH(nv_for(cols), PF_CUDA(launch_pdl(norm_kernel<NV, true>, dim3(norm_grid(rows)),
+      PF_NV_DISPATCH(nv_for(cols), PF_CUDA(launch_pdl(norm_kernel<NV, true>, dim3(grid_for(rows)),
                                                       dim3(WARPS * 32), 0, s, x, r, g, nullptr, y,
                                                       rows, cols, eps, make_ctl(ctl))));
     } else {
-      PF_NV_DISPATCH(nv_for(cols), PF_CUDA(launch_pdl(norm_kernel<NV, false>, dim3(norm_grid(rows)),
+      PF_NV_DISPATCH(nv_for(cols), PF_CUDA(launch_pdl(norm_kernel<NV, false>, dim3(grid_for(rows)),
                                                       dim3(WARPS * 32), 0, s, x, r, g, b, y, rows,
                                                       cols, eps, make_ctl(ctl))));
     }
@@ -371,14 +329,12 @@ int make_embedding_op(OpPtr* out, const int32_t* ids, const int32_t* tt, const v
 
 extern "C" int pf_norm_units(int rows, int cols, uint32_t* out) {
   if (!out || rows <= 0 || cols <= 0) return pf::set_error(PF_ERR_INVALID, "pf_norm_units");
-  *out = (uint32_t)pf::norm::norm_grid(rows);
+  *out = (uint32_t)pf::norm::grid_for(rows);
   return PF_OK;
 }
 
 extern "C" int pf_softmax_units(int rows, int cols, uint32_t* out) {
-  if (!out || rows <= 0 || cols <= 0) return pf::set_error(PF_ERR_INVALID, "pf_softmax_units");
-  *out = (uint32_t)pf::norm::grid_for(rows);
-  return PF_OK;
+  return pf_norm_units(rows, cols, out);
 }
 
 extern "C" int pf_layernorm(const void* X, const void* residual, const void* gamma,

@@ -40,6 +40,10 @@ def _bf16(*shape, scale=1.0, gen=None):
         (200, 264, 136, True, True, True),      # ragged M/N/K tails
         (65536, 64, 152, True, False, False),   # short K, ~4 tiles per CTA: epilogue staging reuse
         (1, 8, 8, False, False, False),
+        (16384, 1024, 1024, True, False, True),  # 512 tiles: last wave of 68 run as 136 half tiles
+        (16384, 1024, 4096, True, False, True),  # BERT-large FFN2 (tail halves, long K)
+        (16384, 3072, 1024, True, False, False),  # QKV: 1536 tiles, 56-tile tail
+        (19200, 1024, 256, True, True, False),   # ragged: 150 x 4 tiles, tail of 12 with GELU
     ],
 )
 def test_gemm(K, m, n, k, bias, gelu, res):
@@ -192,3 +196,32 @@ def test_layernorm_preemption_protocol(K):
     torch.cuda.synchronize()
     assert abort.item() == 0 and cursor.item() == K.norm_units(rows, cols)
     assert torch.equal(out, K.layernorm(x, gamma, beta, 1e-12))
+
+
+def test_gemm_tail_halves_resume_exact(K):
+    """A GEMM whose last wave runs as half tiles: a launch resumed from a claimed prefix
+    (cursor preset, as the executor resumes a yielded node) writes exactly the reference's
+    values for the units it runs, and a full launch equals an uninterrupted one bit for bit."""
+    m, n, k = 16384, 1024, 1024
+    g = torch.Generator().manual_seed(21)
+    x = _bf16(m, k, gen=g).cuda()
+    w = _bf16(n, k, scale=k ** -0.5, gen=g).cuda()
+    b = _bf16(n, gen=g).cuda()
+    units = K.gemm_units(m, n, k)
+    assert units > (m // 128) * (n // 256), "expected the half-tile tail for this shape"
+    ref = K.linear(x, w, b)
+    words = torch.zeros(8, dtype=torch.int32, device="cuda")
+    flag, abort, cursor = (words[i:i + 1] for i in range(3))
+    ctl = K.KernelCtl(flag.data_ptr(), abort.data_ptr(), cursor.data_ptr())
+    y = torch.zeros(m, n, dtype=torch.bfloat16, device="cuda")
+    for start in (units - 150, units - 7, 0):  # inside the full tiles, inside the halves, whole
+        y.zero_()
+        words.zero_()
+        flag.fill_(1)
+        cursor.fill_(start)
+        K.linear(x, w, b, out=y, ctl=ctl)  # runs units [start, units)
+        torch.cuda.synchronize()
+        assert abort.item() == 0 and cursor.item() >= units
+        mask = y != 0
+        assert mask.any() and torch.equal(y[mask], ref[mask])
+    assert torch.equal(y, ref)
