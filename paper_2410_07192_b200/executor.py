@@ -48,7 +48,7 @@ MAX_NODES = 4096
 # graphs: for profilers that do not see kernels inside conditional graph nodes (ncu)
 _USE_GRAPHS = __import__("os").environ.get("PF_EXEC_GRAPHS", "1") != "0"
 # modules per gated graph segment (gate kernel + conditional IF node); see DESIGN.md §3
-_SEG_MODULES = int(__import__("os").environ.get("PF_SEG_MODULES", "2"))
+_SEG_MODULES = int(__import__("os").environ.get("PF_SEG_MODULES", "4"))
 DESC_WORDS = 4  # PF_DESC_WORDS: (input, result, aux input, -) byte offsets per batch
 
 

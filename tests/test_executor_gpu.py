@@ -185,8 +185,8 @@ def test_doubling_probe_matches_measured_bubbles(pf):
     """The paper's doubling-wait probe brackets the direct flag-stamp
     measurement: waiting inside a bubble never slows the main job, so the probe is never
     below the measured bubble; with artificial neighbours (fixed arrival times) later idle
-    gaps absorb part of a longer wait, so it is at most the bubble plus the stage's other
-    idle time in the window."""
+    gaps -- also the next iteration's -- absorb part of a longer wait, so it is only bounded
+    by the iteration period."""
     from paper_2410_07192_b200.engine import (GPT2_SMALL_STAGE, GPTStage, StageEngine, characterize_stage,
                                               measure_stage_times, probe_bubbles)
 
@@ -196,9 +196,8 @@ def test_doubling_probe_matches_measured_bubbles(pf):
     eng = StageEngine(cfg, 1, model, None)
     _, rep = characterize_stage(eng, iterations=2)
     probe = probe_bubbles(eng, start_ms=0.25, tol_ms=0.2, refine=6)
-    idle = rep["measured_period_us"] - int(round((tf + tb) * 1000)) * cfg.num_microbatches
     for got, want in zip(probe["probed_us"], rep["measured_bubbles_us"]):
         if want == 0:
             continue
-        # lower bound: the bisection resolution; upper bound: all idle time of the window
-        assert 0.9 * want - 400 <= got <= want + max(idle, 0) + 0.1 * want + 400, (probe, rep, idle)
+        # lower bound up to the bisection resolution; upper bound: one period
+        assert 0.9 * want - 400 <= got <= rep["measured_period_us"], (probe, rep)
