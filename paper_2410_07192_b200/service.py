@@ -92,6 +92,7 @@ class ServiceReport:
     samples_completed: int = 0
     scalars_extra: dict = field(default_factory=dict)
     gpus: int = 1  # pipeline stages served (one worker each)
+    stage_iterations: int = 0  # stage iterations actually run (a stage with nothing to fill is skipped)
 
     def scalars(self) -> dict:
         done = sorted(self.per_job.values(), key=lambda r: r.job_id)
@@ -119,7 +120,7 @@ class ServiceReport:
         # the reference's SimReport.scalars keys (sim.py:139-153), from measured quantities:
         # bubble_ratio = measured bubble time / stage time, wall-clock TFLOP/s over all GPUs,
         # GPU-hours = measured busy time (sim.py:119-120), gpus_saved (sim.py:156-159)
-        stage_ns = self.rounds * self.period_s * 1e9 * max(1, self.gpus)
+        stage_ns = (self.stage_iterations or self.rounds * max(1, self.gpus)) * self.period_s * 1e9
         ratio = self.bubble_ns / stage_ns if stage_ns > 0 else 0.0
         out.update({
             "bubble_ratio": ratio,
@@ -184,7 +185,7 @@ class FillService:
         rejected: list[str] = []
         inflight: list = [None] * len(self.coordinators)
         bubble_ns = fill_ns = 0
-        rounds = 0
+        rounds = stage_iters = 0
         from .metrics import busy_in_bubbles
 
         for r in range(max_rounds):
@@ -221,6 +222,7 @@ class FillService:
                 if inflight[s] is None:
                     continue  # nothing to fill: the stage's iteration is not needed
                 n0 = len(ex.records)
+                stage_iters += 1
                 t = self.run_iteration(s, ex)
                 ex.settle()
                 recs = {rec.tag: rec for rec in ex.records[n0:]}
@@ -251,7 +253,7 @@ class FillService:
         unfinished = [j.id for j in jobs if j.id not in completion and j.id not in rejected]
         samples = sum(r.samples for r in per_job.values())
         return ServiceReport(per_job, rejected, unfinished, rounds, self.period_s, bubble_ns, fill_ns, samples,
-                             gpus=len(self.coordinators))
+                             gpus=len(self.coordinators), stage_iterations=stage_iters)
 
 
 def predict(config: ServiceConfig, jobs: Sequence[JobSpec],
