@@ -1047,18 +1047,23 @@ struct GemmPairOp final : PreparedOp {
 };
 
 // Variant choice: 0 = single-CTA (BN from pick_bn), 1 = CTA pair BN=256, 2 = CTA pair BN=128.
-// The pair kernel is opt-in (PF_GEMM_PAIR=1): with the TMA-store epilogue the single-CTA
-// kernel is faster on the fill job's K = 1024 GEMMs; the pair kernel wins only at K >= 3072
-// (profiles/r01_gemm_variants.txt).
-static int pick_variant(int M, int N) {
+// Default (PF_GEMM_PAIR unset): the CTA pair with BN 256 for long-K or wide-N GEMMs with at
+// least two waves of pair tiles -- in situ at BERT-large batch 128 it wins on FFN1 (N 4096,
+// bias+GELU: 119 -> 110-114 us) and FFN2 (K 4096: 110 -> 105 us) and loses on QKV (N 3072, tie)
+// and the out-projection (N 1024, K 1024: the single-CTA kernel's half-tile tail wave wins);
+// BN 128 pairs are never chosen by default (their MMA loop runs at ~1/3 of the ideal rate).
+// PF_GEMM_PAIR=0 never pairs, =1 pairs with the round-1 wave-cost choice, =2 always BN 256.
+static int pick_variant(int M, int N, int K) {
   static int mode = -1;
   if (mode < 0) {
     const char* e = getenv("PF_GEMM_PAIR");
-    mode = (e && e[0] == '1') ? 1 : 0;
+    mode = !e ? 3 : e[0] == '1' ? 1 : e[0] == '2' ? 2 : 0;
   }
   if (mode == 0 || M < 2 * BM) return 0;
+  if (mode == 2) return 1;
   const long pairs = device_sm_count() / 2;
   const long t256 = (long)((M + 255) / 256) * ((N + 255) / 256);
+  if (mode == 3) return (K >= 2048 || N >= 4096) && N >= 512 && t256 >= 2 * pairs ? 1 : 0;
   const long t128 = (long)((M + 255) / 256) * ((N + 127) / 128);
   const long c256 = ((t256 + pairs - 1) / pairs) * 256;
   const long c128 = ((t128 + pairs - 1) / pairs) * 128;
@@ -1180,7 +1185,7 @@ int make_gemm_op(OpPtr* out, const void* X, const void* W, const void* bias, con
   if (((uintptr_t)X | (uintptr_t)W | (uintptr_t)Y | (uintptr_t)bias | (uintptr_t)residual) & 15u)
     return set_error(PF_ERR_INVALID, "pf_gemm: pointers must be 16-B aligned");
   if (!device_is_sm100()) return set_error(PF_ERR_UNSUPPORTED, "pf_gemm: needs an sm_100 device");
-  const int variant = gemm::pick_variant(M, N);
+  const int variant = gemm::pick_variant(M, N, K);
   if (variant == 1 || variant == 2) {
     if (variant == 1) {
       auto op = std::make_unique<gemm::GemmPairOp<256>>();
@@ -1339,7 +1344,7 @@ extern "C" int pf_gemm_diag(unsigned long long* out8, int reset) {
 extern "C" int pf_gemm_units(int M, int N, int K, uint32_t* out_units) {
   using namespace pf;
   if (!out_units || M <= 0 || N <= 0 || K <= 0) return set_error(PF_ERR_INVALID, "pf_gemm_units");
-  const int variant = gemm::pick_variant(M, N);
+  const int variant = gemm::pick_variant(M, N, K);
   if (variant) {
     const int bnp = variant == 1 ? 256 : 128;
     *out_units = (uint32_t)(((M + 2 * gemm::BM - 1) / (2 * gemm::BM)) * ((N + bnp - 1) / bnp));

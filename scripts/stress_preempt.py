@@ -29,6 +29,8 @@ x = torch.randn(16384, 1024, device="cuda").bfloat16()
 w = (torch.randn(1024, 1024, device="cuda") * 0.03).bfloat16()
 b = torch.randn(1024, device="cuda").bfloat16()
 r = torch.randn(16384, 1024, device="cuda").bfloat16()
+r4 = torch.randn(16384, 4096, device="cuda").bfloat16()
+w4 = (torch.randn(1024, 4096, device="cuda") * 0.015).bfloat16()
 g1 = torch.ones(1024, device="cuda").bfloat16()
 b0 = torch.zeros(1024, device="cuda").bfloat16()
 cases = {
@@ -36,11 +38,13 @@ cases = {
                   torch.empty(128, 128, 1024, device="cuda").bfloat16(), False),
     "gemm_tail": (lambda out, c: K.linear(x, w, b, residual=r, out=out, ctl=c, stream=work),
                   torch.empty(16384, 1024, device="cuda").bfloat16(), True),
+    "gemm_pair": (lambda out, c: K.linear(r4, w4, b, residual=x, out=out, ctl=c, stream=work),
+                  torch.empty(16384, 1024, device="cuda").bfloat16(), True),
     "layernorm": (lambda out, c: K.layernorm(x, g1, b0, 1e-12, residual=r, out=out, ctl=c, stream=work),
                   torch.empty(16384, 1024, device="cuda").bfloat16(), False),
 }
 units_of = {"attention": K.attention_units(128, 128, 16, 64), "gemm_tail": K.gemm_units(16384, 1024, 1024),
-            "layernorm": K.norm_units(16384, 1024)}
+            "layernorm": K.norm_units(16384, 1024), "gemm_pair": K.gemm_units(16384, 1024, 4096)}
 for name, (fn, out, resumable) in cases.items():
     ref = out.clone()
     with torch.cuda.stream(work):

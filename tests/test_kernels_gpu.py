@@ -198,23 +198,28 @@ def test_layernorm_preemption_protocol(K):
     assert torch.equal(out, K.layernorm(x, gamma, beta, 1e-12))
 
 
-def test_gemm_tail_halves_resume_exact(K):
-    """A GEMM whose last wave runs as half tiles: a launch resumed from a claimed prefix
-    (cursor preset, as the executor resumes a yielded node) writes exactly the reference's
+@pytest.mark.parametrize("m,n,k,variant", [(16384, 1024, 1024, "tail"), (16384, 1024, 4096, "pair"),
+                                           (16384, 4096, 1024, "pair")])
+def test_gemm_tail_halves_resume_exact(K, m, n, k, variant):
+    """Resume from a claimed prefix (cursor preset, as the executor resumes a yielded node):
+    for the single-CTA kernel whose last wave runs as half tiles and for the CTA-pair kernel
+    (the default for long-K / wide-N GEMMs) the resumed launch writes exactly the reference's
     values for the units it runs, and a full launch equals an uninterrupted one bit for bit."""
-    m, n, k = 16384, 1024, 1024
     g = torch.Generator().manual_seed(21)
     x = _bf16(m, k, gen=g).cuda()
     w = _bf16(n, k, scale=k ** -0.5, gen=g).cuda()
     b = _bf16(n, gen=g).cuda()
     units = K.gemm_units(m, n, k)
-    assert units > (m // 128) * (n // 256), "expected the half-tile tail for this shape"
+    if variant == "tail":
+        assert units > (m // 128) * (n // 256), "expected the half-tile tail for this shape"
+    else:
+        assert units == (m // 256) * (n // 256), "expected 256 x 256 CTA-pair tiles for this shape"
     ref = K.linear(x, w, b)
     words = torch.zeros(8, dtype=torch.int32, device="cuda")
     flag, abort, cursor = (words[i:i + 1] for i in range(3))
     ctl = K.KernelCtl(flag.data_ptr(), abort.data_ptr(), cursor.data_ptr())
     y = torch.zeros(m, n, dtype=torch.bfloat16, device="cuda")
-    for start in (units - 150, units - 7, 0):  # inside the full tiles, inside the halves, whole
+    for start in (units - 150, units - 7, 0):  # early, in the last wave, whole
         y.zero_()
         words.zero_()
         flag.fill_(1)
