@@ -642,7 +642,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
 
-  const int num_tiles = p.tiles_m * p.tiles_n;
+  const int num_tiles = p.tail_halves ? 2 * p.tiles_m * p.tiles_n - p.n_full : p.tiles_m * p.tiles_n;
   const int num_kb = (p.K + BK - 1) / BK;
 
   if (warp == PRODUCER_WARP) {
@@ -675,8 +675,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         sphase ^= 1u;
       }
       if (tile < 0) break;
-      int tm, tn, ks;
-      tile_coords(tile, p, tm, tn, ks);
+      int tm, tn, ks, half;
+      unit_info(tile, p, tm, tn, ks, half);
+      // W rows of this CTA (64-row TMA boxes): a full tile takes rows [rank*BN/2, +BN/2) of
+      // the BN-wide tile; a half tile h (N = BN/2 over the pair) takes [h*BN/2 + rank*BN/4, +BN/4)
+      const int brow = half < 0 ? tn * BN + (int)rank * (BN / 2) : tn * BN + half * (BN / 2) + (int)rank * (BN / 4);
+      const uint32_t tx = half < 0 ? 2 * C::STAGE_BYTES : 2 * (C::A_BYTES + C::B_BYTES / 2);
       for (int kb = 0; kb < num_kb; ++kb) {
         {
           DIAG_T0();
@@ -685,9 +689,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
         if (lane == 0) {
           const uint32_t fb = mapa_shared(smem_u32(&full_bar[stage]), 0);
-          if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * C::STAGE_BYTES);
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], tx);
           tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, fb, kb * BK, tm * PM + (int)rank * BM);
-          tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, fb, kb * BK, tn * BN + (int)rank * (BN / 2));
+          tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, fb, kb * BK, brow);
+          if (half < 0)
+            tma_load_2d_pair(sB + stage * C::B_BYTES + (BN / 4) * 128, &tmB, fb, kb * BK, brow + BN / 4);
         }
         __syncwarp();
         if (++stage == C::STAGES) {
@@ -704,6 +710,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const unsigned long long _g0 = globaltimer_ns();
 #endif
       constexpr uint32_t idesc = umma_idesc_bf16(PM, BN, false, false);
+      constexpr uint32_t idesc_half = umma_idesc_bf16(PM, BN / 2, false, false);
       int slot = 0;
       uint32_t sphase = 0;
       int stage = 0;
@@ -730,6 +737,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const long long _tm0 = clock64();
 #endif
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        int utm, utn, uks, uhalf;
+        unit_info(tile, p, utm, utn, uks, uhalf);
+        const uint32_t idesc_u = uhalf < 0 ? idesc : idesc_half;
         for (int kb = 0; kb < num_kb; ++kb) {
           {
             DIAG_T0();
@@ -744,7 +754,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             for (int k = 0; k < BK / UMMA_K; ++k) {
               const uint64_t ad = umma_desc_sw128_kmajor(a_addr + k * UMMA_K * 2);
               const uint64_t bd = umma_desc_sw128_kmajor(b_addr + k * UMMA_K * 2);
-              umma_bf16_ss_pair(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+              umma_bf16_ss_pair(d_tmem, ad, bd, idesc_u, (kb | k) != 0 ? 1u : 0u);
             }
             umma_commit_pair(&empty_bar[stage]);  // frees this stage in BOTH CTAs
           }
@@ -798,14 +808,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         sphase ^= 1u;
       }
       if (tile < 0) break;
-      int tm, tn, ks;
-      tile_coords(tile, p, tm, tn, ks);
+      int tm, tn, ks, half;
+      unit_info(tile, p, tm, tn, ks, half);
       const int row_base = tm * PM + (int)rank * BM + lane_grp * 32;
-      const int col_base = tn * BN + col_half * C::COLS_PER_EPI_WARP;
-      const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) +
-                             (uint32_t)(acc * BN + col_half * C::COLS_PER_EPI_WARP);
-      epilogue_tile<C::CHUNKS, EPI, true>(p, &tmY, my_stg, taddr, &tfull_bar[acc], aphase, row_base,
-                                          col_base, my_bias, 0);
+      if (half < 0) {
+        const int col_base = tn * BN + col_half * C::COLS_PER_EPI_WARP;
+        const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) +
+                               (uint32_t)(acc * BN + col_half * C::COLS_PER_EPI_WARP);
+        epilogue_tile<C::CHUNKS, EPI, true>(p, &tmY, my_stg, taddr, &tfull_bar[acc], aphase, row_base,
+                                            col_base, my_bias, 0);
+      } else if constexpr (C::CHUNKS % 2 == 0) {
+        constexpr int HC = C::COLS_PER_EPI_WARP / 2;
+        const int col_base = tn * BN + half * (BN / 2) + col_half * HC;
+        const uint32_t taddr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(acc * BN + col_half * HC);
+        epilogue_tile<C::CHUNKS / 2, EPI, true>(p, &tmY, my_stg, taddr, &tfull_bar[acc], aphase, row_base,
+                                                col_base, my_bias, 0);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader0 + (uint32_t)(acc * 8));
@@ -930,6 +948,16 @@ static int tail_n_full(int tiles, int bn) {
   return (rem > 0 && 2 * rem <= sms) ? tiles - rem : tiles;
 }
 
+// The same for CTA-pair tiles (grid = SM pairs); BN 256 only (half = 128 columns over the pair).
+static int tail_n_full_pairs(int tiles, int bn) {
+  const int pairs = device_sm_count() / 2;
+  if (bn != 256 || tiles <= pairs) return tiles;
+  const char* e = getenv("PF_GEMM_TAIL");
+  if (e && e[0] == '0') return tiles;
+  const int rem = tiles % pairs;
+  return (rem > 0 && 2 * rem <= pairs) ? tiles - rem : tiles;
+}
+
 // BN choice: minimise waves x per-tile time on 148 SMs.
 static int pick_bn(int M, int N) {
   static int forced = -1;  // PF_GEMM_BN=128|192|256 pins the tile width (experiments)
@@ -1002,7 +1030,7 @@ struct GemmPairOp final : PreparedOp {
   int prepare(const void* X, const void* W, const void* bias, const void* residual, void* Y, int M,
               int N, int K, uint32_t e) {
     PF_TRY(make_tmap(&ta, X, M, K, BM));
-    PF_TRY(make_tmap(&tb, W, N, K, BN / 2));
+    PF_TRY(make_tmap(&tb, W, N, K, BN / 4));  // 64-row boxes: 2 per full tile, 1 per half tile
     PF_TRY(make_tmap_store(&ty, Y, M, N));
     p.Y = reinterpret_cast<__nv_bfloat16*>(Y);
     p.bias = reinterpret_cast<const __nv_bfloat16*>(bias);
@@ -1018,12 +1046,12 @@ struct GemmPairOp final : PreparedOp {
     const int tiles = p.tiles_m * p.tiles_n;
     const int pairs = device_sm_count() / 2;
     grid = 2 * (tiles < pairs ? tiles : pairs);
-    p.n_full = tiles;
-    p.tail_halves = 0;
+    p.n_full = tail_n_full_pairs(tiles, BN);
+    p.tail_halves = p.n_full < tiles ? 1 : 0;
     epi = e & 15u;
     return PF_OK;
   }
-  uint32_t units() const override { return (uint32_t)(p.tiles_m * p.tiles_n); }
+  uint32_t units() const override { return (uint32_t)(2 * p.tiles_m * p.tiles_n - p.n_full); }
   bool resumable() const override { return true; }
   int run(const pf_ctl_t* ctl, cudaStream_t stream, const LaunchArgs& a) override {
     Params p = this->p;
@@ -1347,7 +1375,8 @@ extern "C" int pf_gemm_units(int M, int N, int K, uint32_t* out_units) {
   const int variant = gemm::pick_variant(M, N, K);
   if (variant) {
     const int bnp = variant == 1 ? 256 : 128;
-    *out_units = (uint32_t)(((M + 2 * gemm::BM - 1) / (2 * gemm::BM)) * ((N + bnp - 1) / bnp));
+    const int tiles = ((M + 2 * gemm::BM - 1) / (2 * gemm::BM)) * ((N + bnp - 1) / bnp);
+    *out_units = (uint32_t)(2 * tiles - gemm::tail_n_full_pairs(tiles, bnp));
     return PF_OK;
   }
   const int bn = gemm::pick_bn(M, N);
