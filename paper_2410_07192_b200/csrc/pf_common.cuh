@@ -182,8 +182,7 @@ __device__ __forceinline__ float2 unpack_bf16x2(uint32_t u) {
 // device: atomic work units (HBM-bound kernels: gate on entry, count on exit)
 
 // Entry gate for atomic-unit kernels; returns false when the CTA must skip.
-__device__ __forceinline__ bool atomic_unit_enter(const Ctl& c) {
-  pdl_enter();
+__device__ __forceinline__ bool atomic_unit_check(const Ctl& c) {
   __shared__ int s_go;
   if (threadIdx.x == 0) {
     int go = 1;
@@ -196,6 +195,14 @@ __device__ __forceinline__ bool atomic_unit_enter(const Ctl& c) {
   }
   __syncthreads();
   return s_go != 0;
+}
+
+// Entry gate of an atomic-unit kernel (PDL wait first: the gate reads words the previous
+// kernel may write). A kernel can instead call pdl_enter(), start its loads, and then
+// atomic_unit_check() so the gate's flag read overlaps them.
+__device__ __forceinline__ bool atomic_unit_enter(const Ctl& c) {
+  pdl_enter();
+  return atomic_unit_check(c);
 }
 
 __device__ __forceinline__ void atomic_unit_exit(const Ctl& c) {

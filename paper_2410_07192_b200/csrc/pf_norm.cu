@@ -65,25 +65,40 @@ __global__ void __launch_bounds__(WARPS * 32) norm_kernel(const __nv_bfloat16* _
                                                           const __nv_bfloat16* __restrict__ beta,
                                                           __nv_bfloat16* __restrict__ Y, int rows,
                                                           int cols, float eps, Ctl ctl) {
-  if (!atomic_unit_enter(ctl)) return;
+  static_assert(ROWS_PER_WARP == 1, "one row per warp");
+  pdl_enter();
   const int lane = lane_id();
-  const int row0 = blockIdx.x * ROWS_PER_CTA + warp_id() * ROWS_PER_WARP;
-#pragma unroll
-  for (int rr = 0; rr < ROWS_PER_WARP; ++rr) {
-    const int row = row0 + rr;
-    if (row >= rows) break;
-    float x[NV][8];
-    const size_t off = (size_t)row * cols;
+  const int row = blockIdx.x * ROWS_PER_CTA + warp_id();
+  const size_t off = (size_t)row * cols;
+  // the row's loads are issued before the entry gate resolves, so the gate's flag read
+  // overlaps them (a row loaded for a CTA that then skips is simply dropped)
+  uint4 xa[NV], ra[NV];
+  if (row < rows) {
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const int c = (j * 32 + lane) * 8;
       if (c < cols) {
-        load8(X + off + c, x[j]);
-        if (R) {
-          float r[8];
-          load8(R + off + c, r);
+        xa[j] = __ldg(reinterpret_cast<const uint4*>(X + off + c));
+        if (R) ra[j] = __ldg(reinterpret_cast<const uint4*>(R + off + c));
+      }
+    }
+  }
+  if (!atomic_unit_check(ctl)) return;
+  if (row < rows) {
+    float x[NV][8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) x[j][e] += r[e];
+    for (int j = 0; j < NV; ++j) {
+      const uint32_t w[4] = {xa[j].x, xa[j].y, xa[j].z, xa[j].w};
+      const uint32_t v[4] = {ra[j].x, ra[j].y, ra[j].z, ra[j].w};
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const float2 f = unpack_bf16x2(w[h]);
+        x[j][2 * h] = f.x;
+        x[j][2 * h + 1] = f.y;
+        if (R) {
+          const float2 g = unpack_bf16x2(v[h]);
+          x[j][2 * h] += g.x;
+          x[j][2 * h + 1] += g.y;
         }
       }
     }
