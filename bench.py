@@ -558,8 +558,16 @@ def main() -> None:
     ap.add_argument("--debug", action="store_true", help="per-bubble details to stderr")
     ap.add_argument("--fill-fraction", type=float, default=FILL_FRACTION,
                     help="share of each bubble the planner may fill (reference default 0.68)")
+    ap.add_argument("--max-batches", type=int, default=None,
+                    help="Coordinator max_batches_per_bubble (overrides the config's)")
+    ap.add_argument("--batch-sizes", default=None,
+                    help="comma-separated profiled fill batch sizes (overrides the config's)")
     args = ap.parse_args()
-    conf = CONFIGS[args.config]
+    conf = dict(CONFIGS[args.config])
+    if args.max_batches is not None:
+        conf["max_batches"] = args.max_batches
+    if args.batch_sizes:
+        conf["batch_sizes"] = tuple(int(b) for b in args.batch_sizes.split(","))
     args.fill = args.fill or conf["fill"]
     args.main = args.main or conf["main"]
     if args.impl == "reference":

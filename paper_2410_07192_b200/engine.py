@@ -235,7 +235,13 @@ class StageEngine:
                      for _ in range(config.num_microbatches)]
         self.main.wait_stream(torch.cuda.current_stream())  # inputs were made on the default stream
         self.last_stage = stage_id == config.num_stages - 1
-        self.timeline = program_timeline(config, stage_id)
+        # one steady-state window runs from the stage's first compute instruction to the
+        # next iteration's: the idle head before the first F (s * t_fwd) is the tail of the
+        # previous fill-drain BUBBLE, which program_timeline already spans into the next
+        # window, so it is not idled a second time at the start of this one
+        tl = program_timeline(config, stage_id)
+        head = min(s for ins, s, _ in tl if ins.op != "BUBBLE")
+        self.timeline = [(ins, s - head, e - head) for ins, s, e in tl]
         self.records: list[IterationRecord] = []
         self.outputs: list[torch.Tensor] = []
         self.launches = 0  # our kernels (timer / stamp / flag) enqueued by the engine
