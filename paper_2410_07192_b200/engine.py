@@ -39,7 +39,7 @@ from torch import nn
 
 from . import native
 from .executor import BubbleSlot, Executor
-from .schedule import BubbleKind, Instr, PipelineConfig, program_timeline, stage_program
+from .schedule import BubbleKind, Instr, PipelineConfig, stage_program, steady_state_timeline
 
 US = 1000  # ns per us
 
@@ -235,13 +235,9 @@ class StageEngine:
                      for _ in range(config.num_microbatches)]
         self.main.wait_stream(torch.cuda.current_stream())  # inputs were made on the default stream
         self.last_stage = stage_id == config.num_stages - 1
-        # one steady-state window runs from the stage's first compute instruction to the
-        # next iteration's: the idle head before the first F (s * t_fwd) is the tail of the
-        # previous fill-drain BUBBLE, which program_timeline already spans into the next
-        # window, so it is not idled a second time at the start of this one
-        tl = program_timeline(config, stage_id)
-        head = min(s for ins, s, _ in tl if ins.op != "BUBBLE")
-        self.timeline = [(ins, s - head, e - head) for ins, s, e in tl]
+        # one period from the first compute instruction (the idle head is the previous
+        # fill-drain BUBBLE's tail)
+        self.timeline = steady_state_timeline(config, stage_id)
         self.records: list[IterationRecord] = []
         self.outputs: list[torch.Tensor] = []
         self.launches = 0  # our kernels (timer / stamp / flag) enqueued by the engine

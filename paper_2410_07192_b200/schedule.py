@@ -363,3 +363,15 @@ def program_timeline(config: PipelineConfig, stage_id: int) -> list[tuple[Instr,
             out.append((ins, s, e))
             k += 1
     return out
+
+
+def steady_state_timeline(config: PipelineConfig, stage_id: int) -> list[tuple[Instr, int, int]]:
+    """program_timeline re-based to the stage's steady-state window: the window opens
+    at the stage's first compute instruction and closes at the next iteration's, so it
+    is exactly one period long. The idle head before the first F (s * t_fwd under
+    1F1B/GPipe) is the tail of the previous iteration's fill-drain BUBBLE, which
+    program_timeline already spans into the next window; re-basing keeps it from being
+    idled a second time at the start of every emulated iteration (engine.StageEngine)."""
+    tl = program_timeline(config, stage_id)
+    head = min(s for ins, s, _ in tl if ins.op != "BUBBLE")
+    return [(ins, s - head, e - head) for ins, s, e in tl]

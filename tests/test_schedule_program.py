@@ -12,6 +12,7 @@ from paper_2410_07192_b200.schedule import (
     cycle_from_measurements,
     program_timeline,
     stage_program,
+    steady_state_timeline,
     timeline_bubble_spans,
 )
 
@@ -67,6 +68,21 @@ def test_busy_plus_idle_is_period():
             busy = sum(e - b for i, b, e in tl if i.op != "BUBBLE")
             cyc = build_bubble_cycle(c, s)
             assert busy + cyc.total_idle_us == c.period_us
+
+
+def test_steady_state_window_is_one_period():
+    """The emulated engine's window: first compute at 0, the fill-drain BUBBLE closes at
+    exactly one period, bubble durations and instruction order unchanged."""
+    for c in cfgs():
+        for s in range(c.num_stages):
+            tl, ss = program_timeline(c, s), steady_state_timeline(c, s)
+            assert [i for i, _, _ in tl] == [i for i, _, _ in ss]
+            assert [e - b for _, b, e in tl] == [e - b for _, b, e in ss]
+            assert min(b for i, b, _ in ss if i.op != "BUBBLE") == 0
+            assert max(e for _, _, e in ss) <= c.period_us
+            for i, b, e in ss:
+                if i.op == "BUBBLE" and i.kind is BubbleKind.FILL_DRAIN:
+                    assert e == c.period_us
 
 
 def test_cycle_from_measurements_uses_reference_usable_rule():
