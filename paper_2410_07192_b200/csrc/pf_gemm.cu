@@ -78,6 +78,7 @@ struct Params {
   // full wave instead of a whole one (see pick_bn's cost model).
   int n_full;
   int tail_halves;
+  int group_m;  // m-blocks per rasterisation group (GROUP_M unless PF_GEMM_GROUP_M is set)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -86,11 +87,14 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 
-// Grouped rasterisation: tiles walk GROUP_M m-blocks x all n-blocks, n fastest, so the
-// CTAs in flight share a band of A rows (read from DRAM once) and all of W (the small,
-// L2-resident operand). m-fastest order re-streamed A once per n-block whenever A
-// exceeded L2 (FFN2 at batch 128: A = 134 MB, read 8x).
-constexpr int GROUP_M = 16;
+// Grouped rasterisation: tiles walk GROUP_M m-blocks x all n-blocks, m fastest inside a
+// group, so the tiles of one m-block (all n-blocks) are GROUP_M units apart and start in
+// the same wave: each A row band is read from DRAM once while W (the small operand at the
+// fill shapes, <= 8 MB) stays L2-resident. A tall group spreads an m-block's tiles over
+// waves and the A band is re-read after eviction: in situ at BERT-large batch 128
+// (scripts/bert_batch_profile.py, PF_GEMM_GROUP_M sweep) FFN2 (K = 4096) takes 98 us at
+// GROUP_M 1-2, 100-101 us at 16 and 114 us at 64.
+constexpr int GROUP_M = 2;
 
 #ifdef PF_GEMM_DIAG
 // [0] MMA wait on full (data), [1] MMA wait on tempty (epilogue), [2] producer wait on empty,
@@ -114,10 +118,10 @@ __device__ __forceinline__ void tile_coords(int tile, const Params& p, int& tm, 
   const int per_split = p.tiles_m * p.tiles_n;
   ks = tile / per_split;
   tile -= ks * per_split;
-  const int per_group = GROUP_M * p.tiles_n;
+  const int per_group = p.group_m * p.tiles_n;
   const int g = tile / per_group;
-  const int first_m = g * GROUP_M;
-  const int rows = min(p.tiles_m - first_m, GROUP_M);
+  const int first_m = g * p.group_m;
+  const int rows = min(p.tiles_m - first_m, p.group_m);
   const int r = tile - g * per_group;
   tm = first_m + r % rows;
   tn = r / rows;
@@ -958,6 +962,16 @@ static int tail_n_full_pairs(int tiles, int bn) {
   return (rem > 0 && 2 * rem <= pairs) ? tiles - rem : tiles;
 }
 
+// Rasterisation group height; PF_GEMM_GROUP_M=<n> overrides GROUP_M (experiments).
+static int group_m() {
+  static int g = -1;
+  if (g < 0) {
+    const char* e = getenv("PF_GEMM_GROUP_M");
+    g = (e && atoi(e) > 0) ? atoi(e) : GROUP_M;
+  }
+  return g;
+}
+
 // BN choice: minimise waves x per-tile time on 148 SMs.
 static int pick_bn(int M, int N) {
   static int forced = -1;  // PF_GEMM_BN=128|192|256 pins the tile width (experiments)
@@ -1042,6 +1056,7 @@ struct GemmPairOp final : PreparedOp {
     p.tiles_n = (N + BN - 1) / BN;
     p.stamp = nullptr;
     p.k_splits = 1;
+    p.group_m = group_m();
     p.kb_per_split = (K + BK - 1) / BK;
     const int tiles = p.tiles_m * p.tiles_n;
     const int pairs = device_sm_count() / 2;
@@ -1144,6 +1159,7 @@ struct GemmOp final : PreparedOp {
     p.tiles_n = (N + BN - 1) / BN;
     p.stamp = nullptr;
     p.k_splits = 1;
+    p.group_m = group_m();
     p.kb_per_split = (K + BK - 1) / BK;
     const int tiles = p.tiles_m * p.tiles_n;
     const int sms = device_sm_count();
