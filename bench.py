@@ -558,6 +558,8 @@ def main() -> None:
     ap.add_argument("--debug", action="store_true", help="per-bubble details to stderr")
     ap.add_argument("--fill-fraction", type=float, default=FILL_FRACTION,
                     help="share of each bubble the planner may fill (reference default 0.68)")
+    ap.add_argument("--optimizer-offload", action="store_true",
+                    help="main job keeps its AdamW moments in pinned host memory between steps")
     ap.add_argument("--max-batches", type=int, default=None,
                     help="Coordinator max_batches_per_bubble (overrides the config's)")
     ap.add_argument("--batch-sizes", default=None,
@@ -616,6 +618,10 @@ def main() -> None:
     gcfg = GPT_8B_STAGE if args.main == "gpt8b" else GPT2_SMALL_STAGE
     main_model = GPTStage(gcfg, seed=rank)
     tf_ms, tb_ms = measure_stage_times(main_model)
+    if args.optimizer_offload and args.pipeline == "nccl":
+        raise SystemExit("--optimizer-offload is implemented for the emulated engine (StageEngine) only")
+    if args.optimizer_offload:  # AdamW moments in pinned host memory between steps
+        main_model.enable_optimizer_offload(h2d_gbs=measure_h2d_gbs())
 
     # ---- fill job: BERT with a B200-measured profile
     fcfg = BERT_LARGE if args.fill == "bert_large" else BERT_BASE
@@ -935,6 +941,9 @@ def main() -> None:
             "per_stage_iter_ms": {str(st): {"fill_off": statistics.mean(off.get(st, [0])) / 1e6,
                                             "fill_on": statistics.mean(v) / 1e6} for st, v in on_iter.items()},
             "bubble_characterization": characterization,
+            "optimizer_offload": None if main_model.offload is None else {
+                "state_bytes": main_model.offload.state_bytes, "lead_ms": main_model.offload.lead_us / 1e3,
+                "h2d_gbs": main_model.offload.h2d_gbs, "transfers": main_model.offload.transfers},
             "weight_staging": staging,
             "bubbles_preempted": sum(1 for r in recs if r.aborted),
             "bubbles_filled": len(recs),

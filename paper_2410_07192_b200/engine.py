@@ -100,6 +100,13 @@ class GPTStage(nn.Module):
         self.to(device=device, dtype=torch.bfloat16)
         self.opt = torch.optim.AdamW(self.parameters(), lr=1e-4, fused=True)
         self._saved: dict[int, tuple[torch.Tensor, torch.Tensor]] = {}
+        self.offload: Optional[OptimizerOffload] = None
+
+    def enable_optimizer_offload(self, h2d_gbs: float = 50.0) -> "OptimizerOffload":
+        """Keep AdamW's moment estimates in pinned host memory between optimizer steps
+        (PAPER.md:427): the bubbles before the step see that much more free HBM."""
+        self.offload = OptimizerOffload(self.opt, h2d_gbs)
+        return self.offload
 
     def forward_mb(self, mb: int, x: torch.Tensor) -> torch.Tensor:
         x = x.detach().requires_grad_(True)
@@ -120,8 +127,12 @@ class GPTStage(nn.Module):
         return x.grad
 
     def step(self) -> None:
+        if self.offload is not None:
+            self.offload.wait_resident(torch.cuda.current_stream())
         self.opt.step()
         self.opt.zero_grad(set_to_none=False)
+        if self.offload is not None:
+            self.offload.evict(torch.cuda.current_stream())
 
     def snapshot(self) -> dict:
         """Device copies of parameters and the full optimizer state (to replay iterations)."""
@@ -145,6 +156,98 @@ class GPTStage(nn.Module):
         self.opt.load_state_dict(copy.deepcopy(snap["opt"]))
         self.opt.zero_grad(set_to_none=False)
         torch.cuda.synchronize()
+
+
+class OptimizerOffload:
+    """Main-job optimizer-state offload.
+
+    Between optimizer steps AdamW's ``exp_avg`` / ``exp_avg_sq`` live in pinned host
+    memory. After each step they are copied out on a side stream and their device
+    blocks are released (``evict``). Before the next step they are copied back early
+    enough that the transfer hides behind the last backward passes (``prefetch``, issued by
+    ``StageEngine.run_iteration`` ``lead_us`` ahead of the step). The step waits for the
+    copy-back (``wait_resident``). Copies are exact, so the main job's parameters and
+    losses are bitwise those of a run without offload. The bubbles that fall between
+    eviction and prefetch have ``state_bytes`` more free HBM, which is what the fill job's
+    arena can be sized from."""
+
+    KEYS = ("exp_avg", "exp_avg_sq")
+
+    def __init__(self, opt: torch.optim.Optimizer, h2d_gbs: float = 50.0):
+        self.opt = opt
+        self.stream = torch.cuda.Stream()
+        self.host: dict[tuple[int, str], torch.Tensor] = {}
+        self.h2d_gbs = h2d_gbs
+        self._ready: Optional[torch.cuda.Event] = None
+        self.resident = True  # states on the device (before the first step they do not exist)
+        self.state_bytes = 0
+        self.transfers = 0
+
+    def _states(self):
+        for group in self.opt.param_groups:
+            for p in group["params"]:
+                st = self.opt.state.get(p)
+                if st:
+                    yield p, st
+
+    @property
+    def lead_us(self) -> int:
+        """How far ahead of the step the copy-back must start (1.25x its transfer time)."""
+        return int(1.25 * self.state_bytes / (self.h2d_gbs * 1e3))
+
+    def evict(self, main: torch.cuda.Stream) -> None:
+        ev = torch.cuda.Event()
+        ev.record(main)
+        self.stream.wait_event(ev)
+        nbytes = 0
+        with torch.cuda.stream(self.stream):
+            for p, st in self._states():
+                for k in self.KEYS:
+                    t = st.get(k)
+                    if t is None:
+                        continue
+                    h = self.host.get((id(p), k))
+                    if h is None:
+                        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+                        self.host[(id(p), k)] = h
+                    h.copy_(t, non_blocking=True)
+                    t.record_stream(self.stream)  # the block returns to the pool after the copy
+                    st[k] = None
+                    nbytes += t.numel() * t.element_size()
+        self.state_bytes = nbytes
+        self.resident = False
+        self._ready = None
+        self.transfers += 1
+
+    def prefetch(self, after: Optional[torch.cuda.Stream] = None) -> None:
+        """Copy the states back; with `after`, not before that stream's work enqueued so far
+        (the host runs ahead of the device, so an unordered copy would start too early)."""
+        if self.resident or self._ready is not None:
+            return
+        if after is not None:
+            ev = torch.cuda.Event()
+            ev.record(after)
+            self.stream.wait_event(ev)
+        with torch.cuda.stream(self.stream):
+            for p, st in self._states():
+                for k in self.KEYS:
+                    h = self.host.get((id(p), k))
+                    if h is not None and st.get(k) is None:
+                        st[k] = torch.empty(h.shape, dtype=h.dtype, device=p.device).copy_(h, non_blocking=True)
+            self._ready = torch.cuda.Event()
+            self._ready.record(self.stream)
+        self.transfers += 1
+
+    def wait_resident(self, main: torch.cuda.Stream) -> None:
+        if self.resident:
+            return
+        self.prefetch()  # no-op when run_iteration already issued it
+        main.wait_event(self._ready)
+        for _, st in self._states():
+            for k in self.KEYS:
+                if st.get(k) is not None:
+                    st[k].record_stream(main)
+        self.resident = True
 
 
 # --------------------------------------------------------------------------- device helpers
@@ -265,6 +368,7 @@ class StageEngine:
         prev_end_us = None
         main, comm = self.main, self.comm
         flag = self.words.flag.value
+        step_end_us = max(e for ins, _, e in self.timeline if ins.op != "BUBBLE")
         for ins, start_us, end_us in self.timeline:
             if ins.op == "BUBBLE":
                 ev = torch.cuda.Event()
@@ -295,6 +399,9 @@ class StageEngine:
                 main.wait_event(end_ev)
                 prev_end_us = end_us
                 continue
+            off = self.model.offload
+            if off is not None and not off.resident and start_us >= step_end_us - off.lead_us:
+                off.prefetch(after=main)  # optimizer states back in time for the step
             # F / B: wait for the (emulated) recv if the schedule idles before it
             if prev_end_us is None or start_us > prev_end_us:
                 self.link.wait_until(main, base + start_us * US)
