@@ -3,7 +3,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2410_07192_b200 import kernels as K, native
 from scripts.kernel_bench import timeit
 native.require_device()
-for (m, n, k) in [(4096, 2304, 768), (4096, 3072, 768), (4096, 768, 3072), (16384, 3072, 768), (4096, 3072, 3072)]:
+SHAPES = [(4096, 2304, 768), (4096, 3072, 768), (4096, 768, 3072), (16384, 3072, 768), (4096, 3072, 3072)]
+if len(sys.argv) > 1:  # e.g. 16384x4096x1024 16384x1024x4096
+    SHAPES = [tuple(int(v) for v in a.split("x")) for a in sys.argv[1:]]
+for (m, n, k) in SHAPES:
     x = torch.randn(m, k, device="cuda").bfloat16()
     w = (torch.randn(n, k, device="cuda") * k ** -0.5).bfloat16()
     b = torch.randn(n, device="cuda").bfloat16()
