@@ -168,6 +168,58 @@ __device__ __forceinline__ float gelu_fast(float x) {
   return 0.5f * x * (1.0f + erf_v);
 }
 
+// Packed fp32 pairs for the sm_100 FFMA2 path: fma/mul/add.rn.f32x2 issue two lanes per
+// instruction, each rounded exactly like its scalar counterpart, so code written with them
+// is bitwise the scalar code at half the FP issue slots (the GEMM epilogue is issue-bound
+// at K = 1024).
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 f2_pack(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 f2_splat(float a) { return f2_pack(a, a); }
+__device__ __forceinline__ void f2_unpack(f32x2 v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f32x2 f2_fma(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f32x2 f2_mul(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 f2_add(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// gelu_fast on a pair, op for op (the negated Horner constants give -poly exactly, as
+// fmaf(-poly, e, 1) needs; (-z * z) * L == (z * z) * -L in round-to-nearest).
+__device__ __forceinline__ void gelu_fast2(float& x0, float& x1) {
+  const f32x2 x = f2_pack(x0, x1);
+  const f32x2 z = f2_mul(f2_pack(fabsf(x0), fabsf(x1)), f2_splat(0.70710678118654752440f));
+  float d0, d1;
+  f2_unpack(f2_fma(f2_splat(0.3275911f), z, f2_splat(1.0f)), d0, d1);
+  const f32x2 t = f2_pack(fast_rcp(d0), fast_rcp(d1));
+  f32x2 np = f2_fma(t, f2_splat(-1.061405429f), f2_splat(1.453152027f));
+  np = f2_fma(t, np, f2_splat(-1.421413741f));
+  np = f2_fma(t, np, f2_splat(0.284496736f));
+  np = f2_fma(t, np, f2_splat(-0.254829592f));
+  np = f2_mul(np, t);  // -poly
+  float a0, a1;
+  f2_unpack(f2_mul(f2_mul(z, z), f2_splat(-1.4426950408889634f)), a0, a1);
+  const f32x2 e = f2_pack(fast_ex2(a0), fast_ex2(a1));
+  float ea0, ea1;
+  f2_unpack(f2_fma(np, e, f2_splat(1.0f)), ea0, ea1);
+  const f32x2 erf_v = f2_pack(copysignf(ea0, x0), copysignf(ea1, x1));
+  f2_unpack(f2_mul(f2_mul(f2_splat(0.5f), x), f2_add(f2_splat(1.0f), erf_v)), x0, x1);
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);

@@ -228,14 +228,15 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
           float2 f = unpack_bf16x2(bw[h]);
-          v[q * 8 + h * 2] += f.x;
-          v[q * 8 + h * 2 + 1] += f.y;
+          float& a = v[q * 8 + h * 2];
+          float& b = v[q * 8 + h * 2 + 1];
+          f2_unpack(f2_add(f2_pack(a, b), f2_pack(f.x, f.y)), a, b);
         }
       }
     }
     if (HAS_GELU) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
+      for (int j = 0; j < 32; j += 2) gelu_fast2(v[j], v[j + 1]);
     }
     if (HAS_RES) {
 #pragma unroll
@@ -244,8 +245,9 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
           float2 f = unpack_bf16x2(rw[h]);
-          v[q * 8 + h * 2] += f.x;
-          v[q * 8 + h * 2 + 1] += f.y;
+          float& a = v[q * 8 + h * 2];
+          float& b = v[q * 8 + h * 2 + 1];
+          f2_unpack(f2_add(f2_pack(a, b), f2_pack(f.x, f.y)), a, b);
         }
       }
     }
