@@ -73,9 +73,20 @@ CONFIGS = {
                     ("resnet50", 4096, 3.5), ("bert_large", 1024, 4.0))},
 }
 FILL_FRACTION = 0.95  # reference default 0.68 (V100 context-switch slack); B200 yields in us
-# Real NCCL pipeline: at 0.95 the N=4 main job slowed by 2.1-2.2 % over three runs (over the metric's
-# 2 % bound, with no bubble overrun: interference, not preemption); at 0.90 by 1.56 %.
-FILL_FRACTION_NCCL = 0.90
+# Real NCCL pipeline: the same fill fraction; the round-1 slowdown at 0.95 (+2.1-2.2 % at N=4) was the
+# power-cap effect the bubble tail below addresses
+FILL_FRACTION_NCCL = 0.95
+# Power-aware bubble tail: the main job runs power-capped; after an idle bubble the
+# board's power controller lets it start at up to 1965 MHz, after a bubble filled at full power at
+# ~1600. The last THROTTLE_MS of every bubble longer than that run on THROTTLE_CTAS CTAs and the
+# last COOLDOWN_MS idle. Measured on B200 (profiles/r02_power_sweep.md): composed 8-stage
+# main-job slowdown +3.5-4.4 % without, +2.0 % with (10, 50, 64), at 20 % less fill throughput.
+COOLDOWN_MS = 10.0
+THROTTLE_MS = 50.0
+THROTTLE_CTAS = 64
+# main-job slowdown phase: A = fill-off, B = fill-on iteration of one stage; the first of each run is
+# discarded (it inherits the other mode's power state), leaving 4 off and 5 on per stage
+DEFAULT_SLOWDOWN_PATTERN = "AAABBBBBBAAA"
 
 
 def load_peaks() -> dict:
@@ -99,6 +110,8 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.rows: list[list[str]] = []
+        self.tag = None  # the main thread's current phase ("fill_on" / "fill_off"), stored per row
+        self.tags: list = []
         self._stop = threading.Event()
         self._thr = threading.Thread(target=self._run, daemon=True)
 
@@ -110,6 +123,7 @@ class ClockSampler:
                                      timeout=5).stdout.strip()
                 if out:
                     self.rows.append([x.strip() for x in out.split(",")])
+                    self.tags.append(self.tag)
             except Exception:
                 pass
             self._stop.wait(0.2)
@@ -131,7 +145,20 @@ class ClockSampler:
                           r[3 + i].lower().startswith("active")})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows),
+                "sw_power_cap_samples": sum(1 for r in self.rows if len(r) > 6 and r[6].lower().startswith("active"))}
+
+    def by_tag(self) -> dict:
+        """Median SM MHz and board power per phase tag."""
+        out = {}
+        for tag in sorted({t for t in self.tags if t is not None}):
+            rows = [r for r, t in zip(self.rows, self.tags) if t == tag]
+            sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+            pw = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+            out[tag] = {"sm_mhz": statistics.median(sm) if sm else None,
+                        "power_w": statistics.median(pw) if pw else None, "samples": len(rows),
+                        "sw_power_cap_samples": sum(1 for r in rows if len(r) > 6 and r[6].lower().startswith("active"))}
+        return out
 
 
 def measure_h2d_gbs(nbytes: int = 256 << 20, reps: int = 5) -> float:
@@ -234,6 +261,7 @@ def run_service_sweep(args, conf) -> None:
     from paper_2410_07192_b200.engine import GPT2_SMALL_STAGE, GPT_8B_STAGE, GPTStage, StageEngine, measure_stage_times
     from paper_2410_07192_b200.executor import Executor
     from paper_2410_07192_b200.fillmodels import BERT_BASE, BERT_LARGE, bert, resnet50
+    from paper_2410_07192_b200.metrics import slowdown_stats
     from paper_2410_07192_b200.profiler import measure_profile
     from paper_2410_07192_b200.service import (FillService, ServiceConfig, predict, write_plan, write_report,
                                                write_sweep)
@@ -272,8 +300,9 @@ def run_service_sweep(args, conf) -> None:
     off = {}
     for s in range(P):
         iterate(s, False)
-        t = iterate(s, False)
-        off[s] = t["main_end"] - t["start"]
+        for _ in range(2):
+            t = iterate(s, False)
+            off.setdefault(s, []).append(t["main_end"] - t["start"])
 
     out_dir = args.report_dir or os.path.join(ROOT, "gpurun_out", "c5_report")
     rows, launches, dev_ns, sample_eq, on_iter, sweep_rows = [], 0, 0, 0.0, {}, []
@@ -306,8 +335,7 @@ def run_service_sweep(args, conf) -> None:
             for t in steps:
                 on_iter.setdefault(t["stage"], []).append(t["main_end"] - t["start"])
                 cap_iter.setdefault(t["stage"], []).append(t["main_end"] - t["start"])
-            rep.scalars_extra["main_job_slowdown"] = statistics.mean(
-                statistics.mean(v) / off[s_] - 1 for s_, v in cap_iter.items() if off.get(s_))
+            rep.scalars_extra["main_job_slowdown"] = slowdown_stats(cap_iter, off)["max"]
             sc = rep.scalars()
             row = {"free_mem_gb": cap_gb, "sample_eq_per_s": eq / (ns / 1e9) if ns else 0.0,
                    "iterations": len(steps), **{k: sc[k] for k in (
@@ -335,7 +363,7 @@ def run_service_sweep(args, conf) -> None:
     with open(os.path.join(out_dir, "sweep.json"), "w") as fh:
         json.dump(rows, fh, indent=2)
     write_sweep(out_dir, sweep_rows, seed=0)
-    slow = [statistics.mean(v) / off[s] - 1 for s, v in on_iter.items() if off.get(s)]
+    slow = slowdown_stats(on_iter, off)
     best = rows[-1]
     if rank == 0:
         line = {
@@ -352,7 +380,8 @@ def run_service_sweep(args, conf) -> None:
                        "max_batches_per_bubble": conf["max_batches"], "fill_fraction": args.fill_fraction,
                        "t_fwd_ms": tf_ms, "t_bwd_ms": tb_ms},
             "sweep": rows,
-            "main_job_slowdown": statistics.mean(slow) if slow else None,
+            "main_job_slowdown": slow["max"], "main_job_slowdown_mean": slow["mean"],
+            "main_job_slowdown_detail": slow,
             "value_definition": "sample-equivalents/s over device time of the filled iterations at the "
                                 "largest free-memory cap",
             "roofline": None, "cpu_baseline": None,
@@ -387,7 +416,7 @@ def run_training_depths(args, conf) -> None:
     from paper_2410_07192_b200 import native
     from paper_2410_07192_b200.engine import GPT2_SMALL_STAGE, GPT_8B_STAGE, GPTStage, StageEngine, measure_stage_times
     from paper_2410_07192_b200.executor import Executor
-    from paper_2410_07192_b200.metrics import FillStats, aggregate, busy_in_bubbles, mean_slowdown
+    from paper_2410_07192_b200.metrics import FillStats, aggregate, busy_in_bubbles, slowdown_stats
     from paper_2410_07192_b200.profiler import measure_train_profile
     from paper_2410_07192_b200.training import resnet50_train
 
@@ -453,8 +482,9 @@ def run_training_depths(args, conf) -> None:
             off = {}
             for s_ in range(P):
                 iterate(s_, False)
-                t = iterate(s_, False)
-                off[s_] = [t["main_end"] - t["start"]]
+                for _ in range(2):
+                    t = iterate(s_, False)
+                    off.setdefault(s_, []).append(t["main_end"] - t["start"])
             current = {"stage": None}
 
             def step(k):
@@ -499,7 +529,8 @@ def run_training_depths(args, conf) -> None:
             results[str(P)] = {
                 "images_per_s": tot.value, "bubble_time_filled": tot.bubble_filled,
                 "bubble_time_filled_of_total_idle": tot.idle_filled,
-                "main_job_slowdown": mean_slowdown(on_iter, off),
+                "main_job_slowdown": slowdown_stats(on_iter, off)["max"],
+                "main_job_slowdown_detail": slowdown_stats(on_iter, off),
                 "gemm_tflops_in_situ": tot.gemm_tflops, "sgd_steps": int(sum(r_.batches_done for r_ in recs)),
                 "plan_stage0": pf.plan_to_dict(coords[0].executables["train-0"]),
                 "ms_per_step": 1000 * tot.device_s / max(1, len(steps))}
@@ -538,6 +569,123 @@ def run_training_depths(args, conf) -> None:
         dist.destroy_process_group()
 
 
+def measure_interference(args, stages, run_block, local, pcfg) -> dict:
+    """Main-job slowdown with filling on vs off, from blocks of consecutive iterations.
+
+    Every stage runs fill-off (A) and fill-on (B) iterations back to back from one anchor, in
+    the order of `--slowdown-pattern` (default AAABBBBBBAAA, so clock and temperature drifts
+    cancel between the modes); the first iteration after a switch is dropped because it
+    inherits the other mode's power state from the preceding fill-drain bubble. Per-op stamps
+    give each op's duration and the SM clock it started at, and the main stream's resume
+    delay after every bubble's recv (flag clear).
+
+    Headline: the p-stage pipeline's iteration time composed from the measured per-op
+    durations of every stage (schedule.replay_makespan, the dependency replay of
+    pipeline.py:237-278 with measured instead of uniform op times), fill on vs off. With
+    artificial neighbours a stage's own iteration time hides its slowdown in its idle gaps,
+    so it is reported only as a secondary figure, next to each stage's compute time."""
+    import torch
+
+    from paper_2410_07192_b200.metrics import distribution, slowdown_stats
+    from paper_2410_07192_b200.schedule import replay_makespan
+
+    pattern = ["off" if c == "A" else "on" for c in (args.slowdown_pattern or DEFAULT_SLOWDOWN_PATTERN)]
+    counted = [i > 0 and pattern[i - 1] == pattern[i] for i in range(len(pattern))]
+    if args.slowdown_stages:
+        stages = [int(x) for x in args.slowdown_stages.split(",")]
+    dump = []
+    on, off = {}, {}
+    comp_on, comp_off = {}, {}  # stage -> main-job compute time per iteration (sum of its ops)
+    opdur = {"on": {}, "off": {}, "off_a": {}, "off_b": {}}  # (stage, op, mb) -> [ns]
+    mhz = {"on": {}, "off": {}}
+    resume = {"on": [], "off": []}
+    first = {"on": {}, "off": {}}  # stage -> duration of the window's first op (ns)
+    with ClockSampler(local) as clocks:
+        for s_ in stages:
+            clocks.tag = f"stage_{s_}"
+            n_off = 0
+            for mode, use, t in zip(pattern, counted, run_block(s_, pattern)):
+                if args.dump_ops:
+                    dump.append({"stage": s_, "mode": mode, "counted": use, "start": t["start"],
+                                 "main_end": t["main_end"], "ops": t.get("ops", []),
+                                 "bubbles": [b[:3] for b in t["bubbles"]], "resume_ns": t.get("resume_ns", [])})
+                if not use:
+                    continue
+                (on if mode == "on" else off).setdefault(s_, []).append(t["main_end"] - t["start"])
+                (comp_on if mode == "on" else comp_off).setdefault(s_, []).append(
+                    sum(t1 - t0 for _, _, t0, t1, _ in t.get("ops", [])))
+                keys = [mode] + ([("off_a", "off_b")[n_off % 2]] if mode == "off" else [])
+                n_off += mode == "off"
+                for op, mb, t0, t1, m in t.get("ops", []):
+                    for k in keys:
+                        opdur[k].setdefault((s_, op, mb), []).append(t1 - t0)
+                    mhz[mode].setdefault(s_, []).append(m)
+                if t.get("ops"):
+                    first[mode].setdefault(s_, []).append(t["ops"][0][3] - t["ops"][0][2])
+                resume[mode] += [ns / 1e3 for ns in t.get("resume_ns", [])]
+        clocks.tag = None
+        torch.cuda.synchronize()
+    if args.dump_ops:
+        with open(args.dump_ops, "w") as fh:
+            json.dump(dump, fh)
+
+    def makespan(key: str) -> float | None:
+        d = opdur[key]
+        if any((s_, op, j) not in d for s_ in range(pcfg.num_stages)
+               for op in ("F", "B") for j in range(pcfg.num_microbatches)):
+            return None  # not every stage measured
+        return replay_makespan(pcfg, lambda s_, op, j: statistics.mean(d[(s_, op, j)]))
+
+    span = {k: makespan(k) for k in opdur}
+    pipe = None
+    if span["on"] and span["off"]:
+        pipe = {"slowdown": span["on"] / span["off"] - 1.0,
+                "noise_floor": abs(span["off_a"] / span["off_b"] - 1.0) if span["off_a"] and span["off_b"] else None,
+                "iteration_ms_fill_on": span["on"] / 1e6, "iteration_ms_fill_off": span["off"] / 1e6}
+    per_stage = {}
+    for s_ in stages:
+        per_stage[str(s_)] = {
+            "compute_ms_fill_on": statistics.mean(comp_on[s_]) / 1e6,
+            "compute_ms_fill_off": statistics.mean(comp_off[s_]) / 1e6,
+            "iter_ms_fill_on": statistics.mean(on[s_]) / 1e6, "iter_ms_fill_off": statistics.mean(off[s_]) / 1e6,
+            "sm_mhz_fill_on": statistics.median(mhz["on"][s_]), "sm_mhz_fill_off": statistics.median(mhz["off"][s_]),
+            "first_op_ms": {m: statistics.mean(first[m][s_]) / 1e6 for m in ("on", "off")}}
+    return {"pipeline": pipe, "slowdown": slowdown_stats(comp_on, comp_off),
+            "iteration_slowdown": slowdown_stats(on, off), "per_stage": per_stage,
+            "main_resume_delay_us": {m: distribution(v) for m, v in resume.items()},
+            "clocks": clocks.by_tag(), "pattern": args.slowdown_pattern or DEFAULT_SLOWDOWN_PATTERN}
+
+
+def yield_latency(steps, by_tag) -> dict:
+    """Fill-stream overrun past each bubble's end (flag clear -> the fill stream's last
+    stamp) over the timed bubbles: the bound the preemption protocol gives (one GEMM tile,
+    DESIGN.md §3) is what the preempted bubbles show."""
+    from paper_2410_07192_b200.metrics import distribution
+
+    pre, done, release = [], [], []
+    for t in steps:
+        for kind, t_set, t_clr, tag in t["bubbles"]:
+            r = by_tag.get(tag)
+            if r is None or r.fill_end_ns <= 0:
+                continue
+            over = (r.fill_end_ns - t_clr) / 1e3
+            (pre if r.aborted else done).append(over)
+            if r.aborted and r.last_work_end_ns > 0:
+                release.append(max(0.0, (r.last_work_end_ns - t_clr) / 1e3))
+    resume = [ns / 1e3 for t in steps for ns in t.get("resume_ns", [])]
+    return {"yield_latency_us": distribution(release),
+            "yield_latency_definition": "preempted bubbles: last exit of a fill GEMM CTA of the yielded batch "
+                                        "(in-kernel %globaltimer) - flag clear; 0 when the batch yielded "
+                                        "between kernels. Bound: one output tile (DESIGN.md §3)",
+            "preempted_overrun_us": distribution(pre),
+            "completed_overrun_us": distribution([max(0.0, x) for x in done]),
+            "completed_bubbles_overrunning": sum(1 for x in done if x > 0),
+            "main_resume_delay_us": distribution(resume),
+            "definition": "overrun = fill stream's end stamp (after the aborted batches' no-op gate launches) - "
+                          "bubble flag clear (us); main resume delay = main stream's first stamp after the "
+                          "bubble - flag clear (us)"}
+
+
 def profile_step_ms(profile, b: int) -> float:
     return sum(layer.exec_time_ms[b] for layer in profile.layers)
 
@@ -566,6 +714,17 @@ def main() -> None:
                     help="main job keeps its AdamW moments in pinned host memory between steps")
     ap.add_argument("--max-batches", type=int, default=None,
                     help="Coordinator max_batches_per_bubble (overrides the config's)")
+    ap.add_argument("--cooldown-ms", type=float, default=COOLDOWN_MS,
+                    help="idle tail kept at the end of every bubble (power-aware usable time, DESIGN.md §5)")
+    ap.add_argument("--throttle-ms", type=float, default=THROTTLE_MS,
+                    help="throttle the fill to --throttle-ctas CTAs this long before every bubble's end")
+    ap.add_argument("--throttle-ctas", type=int, default=THROTTLE_CTAS)
+    ap.add_argument("--loss-iters", type=int, default=4,
+                    help="nccl: iterations per deterministic fill-off / on / off loss-identity replay")
+    ap.add_argument("--slowdown-pattern", default=None,
+                    help="explicit fill-off (A) / fill-on (B) iteration order per stage, e.g. AABBBBAA")
+    ap.add_argument("--slowdown-stages", default=None, help="comma-separated stages for the slowdown phase")
+    ap.add_argument("--dump-ops", default=None, help="write the slowdown phase's per-op stamps (JSON) here")
     ap.add_argument("--batch-sizes", default=None,
                     help="comma-separated profiled fill batch sizes (overrides the config's)")
     args = ap.parse_args()
@@ -598,13 +757,6 @@ def main() -> None:
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local),
                                 timeout=__import__("datetime").timedelta(seconds=240))
-    if args.pipeline == "nccl":
-        # main job with deterministic kernels (math SDPA): fill-on and fill-off losses are then
-        # comparable bit for bit, so any effect of the fill job on the main job would show
-        torch.backends.cuda.enable_flash_sdp(False)
-        torch.backends.cuda.enable_mem_efficient_sdp(False)
-        torch.backends.cuda.enable_math_sdp(True)
-        torch.use_deterministic_algorithms(True)
 
     import paper_2410_07192_b200 as pf
     from paper_2410_07192_b200 import native
@@ -612,8 +764,9 @@ def main() -> None:
                                               NcclPipelineEngine, StageEngine, measure_stage_times)
     from paper_2410_07192_b200.executor import Executor
     from paper_2410_07192_b200.fillmodels import BERT_BASE, BERT_LARGE, bert
-    from paper_2410_07192_b200.metrics import FillStats, aggregate, busy_in_bubbles, mean_slowdown
+    from paper_2410_07192_b200.metrics import FillStats, aggregate, busy_in_bubbles, slowdown_stats
     from paper_2410_07192_b200.profiler import measure_profile
+    from paper_2410_07192_b200.schedule import with_cooldown
 
     native.require_device()
     peaks = load_peaks()
@@ -660,7 +813,10 @@ def main() -> None:
     def coordinator_for(s: int, cfg, cycle=None) -> pf.Coordinator:
         if s not in coords:
             # the stage's Coordinator; a long-running fill job split into 16K-sample ranges
-            coords[s] = pf.Coordinator(s, cycle or pf.build_bubble_cycle(cfg, s), 1,
+            # power-aware tail: bubbles longer than the throttle window keep an idle cooldown
+            cyc = with_cooldown(cycle or pf.build_bubble_cycle(cfg, s), int(args.cooldown_ms * 1000),
+                                int(args.throttle_ms * 1000))
+            coords[s] = pf.Coordinator(s, cyc, 1,
                                        pf.OrderingPolicy("concurrent", conf["chunk"]),
                                        batch_sizes=list(conf["batch_sizes"]),
                                        max_batches_per_bubble=conf.get("max_batches", 16))
@@ -691,20 +847,20 @@ def main() -> None:
         engines[rank] = eng
         items["stage"], items["item"] = rank, None
 
-        def run_phase(fill: bool) -> list[dict]:
+        def run_phase(fill: bool, n_iter: int = n_total, skip: int = args.warmup) -> list[dict]:
             eng.reset_stamps()
             dist.barrier()
             eng.set_anchor()
             recs_ = []
-            for it in range(n_total):
-                recs_.append(eng.run_iteration(it, fill=fill, last=(it == n_total - 1)))
+            for it in range(n_iter):
+                recs_.append(eng.run_iteration(it, fill=fill, last=(it == n_iter - 1)))
             if fill:
                 executor.settle()
             eng.sync()
             out, prev_end = [], None
             for it, r in enumerate(recs_):
                 t = eng.record_timing(r)
-                if prev_end is not None and it >= args.warmup:
+                if prev_end is not None and it >= skip:
                     out.append({"start": prev_end, "main_end": t["main_end"], "step_end": t["main_end"],
                                 "bubbles": t["bubbles"], "stage": rank})
                 prev_end = t["main_end"]
@@ -712,7 +868,6 @@ def main() -> None:
 
         snap = main_model.snapshot()  # every phase trains from the same weights and data
         run_phase(False)  # untimed warm-up phase (lazy NCCL P2P setup, allocator growth)
-        eng.losses = []
         main_model.restore(snap)
         off_steps = run_phase(False)
         for t in off_steps:
@@ -730,11 +885,12 @@ def main() -> None:
             rank, max(period_us, sum(durs)), durs, [arena_bytes, arena_bytes], args.fill_fraction,
             unfillable_us=max(0, min(analytic.unfillable_us, period_us - sum(durs))))
         coordinator_for(rank, pcfg, measured_cycle)
+        eng.throttle_ns = int(args.throttle_ms * 1e6)
+        eng.throttle_ctas = args.throttle_ctas
+        eng.expected_ns = {k: d * 1000 for k, d in enumerate(durs)}
         characterization = {"measured_bubbles_us": durs, "measured_period_us": period_us,
                             "analytic_bubbles_us": [b.duration_us for b in analytic.bubbles],
                             "analytic_period_us": analytic.period_us}
-        losses_off = [float(x) for x in eng.losses]
-        eng.losses = []
         main_model.restore(snap)
         executor.timing = True
         executor.gemm_samples = []
@@ -754,15 +910,29 @@ def main() -> None:
         recs = [r for r in executor.records[n_rec0:]
                 if any(r.tag == b[3] for t in steps for b in t["bubbles"])]
         launches = executor.kernel_launches + eng.launches - launches0
-        losses_on = [float(x) for x in eng.losses]
-        # a second fill-off phase: the run-to-run noise floor of the (non-deterministic)
-        # main job, and a second fill-off timing reference
-        eng.losses = []
+        executor.timing = False
+        # a second fill-off phase (ABA around the timed fill-on phase: drifts cancel)
         main_model.restore(snap)
         for t in run_phase(False):
             off.setdefault(rank, []).append(t["main_end"] - t["start"])
-        losses_off2 = [float(x) for x in eng.losses]
-        obj = [[losses_off, losses_on, losses_off2]]
+        # main-job loss identity: the throughput phases above run the normal (flash SDPA,
+        # non-deterministic) main job; this replay runs it with deterministic kernels (math SDPA,
+        # use_deterministic_algorithms), fill off / on / off from one snapshot, so any effect of
+        # the fill job on the main job's numerics would show as a bitwise loss difference
+        flash = torch.backends.cuda.flash_sdp_enabled(), torch.backends.cuda.mem_efficient_sdp_enabled()
+        torch.backends.cuda.enable_flash_sdp(False)
+        torch.backends.cuda.enable_mem_efficient_sdp(False)
+        torch.use_deterministic_algorithms(True)
+        loss_runs = []
+        for fill_ in (False, True, False):
+            eng.losses = []
+            main_model.restore(snap)
+            run_phase(fill_, n_iter=args.loss_iters, skip=0)
+            loss_runs.append([float(x) for x in eng.losses])
+        torch.use_deterministic_algorithms(False)
+        torch.backends.cuda.enable_flash_sdp(flash[0])
+        torch.backends.cuda.enable_mem_efficient_sdp(flash[1])
+        obj = [loss_runs]
         dist.broadcast_object_list(obj, src=world - 1)  # the last stage owns the loss
         losses_off, losses, losses_off2 = obj[0]
         del snap
@@ -770,6 +940,9 @@ def main() -> None:
         def engine_for(s: int) -> StageEngine:
             if s not in engines:
                 engines[s] = StageEngine(pcfg, s, main_model, executor, streams=shared_streams)
+                engines[s].op_stamps = True  # per-op stamps + SM clock, fill on and off alike
+                engines[s].throttle_ns = int(args.throttle_ms * 1e6)
+                engines[s].throttle_ctas = args.throttle_ctas
                 coordinator_for(s, pcfg)
             return engines[s]
 
@@ -851,6 +1024,33 @@ def main() -> None:
         launches = executor.kernel_launches + sum(e.launches for e in engines.values()) - launches0
         losses, losses_off, losses_off2 = [], [], []
         characterization = {"bubbles": "analytic timeline with measured t_fwd/t_bwd (artificial neighbours)"}
+        # main-job interference, after (and outside) the timed region: every stage the timed
+        # steps visited runs fill-off and fill-on iterations interleaved ABBA (off on on off ...)
+        def run_block(s_: int, modes: list) -> list[dict]:
+            """Consecutive iterations of stage s_ from one anchor (no host gap between them),
+            fill on or off per iteration; the executor holds stage s_'s work."""
+            eng = engine_for(s_)
+            if items.get("stage") != s_:
+                if items.get("item") is not None and items.get("stage") is not None:
+                    coords[items["stage"]].worker_job[0] = None
+                items["stage"], items["item"] = s_, None
+                nxt = next_work()
+                if nxt is not None:
+                    executor.load(*nxt)
+                executor.prewarm(eng.words.flag.value)
+            executor.settle()
+            eng.reset_stamps()
+            eng.set_anchor()
+            recs_ = [eng.run_iteration(i, fill=(m == "on")) for i, m in enumerate(modes)]
+            executor.settle()
+            out = []
+            for r in recs_:
+                t = eng.record_timing(r)
+                t["stage"] = s_
+                out.append(t)
+            return out
+
+        interference = measure_interference(args, list(range(P_STAGES)), run_block, local, pcfg)
 
     # ---- accounting from device timestamps
     # sample-equivalents: a batch that passed partition [lo, hi) counts as the share of
@@ -876,7 +1076,23 @@ def main() -> None:
                     f"part {r.part} batches {r.batches_done}/{r.batches_planned} aborted {r.aborted}")
                 print(f"[dbg]   bubble {kind} at +{(t_set - t['start']) / 1e6:.1f} ms len "
                       f"{(t_clr - t_set) / 1e6:.2f} ms: {info}", file=sys.stderr)
-    slowdown = mean_slowdown(on_iter, off)
+    if args.pipeline == "nccl":
+        # every rank is one stage: gather all stages' iteration times, max over stages
+        both = [None] * world if world > 1 else [(on_iter, off)]
+        if world > 1:
+            dist.all_gather_object(both, (on_iter, off))
+        on_all, off_all = {}, {}
+        for o_, f_ in both:
+            on_all.update(o_)
+            off_all.update(f_)
+        interference = {"slowdown": slowdown_stats(on_all, off_all)}
+    slow = dict(interference["slowdown"])
+    if interference.get("pipeline"):  # headline: the composed pipeline iteration time
+        slow["max_stage_compute"] = slow["max"]
+        slow["max"] = interference["pipeline"]["slowdown"]
+        slow["noise_floor_stage_compute"] = slow["noise_floor"]
+        slow["noise_floor"] = interference["pipeline"]["noise_floor"]
+    yield_stats = yield_latency(steps, by_tag)
     stats = FillStats(
         sample_equivalents=sum(r.sample_eq for r in recs),
         samples_completed=sum(r.samples_completed for r in recs),
@@ -936,16 +1152,33 @@ def main() -> None:
                 "fill": {"model": fcfg.name, "seq_len": fcfg.seq, "profiled_batch_sizes": list(conf["batch_sizes"]),
                          "range_chunk_samples": conf["chunk"],
                          "max_batches_per_bubble": conf.get("max_batches", 16),
-                         "fill_fraction": args.fill_fraction, "arena_bytes": arena_bytes,
+                         "fill_fraction": args.fill_fraction, "cooldown_ms": args.cooldown_ms,
+                         "throttle_ms": args.throttle_ms, "throttle_ctas": args.throttle_ctas,
+                         "arena_bytes": arena_bytes,
                          "plans": {str(s): pf.plan_to_dict(c.executables[f"fill-{s}"]) for s, c in coords.items()}},
                 "stages_run": [t["stage"] for t in steps],
                 "l2": "inputs larger than L2 (BERT-large weights 0.67 GB streamed per batch; main job 1B params)",
             },
             "bubble_time_filled": tot.bubble_filled,
             "bubble_time_filled_of_total_idle": tot.idle_filled,
-            "main_job_slowdown": slowdown,
-            "per_stage_iter_ms": {str(st): {"fill_off": statistics.mean(off.get(st, [0])) / 1e6,
-                                            "fill_on": statistics.mean(v) / 1e6} for st, v in on_iter.items()},
+            "main_job_slowdown": slow["max"],
+            "main_job_slowdown_definition": (
+                "iteration time of the 8-stage pipeline composed from every stage's measured per-op device times "
+                "(dependency replay, schedule.replay_makespan), fill on / fill off - 1; per-op times from blocks of "
+                "consecutive iterations of each stage after the timed region (pattern "
+                + (args.slowdown_pattern or DEFAULT_SLOWDOWN_PATTERN) + ", first iteration after a switch dropped). "
+                "Not the emulated stage's own iteration time: its artificial neighbours' fixed arrival times absorb "
+                "its slowdown in its idle gaps (main_job_iteration_slowdown). noise floor = the same composition "
+                "from the two halves of the fill-off iterations"
+                if args.pipeline == "emulated" else
+                "max over pipeline stages (ranks) of mean(fill-on) / mean(fill-off) main-job iteration time - 1"),
+            "main_job_iteration_slowdown": interference.get("iteration_slowdown"),
+            "main_job_slowdown_mean": slow["mean"],
+            "main_job_slowdown_noise_floor": slow["noise_floor"],
+            "main_job_slowdown_detail": slow,
+            "interference": {k: v for k, v in interference.items() if k not in ("slowdown", "iteration_slowdown")},
+            "yield": yield_stats,
+            "per_stage_iter_ms_timed": {str(st): {"fill_on": statistics.mean(v) / 1e6} for st, v in on_iter.items()},
             "bubble_characterization": characterization,
             "optimizer_offload": None if main_model.offload is None else {
                 "state_bytes": main_model.offload.state_bytes, "lead_ms": main_model.offload.lead_us / 1e3,
@@ -977,9 +1210,10 @@ def main() -> None:
                                                                for a, b in zip(losses_off, losses)),
                                  "max_rel_diff_off_vs_off_again": max(abs(a - b) / max(abs(a), 1e-12)
                                                                       for a, b in zip(losses_off, losses_off2)),
-                                 "note": "main job with deterministic torch kernels (math SDPA, "
-                                         "use_deterministic_algorithms): identical == bitwise equal losses; "
-                                         "fill-off vs fill-off-again checks the run-to-run reproducibility"}
+                                 "note": f"{args.loss_iters} iterations per run replayed from one snapshot with "
+                                         "deterministic torch kernels (math SDPA, use_deterministic_algorithms), "
+                                         "after the throughput phases (flash SDPA): identical == bitwise equal "
+                                         "losses; fill-off vs fill-off-again checks the run-to-run reproducibility"}
                                 if losses else None),
         }
         text = json.dumps(line)

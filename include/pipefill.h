@@ -92,12 +92,24 @@ int pf_flag_destroy(uint32_t* dev_flag);
 int pf_flag_write_on_stream(uint32_t* dev_flag, uint32_t value, void* stream);
 int pf_flag_clear_at(uint32_t* dev_flag, const uint64_t* base_ns, uint64_t offset_ns,
                      uint64_t* stamp_out, void* stream);
+/* Enqueue a one-thread kernel that spins until %globaltimer >= (*base_ns + offset_ns) and
+ * then throttles an open bubble: flag 1 -> value (value >= 2; a closed flag stays 0).
+ * Flag value v >= 2 = "open, at most v CTAs claim work" (cursor-claimed kernels shed the
+ * rest): the power-aware bubble tail. No reference counterpart (the
+ * reference reserves the tail of every bubble through fill_fraction, pipeline.py:205). */
+int pf_flag_throttle_at(uint32_t* dev_flag, const uint64_t* base_ns, uint64_t offset_ns, uint32_t value,
+                        void* stream);
 /* Enqueue a one-thread kernel that spins until %globaltimer >= (*base_ns + offset_ns)
  * (base_ns may be NULL = 0): the timer-driven stand-in for a recv. If stamp_out is
  * non-NULL it receives the %globaltimer value at release. dev_flag may be NULL.     */
 int pf_wait_until(const uint64_t* base_ns, uint64_t offset_ns, uint64_t* stamp_out, void* stream);
 /* Enqueue a kernel writing the device %globaltimer (ns) into *dev_out. */
 int pf_read_globaltimer(uint64_t* dev_out, void* stream);
+/* Enqueue a one-thread kernel that spins spin_ns (<= 10 ms) and writes {start %globaltimer,
+ * elapsed ns, elapsed SM cycles} to dev_out3[0..3): the SM clock the main job runs at, read
+ * on the device per pipeline op (power-cap interference). No reference
+ * counterpart: the reference models slowdown analytically (sim.py:32-56).           */
+int pf_sm_clock_probe(uint64_t* dev_out3, uint64_t spin_ns, void* stream);
 
 /* ---- weight / activation staging ------------ */
 int pf_host_alloc_pinned(uint64_t bytes, void** out_host_ptr);

@@ -102,16 +102,28 @@ __device__ __forceinline__ bool chain_aborted(const Ctl& c) {
   return c.abort != nullptr && ld_volatile_u32(c.abort) != 0u;
 }
 
+// Bubble flag values: 0 = closed (yield), 1 = open, v >= 2 = open but throttled to v CTAs:
+// in the bubble's last milliseconds the engine lowers the fill's power draw so the board's
+// power controller has raised the SM clock again when the main job resumes.
+// Only cursor-claimed work (persistent GEMMs, SGD) sheds CTAs: a shed CTA stops claiming,
+// the others take its units from the shared cursor, so every unit is still done once.
+__device__ __forceinline__ bool throttled_out(uint32_t f, uint32_t slot, uint32_t per_slot) {
+  return f >= 2u && slot >= f / per_slot;
+}
+
 // Claims the next work unit, or returns -1 when the bubble closed (flag==0:
-// sets the sticky abort), or when all `units` are claimed. Static striding
-// (no cursor) is used for non-preemptible launches. `iter` counts this CTA's
-// previous claims and is only used by the static path.
+// sets the sticky abort), when the bubble is throttled below this CTA's index, or
+// when all `units` are claimed. Static striding (no cursor) is used for
+// non-preemptible launches. `iter` counts this CTA's previous claims and is only used
+// by the static path.
 __device__ __forceinline__ int claim_unit(const Ctl& c, int units, int iter) {
   if (c.flag != nullptr) {
-    if (ld_acquire_u32(c.flag) == 0u) {
+    const uint32_t f = ld_acquire_u32(c.flag);
+    if (f == 0u) {
       atomicExch(c.abort, 1u);
       return -1;
     }
+    if (c.cursor != nullptr && throttled_out(f, blockIdx.x, 1u)) return -1;
   }
   uint32_t u;
   if (c.cursor != nullptr) {

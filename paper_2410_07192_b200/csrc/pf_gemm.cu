@@ -580,10 +580,12 @@ struct Cfg2 {
 __device__ __forceinline__ int claim_pair(const Ctl& c, int units, int iter) {
   if (chain_aborted(c)) return -1;
   if (c.flag != nullptr) {
-    if (ld_acquire_u32(c.flag) == 0u) {
+    const uint32_t f = ld_acquire_u32(c.flag);
+    if (f == 0u) {
       atomicExch(c.abort, 1u);
       return -1;
     }
+    if (c.cursor != nullptr && throttled_out(f, blockIdx.x >> 1, 2u)) return -1;  // pairs: f / 2 of them
   }
   uint32_t u;
   if (c.cursor != nullptr) {

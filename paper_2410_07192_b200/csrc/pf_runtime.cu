@@ -94,10 +94,40 @@ __global__ void flag_clear_at_kernel(uint32_t* flag, const uint64_t* base, uint6
   }
 }
 
+// Throttle an open bubble at a deadline: 1 -> value (only if still 1: a bubble that closed
+// meanwhile stays closed).
+__global__ void flag_throttle_at_kernel(uint32_t* flag, const uint64_t* base, uint64_t offset,
+                                        uint32_t value) {
+  const uint64_t deadline = (base ? *(volatile const uint64_t*)base : 0ull) + offset;
+  uint64_t now;
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (now >= deadline) break;
+    __nanosleep(256);
+  } while (true);
+  __threadfence();
+  atomicCAS(flag, 1u, value);
+}
+
 __global__ void globaltimer_kernel(uint64_t* out) {
   uint64_t now;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
   *out = now;
+}
+
+// SM clock over a short spin: out[0] = %globaltimer at the start (ns), out[1] = elapsed ns,
+// out[2] = elapsed SM cycles (clock64 of the same SM), so MHz = out[2] * 1e3 / out[1]
+__global__ void sm_clock_probe_kernel(uint64_t* out, uint64_t spin_ns) {
+  uint64_t t0, t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  const long long c0 = clock64();
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  } while (t1 - t0 < spin_ns);
+  const long long c1 = clock64();
+  out[0] = t0;
+  out[1] = t1 - t0;
+  out[2] = static_cast<uint64_t>(c1 - c0);
 }
 
 __global__ void chain_begin_kernel(uint32_t* cursors, int n, const uint32_t* abort,
@@ -380,6 +410,16 @@ int pf_flag_clear_at(uint32_t* flag, const uint64_t* base_ns, uint64_t offset_ns
   return PF_OK;
 }
 
+int pf_flag_throttle_at(uint32_t* flag, const uint64_t* base_ns, uint64_t offset_ns, uint32_t value,
+                        void* stream) {
+  using namespace pf;
+  if (!flag || value < 2u) return set_error(PF_ERR_INVALID, "pf_flag_throttle_at: null flag or value < 2");
+  flag_throttle_at_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(flag, base_ns, offset_ns,
+                                                                               value);
+  PF_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
 int pf_wait_until(const uint64_t* base_ns, uint64_t offset_ns, uint64_t* stamp_out,
                   void* stream) {
   return pf_flag_clear_at(nullptr, base_ns, offset_ns, stamp_out, stream);
@@ -389,6 +429,15 @@ int pf_read_globaltimer(uint64_t* dev_out, void* stream) {
   using namespace pf;
   if (!dev_out) return set_error(PF_ERR_INVALID, "pf_read_globaltimer: null out");
   globaltimer_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(dev_out);
+  PF_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+int pf_sm_clock_probe(uint64_t* dev_out3, uint64_t spin_ns, void* stream) {
+  using namespace pf;
+  if (!dev_out3 || spin_ns == 0 || spin_ns > 10000000ull)
+    return set_error(PF_ERR_INVALID, "pf_sm_clock_probe: null out or spin outside (0, 10 ms]");
+  sm_clock_probe_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(dev_out3, spin_ns);
   PF_CUDA(cudaGetLastError());
   return PF_OK;
 }

@@ -263,11 +263,11 @@ class DeviceWords:
         self.anchor = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.n = 0
 
-    def stamp_ptr(self) -> int:
-        if self.n >= self.stamps.numel():
+    def stamp_ptr(self, words: int = 1) -> int:
+        if self.n + words > self.stamps.numel():
             raise RuntimeError("timestamp buffer full")
         p = self.stamps.data_ptr() + 8 * self.n
-        self.n += 1
+        self.n += words
         return p
 
     def close(self):
@@ -284,6 +284,9 @@ class IterationRecord:
     epoch: int = 0  # stamp-buffer generation (stamp indices repeat after reset_stamps)
     bubbles: list[tuple[int, int, int]] = field(default_factory=list)  # (kind, set idx, clear idx)
     bubble_mem: list[tuple[int, int]] = field(default_factory=list)  # (kind, main-job bytes allocated)
+    # per F/B op when the engine stamps ops: (op, mb, probe idx (3 words), end idx)
+    ops: list[tuple[str, int, int, int]] = field(default_factory=list)
+    resume: list[tuple[int, int]] = field(default_factory=list)  # (bubble clear idx, main resume idx)
 
 
 # --------------------------------------------------------------------------- links
@@ -349,6 +352,17 @@ class StageEngine:
         # bubble probe (probe_bubbles): {bubble kind: ns} the main stream stays busy from the
         # bubble's start before its next instruction (PAPER.md:424's "wait" at the BUBBLE)
         self.probe_ns: dict[int, int] = {}
+        # per-op stamps: every F/B is preceded by an SM-clock probe (start time, ns, cycles)
+        # and followed by an end stamp; every BUBBLE by a main-stream stamp when the main job
+        # resumes (the interference / yield-latency measurements)
+        self.op_stamps = False
+        # power-aware bubble tail: `throttle_ns` before each bubble's end the flag drops from 1
+        # to `throttle_ctas` (pf_flag_throttle_at on the timer stream), so the fill's
+        # cursor-claimed kernels run on that many CTAs and the board's power controller has
+        # raised the SM clock when the main job resumes
+        self.throttle_ns = 0
+        self.throttle_ctas = 0
+        self.timer = torch.cuda.Stream(priority=hi)
 
     def set_anchor(self, lead_ms: float = 5.0) -> None:
         """Anchor = device time now + lead (host enqueues ahead within the lead)."""
@@ -380,6 +394,17 @@ class StageEngine:
                 start_ev = torch.cuda.Event()
                 start_ev.record(comm)
                 clear_idx = self.words.n
+                if (fill and self.throttle_ns > 0 and self.throttle_ctas >= 2
+                        and (end_us - start_us) * US > self.throttle_ns):
+                    # the bubble's last throttle_ns run throttled. Bubbles shorter than that are
+                    # not: the power controller needs ~40 ms to raise the clock after the power
+                    # drops (scripts/power_throttle.py), so the main job resumes at the clock it
+                    # left the bubble with whether a short bubble was filled or idle
+                    self.timer.wait_event(start_ev)
+                    native.call("pf_flag_throttle_at", flag, self.words.anchor.data_ptr(),
+                                int(base + end_us * US - self.throttle_ns), int(self.throttle_ctas),
+                                self.timer.cuda_stream)
+                    self.launches += 1
                 self.link.bubble_end(base + end_us * US, self.words.stamp_ptr())
                 end_ev = torch.cuda.Event()
                 end_ev.record(comm)
@@ -397,6 +422,11 @@ class StageEngine:
                                 int(self.probe_ns[kind]), None, main.cuda_stream)
                     self.launches += 1
                 main.wait_event(end_ev)
+                if self.op_stamps:
+                    ri = self.words.n
+                    native.call("pf_read_globaltimer", self.words.stamp_ptr(), main.cuda_stream)
+                    rec.resume.append((clear_idx, ri))
+                    self.launches += 1
                 prev_end_us = end_us
                 continue
             off = self.model.offload
@@ -407,6 +437,10 @@ class StageEngine:
                 self.link.wait_until(main, base + start_us * US)
                 self.launches += 1
             with torch.cuda.stream(main):
+                if self.op_stamps:
+                    pi = self.words.n
+                    native.call("pf_sm_clock_probe", self.words.stamp_ptr(3), OP_PROBE_NS, main.cuda_stream)
+                    self.launches += 1
                 if ins.op == "F":
                     y = self.model.forward_mb(ins.mb, self.x_in[ins.mb])
                     if keep_outputs:
@@ -418,6 +452,12 @@ class StageEngine:
                     rec.end_stamp = self.words.n
                     native.call("pf_read_globaltimer", self.words.stamp_ptr(), main.cuda_stream)
                     self.launches += 1
+                if self.op_stamps:
+                    ei = rec.end_stamp if ins == self._last_compute() else self.words.n
+                    if ei != rec.end_stamp:
+                        native.call("pf_read_globaltimer", self.words.stamp_ptr(), main.cuda_stream)
+                        self.launches += 1
+                    rec.ops.append((ins.op, ins.mb, pi, ei))
             prev_end_us = end_us
         self.records.append(rec)
         return rec
@@ -434,7 +474,10 @@ class StageEngine:
         end = int(st[rec.end_stamp])
         bubbles = [(kind, int(st[si]), int(st[ci]), (id(self), rec.epoch, ci)) for kind, si, ci in rec.bubbles]
         last = max([end] + [b[2] for b in bubbles])
-        return {"start": start, "main_end": end, "step_end": last, "bubbles": bubbles}
+        out = {"start": start, "main_end": end, "step_end": last, "bubbles": bubbles}
+        if rec.ops:
+            out.update(op_timing(st, rec))
+        return out
 
     def reset_stamps(self) -> None:
         torch.cuda.synchronize()
@@ -447,9 +490,45 @@ class StageEngine:
         return (id(self), self.epoch, clear_idx)
 
 
-def measure_stage_times(model: GPTStage, reps: int = 5, warmup: int = 2) -> tuple[float, float]:
+OP_PROBE_NS = 4000  # SM-clock probe before every stamped op (4 us of one thread)
+
+
+def op_timing(st: torch.Tensor, rec: IterationRecord) -> dict:
+    """Per-op device timing of a stamped iteration: [(op, mb, start ns, end ns, SM MHz)]
+    and, per BUBBLE, the main stream's resume delay after the flag cleared (ns)."""
+    ops = []
+    for op, mb, pi, ei in rec.ops:
+        t0, dt, cyc = int(st[pi]), int(st[pi + 1]), int(st[pi + 2])
+        ops.append((op, mb, t0 + dt, int(st[ei]), cyc * 1e3 / dt if dt > 0 else 0.0))
+    resume = [int(st[ri]) - int(st[ci]) for ci, ri in rec.resume]
+    return {"ops": ops, "resume_ns": resume}
+
+
+def warm_up_gpu(ms: float = 1500.0) -> None:
+    """Keep the tensor cores busy for ~ms so the SM clock leaves its idle state before any
+    timing is taken (a fresh box starts at 120 MHz; measure_stage_times after 2 short reps
+    under-measured t_fwd/t_bwd by up to 28 %)."""
+    a = torch.randn(8192, 8192, device="cuda", dtype=torch.bfloat16)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    while True:
+        for _ in range(20):
+            a = (a @ a).mul_(1e-4)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t1.record()
+        t1.synchronize()
+        if t0.elapsed_time(t1) >= ms:
+            break
+    del a
+
+
+def measure_stage_times(model: GPTStage, reps: int = 7, warmup: int = 3,
+                        warm_ms: float = 1500.0) -> tuple[float, float]:
     """t_fwd / t_bwd of one microbatch on this stage (ms, CUDA events): the
-    per-stage timings PipelineConfig takes (pipeline.py:48-97)."""
+    per-stage timings PipelineConfig takes (pipeline.py:48-97). The GPU is warmed up
+    first; the medians of `reps` back-to-back repetitions are returned."""
+    if warm_ms > 0:
+        warm_up_gpu(warm_ms)
     c = model.c
     x = (torch.randn(c.micro_batch, c.seq, c.hidden, device="cuda") * 0.5).to(torch.bfloat16)
     g = (torch.randn(c.micro_batch, c.seq, c.hidden, device="cuda") * 1e-3).to(torch.bfloat16)
@@ -525,6 +604,13 @@ class NcclPipelineEngine:
         self._prefetched: Optional[tuple[torch.Tensor, torch.cuda.Event]] = None
         self._anchor_stamp = -1
         self.epoch = 0
+        # power-aware bubble tail (StageEngine.throttle_ns): the recv's completion time is not
+        # known in advance here, so the throttle deadline is the bubble's start stamp plus its
+        # measured duration (expected_ns, from the fill-off characterization) minus throttle_ns
+        self.throttle_ns = 0
+        self.throttle_ctas = 0
+        self.expected_ns: dict[int, int] = {}
+        self.timer = torch.cuda.Stream(priority=hi)
 
     # ---- P2P helpers (comm stream) ------------------------------------------------
     def _recv(self, src: int, group) -> tuple[torch.Tensor, torch.cuda.Event]:
@@ -560,6 +646,13 @@ class NcclPipelineEngine:
         native.call("pf_read_globaltimer", self.words.stamp_ptr(), self.comm.cuda_stream)
         start_ev = torch.cuda.Event()
         start_ev.record(self.comm)
+        k = 0 if kind is BubbleKind.FWD_BWD else 1
+        exp = self.expected_ns.get(k, 0)
+        if fill and self.throttle_ns > 0 and self.throttle_ctas >= 2 and exp > self.throttle_ns:
+            self.timer.wait_event(start_ev)
+            native.call("pf_flag_throttle_at", flag, self.words.stamps.data_ptr() + 8 * set_idx,
+                        int(exp - self.throttle_ns), int(self.throttle_ctas), self.timer.cuda_stream)
+            self.launches += 1
         got = None
         if end_recv is not None:
             got = self._recv(*end_recv)
@@ -569,7 +662,6 @@ class NcclPipelineEngine:
         end_ev = torch.cuda.Event()
         end_ev.record(self.comm)
         self.launches += 2
-        k = 0 if kind is BubbleKind.FWD_BWD else 1
         rec.bubbles.append((k, set_idx, clear_idx))
         rec.bubble_mem.append((k, torch.cuda.memory_allocated()))
         if fill and self.executor is not None:
@@ -730,8 +822,14 @@ def probe_bubbles(engine: "StageEngine", start_ms: float = 1.0, tol_ms: float = 
         return t1["main_end"] - t0["start"]
 
     run({})  # warm-up
-    base = min(run({}) for _ in range(2))
-    tol = int(tol_ms * 1e6)
+    base_runs = [run({}) for _ in range(3)]
+    base = min(base_runs)
+    # the decision threshold is at least twice the run-to-run spread of the unprobed
+    # iterations, and every probe is the min of two runs (clock noise only adds time)
+    tol = max(int(tol_ms * 1e6), 2 * (max(base_runs) - base))
+
+    def slowed(probe: dict) -> bool:
+        return min(run(probe), run(probe)) > base + tol
     kinds_present = {ins.kind for ins, s, e in engine.timeline if ins.op == "BUBBLE" and e > s}
     period_ns = engine.cfg.period_us * US
     out = []
@@ -741,33 +839,69 @@ def probe_bubbles(engine: "StageEngine", start_ms: float = 1.0, tol_ms: float = 
             out.append(0)
             continue
         ok, w = 0, int(start_ms * 1e6)
-        while w <= period_ns and run({k: w}) <= base + tol:
+        while w <= period_ns and not slowed({k: w}):
             ok, w = w, 2 * w
         lo, hi = ok, w
         for _ in range(refine):
             mid = (lo + hi) // 2
-            if run({k: mid}) <= base + tol:
+            if not slowed({k: mid}):
                 lo = mid
             else:
                 hi = mid
         out.append(lo // 1000)
-    return {"probed_us": out, "base_iteration_us": base // 1000, "probes": calls[0]}
+    return {"probed_us": out, "base_iteration_us": base // 1000, "probes": calls[0], "tol_us": tol // 1000}
 
 
 def characterize_stage(engine: "StageEngine", iterations: int = 3, fill_fraction: float = 0.68,
                        reserve_bytes: int = 2 << 30):
-    """Run `iterations` fill-off iterations of an emulated stage and characterize its bubbles."""
+    """Run `iterations` fill-off iterations of an emulated stage and characterize its bubbles.
+
+    The report also carries the stage's in-situ op timing (per-op stamps): the medians of its
+    own forward / backward durations inside the iterations, and `expected_bubbles_us` -- the
+    neighbour's (analytic) arrival minus the measured end of the stage's own op before the
+    BUBBLE. A stage that computes faster or slower than measure_stage_times said reaches its
+    BUBBLE earlier or later, and the measured bubble grows or shrinks by exactly that drift."""
+    import statistics
+
     from .schedule import build_bubble_cycle
 
     timings, records = [], []
-    for k in range(iterations + 1):  # the first iteration warms the main job up (discarded)
-        engine.reset_stamps()
-        engine.set_anchor()
-        rec = engine.run_iteration(0, fill=False)
-        t = engine.record_timing(rec)
-        if k:
-            timings.append(t)
-            records.append(rec)
+    stamped = engine.op_stamps
+    engine.op_stamps = True
+    try:
+        for k in range(iterations + 1):  # the first iteration warms the main job up (discarded)
+            engine.reset_stamps()
+            engine.set_anchor()
+            rec = engine.run_iteration(0, fill=False)
+            t = engine.record_timing(rec)
+            if k:
+                timings.append(t)
+                records.append(rec)
+    finally:
+        engine.op_stamps = stamped
     _, total = torch.cuda.mem_get_info()
-    return characterize_bubbles(engine.stage, timings, records, fill_fraction, total, reserve_bytes,
-                                analytic=build_bubble_cycle(engine.cfg, engine.stage))
+    cycle, rep = characterize_bubbles(engine.stage, timings, records, fill_fraction, total, reserve_bytes,
+                                      analytic=build_bubble_cycle(engine.cfg, engine.stage))
+    fwd = [(t1 - t0) / 1e6 for t in timings for op, _, t0, t1, _ in t["ops"] if op == "F"]
+    bwd = [(t1 - t0) / 1e6 for t in timings for op, _, t0, t1, _ in t["ops"] if op == "B"]
+    rep["insitu_t_fwd_ms"] = statistics.median(fwd) if fwd else None
+    rep["insitu_t_bwd_ms"] = statistics.median(bwd) if bwd else None
+    rep["sm_mhz"] = statistics.median(m for t in timings for *_, m in t["ops"]) if timings else None
+    # expected bubble durations from the stage's own stamps
+    tl = engine.timeline
+    exp = {0: [], 1: []}
+    for t in timings:
+        ends = [t1 for _, _, _, t1, _ in t["ops"]]
+        k_op = -1
+        b_i = 0
+        for ins, s_us, e_us in tl:
+            if ins.op == "BUBBLE":
+                if b_i < len(t["bubbles"]):
+                    kind, t_set, t_clr, _ = t["bubbles"][b_i]
+                    own_ready = ends[k_op] if k_op >= 0 else t["start"]
+                    exp[kind].append(max(0, t["start"] + e_us * US - own_ready) // 1000)
+                b_i += 1
+            else:
+                k_op += 1
+    rep["expected_bubbles_us"] = [int(statistics.median(exp[k])) if exp[k] else 0 for k in (0, 1)]
+    return cycle, rep

@@ -78,6 +78,9 @@ class BubbleRecord:
     tag: object = None
     sample_eq: float = 0.0  # completed batches x their partition's share of the model (all partitions)
     ran_ahead: bool = False  # the bubble also enqueued batches of the next partition
+    # preempted bubbles: %globaltimer when the last CTA of the yielded batch's GEMMs exited
+    # (in-kernel stamps), i.e. when the fill released the SMs -- the yield latency's end
+    last_work_end_ns: int = 0
 
 
 @dataclass
@@ -693,7 +696,8 @@ class Executor:
         if self.timing and done > 0 and not aborted:
             # in-kernel stamps of the bubble's last batch: (FLOPs, ms) of every GEMM node
             last_cnt = pend.batches[len(pend.batches) - 1][1]
-            ch = self._chains.get((pend.part, last_cnt, pend.slot.flag_ptr or None))
+            last_part = (pend.parts or [pend.part])[-1]  # a run-ahead's last batch is in part + 1
+            ch = self._chains.get((last_part, last_cnt, pend.slot.flag_ptr or None))
             if ch is not None and ch.gemm_flops:
                 n = len(ch.units)
                 native.call("pf_stage_d2h", self._stamps_host.ptr, self._stamps.data_ptr(), 16 * n,
@@ -731,6 +735,7 @@ class Executor:
                     pr.next_sample = max(pr.next_sample, first + cnt)
             elif k == done and aborted:
                 ch = self._chains[(parts[k], cnt, pend.slot.flag_ptr or None)]
+                rec.last_work_end_ns = self._last_work_end(ch)
                 cur = w[_CURSOR0:_CURSOR0 + len(ch.units)]
                 resume_node = len(ch.units)
                 for j, (u, _) in enumerate(ch.units):
@@ -767,6 +772,21 @@ class Executor:
                 self.prewarm()
         self.records.append(rec)
         return rec
+
+    def _last_work_end(self, ch: _Chain) -> int:
+        """Latest in-kernel end stamp over the GEMM nodes of the batch that yielded. Later
+        launches of the aborted chain exit before stamping and chain_begin leaves the stamps
+        alone once the abort word is set, so these are the yielded batch's own."""
+        nodes = sorted(ch.gemm_flops)
+        if not nodes:
+            return 0
+        n = len(ch.units)
+        native.call("pf_stage_d2h", self._stamps_host.ptr, self._stamps.data_ptr(), 16 * n,
+                    self.stream.cuda_stream)
+        self.stream.synchronize()
+        sh = self._stamps_host.tensor
+        ends = [int(sh[i, 1]) for i in nodes if 0 < int(sh[i, 0]) <= int(sh[i, 1])]
+        return max(ends) if ends else 0
 
     def staging_stats(self, since: int = 0) -> dict:
         """H2D weight staging since `self.stagings[since]`: bytes, device ms (copy-stream

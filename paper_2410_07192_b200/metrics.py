@@ -88,3 +88,43 @@ def mean_slowdown(on: dict[int, Iterable[float]], off: dict[int, Iterable[float]
         if s in off:
             vals.append(statistics.mean(v) / statistics.mean(off[s]) - 1.0)
     return statistics.mean(vals) if vals else None
+
+
+def slowdown_stats(on: dict[int, Sequence[float]], off: dict[int, Sequence[float]]) -> dict:
+    """Main-job slowdown from interleaved fill-on / fill-off iterations of every stage.
+
+    In a pipeline the slowest stage paces all of them, so the headline `max` is the
+    maximum over stages of mean(on) / mean(off) - 1 (the reference's OverheadModel is one
+    factor for the whole job, sim.py:32-56); `mean` is kept as a secondary figure.
+    `noise_floor` is the same statistic between the two halves of the fill-off iterations
+    (off[0::2] vs off[1::2]) -- what the measurement reports when nothing changed."""
+    import statistics
+
+    per_stage, noise = {}, {}
+    for s in sorted(on):
+        if s not in off or not on[s] or not off[s]:
+            continue
+        per_stage[s] = statistics.mean(on[s]) / statistics.mean(off[s]) - 1.0
+        a, b = list(off[s])[0::2], list(off[s])[1::2]
+        if a and b:
+            noise[s] = abs(statistics.mean(a) / statistics.mean(b) - 1.0)
+    if not per_stage:
+        return {"max": None, "mean": None, "argmax_stage": None, "noise_floor": None, "per_stage": {}}
+    worst = max(per_stage, key=lambda s: per_stage[s])
+    return {"max": per_stage[worst], "mean": statistics.mean(per_stage.values()), "argmax_stage": worst,
+            "noise_floor": max(noise.values()) if noise else None,
+            "per_stage": {str(s): v for s, v in per_stage.items()},
+            "per_stage_noise": {str(s): v for s, v in noise.items()},
+            "iterations": {"fill_on": sum(len(v) for v in on.values()),
+                           "fill_off": sum(len(v) for v in off.values())}}
+
+
+def distribution(values: Sequence[float]) -> dict:
+    """n, p50, p99 and max of a sample (nearest-rank percentiles)."""
+    v = sorted(values)
+    if not v:
+        return {"n": 0, "p50": None, "p99": None, "max": None}
+
+    def rank(q: float) -> float:
+        return v[min(len(v) - 1, max(0, int(-(-q * len(v) // 1)) - 1))]
+    return {"n": len(v), "p50": rank(0.50), "p99": rank(0.99), "max": v[-1]}

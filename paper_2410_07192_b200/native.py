@@ -80,6 +80,8 @@ _SIGNATURES: dict[str, tuple] = {
     "pf_flag_clear_at": (c_int, [c_void_p, c_void_p, c_uint64, c_void_p, c_void_p]),
     "pf_wait_until": (c_int, [c_void_p, c_uint64, c_void_p, c_void_p]),
     "pf_read_globaltimer": (c_int, [c_void_p, c_void_p]),
+    "pf_sm_clock_probe": (c_int, [c_void_p, c_uint64, c_void_p]),
+    "pf_flag_throttle_at": (c_int, [c_void_p, c_void_p, c_uint64, c_uint32, c_void_p]),
     "pf_host_alloc_pinned": (c_int, [c_uint64, POINTER(c_void_p)]),
     "pf_host_free_pinned": (c_int, [c_void_p]),
     "pf_stage_h2d": (c_int, [c_void_p, c_void_p, c_uint64, c_void_p]),

@@ -215,6 +215,23 @@ def cycle_from_measurements(
     return BubbleCycle(bubbles, int(period_us), stage_id, int(unfillable_us))
 
 
+def with_cooldown(cycle: BubbleCycle, cooldown_us: int, min_duration_us: int = 0) -> BubbleCycle:
+    """The same cycle with the usable time of every bubble longer than min_duration_us capped
+    at duration - cooldown_us.
+
+    Power-aware usable time: under the board power cap the SM clock the main
+    job resumes at depends on the power the end of the preceding bubble drew. An idle tail
+    before the recv lets the power controller raise the clock again. The controller needs
+    ~40 ms to react, so a short bubble gains nothing from a tail and is filled whole. The
+    reference's usable rule (pipeline.py:205, floor(duration * fill_fraction)) applies first."""
+    if cooldown_us <= 0:
+        return cycle
+    bubbles = tuple(b if b.duration_us <= min_duration_us else
+                    BubbleSpec(b.duration_us, max(0, min(b.usable_us, b.duration_us - int(cooldown_us))),
+                               b.free_mem_bytes, b.kind) for b in cycle.bubbles)
+    return BubbleCycle(bubbles, cycle.period_us, cycle.stage_id, cycle.unfillable_us)
+
+
 # ---------------------------------------------------------------------------
 # instruction streams
 
@@ -306,6 +323,38 @@ def _busy_spans(config: PipelineConfig) -> list[list[tuple[int, int, str]]]:
 
 
 _enumerate_busy_spans = _busy_spans
+
+
+def replay_makespan(config: PipelineConfig, duration) -> float:
+    """One iteration's makespan of the p-stage pipeline when op (stage, op, mb) takes
+    `duration(stage, op, mb)` (any unit): the dependency replay of _busy_spans with
+    per-op instead of uniform times. Used to compose a pipeline iteration time from the
+    per-op device timings measured on each stage (bench.py: main-job slowdown)."""
+    p = config.num_stages
+    orders = _instruction_sequences(config)
+    done: dict[tuple[str, int, int], float] = {}
+    pos = [0] * p
+    clock = [0.0] * p
+    pending = sum(len(o) for o in orders)
+    while pending:
+        advanced = False
+        for s in range(p):
+            while pos[s] < len(orders[s]):
+                op, j = orders[s][pos[s]]
+                if op == "F":
+                    dep = None if s == 0 else ("F", s - 1, j)
+                else:
+                    dep = ("F", s, j) if s == p - 1 else ("B", s + 1, j)
+                if dep is not None and dep not in done:
+                    break
+                start = max(clock[s], 0.0 if dep is None else done[dep])
+                clock[s] = done[(op, s, j)] = start + duration(s, op, j)
+                pos[s] += 1
+                pending -= 1
+                advanced = True
+        if not advanced:  # pragma: no cover - valid schedules never deadlock
+            raise AssertionError("dependency deadlock: invalid schedule")
+    return max(clock)
 
 
 def brute_force_schedule_timeline(config: PipelineConfig) -> list[list[tuple[int, int]]]:

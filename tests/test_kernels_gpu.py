@@ -230,3 +230,46 @@ def test_gemm_tail_halves_resume_exact(K, m, n, k, variant):
         mask = y != 0
         assert mask.any() and torch.equal(y[mask], ref[mask])
     assert torch.equal(y, ref)
+
+
+@pytest.mark.parametrize("m,n,k,v", [(16384, 1024, 1024, 8), (16384, 4096, 1024, 16), (4096, 3072, 768, 2),
+                                     (16384, 4096, 1024, 3)])
+def test_gemm_throttled_flag_is_exact(K, m, n, k, v):
+    """Flag value v >= 2 (power-aware bubble tail): at most v CTAs (v / 2 CTA pairs) claim
+    tiles, no abort is raised, every unit still runs once, and the result equals the
+    unthrottled launch bit for bit -- single-CTA (tail halves) and CTA-pair variants."""
+    g = torch.Generator().manual_seed(31)
+    x = _bf16(m, k, gen=g).cuda()
+    w = _bf16(n, k, scale=k ** -0.5, gen=g).cuda()
+    b = _bf16(n, gen=g).cuda()
+    ref = K.linear(x, w, b, gelu=True)
+    words = torch.zeros(8, dtype=torch.int32, device="cuda")
+    flag, abort, cursor = (words[i:i + 1] for i in range(3))
+    ctl = K.KernelCtl(flag.data_ptr(), abort.data_ptr(), cursor.data_ptr())
+    y = torch.zeros(m, n, dtype=torch.bfloat16, device="cuda")
+    flag.fill_(v)
+    K.linear(x, w, b, gelu=True, out=y, ctl=ctl)
+    torch.cuda.synchronize()
+    assert abort.item() == 0 and cursor.item() >= K.gemm_units(m, n, k)
+    assert torch.equal(y, ref)
+
+
+def test_flag_throttle_at_respects_a_closed_bubble(K):
+    """pf_flag_throttle_at: 1 -> v at the deadline; a flag already cleared (0) stays 0."""
+    import ctypes
+
+    from paper_2410_07192_b200 import native
+
+    s = torch.cuda.current_stream().cuda_stream
+    for start, want in ((1, 7), (0, 0)):
+        flag = ctypes.c_void_p()
+        native.call("pf_flag_create", ctypes.byref(flag))
+        native.call("pf_flag_write_on_stream", flag, start, s)
+        anchor = torch.zeros(1, dtype=torch.int64, device="cuda")
+        native.call("pf_read_globaltimer", anchor.data_ptr(), s)
+        native.call("pf_flag_throttle_at", flag, anchor.data_ptr(), 20_000, 7, s)
+        val = torch.full((1,), -1, dtype=torch.int32).pin_memory()
+        native.call("pf_stage_d2h", val.data_ptr(), flag, 4, s)
+        torch.cuda.synchronize()
+        native.call("pf_flag_destroy", flag)
+        assert int(val.item()) == want
