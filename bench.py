@@ -177,6 +177,17 @@ def measure_h2d_gbs(nbytes: int = 256 << 20, reps: int = 5) -> float:
     return nbytes * reps / e0.elapsed_time(e1) / 1e6
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -188,28 +199,87 @@ def dist_env():
 
 
 def cpu_fill_throughput(batch: int, reps: int, threads: int | None = None) -> dict:
-    """The oracle CPU execution of the fill job (BERT-large fp32 forward, torch CPU)."""
+    """The oracle CPU execution of the fill job (BERT-large fp32 forward, torch CPU), with
+    the oracle's own random weights and token ids: nothing of this package (its models,
+    kernels or native library) is on this path."""
     import torch
 
     from oracle import fill_ref
-    from paper_2410_07192_b200.fillmodels import BERT_LARGE, bert, synthetic_ids
 
     if threads:
         torch.set_num_threads(threads)
-    model = bert(BERT_LARGE, seed=0)
-    params = [model.oracle_params(i) for i in range(len(model))]
-    cfg = model.cfg
+    h, heads, ffn, layers, vocab, seq = 1024, 16, 4096, 24, 30522, 128  # BERT-large
+    emb, params = fill_ref.bert_random_params(h, ffn, layers, vocab, seq, seed=0)
+    g = torch.Generator().manual_seed(1)
     times = []
     for r in range(reps):
-        ids = synthetic_ids(0, r * batch, batch, cfg.seq, cfg.vocab)
+        ids = torch.randint(0, vocab, (batch, seq), generator=g, dtype=torch.int32)
         t0 = time.perf_counter()
         with torch.no_grad():
-            x = fill_ref.bert_embeddings(ids, params[0], cfg.eps)
-            for i in range(1, len(model)):
-                x = fill_ref.bert_layer(x, params[i], cfg.heads, cfg.eps)
+            x = fill_ref.bert_embeddings(ids, emb, 1e-12)
+            for p in params:
+                x = fill_ref.bert_layer(x, p, heads, 1e-12)
             _ = x[:, 0, :].sum().item()
         times.append(time.perf_counter() - t0)
     return {"times": times, "batch": batch, "threads": torch.get_num_threads()}
+
+
+def control_plane_timings(pkg, partition_mod, budget_s: float = 8.0) -> dict:
+    """the control plane on the host CPU (single thread, the GIL) on identical
+    inputs -- build_bubble_cycle (8 stages), dp_optimal_plan (BERT-base / BERT-large /
+    XLM-R-XL synthetic profiles), greedy_pack_model, route_avg_jct (8 Coordinators with
+    queued jobs) and run_sim (48 jobs). `pkg` is the reference's bubblefill (baseline/_ref)
+    or this package; both expose the same API (bubblefill/__init__.py:5-51). Medians in ms."""
+    def timed(fn, reps):
+        ts = []
+        t_end = time.perf_counter() + budget_s / 6
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+            if time.perf_counter() > t_end:
+                break
+        return 1e3 * statistics.median(ts)
+
+    cfg = pkg.PipelineConfig(8, 8, 7.2, 16.1, pkg.ScheduleKind.ONE_F_ONE_B, 4_500_000_000, 4_500_000_000, 0.68)
+    profs = {n: pkg.synth_profile(pkg.ModelTemplate.by_name(n), kind=pkg.JobKind.BATCH_INFERENCE)
+             for n in ("bert_base", "bert_large", "xlm_roberta_xl")}
+    cyc = pkg.build_bubble_cycle(cfg, 3)
+    out = {"build_bubble_cycle_8_stages_ms": timed(lambda: [pkg.build_bubble_cycle(cfg, s) for s in range(8)], 200)}
+    for n, prof in profs.items():
+        out[f"dp_optimal_plan_{n}_L{len(prof.layers)}_ms"] = timed(lambda p=prof: pkg.dp_optimal_plan(p, cyc), 20)
+    out["greedy_pack_model_bert_large_bs8_ms"] = timed(
+        lambda: partition_mod.greedy_pack_model(profs["bert_large"], cyc, 8), 50)
+    period = cfg.period_us / 1e6
+    names = list(profs)
+    jobs = [pkg.JobSpec(f"j{i}", i * 0.3 * period, profs[names[i % 3]], pkg.JobKind.BATCH_INFERENCE,
+                        2000 + 500 * (i % 7)) for i in range(48)]
+
+    def route():
+        cs = [pkg.Coordinator(s, pkg.build_bubble_cycle(cfg, s), 1) for s in range(8)]
+        for j in jobs[:40]:
+            cs[int(j.id[1:]) % 8].admit(j)
+        t0 = time.perf_counter()
+        pkg.route_avg_jct(cs, jobs[40], jobs[40].arrival_s)
+        return time.perf_counter() - t0
+    rt = [route() for _ in range(5)]
+    out["route_avg_jct_8_coords_40_queued_ms"] = 1e3 * statistics.median(rt)
+    out["run_sim_48_jobs_ms"] = timed(lambda: pkg.run_sim(pkg.SimConfig(cfg), jobs), 3)
+    return out
+
+
+def reference_package():
+    """The unmodified reference (`pip install --target baseline/_ref /root/reference/pkg`,
+    DESIGN.md §5), or None when it is not installed."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "bubblefill")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import bubblefill
+    import bubblefill.partition
+
+    return bubblefill, bubblefill.partition
 
 
 def run_reference(args) -> None:
@@ -223,6 +293,10 @@ def run_reference(args) -> None:
     res = cpu_fill_throughput(batch, args.warmup + args.steps, threads)
     timed = res["times"][args.warmup:]
     value = batch * len(timed) / sum(timed)
+    ref = reference_package()
+    control = ({"impl": "reference (baseline/_ref bubblefill, unmodified)", "cores": 1,
+                **control_plane_timings(*ref)} if ref else
+               {"unavailable": "baseline/_ref not installed (pip install --target baseline/_ref /root/reference/pkg)"})
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -234,9 +308,14 @@ def run_reference(args) -> None:
                          "sample": f"{len(timed)} batches of {batch} BERT-large sequences, torch CPU fp32 "
                                    f"(oracle/fill_ref.py; the reference has no fill-compute code)"},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "control_plane_cpu_baseline": control,
+        "cpu_model": cpu_model(),
     }
     _ = torch
     print(json.dumps(line), flush=True)
+    if args.out:
+        with open(args.out, "w") as fh:
+            fh.write(json.dumps(line) + "\n")
 
 
 # --------------------------------------------------------------------------- our arm
@@ -1129,7 +1208,14 @@ def main() -> None:
         t = res["times"][1:]
         cpu = {"value": 4 * len(t) / sum(t), "unit": "samples/s", "cores": res["threads"], "kind": "port",
                "sample": "2 batches x 4 BERT-large seq-128 sequences, torch CPU fp32 oracle "
-                         "(oracle/fill_ref.py), after 1 warm-up batch"}
+                         "(oracle/fill_ref.py), after 1 warm-up batch", "cpu_model": cpu_model()}
+        ref = reference_package()
+        cpu["control_plane"] = {
+            "reference": ({"cores": 1, **control_plane_timings(*ref)} if ref else "baseline/_ref not installed"),
+            "ours": {"cores": 1, **control_plane_timings(pf, __import__("paper_2410_07192_b200.planner",
+                                                                        fromlist=["x"]))},
+            "note": "the same control-plane calls on identical inputs, single-threaded Python on the host: "
+                    "the reference package vs this package's bit-exact restatement (BASELINE.md §4)"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,

@@ -107,6 +107,24 @@ def bert_embeddings(ids: torch.Tensor, p: dict, eps: float = 1e-12) -> torch.Ten
     return embedding_ln(ids, p["word"], p["pos"], p["type"], p["ln_g"], p["ln_b"], eps)
 
 
+def bert_random_params(hidden: int, ffn: int, layers: int, vocab: int, seq: int, seed: int = 0):
+    """Random-init BERT weights for the CPU baseline (N(0, 0.02), LN gamma 1 / beta 0 as the
+    synthetic-input contract says): (embedding dict, [layer dicts]) in the
+    shapes bert_embeddings / bert_layer take. Independent of the product package."""
+    g = torch.Generator().manual_seed(seed)
+
+    def n(*shape):
+        return torch.randn(*shape, generator=g) * 0.02
+
+    h = hidden
+    emb = {"word": n(vocab, h), "pos": n(seq, h), "type": n(2, h), "ln_g": torch.ones(h), "ln_b": torch.zeros(h)}
+    params = [{"qkv_w": n(3 * h, h), "qkv_b": torch.zeros(3 * h), "out_w": n(h, h), "out_b": torch.zeros(h),
+               "ln1_g": torch.ones(h), "ln1_b": torch.zeros(h), "ffn1_w": n(ffn, h), "ffn1_b": torch.zeros(ffn),
+               "ffn2_w": n(h, ffn), "ffn2_b": torch.zeros(h), "ln2_g": torch.ones(h), "ln2_b": torch.zeros(h)}
+              for _ in range(layers)]
+    return emb, params
+
+
 def run_sequential(modules: list, x, lo: int, hi: int):
     """Run modules[lo:hi] in order — one partition of the linearized model
     (ExecutionPlan partition [lo, hi), pkg/src/bubblefill/partition.py:64-86)."""

@@ -110,6 +110,14 @@ class PinnedBuffer:
         return self._p.value
 
     def close(self) -> None:
+        """Free the page-locked memory. `tensor` (and every view of it) is invalid after."""
         if self._p:
             native.call("pf_host_free_pinned", self._p)
             self._p = ctypes.c_void_p()
+            self.tensor = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -42,7 +42,8 @@ from .planner import ExecutionPlan
 _CTL_WORDS = 64 + 4096  # [0]=abort, [1]=batches done, [2]=run-ahead staged, [8..12)=timestamps (2 x u64),
 #                        [64..)=cursors
 _CURSOR0 = 64
-MAX_BATCHES = 64  # per bubble (device batch descriptors)
+MAX_BATCHES = 256  # per bubble (device batch descriptors): planned + a resumed + run-ahead batches
+STARVE_LIMIT = 256  # consecutive bubbles without progress before FillStarvation
 MAX_NODES = 4096
 # PF_EXEC_GRAPHS=0 replays chains node by node (pf_chain_launch) instead of as gated CUDA
 # graphs: for profilers that do not see kernels inside conditional graph nodes (ncu)
@@ -50,6 +51,12 @@ _USE_GRAPHS = __import__("os").environ.get("PF_EXEC_GRAPHS", "1") != "0"
 # modules per gated graph segment (gate kernel + conditional IF node); see DESIGN.md §3
 _SEG_MODULES = int(__import__("os").environ.get("PF_SEG_MODULES", "4"))
 DESC_WORDS = 4  # PF_DESC_WORDS: (input, result, aux input, -) byte offsets per batch
+
+
+class FillStarvation(RuntimeError):
+    """The bubbles are too short for the fill to make any progress: the same unit of work
+    was yielded STARVE_LIMIT times in a row (e.g. bubbles shorter than one GEMM tile, or a
+    profiler serialising the timer that closes every bubble ahead of the fill)."""
 
 
 @dataclass
@@ -101,6 +108,7 @@ class _Pending:
     part: int
     has_resume: bool = False
     parts: list[int] = None  # partition of every batch (run-ahead appends partition part + 1)
+    progress_key: tuple = ()  # (part, next sample, resume point, resume cursor) when enqueued
 
 
 class _Chain:
@@ -139,8 +147,11 @@ class Executor:
     """One per GPU (pipeline-stage worker). Not thread-safe; driven by the engine."""
 
     def __init__(self, arena_bytes: int, *, priority: int = 1, job_seed: int = 0,
-                 activation_store: str = "auto", run_ahead: bool = True):
+                 activation_store: str = "auto", run_ahead: bool = True, use_graphs: Optional[bool] = None):
         native.require_device()
+        # gated CUDA graphs per batch (default), or node-by-node launches (PF_EXEC_GRAPHS=0 /
+        # use_graphs=False): profilers do not see kernels inside conditional graph nodes
+        self.use_graphs = _USE_GRAPHS if use_graphs is None else bool(use_graphs)
         self.arena = Arena(arena_bytes)
         lo_prio, hi_prio = torch.cuda.Stream.priority_range()
         self.stream = torch.cuda.Stream(priority=hi_prio if priority == 0 else lo_prio)
@@ -188,6 +199,9 @@ class Executor:
         self._layouts: dict[tuple, dict] = {}
         # weight-partition stagings: (bytes, start event, end event) on the copy stream
         self.stagings: list[tuple[int, torch.cuda.Event, torch.cuda.Event]] = []
+        self._aux_host: Optional[PinnedBuffer] = None
+        self.starved = 0  # consecutive settled bubbles that enqueued work but made no progress
+        self._cursor_now = -1  # the resume node's cursor as of the last settle
 
     # ------------------------------------------------------------------ loading
 
@@ -214,6 +228,10 @@ class Executor:
         and cached for executables seen before."""
         if self.pending is not None:
             self.settle()
+        worst = max((e.num_batches for p in item.plan.partitions for e in p.per_bubble), default=0)
+        if 2 * worst + 1 > MAX_BATCHES:  # planned + a resumed batch + a run-ahead partition's
+            raise ValueError(f"plan has {worst} batches in one bubble; the executor's batch descriptor "
+                             f"table holds {MAX_BATCHES} (max_batches_per_bubble <= {(MAX_BATCHES - 1) // 2})")
         n = item.entry.size
         key = (id(model), id(item.plan))
         if key != self._layout_key or n > self._cap:
@@ -221,12 +239,18 @@ class Executor:
             if key in self._layouts and n <= self._layouts[key]["_cap"]:
                 self._restore_layout(key)
             else:
-                self._layouts.pop(key, None)
+                stale = self._layouts.pop(key, None)
+                if stale is not None:  # cached for fewer samples: its buffers and graphs go
+                    self.stream.synchronize()
+                    self.copy_stream.synchronize()
+                    _close_layout(stale)
                 self.model, self.plan = model, item.plan
                 self._layout(n)
                 self._layout_key = key
         self.item = item
         self.progress = _Progress()
+        self._cursor_now = -1
+        self.starved = 0
         self._in_host.tensor[:n].copy_(self.model.make_inputs(self.job_seed, item.entry.lo - 1, n))
         if self._aux_host is not None:
             self._aux_host.tensor[:n].copy_(self.model.make_aux(self.job_seed, item.entry.lo - 1, n))
@@ -239,12 +263,12 @@ class Executor:
         try:
             self._carve(cap)
         except native.ArenaExhausted:
+            self.stream.synchronize()  # the arena is about to be re-carved, host buffers freed
+            self.copy_stream.synchronize()
             for saved in self._layouts.values():
                 _close_layout(saved)
             self._layouts = {}
             self._chains = {}
-            self.stream.synchronize()  # the arena is about to be re-carved
-            self.copy_stream.synchronize()
             self.arena.reset()
             self._carve(cap)
 
@@ -532,10 +556,12 @@ class Executor:
         entry = part.per_bubble[slot.index] if slot.index < len(part.per_bubble) else None
         n_total = self.item.entry.size
         batches: list[tuple[int, int, int]] = []
+        if entry is None or entry.num_batches == 0:
+            return prev  # the plan gives this partition no work in this bubble (e.g. zero-length)
         if pr.resume is not None:
             batches.append(pr.resume)
         start = pr.next_sample
-        if entry is not None and entry.num_batches > 0:
+        if entry.num_batches > 0:
             for _ in range(entry.num_batches - (1 if pr.resume is not None else 0)):
                 if start >= n_total:
                     break
@@ -606,7 +632,7 @@ class Executor:
                 if parts[k] != pr.part and parts[k - 1] == pr.part:
                     self._stage_in_stream(parts[k], st)  # run-ahead: after this partition's batches
                 ch = self._chain(parts[k], cnt, flag)
-                if node > 0 or not _USE_GRAPHS:  # resume a yielded batch at its first incomplete node
+                if node > 0 or not self.use_graphs:  # resume a yielded batch at its first incomplete node
                     native.call("pf_chain_launch", ch.h, flag, abort_ptr if flag else None,
                                 cursors if flag else None, done_ptr, node, 0, 0, st.cuda_stream)
                     launches += len(ch.units) - node + 1
@@ -618,7 +644,7 @@ class Executor:
         ev = torch.cuda.Event()
         ev.record(st)
         self.pending = _Pending(slot, batches, ev, launches, pr.part, has_resume=pr.resume is not None,
-                                parts=parts)
+                                parts=parts, progress_key=(pr.part, pr.next_sample, pr.resume, self._cursor_now))
         self.kernel_launches += launches
         return prev
 
@@ -760,6 +786,9 @@ class Executor:
         rec.samples_done = samples
         rec.samples_completed = completed_last
         self.samples_completed += completed_last
+        key_after = (pr.part, pr.next_sample, pr.resume, self._resume_cursor(pend, parts, w))
+        self.starved = self.starved + 1 if (done == 0 and aborted and key_after == pend.progress_key) else 0
+        self._cursor_now = key_after[3]
         if pr.resume is None and pr.next_sample >= n_total:
             if pr.part == len(self.plan.partitions) - 1:
                 pr.finished = True
@@ -771,7 +800,21 @@ class Executor:
                 self._stage_partition(pr.part)
                 self.prewarm()
         self.records.append(rec)
+        if self.starved >= STARVE_LIMIT:
+            raise FillStarvation(f"no fill progress in {self.starved} consecutive bubbles (partition "
+                                 f"{pr.part}, resume point {pr.resume}): bubbles shorter than one unit")
         return rec
+
+    def _resume_cursor(self, pend: _Pending, parts: list, w: torch.Tensor) -> int:
+        """Cursor of the resume node (its claimed units) -- progress inside one node."""
+        pr = self.progress
+        if pr.resume is None:
+            return -1
+        first, cnt, node = pr.resume
+        ch = self._chains.get((pr.part, cnt, pend.slot.flag_ptr or None))
+        if ch is None or node >= len(ch.units):
+            return -1
+        return int(w[_CURSOR0 + node])
 
     def _last_work_end(self, ch: _Chain) -> int:
         """Latest in-kernel end stamp over the GEMM nodes of the batch that yielded. Later
@@ -805,23 +848,35 @@ class Executor:
         return self._results.tensor[: self.item.entry.size]
 
     def close(self) -> None:
+        """Release everything: graphs and chains of every cached executable, their pinned
+        host buffers, the control-block mirrors and the arena."""
         self.settle()
         torch.cuda.synchronize()
-        self._drop_chains()
-        for g in getattr(self, "_gated", {}).values():
-            native.call("pf_staging_destroy", g)
-        self._gated = {}
+        if self._layout_key is not None:
+            self._save_layout()
+            self._layout_key = None
         for saved in self._layouts.values():
             _close_layout(saved)
         self._layouts = {}
+        self._chains = {}
+        self._gated = {}
+        for buf in (self._ctl_host, self._desc_host, self._stamps_host):
+            buf.close()
         self.arena.close()
 
 
 def _close_layout(saved: dict) -> None:
+    """Destroy one cached executable: its chains / graphs and its pinned host buffers."""
     for ch in saved["_chains"].values():
         ch.close()
     for g in saved.get("_gated", {}).values():
         native.call("pf_staging_destroy", g)
+    for name in ("_in_host", "_results", "_aux_host"):
+        buf = saved.get(name)
+        if buf is not None:
+            buf.close()
+    for buf in saved.get("_store_host") or []:
+        buf.close()
 
 
 def _pad256(n: int) -> int:

@@ -191,10 +191,13 @@ class FillService:
         for r in range(max_rounds):
             t0 = r * self.period_s
             t1 = t0 + self.period_s
-            # arrivals of this round are routed at their own arrival time
-            while pending and pending[0].arrival_s < t1:
+            # causality: a job is routed and dispatched at the first round start at or after its
+            # arrival (a job arriving mid-round waits for the next round, as a real service
+            # dispatching at iteration boundaries would); 1 ns of slack absorbs the float
+            # rounding of arrivals placed exactly on an iteration boundary
+            while pending and pending[0].arrival_s <= t0 + 1e-9:
                 job = pending.pop(0)
-                cidx = self._route(job, job.arrival_s)
+                cidx = self._route(job, max(job.arrival_s, t0))
                 ok = False
                 if cidx is not None:
                     try:

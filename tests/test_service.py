@@ -180,3 +180,28 @@ def test_report_files_follow_reference_layout(tmp_path):
     assert {k: doc[k] for k in plan_to_dict(plan)} == json.loads(json.dumps(plan_to_dict(plan)))
     write_manifest(tmp_path / "m", "serve", 0, {"x": 1})
     assert json.loads((tmp_path / "m" / "manifest.json").read_text())["config"] == {"x": 1}
+
+
+def test_service_never_starts_a_job_before_it_arrives():
+    """Arrivals in the middle of an iteration are dispatched at the next iteration start:
+    start_s >= arrival_s for every job, and no job waits more than one period to start
+    when a stage is idle (sim.py:213-261 orders events by time; here time is quantised)."""
+    cfg = _pipeline()
+    period = cfg.period_us / 1e6
+    jobs = [pf.JobSpec(j.id, (i * 0.37 + 0.11) * period, j.model, j.kind, j.samples)
+            for i, j in enumerate(_jobs(cfg))]
+    scfg = ServiceConfig(cfg, routing="avg_jct", ordering=SJF)
+    exs = [_StandIn(period) for _ in range(cfg.num_stages)]
+
+    def run_iteration(stage, ex):
+        ex.left -= 1
+        ex.records.append(BubbleRecord(0, 1, 1, 1, False, 100, 900, tag=(stage,)))
+        return {"start": 0, "main_end": 1000, "step_end": 1000, "bubbles": [(0, 0, 1000, (stage,))]}
+
+    rep = FillService(scfg, {j.model.name: j.model.name for j in jobs}, exs, run_iteration).run(jobs, 10_000)
+    assert not rep.unfinished and not rep.rejected
+    for r in rep.per_job.values():
+        assert r.start_s >= r.arrival_s, r
+        assert r.completion_s > r.start_s
+    first = min(rep.per_job.values(), key=lambda r: r.arrival_s)
+    assert first.start_s - first.arrival_s < period + 1e-9

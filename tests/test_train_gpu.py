@@ -85,7 +85,7 @@ def test_resnet50_training_step_matches_torchvision_module_by_module():
 
     Why per module: with train-mode BatchNorm and random weights the network amplifies
     any bf16 rounding -- rounding torchvision's own activations to bf16 moves its
-    logits by 31 % (scripts/dbg_train.py) -- so whole-network agreement is not a test
+    logits by 31 % (round-1 debugging) -- so whole-network agreement is not a test
     of the kernels. Tolerances: forward and loss rel 2e-2 (north star, bf16 path);
     gradients rel 1.5e-1: a torchvision block whose tensors are rounded to bf16 at
     the same points deviates from fp32 by 7-8 % in dx / dW / dgamma
