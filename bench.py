@@ -600,7 +600,7 @@ def run_training_depths(args, conf) -> None:
                 samples_completed=sum(r_.samples_completed for r_ in recs),
                 fill_busy_ns=busy_in_bubbles(bubbles, fills), bubble_ns=sum(b1 - b0 for b0, b1 in bubbles),
                 idle_ns=sum(pf.build_bubble_cycle(pcfg, t["stage"]).total_idle_us * 1000 for t in steps),
-                gemm_flops=sum(f for f, _ in executor.gemm_samples), gemm_ms=sum(ms for _, ms in executor.gemm_samples),
+                gemm_flops=sum(g[0] for g in executor.gemm_samples), gemm_ms=sum(g[1] for g in executor.gemm_samples),
                 launches=executor.kernel_launches + sum(e.launches for e in engines.values()) - launches0,
                 device_s=sum(t["step_end"] - t["start"] for t in steps) / 1e9)
             tot = aggregate(st, device=torch.device("cuda", local))
@@ -1172,17 +1172,38 @@ def main() -> None:
         slow["noise_floor_stage_compute"] = slow["noise_floor"]
         slow["noise_floor"] = interference["pipeline"]["noise_floor"]
     yield_stats = yield_latency(steps, by_tag)
+    # roofline samples: GEMMs of bubbles that ran at full width -- bubbles no longer than the
+    # throttle window, or whose fill ended before the window opened; the
+    # throttled tail's GEMMs run on throttle_ctas of the 148 SMs by design
+    thr_ns = int(args.throttle_ms * 1e6)
+    full_width = set()
+    for t in steps:
+        for kind, t_set, t_clr, tag in t["bubbles"]:
+            r = by_tag.get(tag)
+            if r is not None and (thr_ns <= 0 or t_clr - t_set <= thr_ns or r.fill_end_ns <= t_clr - thr_ns):
+                full_width.add(tag)
+    gemm_full = [g for g in executor.gemm_samples if g[2] in full_width]
+    gemm_all = list(executor.gemm_samples)
     stats = FillStats(
         sample_equivalents=sum(r.sample_eq for r in recs),
         samples_completed=sum(r.samples_completed for r in recs),
         fill_busy_ns=busy_in_bubbles(bubbles, fills),
         bubble_ns=sum(b1 - b0 for b0, b1 in bubbles),
         idle_ns=sum(pf.build_bubble_cycle(pcfg, t["stage"]).total_idle_us * 1000 for t in steps),
-        gemm_flops=sum(f for f, _ in executor.gemm_samples),
-        gemm_ms=sum(ms for _, ms in executor.gemm_samples),
+        gemm_flops=sum(g[0] for g in gemm_full),
+        gemm_ms=sum(g[1] for g in gemm_full),
         launches=launches, wall_s=w1 - w0,
         device_s=sum(t["step_end"] - t["start"] for t in steps) / 1e9)
-    gemm_launches = len(executor.gemm_samples)
+    gemm_launches = len(gemm_full)
+    gemm_by_batch = {}
+    for fl, ms, _, cnt in gemm_full:
+        a = gemm_by_batch.setdefault(str(cnt), [0.0, 0.0, 0])
+        a[0] += fl
+        a[1] += ms
+        a[2] += 1
+    gemm_by_batch = {b: {"tflops": f / (ms / 1e3) / 1e12, "launches": n} for b, (f, ms, n) in gemm_by_batch.items()}
+    all_ms = sum(g[1] for g in gemm_all)
+    gemm_all_tflops = sum(g[0] for g in gemm_all) / (all_ms / 1e3) / 1e12 if all_ms else None
     executor.timing = False
     traffic, traffic_src = None, None
     try:  # DRAM bytes per GEMM launch from the committed ncu --set full capture
@@ -1280,6 +1301,12 @@ def main() -> None:
                          "frac": achieved / peak if peak else None, "traffic": traffic,
                          "traffic_source": traffic_src,
                          "kernel": "pf_gemm (tcgen05)", "launches_timed": gemm_launches,
+                         "by_batch_size": gemm_by_batch,
+                         "sampling": "in-kernel %globaltimer span (first CTA start -> last working CTA end) of "
+                                     "every GEMM node of the last batch of each completed bubble that ran at "
+                                     "full width (not in the throttled bubble tail)",
+                         "achieved_incl_throttled_tail": gemm_all_tflops,
+                         "launches_incl_throttled_tail": len(gemm_all),
                          "peak_source": peaks["source"] + " bf16_tflops_sustained"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "samples/s",

@@ -340,6 +340,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&sfull_bar[s], 1);
       mbar_init(&sempty_bar[s], 1 + NUM_EPI_WARPS);
     }
+    tmem_base_smem[1] = 0u;  // "ran a tile" (set by the scheduler, read at exit)
     fence_barrier_init();
   }
   if (warp == ALLOC_WARP) tmem_alloc(tmem_base_smem, C::TMEM_COLS);
@@ -371,6 +372,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         sphase ^= 1u;
       }
       if (tile < 0) break;
+      if (lane == 0) tmem_base_smem[1] = 1u;  // this CTA ran a tile (end stamp below)
       int tm, tn, ks, half;  // a half unit loads the whole BN rows of W (L2-resident) and uses half
       unit_info(tile, p, tm, tn, ks, half);
       const int kb0 = ks * p.kb_per_split;
@@ -545,7 +547,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
   if (warp == ALLOC_WARP) tmem_dealloc(tmem_base, C::TMEM_COLS);
   DIAG_FLUSH();
-  if (threadIdx.x == 0 && p.stamp) atomicMax(&p.stamp[1], globaltimer_ns());
+  // end stamp only from CTAs that ran a tile: a CTA that starts after the bubble closed (its
+  // SM was busy with the main job) and exits without work does not extend the kernel's span
+  if (threadIdx.x == 0 && p.stamp && tmem_base_smem[1] != 0u) atomicMax(&p.stamp[1], globaltimer_ns());
 }
 
 
@@ -642,6 +646,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       // leader: its MMA + epilogue warps (local) and the peer's producer + epilogue (remote)
       mbar_init(&sempty_bar[s], 2 + 2 * NUM_EPI_WARPS);
     }
+    tmem_base_smem[1] = 0u;  // "ran a tile" (set by the scheduler, read at exit)
     fence_barrier_init();
   }
   if (warp == ALLOC_WARP) tmem_alloc_pair(tmem_base_smem, C::TMEM_COLS);
@@ -683,6 +688,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         sphase ^= 1u;
       }
       if (tile < 0) break;
+      if (lane == 0) tmem_base_smem[1] = 1u;  // this CTA ran a tile (end stamp below)
       int tm, tn, ks, half;
       unit_info(tile, p, tm, tn, ks, half);
       // W rows of this CTA (64-row TMA boxes): a full tile takes rows [rank*BN/2, +BN/2) of
@@ -848,7 +854,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
   if (warp == ALLOC_WARP) tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
   DIAG_FLUSH();
-  if (threadIdx.x == 0 && p.stamp) atomicMax(&p.stamp[1], globaltimer_ns());
+  // end stamp only from CTAs that ran a tile: a CTA that starts after the bubble closed (its
+  // SM was busy with the main job) and exits without work does not extend the kernel's span
+  if (threadIdx.x == 0 && p.stamp && tmem_base_smem[1] != 0u) atomicMax(&p.stamp[1], globaltimer_ns());
 }
 
 // ---------------------------------------------------------------------------

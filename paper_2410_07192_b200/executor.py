@@ -173,7 +173,9 @@ class Executor:
         self.h2d_bytes = 0
         self.d2h_bytes = 0
         self.timing = False  # live per-GEMM device timing (bench roofline)
-        self.gemm_samples: list[tuple[float, float]] = []  # (flops, ms)
+        # (flops, ms, bubble tag, batch size) of every GEMM node of the last batch of each
+        # completed bubble (in-kernel stamps)
+        self.gemm_samples: list[tuple[float, float, object, int]] = []
         # called when the executor runs out of work at a bubble: returns the next
         # (WorkItem, model) from the stage's Coordinator, or None
         self.work_source: Optional[Callable[[], Optional[tuple[WorkItem, FillSequential]]]] = None
@@ -733,7 +735,7 @@ class Executor:
                 for node, fl in ch.gemm_flops.items():
                     t0, t1 = int(sh[node, 0]), int(sh[node, 1])
                     if 0 < t0 < t1:
-                        self.gemm_samples.append((fl, (t1 - t0) / 1e6))
+                        self.gemm_samples.append((fl, (t1 - t0) / 1e6, pend.slot.tag, last_cnt))
         n_total = self.item.entry.size
         samples = 0
         parts = pend.parts or [pend.part] * len(pend.batches)

@@ -40,8 +40,8 @@ names = ["QKV", "out+res", "FFN1+gelu", "FFN2+res"]
 gsum = 0.0
 for j, nm in enumerate(names):
     v = g[j::4]
-    ms = sum(t for _, t in v) / len(v)
-    gsum += sum(t for _, t in v)
+    ms = sum(t for _, t, *_ in v) / len(v)
+    gsum += sum(t for _, t, *_ in v)
     print(f"{nm:10s} {ms * 1e3:7.1f} us  {v[0][0] / ms / 1e9:7.0f} TFLOP/s")
 print(f"batch {tot:.3f} ms: GEMMs {gsum:.3f} ms ({gsum / tot * 100:.1f}%), rest {tot - gsum:.3f} ms "
       f"({(tot - gsum) / cfg.layers * 1e3:.1f} us per layer: attention + 2 LN + gates)")
