@@ -595,6 +595,7 @@ def run_training_depths(args, conf) -> None:
                     r_ = by_tag.get(tag)
                     bubbles.append((t_set, t_clr))
                     fills.append((r_.fill_start_ns, r_.fill_end_ns) if r_ is not None else (0, 0))
+            launch_roof = gemm_launch_roofline(executor.gemm_samples, peaks)
             st = FillStats(
                 sample_equivalents=sum(r_.sample_eq for r_ in recs),
                 samples_completed=sum(r_.samples_completed for r_ in recs),
@@ -610,7 +611,8 @@ def run_training_depths(args, conf) -> None:
                 "bubble_time_filled_of_total_idle": tot.idle_filled,
                 "main_job_slowdown": slowdown_stats(on_iter, off)["max"],
                 "main_job_slowdown_detail": slowdown_stats(on_iter, off),
-                "gemm_tflops_in_situ": tot.gemm_tflops, "sgd_steps": int(sum(r_.batches_done for r_ in recs)),
+                "gemm_tflops_in_situ": tot.gemm_tflops, "gemm_launch_roofline": launch_roof,
+                "sgd_steps": int(sum(r_.batches_done for r_ in recs)),
                 "plan_stage0": pf.plan_to_dict(coords[0].executables["train-0"]),
                 "ms_per_step": 1000 * tot.device_s / max(1, len(steps))}
             executor.work_source = None
@@ -635,7 +637,8 @@ def run_training_depths(args, conf) -> None:
             "main_job_slowdown": deepest["main_job_slowdown"],
             "roofline": {"bound": "tensor", "achieved": deepest["gemm_tflops_in_situ"], "peak": peak,
                          "unit": "TFLOP/s", "frac": deepest["gemm_tflops_in_situ"] / peak, "traffic": None,
-                         "kernel": "pf_gemm + pf_gemm_splitk (tcgen05)"},
+                         "kernel": "pf_gemm + pf_gemm_splitk (tcgen05)",
+                         **deepest["gemm_launch_roofline"]},
             "cpu_baseline": None,
             "e2e": None, "gpu_launches": int(sum(t.launches for t in stats_all)), "clocks": clocks.summary(),
         }
@@ -763,6 +766,22 @@ def yield_latency(steps, by_tag) -> dict:
             "definition": "overrun = fill stream's end stamp (after the aborted batches' no-op gate launches) - "
                           "bubble flag clear (us); main resume delay = main stream's first stamp after the "
                           "bubble - flag clear (us)"}
+
+
+def gemm_launch_roofline(samples, peaks) -> dict:
+    """Per-launch roofline of in-situ GEMM samples (flops, ms, tag, batch, min bytes): each
+    launch's bound is max(F / tensor peak, B / HBM peak); the fraction is the sum of those
+    bounds over the sum of the measured times. Many ResNet GEMMs (K or N = 64..256, M up
+    to 200 K rows) are HBM-bound, so their tensor-peak fraction alone understates them."""
+    pt = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) * 1e12
+    pb = peaks.get("hbm_gbs", 6466.1) * 1e9
+    t = sum(g[1] for g in samples) / 1e3
+    if t <= 0:
+        return {"frac_of_launch_roofline": None}
+    bound = sum(max(g[0] / pt, (g[4] if len(g) > 4 else 0.0) / pb) for g in samples)
+    hbm = sum(1 for g in samples if len(g) > 4 and g[4] / pb > g[0] / pt)
+    return {"frac_of_launch_roofline": bound / t, "hbm_bound_launches": hbm, "launches": len(samples),
+            "bytes_per_s_gbs": sum(g[4] for g in samples if len(g) > 4) / t / 1e9}
 
 
 def profile_step_ms(profile, b: int) -> float:
@@ -1305,6 +1324,7 @@ def main() -> None:
                          "sampling": "in-kernel %globaltimer span (first CTA start -> last working CTA end) of "
                                      "every GEMM node of the last batch of each completed bubble that ran at "
                                      "full width (not in the throttled bubble tail)",
+                         **gemm_launch_roofline(gemm_full, peaks),
                          "achieved_incl_throttled_tail": gemm_all_tflops,
                          "launches_incl_throttled_tail": len(gemm_all),
                          "peak_source": peaks["source"] + " bf16_tflops_sustained"},

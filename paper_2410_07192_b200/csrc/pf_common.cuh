@@ -299,6 +299,22 @@ __device__ __forceinline__ bool atomic_unit_poll(const Ctl& c) {
 // items once, capped at one full wave (2048 threads per SM); every CTA strides over the rest. Entry and exit
 // are paid once per CTA instead of once per 256 items (the gate's flag load and barrier
 // cost ~1 us per CTA, which dominated the element-wise training kernels).
+// Division by a runtime divisor as a multiply-high and a shift (the HBM-bound image and
+// BatchNorm kernels decode every vector index into (pixel, channel) / (row, column) with
+// several divisions; 64-bit division is a ~100-instruction subroutine). Exact for n < 2^31.
+struct FastDiv {
+  uint32_t d = 1, m = 1, s = 0;
+  FastDiv() = default;
+  explicit FastDiv(uint32_t div) : d(div) {
+    for (s = 0; s < 32; ++s)
+      if ((1ull << s) >= div) break;
+    const uint64_t magic = ((1ull << 32) * ((1ull << s) - div)) / div + 1;
+    m = (uint32_t)magic;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, m) + n) >> s; }
+  __device__ __forceinline__ uint32_t mod(uint32_t n) const { return n - div(n) * d; }
+};
+
 inline unsigned persistent_grid(long long items, int threads) {
   const long long need = (items + threads - 1) / threads;
   const long long cap = (2048LL / threads) * device_sm_count();  // one full wave of resident threads

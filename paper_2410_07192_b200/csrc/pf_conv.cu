@@ -22,23 +22,29 @@ namespace conv {
 
 constexpr int THREADS = 256;
 
+// Index decode: vector v -> (row m, 8 columns at k0) -> (b, oy, ox) and (ky, kx, c) with
+// FastDiv (every total is < 2^31, checked at op creation).
+struct Im2colDiv {
+  FastDiv vpr, C, kw, Wo, Ho;
+};
+
 __global__ void __launch_bounds__(THREADS) im2col_vec_kernel(
     const __nv_bfloat16* __restrict__ X, __nv_bfloat16* __restrict__ Col, int H, int W, int C,
-    int Ho, int Wo, int kw, int stride, int pad, int K, int Kp, long long total_vec, Ctl ctl) {
+    int stride, int pad, int K, int Kp, long long total_vec, Im2colDiv dv, Ctl ctl) {
   PF_ITEMS_BEGIN(total_vec) {
-    const int vpr = Kp >> 3;  // vectors per Col row
-    const long long m = v / vpr;
-    const int k0 = (int)(v - m * vpr) << 3;
+    const uint32_t m = dv.vpr.div((uint32_t)v);
+    const int k0 = (int)((uint32_t)v - m * dv.vpr.d) << 3;
     uint4 out = make_uint4(0, 0, 0, 0);
     if (k0 < K) {
-      const int tap = k0 / C;
-      const int c0 = k0 - tap * C;
-      const int ky = tap / kw, kx = tap - (tap / kw) * kw;
-      const int ox = (int)(m % Wo);
-      const long long t = m / Wo;
-      const int oy = (int)(t % Ho);
-      const int b = (int)(t / Ho);
-      const int iy = oy * stride - pad + ky, ix = ox * stride - pad + kx;
+      const uint32_t tap = dv.C.div((uint32_t)k0);
+      const int c0 = k0 - (int)(tap * dv.C.d);
+      const uint32_t ky = dv.kw.div(tap);
+      const int kx = (int)(tap - ky * dv.kw.d);
+      const uint32_t t = dv.Wo.div(m);
+      const int ox = (int)(m - t * dv.Wo.d);
+      const uint32_t b = dv.Ho.div(t);
+      const int oy = (int)(t - b * dv.Ho.d);
+      const int iy = oy * stride - pad + (int)ky, ix = ox * stride - pad + kx;
       if (iy >= 0 && iy < H && ix >= 0 && ix < W)
         out = __ldg(reinterpret_cast<const uint4*>(X + (((size_t)b * H + iy) * W + ix) * C + c0));
     }
@@ -47,41 +53,55 @@ __global__ void __launch_bounds__(THREADS) im2col_vec_kernel(
   PF_ITEMS_END
 }
 
-__global__ void __launch_bounds__(THREADS) im2col_scalar_kernel(
+// C % 8 != 0 (the 3-channel stem): still 8 output columns (one 16-B store) per thread; the
+// (ky, kx, c) of the first column is decoded once and the rest follow incrementally.
+__global__ void __launch_bounds__(THREADS) im2col_small_c_kernel(
     const __nv_bfloat16* __restrict__ X, __nv_bfloat16* __restrict__ Col, int H, int W, int C,
-    int Ho, int Wo, int kw, int stride, int pad, int K, int Kp, long long total, Ctl ctl) {
-  PF_ITEMS_BEGIN(total) {
-    const long long e = v;
-    const long long m = e / Kp;
-    const int k = (int)(e - m * Kp);
-    __nv_bfloat16 val = __float2bfloat16(0.f);
-    if (k < K) {
-      const int tap = k / C;
-      const int c = k - tap * C;
-      const int ky = tap / kw, kx = tap - (tap / kw) * kw;
-      const int ox = (int)(m % Wo);
-      const long long t = m / Wo;
-      const int oy = (int)(t % Ho);
-      const int b = (int)(t / Ho);
-      const int iy = oy * stride - pad + ky, ix = ox * stride - pad + kx;
-      if (iy >= 0 && iy < H && ix >= 0 && ix < W) val = X[(((size_t)b * H + iy) * W + ix) * C + c];
+    int stride, int pad, int K, int Kp, long long total_vec, Im2colDiv dv, Ctl ctl) {
+  PF_ITEMS_BEGIN(total_vec) {
+    const uint32_t m = dv.vpr.div((uint32_t)v);
+    const int k0 = (int)((uint32_t)v - m * dv.vpr.d) << 3;
+    const uint32_t t = dv.Wo.div(m);
+    const int ox = (int)(m - t * dv.Wo.d);
+    const uint32_t b = dv.Ho.div(t);
+    const int oy = (int)(t - b * dv.Ho.d);
+    const uint32_t tap0 = dv.C.div((uint32_t)min(k0, K));
+    int c = min(k0, K) - (int)(tap0 * dv.C.d);
+    const uint32_t ky0 = dv.kw.div(tap0);
+    int ky = (int)ky0, kx = (int)(tap0 - ky0 * dv.kw.d);
+    const __nv_bfloat16* xb = X + (size_t)b * H * W * C;
+    __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      __nv_bfloat16 val = __float2bfloat16(0.f);
+      if (k0 + e < K) {
+        const int iy = oy * stride - pad + ky, ix = ox * stride - pad + kx;
+        if (iy >= 0 && iy < H && ix >= 0 && ix < W) val = xb[((size_t)iy * W + ix) * C + c];
+      }
+      o[e] = val;
+      if (++c == C) {
+        c = 0;
+        if (++kx == (int)dv.kw.d) {
+          kx = 0;
+          ++ky;
+        }
+      }
     }
-    Col[e] = val;
+    *reinterpret_cast<uint4*>(Col + (size_t)m * Kp + k0) = *reinterpret_cast<const uint4*>(o);
   }
   PF_ITEMS_END
 }
 
 __global__ void __launch_bounds__(THREADS) maxpool_kernel(
     const __nv_bfloat16* __restrict__ X, __nv_bfloat16* __restrict__ Y, int H, int W, int C,
-    int Ho, int Wo, int k, int stride, int pad, long long total_vec, Ctl ctl) {
+    int k, int stride, int pad, long long total_vec, FastDiv dcv, FastDiv dWo, FastDiv dHo, Ctl ctl) {
   PF_ITEMS_BEGIN(total_vec) {
-    const int cv = C >> 3;
-    const int c0 = (int)(v % cv) << 3;
-    const long long pix = v / cv;
-    const int ox = (int)(pix % Wo);
-    const long long t = pix / Wo;
-    const int oy = (int)(t % Ho);
-    const int b = (int)(t / Ho);
+    const uint32_t pix = dcv.div((uint32_t)v);
+    const int c0 = (int)((uint32_t)v - pix * dcv.d) << 3;
+    const uint32_t t = dWo.div(pix);
+    const int ox = (int)(pix - t * dWo.d);
+    const uint32_t b = dHo.div(t);
+    const int oy = (int)(t - b * dHo.d);
     float mx[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
@@ -107,8 +127,8 @@ __global__ void __launch_bounds__(THREADS) avgpool_kernel(const __nv_bfloat16* _
                                                           int C, long long total_vec, Ctl ctl) {
   PF_ITEMS_BEGIN(total_vec) {
     const int cv = C >> 3;
-    const int c0 = (int)(v % cv) << 3;
-    const long long b = v / cv;
+    const int c0 = (int)((uint32_t)v % (uint32_t)cv) << 3;
+    const uint32_t b = (uint32_t)v / (uint32_t)cv;
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     const __nv_bfloat16* base = X + (size_t)b * HW * C + c0;
     for (int p = 0; p < HW; ++p) {
@@ -138,12 +158,13 @@ struct Im2colOp final : PreparedOp {
   uint32_t units() const override { return blocks_for(n); }
   bool resumable() const override { return false; }
   int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
+    const Im2colDiv dv{FastDiv((uint32_t)(Kp / 8)), FastDiv((uint32_t)C), FastDiv((uint32_t)kw),
+                       FastDiv((uint32_t)Wo), FastDiv((uint32_t)Ho)};
     if (vec)
-      im2col_vec_kernel<<<units(), THREADS, 0, s>>>(x, col, H, W, C, Ho, Wo, kw, stride, pad, K, Kp, n,
-                                                   make_ctl(ctl));
+      im2col_vec_kernel<<<units(), THREADS, 0, s>>>(x, col, H, W, C, stride, pad, K, Kp, n, dv, make_ctl(ctl));
     else
-      im2col_scalar_kernel<<<units(), THREADS, 0, s>>>(x, col, H, W, C, Ho, Wo, kw, stride, pad, K, Kp,
-                                                      n, make_ctl(ctl));
+      im2col_small_c_kernel<<<units(), THREADS, 0, s>>>(x, col, H, W, C, stride, pad, K, Kp, n, dv,
+                                                        make_ctl(ctl));
     PF_CUDA(cudaGetLastError());
     return PF_OK;
   }
@@ -157,7 +178,8 @@ struct MaxpoolOp final : PreparedOp {
   uint32_t units() const override { return blocks_for(n); }
   bool resumable() const override { return false; }
   int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
-    maxpool_kernel<<<units(), THREADS, 0, s>>>(x, y, H, W, C, Ho, Wo, k, stride, pad, n, make_ctl(ctl));
+    maxpool_kernel<<<units(), THREADS, 0, s>>>(x, y, H, W, C, k, stride, pad, n, FastDiv((uint32_t)(C / 8)),
+                                                FastDiv((uint32_t)Wo), FastDiv((uint32_t)Ho), make_ctl(ctl));
     PF_CUDA(cudaGetLastError());
     return PF_OK;
   }
@@ -210,7 +232,9 @@ int make_im2col_op(OpPtr* out, const void* X, void* Col, int B, int H, int W, in
   op->Kp = Kp;
   op->vec = C % 8 == 0;
   const long long rows = (long long)B * op->Ho * op->Wo;
-  op->n = op->vec ? rows * (Kp / 8) : rows * Kp;
+  op->n = rows * (Kp / 8);  // 8 output columns per item on both paths
+  if (op->n >= (1ll << 31) || (long long)B * H * W * C >= (1ll << 31))
+    return set_error(PF_ERR_INVALID, "pf_im2col: more than 2^31 vectors");
   *out = std::move(op);
   return PF_OK;
 }
@@ -233,6 +257,7 @@ int make_maxpool_op(OpPtr* out, const void* X, void* Y, int B, int H, int W, int
   op->stride = stride;
   op->pad = pad;
   op->n = (long long)B * op->Ho * op->Wo * (C / 8);
+  if (op->n >= (1ll << 31)) return set_error(PF_ERR_INVALID, "pf_maxpool: more than 2^31 vectors");
   *out = std::move(op);
   return PF_OK;
 }
@@ -280,7 +305,7 @@ extern "C" int pf_avgpool(const void* X, void* Y, int B, int HW, int C, const pf
 extern "C" int pf_image_units(int kind, long long out_elems, int C, uint32_t* out_units) {
   // kind 0: im2col (out_elems = rows * Kp), 1: maxpool / avgpool (out_elems = pixels * C)
   if (!out_units || out_elems <= 0 || C <= 0) return pf::set_error(PF_ERR_INVALID, "pf_image_units");
-  const bool vec = kind != 0 || C % 8 == 0;
-  *out_units = pf::conv::blocks_for(vec ? out_elems / 8 : out_elems);
+  (void)C;  // every image kernel handles 8 output elements per item (im2col: Kp % 8 == 0)
+  *out_units = pf::conv::blocks_for(out_elems / 8);
   return PF_OK;
 }

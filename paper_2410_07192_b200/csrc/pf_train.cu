@@ -180,11 +180,27 @@ __device__ __forceinline__ void sum_partials(const float* __restrict__ partial, 
   __shared__ double red[2][FT / 32][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double a = 0.0, b = 0.0;
-  if (c < C)
-    for (int p = w; p < P; p += FT / 32) {
+  if (c < C) {
+    // loads of 4 partial rows in flight per warp, accumulated in row order (deterministic)
+    int p = w;
+    for (; p + 3 * (FT / 32) < P; p += 4 * (FT / 32)) {
+      float x[4], y[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        x[u] = partial[(size_t)(p + u * (FT / 32)) * 2 * C + c];
+        y[u] = partial[(size_t)(p + u * (FT / 32)) * 2 * C + C + c];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a += x[u];
+        b += y[u];
+      }
+    }
+    for (; p < P; p += FT / 32) {
       a += partial[(size_t)p * 2 * C + c];
       b += partial[(size_t)p * 2 * C + C + c];
     }
+  }
   red[0][w][lane] = a;
   red[1][w][lane] = b;
   __syncthreads();
@@ -237,13 +253,22 @@ __global__ void __launch_bounds__(FT) bn_bwd_finalize_kernel(const float* __rest
 __global__ void __launch_bounds__(T) bn_apply_kernel(const bf* __restrict__ X, const float* __restrict__ scale,
                                                      const float* __restrict__ shift, const bf* __restrict__ R,
                                                      bf* __restrict__ Y, int C, long long nvec, int relu,
-                                                     Ctl ctl) {
+                                                     FastDiv dcv, Ctl ctl) {
+  // the grid stride is a multiple of C / 8 whenever C / 8 divides 256 * gridDim (every
+  // power-of-two channel count): a thread then always sees the same 8 channels and loads
+  // their scale / shift once instead of once per 16-B vector
+  const bool hoist = ((long long)gridDim.x * blockDim.x) % dcv.d == 0;
+  bool have = false;
+  float sc[8], sh[8];
   PF_ITEMS_BEGIN(nvec) {
-    const int c0 = (int)(v % (C >> 3)) << 3;
-    float x[8], sc[8], sh[8];
+    const int c0 = (int)dcv.mod((uint32_t)v) << 3;
+    float x[8];
     load8(X + v * 8, x);
-    ld8f(scale + c0, sc);
-    ld8f(shift + c0, sh);
+    if (!have || !hoist) {
+      ld8f(scale + c0, sc);
+      ld8f(shift + c0, sh);
+      have = true;
+    }
 #pragma unroll
     for (int e = 0; e < 8; ++e) x[e] = x[e] * sc[e] + sh[e];
     if (R) {
@@ -267,9 +292,12 @@ __global__ void __launch_bounds__(T) bn_bwd_apply_kernel(
     const bf* __restrict__ X, const bf* __restrict__ G, const bf* __restrict__ Ymask,
     const float* __restrict__ mean, const float* __restrict__ invstd, const float* __restrict__ gamma,
     const float* __restrict__ dgamma, const float* __restrict__ dbeta, bf* __restrict__ dX,
-    bf* __restrict__ dA_out, int M, int C, long long nvec, Ctl ctl) {
+    bf* __restrict__ dA_out, int M, int C, long long nvec, FastDiv dcv, Ctl ctl) {
+  const bool hoist = ((long long)gridDim.x * blockDim.x) % dcv.d == 0;  // see bn_apply_kernel
+  bool have = false;
+  float mu[8], is[8], ga[8], dg[8], db[8];
   PF_ITEMS_BEGIN(nvec) {
-    const int c0 = (int)(v % (C >> 3)) << 3;
+    const int c0 = (int)dcv.mod((uint32_t)v) << 3;
     float x[8], g[8];
     load8(X + v * 8, x);
     load8(G + v * 8, g);
@@ -281,12 +309,15 @@ __global__ void __launch_bounds__(T) bn_bwd_apply_kernel(
     }
     if (dA_out) store8(dA_out + v * 8, g);
     const float inv_m = 1.f / (float)M;
-    float o[8], mu[8], is[8], ga[8], dg[8], db[8];
-    ld8f(mean + c0, mu);
-    ld8f(invstd + c0, is);
-    ld8f(gamma + c0, ga);
-    ld8f(dgamma + c0, dg);
-    ld8f(dbeta + c0, db);
+    float o[8];
+    if (!have || !hoist) {
+      ld8f(mean + c0, mu);
+      ld8f(invstd + c0, is);
+      ld8f(gamma + c0, ga);
+      ld8f(dgamma + c0, dg);
+      ld8f(dbeta + c0, db);
+      have = true;
+    }
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const float xh = (x[e] - mu[e]) * is[e];
@@ -302,15 +333,15 @@ __global__ void __launch_bounds__(T) bn_bwd_apply_kernel(
 __global__ void __launch_bounds__(T) col2im_kernel(const bf* __restrict__ dCol, const bf* __restrict__ R,
                                                    bf* __restrict__ dX, int H, int W, int C, int Ho, int Wo,
                                                    int kh, int kw, int stride, int pad, int Kp,
-                                                   long long nvec, Ctl ctl) {
+                                                   long long nvec, FastDiv dcv, FastDiv dW, FastDiv dH,
+                                                   Ctl ctl) {
   PF_ITEMS_BEGIN(nvec) {
-    const int cv = C >> 3;
-    const int c0 = (int)(v % cv) << 3;
-    const long long pix = v / cv;
-    const int ix = (int)(pix % W);
-    const long long t = pix / W;
-    const int iy = (int)(t % H);
-    const int b = (int)(t / H);
+    const uint32_t pix = dcv.div((uint32_t)v);
+    const int c0 = (int)((uint32_t)v - pix * dcv.d) << 3;
+    const uint32_t t = dW.div(pix);
+    const int ix = (int)(pix - t * dW.d);
+    const uint32_t b = dH.div(t);
+    const int iy = (int)(t - b * dH.d);
     float acc[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] = 0.f;
@@ -332,11 +363,11 @@ __global__ void __launch_bounds__(T) col2im_kernel(const bf* __restrict__ dCol, 
     }
     if (R) {
       float r[8];
-      load8(R + pix * C + c0, r);
+      load8(R + (size_t)pix * C + c0, r);
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[e] += r[e];
     }
-    store8(dX + pix * C + c0, acc);
+    store8(dX + (size_t)pix * C + c0, acc);
   }
   PF_ITEMS_END
 }
@@ -344,15 +375,14 @@ __global__ void __launch_bounds__(T) col2im_kernel(const bf* __restrict__ dCol, 
 __global__ void __launch_bounds__(T) maxpool_bwd_kernel(const bf* __restrict__ X, const bf* __restrict__ dY,
                                                         bf* __restrict__ dX, int H, int W, int C, int Ho,
                                                         int Wo, int k, int stride, int pad, long long nvec,
-                                                        Ctl ctl) {
+                                                        FastDiv dcv, FastDiv dW, FastDiv dH, Ctl ctl) {
   PF_ITEMS_BEGIN(nvec) {
-    const int cv = C >> 3;
-    const int c0 = (int)(v % cv) << 3;
-    const long long pix = v / cv;
-    const int ix = (int)(pix % W);
-    const long long t = pix / W;
-    const int iy = (int)(t % H);
-    const int b = (int)(t / H);
+    const uint32_t pix = dcv.div((uint32_t)v);
+    const int c0 = (int)((uint32_t)v - pix * dcv.d) << 3;
+    const uint32_t t = dW.div(pix);
+    const int ix = (int)(pix - t * dW.d);
+    const uint32_t b = dH.div(t);
+    const int iy = (int)(t - b * dH.d);
     float acc[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] = 0.f;
@@ -397,19 +427,19 @@ __global__ void __launch_bounds__(T) maxpool_bwd_kernel(const bf* __restrict__ X
           if (arg[e] == iy * W + ix) acc[e] += g[e];
       }
     }
-    store8(dX + pix * C + c0, acc);
+    store8(dX + (size_t)pix * C + c0, acc);
   }
   PF_ITEMS_END
 }
 
 __global__ void __launch_bounds__(T) avgpool_bwd_kernel(const bf* __restrict__ dY, bf* __restrict__ dX,
-                                                        int HW, int C, long long nvec, Ctl ctl) {
+                                                        int HW, int C, long long nvec, FastDiv dcv,
+                                                        FastDiv dhwcv, Ctl ctl) {
   PF_ITEMS_BEGIN(nvec) {
-    const int cv = C >> 3;
-    const int c0 = (int)(v % cv) << 3;
-    const long long b = v / ((long long)HW * cv);
+    const int c0 = (int)dcv.mod((uint32_t)v) << 3;
+    const uint32_t b = dhwcv.div((uint32_t)v);
     float g[8];
-    load8(dY + b * C + c0, g);
+    load8(dY + (size_t)b * C + c0, g);
     const float inv = 1.f / (float)HW;
 #pragma unroll
     for (int e = 0; e < 8; ++e) g[e] *= inv;
@@ -590,7 +620,8 @@ struct BnApplyOp final : PreparedOp {
   uint32_t units() const override { return blocks_for(nvec); }
   bool resumable() const override { return false; }
   int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
-    bn_apply_kernel<<<units(), T, 0, s>>>(x, scale, shift, r, y, C, nvec, relu, make_ctl(ctl));
+    bn_apply_kernel<<<units(), T, 0, s>>>(x, scale, shift, r, y, C, nvec, relu, FastDiv((uint32_t)(C / 8)),
+                                          make_ctl(ctl));
     PF_CUDA(cudaGetLastError());
     return PF_OK;
   }
@@ -606,7 +637,7 @@ struct BnBwdApplyOp final : PreparedOp {
   bool resumable() const override { return false; }
   int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
     bn_bwd_apply_kernel<<<units(), T, 0, s>>>(x, g, ymask, mean, invstd, gamma, dgamma, dbeta, dx, da, M, C,
-                                              nvec, make_ctl(ctl));
+                                              nvec, FastDiv((uint32_t)(C / 8)), make_ctl(ctl));
     PF_CUDA(cudaGetLastError());
     return PF_OK;
   }
@@ -621,7 +652,8 @@ struct Col2imOp final : PreparedOp {
   bool resumable() const override { return false; }
   int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
     col2im_kernel<<<units(), T, 0, s>>>(dcol, r, dx, H, W, C, Ho, Wo, kh, kw, stride, pad, Kp, nvec,
-                                        make_ctl(ctl));
+                                        FastDiv((uint32_t)(C / 8)), FastDiv((uint32_t)W),
+                                        FastDiv((uint32_t)H), make_ctl(ctl));
     PF_CUDA(cudaGetLastError());
     return PF_OK;
   }
@@ -637,10 +669,12 @@ struct PoolBwdOp final : PreparedOp {
   bool resumable() const override { return false; }
   int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
     if (avg)
-      avgpool_bwd_kernel<<<units(), T, 0, s>>>(dy, dx, HW, C, nvec, make_ctl(ctl));
+      avgpool_bwd_kernel<<<units(), T, 0, s>>>(dy, dx, HW, C, nvec, FastDiv((uint32_t)(C / 8)),
+                                               FastDiv((uint32_t)(HW * (C / 8))), make_ctl(ctl));
     else
       maxpool_bwd_kernel<<<units(), T, 0, s>>>(x, dy, dx, H, W, C, Ho, Wo, k, stride, pad, nvec,
-                                               make_ctl(ctl));
+                                               FastDiv((uint32_t)(C / 8)), FastDiv((uint32_t)W),
+                                               FastDiv((uint32_t)H), make_ctl(ctl));
     PF_CUDA(cudaGetLastError());
     return PF_OK;
   }
@@ -776,6 +810,7 @@ int make_bn_apply_op(OpPtr* out, const void* X, const float* scale, const float*
   op->C = C;
   op->relu = relu;
   op->nvec = M * C / 8;
+  if (op->nvec >= (1ll << 31)) return set_error(PF_ERR_INVALID, "more than 2^31 vectors (32-bit index decode)");
   *out = std::move(op);
   return PF_OK;
 }
@@ -801,6 +836,7 @@ int make_bn_bwd_apply_op(OpPtr* out, const void* X, const void* G, const void* Y
   op->M = M;
   op->C = C;
   op->nvec = (long long)M * C / 8;
+  if (op->nvec >= (1ll << 31)) return set_error(PF_ERR_INVALID, "more than 2^31 vectors (32-bit index decode)");
   *out = std::move(op);
   return PF_OK;
 }
@@ -825,6 +861,7 @@ int make_col2im_op(OpPtr* out, const void* dCol, const void* R, void* dX, int B,
   op->pad = pad;
   op->Kp = Kp;
   op->nvec = (long long)B * H * W * C / 8;
+  if (op->nvec >= (1ll << 31)) return set_error(PF_ERR_INVALID, "more than 2^31 vectors (32-bit index decode)");
   *out = std::move(op);
   return PF_OK;
 }
@@ -845,6 +882,7 @@ int make_maxpool_bwd_op(OpPtr* out, const void* X, const void* dY, void* dX, int
   op->stride = stride;
   op->pad = pad;
   op->nvec = (long long)B * H * W * C / 8;
+  if (op->nvec >= (1ll << 31)) return set_error(PF_ERR_INVALID, "more than 2^31 vectors (32-bit index decode)");
   *out = std::move(op);
   return PF_OK;
 }
@@ -858,6 +896,7 @@ int make_avgpool_bwd_op(OpPtr* out, const void* dY, void* dX, int B, int HW, int
   op->HW = HW;
   op->C = C;
   op->nvec = (long long)B * HW * C / 8;
+  if (op->nvec >= (1ll << 31)) return set_error(PF_ERR_INVALID, "more than 2^31 vectors (32-bit index decode)");
   *out = std::move(op);
   return PF_OK;
 }

@@ -119,6 +119,7 @@ class _Chain:
         native.call("pf_chain_create", ctypes.byref(self.h))
         self.units: list[tuple[int, bool]] = []
         self.gemm_flops: dict[int, float] = {}
+        self.gemm_bytes: dict[int, float] = {}  # minimum DRAM bytes per GEMM node (roofline)
         self.seg_ends: list[int] = []
         self.timing = False
         self.graph = False
@@ -173,9 +174,9 @@ class Executor:
         self.h2d_bytes = 0
         self.d2h_bytes = 0
         self.timing = False  # live per-GEMM device timing (bench roofline)
-        # (flops, ms, bubble tag, batch size) of every GEMM node of the last batch of each
-        # completed bubble (in-kernel stamps)
-        self.gemm_samples: list[tuple[float, float, object, int]] = []
+        # (flops, ms, bubble tag, batch size, minimum DRAM bytes) of every GEMM node of the last
+        # batch of each completed bubble (in-kernel stamps)
+        self.gemm_samples: list[tuple[float, float, object, int, float]] = []
         # called when the executor runs out of work at a bubble: returns the next
         # (WorkItem, model) from the stage's Coordinator, or None
         self.work_source: Optional[Callable[[], Optional[tuple[WorkItem, FillSequential]]]] = None
@@ -455,6 +456,8 @@ class Executor:
             x = model[i](x, ctx)
             for node, fl in model[i].gemm_node_flops(cnt):
                 ch.gemm_flops[before + node] = fl
+            for node, nb in model[i].gemm_node_bytes(cnt):
+                ch.gemm_bytes[before + node] = nb
             if (i - part.lo + 1) % _SEG_MODULES == 0 or i == part.hi - 1:
                 ch.seg_ends.append(ctx.node)  # one gated graph segment per _SEG_MODULES modules
         # last node: the batch's output slice (role 2: destination + out_off)
@@ -490,6 +493,7 @@ class Executor:
         seg_ends, gemm_flops = model.record_step(self.in_dev[:cnt], self.aux_dev[:cnt], loss, ctx)
         ch.seg_ends = seg_ends
         ch.gemm_flops = gemm_flops
+        ch.gemm_bytes = dict(getattr(model, "last_gemm_bytes", {}))
         rb = cnt * 16
         native.call("pf_chain_add_copy", ch.h, self._results.ptr, rb, loss.data_ptr(), rb, rb, 1, 2)
         ch.finalize()
@@ -735,7 +739,8 @@ class Executor:
                 for node, fl in ch.gemm_flops.items():
                     t0, t1 = int(sh[node, 0]), int(sh[node, 1])
                     if 0 < t0 < t1:
-                        self.gemm_samples.append((fl, (t1 - t0) / 1e6, pend.slot.tag, last_cnt))
+                        self.gemm_samples.append((fl, (t1 - t0) / 1e6, pend.slot.tag, last_cnt,
+                                                  ch.gemm_bytes.get(node, 0.0)))
         n_total = self.item.entry.size
         samples = 0
         parts = pend.parts or [pend.part] * len(pend.batches)

@@ -305,6 +305,11 @@ class FillModule(nn.Module):
         """(node index within this module, algorithmic FLOPs) of its GEMM nodes."""
         return []
 
+    def gemm_node_bytes(self, batch: int) -> list[tuple[int, float]]:
+        """(node index, minimum DRAM bytes: operands read once + output written) of its GEMM
+        nodes -- with the FLOPs, the per-launch roofline max(F / tensor peak, B / HBM)."""
+        return []
+
     def node_units(self, batch: int) -> list[tuple[int, str]]:
         raise NotImplementedError
 
@@ -385,6 +390,12 @@ class BertLayer(FillModule):
         m, h, f = batch * self.cfg.seq, self.cfg.hidden, self.cfg.ffn
         return [(0, 2.0 * m * 3 * h * h), (2, 2.0 * m * h * h), (4, 2.0 * m * h * f),
                 (5, 2.0 * m * f * h)]
+
+    def gemm_node_bytes(self, batch):
+        m, h, f = batch * self.cfg.seq, self.cfg.hidden, self.cfg.ffn
+        e = 4 if self.cfg.precision == "fp32" else 2
+        return [(0, e * (m * h + 3 * h * h + 3 * m * h)), (2, e * (m * h + h * h + 2 * m * h)),
+                (4, e * (m * h + f * h + m * f)), (5, e * (m * f + h * f + 2 * m * h))]
 
     def node_units(self, batch):
         seq = self.cfg.seq
@@ -609,6 +620,10 @@ class ResNetStem(FillModule):
     def gemm_node_flops(self, batch):
         return [(1, batch * self.flops_per_sample())]
 
+    def gemm_node_bytes(self, batch):
+        c, m = self.cfg, batch * self.h1 * self.h1
+        return [(1, 2.0 * (m * c.stem_kp + c.stem_ch * c.stem_kp + m * c.stem_ch))]
+
     def node_units(self, batch):
         c, m = self.cfg, batch * self.h1 * self.h1
         return [(K.image_units(0, m * c.stem_kp, c.in_ch), ATOMIC),
@@ -684,6 +699,11 @@ class Bottleneck(FillModule):
     def gemm_node_flops(self, batch):
         return [(node, 2.0 * m * n * k) for node, m, n, k in self._gemms(batch)]
 
+    def gemm_node_bytes(self, batch):
+        last = self._gemms(batch)[-1][0]  # the last GEMM adds the residual in its epilogue
+        return [(node, 2.0 * (m * k + n * k + m * n * (2 if node == last else 1)))
+                for node, m, n, k in self._gemms(batch)]
+
     def node_units(self, batch):
         ow = batch * self.ho * self.ho
         units = {node: (K.gemm_units(m, n, k), PREFIX) for node, m, n, k in self._gemms(batch)}
@@ -741,6 +761,9 @@ class ResNetHead(FillModule):
 
     def gemm_node_flops(self, batch):
         return [(1, batch * self.flops_per_sample())]
+
+    def gemm_node_bytes(self, batch):
+        return [(1, 2.0 * (batch * self.in_ch + self.cfg.classes * self.in_ch + batch * self.cfg.classes))]
 
     def node_units(self, batch):
         return [(K.image_units(1, batch * self.in_ch, self.in_ch), ATOMIC),

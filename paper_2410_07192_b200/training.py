@@ -185,8 +185,9 @@ class _Rec:
     """Shorthand over an ExecContext in chain-record mode (training chains are recorded,
     never eager), counting GEMM FLOPs per node for the in-kernel timing."""
 
-    def __init__(self, ctx: ExecContext, flops: dict):
+    def __init__(self, ctx: ExecContext, flops: dict, nbytes: dict | None = None):
         self.ctx, self.flops = ctx, flops
+        self.nbytes = {} if nbytes is None else nbytes  # minimum DRAM bytes per GEMM node (roofline)
 
     def call(self, fn, *args):
         native.call(fn, self.ctx.chain, *args)
@@ -197,12 +198,14 @@ class _Rec:
         m = x.numel() // k
         n = w.shape[0]
         self.flops[self.ctx.node] = 2.0 * m * n * k
+        self.nbytes[self.ctx.node] = 2.0 * (m * k + n * k + m * n * (2 if residual is not None else 1))
         self.ctx.gemm(x.reshape(m, k), w, bias, out, residual=residual, relu=relu)
 
     def gemm_splitk(self, a, b, out, splits):
         m, k = a.shape
         n = b.shape[0]
         self.flops[self.ctx.node] = 2.0 * m * n * k
+        self.nbytes[self.ctx.node] = 2.0 * (m * k + n * k + splits * m * n)
         self.call("pf_chain_add_gemm_splitk", a.data_ptr(), b.data_ptr(), out.data_ptr(), m, n, k, splits)
 
     def transpose(self, x, out):
@@ -252,6 +255,7 @@ class _Rec:
         m, n = dz.shape
         k = x.shape[-1]
         self.flops[self.ctx.node] = 2.0 * m * n * k
+        self.nbytes[self.ctx.node] = 2.0 * (m * n + m * k + splits * n * k)
         self.call("pf_chain_add_gemm_splitk_tn", dz.data_ptr(), x.data_ptr(), gbuf.data_ptr(), n, k, m, splits)
 
     def dgrad(self, dz, w, out, residual=None):
@@ -259,6 +263,7 @@ class _Rec:
         n, k = w.shape
         m = dz.shape[0]
         self.flops[self.ctx.node] = 2.0 * m * n * k
+        self.nbytes[self.ctx.node] = 2.0 * (m * n + n * k + m * k * (2 if residual is not None else 1))
         self.call("pf_chain_add_gemm_nn", dz.data_ptr(), w.data_ptr(),
                   None if residual is None else residual.data_ptr(), out.data_ptr(), m, k, n)
 
@@ -664,7 +669,8 @@ class ResNetTrainSequential(FillSequential):
         """Record forward, loss, backward and the SGD step; returns (segment ends, GEMM FLOPs
         per node)."""
         flops: dict[int, float] = {}
-        r = _Rec(ctx, flops)
+        self.last_gemm_bytes: dict[int, float] = {}
+        r = _Rec(ctx, flops, self.last_gemm_bytes)
         b = x.shape[0]
         if b % 8:
             raise ValueError("training batches must be a multiple of 8 samples")
