@@ -80,8 +80,8 @@ FILL_FRACTION_NCCL = 0.95
 # board's power controller lets it start at up to 1965 MHz, after a bubble filled at full power at
 # ~1600. The last THROTTLE_MS of every bubble longer than that run on THROTTLE_CTAS CTAs and the
 # last COOLDOWN_MS idle. Measured on B200 (profiles/r02_power_sweep.md): composed 8-stage
-# main-job slowdown +3.5-4.4 % without, +2.0 % with (10, 50, 64), at 20 % less fill throughput.
-COOLDOWN_MS = 10.0
+# main-job slowdown +3.5-4.6 % without; with (20 ms idle, 50 ms at 64 CTAs) +1.6 %, at ~16 % less fill.
+COOLDOWN_MS = 20.0
 THROTTLE_MS = 50.0
 THROTTLE_CTAS = 64
 # main-job slowdown phase: A = fill-off, B = fill-on iteration of one stage; the first of each run is
@@ -1215,7 +1215,7 @@ def main() -> None:
         device_s=sum(t["step_end"] - t["start"] for t in steps) / 1e9)
     gemm_launches = len(gemm_full)
     gemm_by_batch = {}
-    for fl, ms, _, cnt in gemm_full:
+    for fl, ms, _, cnt, *_ in gemm_full:
         a = gemm_by_batch.setdefault(str(cnt), [0.0, 0.0, 0])
         a[0] += fl
         a[1] += ms

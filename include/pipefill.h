@@ -250,6 +250,14 @@ int pf_col2im(const void* dCol, const void* R, void* dX, int B, int H, int W, in
 int pf_maxpool_bwd(const void* X, const void* dY, void* dX, int B, int H, int W, int C, int k, int stride,
                    int pad, const pf_ctl_t* ctl, void* stream);
 int pf_avgpool_bwd(const void* dY, void* dX, int B, int HW, int C, const pf_ctl_t* ctl, void* stream);
+/* Max pooling that also writes the window position (wy * k + wx, uint8, k <= 16) of each
+ * output's first maximum, and the backward that reads it instead of re-scanning X:
+ * training's stem (torch's max_pool2d "first maximum" rule; bit-identical to pf_maxpool /
+ * pf_maxpool_bwd). Idx is [B, Ho, Wo, C] bytes, 8-B aligned.                            */
+int pf_maxpool_argmax(const void* X, void* Y, uint8_t* Idx, int B, int H, int W, int C, int k, int stride,
+                      int pad, const pf_ctl_t* ctl, void* stream);
+int pf_maxpool_bwd_argmax(const uint8_t* Idx, const void* dY, void* dX, int B, int H, int W, int C, int k,
+                          int stride, int pad, const pf_ctl_t* ctl, void* stream);
 /* Softmax cross-entropy, warp per row: loss[4*b] = logsumexp(Z_b) - Z_b[label_b],
  * dZ = (softmax(Z) - onehot) * grad_scale. labels int32, 4-word stride per sample.   */
 int pf_softmax_xent(const void* Z, const int32_t* labels, float* loss, void* dZ, int B, int N,
@@ -335,6 +343,10 @@ int pf_chain_add_col2im(pf_chain_t* chain, const void* dCol, const void* R, void
 int pf_chain_add_maxpool_bwd(pf_chain_t* chain, const void* X, const void* dY, void* dX, int B, int H, int W,
                              int C, int k, int stride, int pad);
 int pf_chain_add_avgpool_bwd(pf_chain_t* chain, const void* dY, void* dX, int B, int HW, int C);
+int pf_chain_add_maxpool_argmax(pf_chain_t* chain, const void* X, void* Y, uint8_t* Idx, int B, int H, int W,
+                                int C, int k, int stride, int pad);
+int pf_chain_add_maxpool_bwd_argmax(pf_chain_t* chain, const uint8_t* Idx, const void* dY, void* dX, int B,
+                                    int H, int W, int C, int k, int stride, int pad);
 int pf_chain_add_softmax_xent(pf_chain_t* chain, const void* Z, const int32_t* labels, float* loss, void* dZ,
                               int B, int N, float grad_scale);
 int pf_chain_add_sgd(pf_chain_t* chain, const pf_sgd_segment_t* segs, int nseg, float lr, float momentum);

@@ -92,9 +92,12 @@ __global__ void __launch_bounds__(THREADS) im2col_small_c_kernel(
   PF_ITEMS_END
 }
 
+// Idx (optional, training): the window position (wy * k + wx) of each output's first
+// maximum, uint8 per element -- the backward then reads 8 bytes per window instead of
+// re-scanning the window's inputs.
 __global__ void __launch_bounds__(THREADS) maxpool_kernel(
-    const __nv_bfloat16* __restrict__ X, __nv_bfloat16* __restrict__ Y, int H, int W, int C,
-    int k, int stride, int pad, long long total_vec, FastDiv dcv, FastDiv dWo, FastDiv dHo, Ctl ctl) {
+    const __nv_bfloat16* __restrict__ X, __nv_bfloat16* __restrict__ Y, uint8_t* __restrict__ Idx, int H, int W,
+    int C, int k, int stride, int pad, long long total_vec, FastDiv dcv, FastDiv dWo, FastDiv dHo, Ctl ctl) {
   PF_ITEMS_BEGIN(total_vec) {
     const uint32_t pix = dcv.div((uint32_t)v);
     const int c0 = (int)((uint32_t)v - pix * dcv.d) << 3;
@@ -103,8 +106,12 @@ __global__ void __launch_bounds__(THREADS) maxpool_kernel(
     const uint32_t b = dHo.div(t);
     const int oy = (int)(t - b * dHo.d);
     float mx[8];
+    uint32_t arg[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
+    for (int e = 0; e < 8; ++e) {
+      mx[e] = -INFINITY;
+      arg[e] = 0;
+    }
     for (int ky = 0; ky < k; ++ky) {
       const int iy = oy * stride - pad + ky;
       if (iy < 0 || iy >= H) continue;
@@ -114,10 +121,20 @@ __global__ void __launch_bounds__(THREADS) maxpool_kernel(
         float x[8];
         load8(X + (((size_t)b * H + iy) * W + ix) * C + c0, x);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) mx[e] = fmaxf(mx[e], x[e]);
+        for (int e = 0; e < 8; ++e)
+          if (x[e] > mx[e]) {  // strict: the first maximum in (ky, kx) scan order
+            mx[e] = x[e];
+            arg[e] = (uint32_t)(ky * k + kx);
+          }
       }
     }
     store8(Y + (size_t)pix * C + c0, mx);
+    if (Idx) {
+      uint2 u;
+      u.x = arg[0] | (arg[1] << 8) | (arg[2] << 16) | (arg[3] << 24);
+      u.y = arg[4] | (arg[5] << 8) | (arg[6] << 16) | (arg[7] << 24);
+      *reinterpret_cast<uint2*>(Idx + (size_t)pix * C + c0) = u;
+    }
   }
   PF_ITEMS_END
 }
@@ -173,12 +190,13 @@ struct Im2colOp final : PreparedOp {
 struct MaxpoolOp final : PreparedOp {
   const __nv_bfloat16* x = nullptr;
   __nv_bfloat16* y = nullptr;
+  uint8_t* idx = nullptr;  // optional argmax output (training)
   int H = 0, W = 0, C = 0, Ho = 0, Wo = 0, k = 0, stride = 1, pad = 0;
   long long n = 0;
   uint32_t units() const override { return blocks_for(n); }
   bool resumable() const override { return false; }
   int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
-    maxpool_kernel<<<units(), THREADS, 0, s>>>(x, y, H, W, C, k, stride, pad, n, FastDiv((uint32_t)(C / 8)),
+    maxpool_kernel<<<units(), THREADS, 0, s>>>(x, y, idx, H, W, C, k, stride, pad, n, FastDiv((uint32_t)(C / 8)),
                                                 FastDiv((uint32_t)Wo), FastDiv((uint32_t)Ho), make_ctl(ctl));
     PF_CUDA(cudaGetLastError());
     return PF_OK;
@@ -240,13 +258,16 @@ int make_im2col_op(OpPtr* out, const void* X, void* Col, int B, int H, int W, in
 }
 
 int make_maxpool_op(OpPtr* out, const void* X, void* Y, int B, int H, int W, int C, int k, int stride,
-                    int pad) {
+                    int pad, void* Idx) {
   PF_TRY(conv::check_ptrs(X, Y, "pf_maxpool"));
+  if (Idx && (k > 16 || ((uintptr_t)Idx & 7u)))
+    return set_error(PF_ERR_INVALID, "pf_maxpool_argmax: need k <= 16 and an 8-B aligned index buffer");
   if (B <= 0 || H <= 0 || W <= 0 || C <= 0 || C % 8 != 0 || k <= 0 || stride <= 0 || pad < 0 || pad >= k)
     return set_error(PF_ERR_INVALID, "pf_maxpool: bad shape (C %% 8 == 0, 0 <= pad < k)");
   auto op = std::make_unique<conv::MaxpoolOp>();
   op->x = reinterpret_cast<const bf*>(X);
   op->y = reinterpret_cast<bf*>(Y);
+  op->idx = reinterpret_cast<uint8_t*>(Idx);
   op->H = H;
   op->W = W;
   op->C = C;
@@ -290,7 +311,16 @@ extern "C" int pf_maxpool(const void* X, void* Y, int B, int H, int W, int C, in
                           int pad, const pf_ctl_t* ctl, void* stream) {
   PF_TRY(pf::validate_ctl(ctl));
   pf::OpPtr op;
-  PF_TRY(pf::make_maxpool_op(&op, X, Y, B, H, W, C, k, stride, pad));
+  PF_TRY(pf::make_maxpool_op(&op, X, Y, B, H, W, C, k, stride, pad, nullptr));
+  return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), pf::LaunchArgs{});
+}
+
+extern "C" int pf_maxpool_argmax(const void* X, void* Y, uint8_t* Idx, int B, int H, int W, int C, int k,
+                                 int stride, int pad, const pf_ctl_t* ctl, void* stream) {
+  PF_TRY(pf::validate_ctl(ctl));
+  if (!Idx) return pf::set_error(PF_ERR_INVALID, "pf_maxpool_argmax: null index buffer");
+  pf::OpPtr op;
+  PF_TRY(pf::make_maxpool_op(&op, X, Y, B, H, W, C, k, stride, pad, Idx));
   return op->run(ctl, reinterpret_cast<cudaStream_t>(stream), pf::LaunchArgs{});
 }
 

@@ -18,7 +18,8 @@ constexpr int ROWS_PER_CTA = WARPS * ROWS_PER_WARP;
 constexpr int MAX_NV = 8;  // 8 vectors x 8 bf16 x 32 lanes = 2048 columns
 
 // Normalise one row held as NV vectors of 8 per lane (vector j covers columns
-// (j*32 + lane)*8 .. +8), then write gamma/beta-scaled bf16.
+// (j*32 + lane)*8 .. +8), then write gamma/beta-scaled bf16. (Preloading gamma / beta with
+// the row cost 90 registers and occupancy: 15.6 -> 17.9 us per BERT-large LN, reverted.)
 template <int NV, bool RMS>
 __device__ __forceinline__ void norm_row_store(float (&x)[NV][8], int cols, float eps,
                                                const __nv_bfloat16* gamma,

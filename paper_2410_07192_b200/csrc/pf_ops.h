@@ -52,6 +52,8 @@ int make_col2im_op(OpPtr* out, const void* dCol, const void* R, void* dX, int B,
                    int kw, int stride, int pad, int Kp);
 int make_maxpool_bwd_op(OpPtr* out, const void* X, const void* dY, void* dX, int B, int H, int W, int C, int k,
                         int stride, int pad);
+int make_maxpool_bwd_idx_op(OpPtr* out, const void* Idx, const void* dY, void* dX, int B, int H, int W, int C,
+                            int k, int stride, int pad);
 int make_avgpool_bwd_op(OpPtr* out, const void* dY, void* dX, int B, int HW, int C);
 int make_xent_op(OpPtr* out, const void* Z, const int32_t* labels, float* loss, void* dZ, int B, int N,
                  float grad_scale);
@@ -80,7 +82,7 @@ int make_copy_op(OpPtr* out, void* dst, int64_t dst_pitch, const void* src, int6
 int make_im2col_op(OpPtr* out, const void* X, void* Col, int B, int H, int W, int C, int kh, int kw,
                    int stride, int pad, int Kp);
 int make_maxpool_op(OpPtr* out, const void* X, void* Y, int B, int H, int W, int C, int k, int stride,
-                    int pad);
+                    int pad, void* Idx = nullptr);
 int make_avgpool_op(OpPtr* out, const void* X, void* Y, int B, int HW, int C);
 
 }  // namespace pf

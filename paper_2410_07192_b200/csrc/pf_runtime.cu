@@ -747,6 +747,10 @@ int pf_chain_add_maxpool_bwd(pf_chain_t* c, const void* X, const void* dY, void*
                              int k, int stride, int pad) {
   PF_CHAIN_ADD(pf::make_maxpool_bwd_op(&op, X, dY, dX, B, H, W, C, k, stride, pad));
 }
+int pf_chain_add_maxpool_bwd_argmax(pf_chain_t* c, const uint8_t* Idx, const void* dY, void* dX, int B, int H,
+                                    int W, int C, int k, int stride, int pad) {
+  PF_CHAIN_ADD(pf::make_maxpool_bwd_idx_op(&op, Idx, dY, dX, B, H, W, C, k, stride, pad));
+}
 int pf_chain_add_avgpool_bwd(pf_chain_t* c, const void* dY, void* dX, int B, int HW, int C) {
   PF_CHAIN_ADD(pf::make_avgpool_bwd_op(&op, dY, dX, B, HW, C));
 }
@@ -784,6 +788,14 @@ int pf_chain_add_maxpool(pf_chain_t* c, const void* X, void* Y, int B, int H, in
   if (!c) return pf::set_error(PF_ERR_INVALID, "null chain");
   pf::OpPtr op;
   return chain_push(c, pf::make_maxpool_op(&op, X, Y, B, H, W, C, k, stride, pad), op);
+}
+
+int pf_chain_add_maxpool_argmax(pf_chain_t* c, const void* X, void* Y, uint8_t* Idx, int B, int H, int W, int C,
+                                int k, int stride, int pad) {
+  if (!c) return pf::set_error(PF_ERR_INVALID, "null chain");
+  if (!Idx) return pf::set_error(PF_ERR_INVALID, "pf_chain_add_maxpool_argmax: null index buffer");
+  pf::OpPtr op;
+  return chain_push(c, pf::make_maxpool_op(&op, X, Y, B, H, W, C, k, stride, pad, Idx), op);
 }
 
 int pf_chain_add_avgpool(pf_chain_t* c, const void* X, void* Y, int B, int HW, int C) {

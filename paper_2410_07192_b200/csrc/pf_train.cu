@@ -432,6 +432,52 @@ __global__ void __launch_bounds__(T) maxpool_bwd_kernel(const bf* __restrict__ X
   PF_ITEMS_END
 }
 
+// Max-pool backward from the forward's argmax bytes (pf_maxpool_argmax): every input pixel
+// gathers dY from the <= ceil(k / stride)^2 windows that contain it, where that window's
+// first maximum sits at this pixel -- 8 index bytes and 16 B of dY per window instead of
+// re-scanning the window's k * k inputs. Same (ky, kx) order and fp32 sums as
+// maxpool_bwd_kernel, so the two agree bit for bit.
+__global__ void __launch_bounds__(T) maxpool_bwd_idx_kernel(const uint8_t* __restrict__ Idx, const bf* __restrict__ dY,
+                                                            bf* __restrict__ dX, int H, int W, int C, int Ho,
+                                                            int Wo, int k, int stride, int pad, long long nvec,
+                                                            FastDiv dcv, FastDiv dW, FastDiv dH, Ctl ctl) {
+  PF_ITEMS_BEGIN(nvec) {
+    const uint32_t pix = dcv.div((uint32_t)v);
+    const int c0 = (int)((uint32_t)v - pix * dcv.d) << 3;
+    const uint32_t t = dW.div(pix);
+    const int ix = (int)(pix - t * dW.d);
+    const uint32_t b = dH.div(t);
+    const int iy = (int)(t - b * dH.d);
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+    for (int ky = 0; ky < k; ++ky) {
+      const int ny = iy + pad - ky;
+      if (ny < 0 || ny % stride) continue;
+      const int oy = ny / stride;
+      if (oy >= Ho) continue;
+      for (int kx = 0; kx < k; ++kx) {
+        const int nx = ix + pad - kx;
+        if (nx < 0 || nx % stride) continue;
+        const int ox = nx / stride;
+        if (ox >= Wo) continue;
+        const size_t o = (((size_t)b * Ho + oy) * Wo + ox) * C + c0;
+        const uint2 id = *reinterpret_cast<const uint2*>(Idx + o);
+        const uint32_t pos = (uint32_t)(ky * k + kx);  // this pixel's position in window (oy, ox)
+        float g[8];
+        load8(dY + o, g);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint32_t a = ((e < 4 ? id.x : id.y) >> (8 * (e & 3))) & 0xffu;
+          if (a == pos) acc[e] += g[e];
+        }
+      }
+    }
+    store8(dX + (size_t)pix * C + c0, acc);
+  }
+  PF_ITEMS_END
+}
+
 __global__ void __launch_bounds__(T) avgpool_bwd_kernel(const bf* __restrict__ dY, bf* __restrict__ dX,
                                                         int HW, int C, long long nvec, FastDiv dcv,
                                                         FastDiv dhwcv, Ctl ctl) {
@@ -661,6 +707,7 @@ struct Col2imOp final : PreparedOp {
 
 struct PoolBwdOp final : PreparedOp {
   const bf *x = nullptr, *dy = nullptr;
+  const uint8_t* idx = nullptr;  // argmax bytes of the forward (maxpool_bwd_idx_kernel) instead of x
   bf* dx = nullptr;
   int H = 0, W = 0, C = 0, Ho = 0, Wo = 0, k = 0, stride = 1, pad = 0, HW = 0;
   bool avg = false;
@@ -672,7 +719,12 @@ struct PoolBwdOp final : PreparedOp {
       avgpool_bwd_kernel<<<units(), T, 0, s>>>(dy, dx, HW, C, nvec, FastDiv((uint32_t)(C / 8)),
                                                FastDiv((uint32_t)(HW * (C / 8))), make_ctl(ctl));
     else
-      maxpool_bwd_kernel<<<units(), T, 0, s>>>(x, dy, dx, H, W, C, Ho, Wo, k, stride, pad, nvec,
+      if (idx)
+        maxpool_bwd_idx_kernel<<<units(), T, 0, s>>>(idx, dy, dx, H, W, C, Ho, Wo, k, stride, pad, nvec,
+                                                     FastDiv((uint32_t)(C / 8)), FastDiv((uint32_t)W),
+                                                     FastDiv((uint32_t)H), make_ctl(ctl));
+      else
+  maxpool_bwd_kernel<<<units(), T, 0, s>>>(x, dy, dx, H, W, C, Ho, Wo, k, stride, pad, nvec,
                                                FastDiv((uint32_t)(C / 8)), FastDiv((uint32_t)W),
                                                FastDiv((uint32_t)H), make_ctl(ctl));
     PF_CUDA(cudaGetLastError());
@@ -887,6 +939,15 @@ int make_maxpool_bwd_op(OpPtr* out, const void* X, const void* dY, void* dX, int
   return PF_OK;
 }
 
+int make_maxpool_bwd_idx_op(OpPtr* out, const void* Idx, const void* dY, void* dX, int B, int H, int W, int C,
+                            int k, int stride, int pad) {
+  if (!Idx || ((uintptr_t)Idx & 7u) || k > 16)
+    return set_error(PF_ERR_INVALID, "pf_maxpool_bwd_argmax: need an 8-B aligned index buffer and k <= 16");
+  PF_TRY(make_maxpool_bwd_op(out, dY, dY, dX, B, H, W, C, k, stride, pad));
+  static_cast<train::PoolBwdOp*>(out->get())->idx = reinterpret_cast<const uint8_t*>(Idx);
+  return PF_OK;
+}
+
 int make_avgpool_bwd_op(OpPtr* out, const void* dY, void* dX, int B, int HW, int C) {
   if (!dY || !dX || B <= 0 || HW <= 0 || C % 8 != 0) return set_error(PF_ERR_INVALID, "pf_avgpool_bwd: bad arguments");
   auto op = std::make_unique<train::PoolBwdOp>();
@@ -1004,6 +1065,11 @@ extern "C" int pf_col2im(const void* dCol, const void* R, void* dX, int B, int H
 extern "C" int pf_maxpool_bwd(const void* X, const void* dY, void* dX, int B, int H, int W, int C, int k,
                               int stride, int pad, const pf_ctl_t* ctl, void* stream) {
   PF_RUN_OP(pf::make_maxpool_bwd_op(&op, X, dY, dX, B, H, W, C, k, stride, pad));
+}
+
+extern "C" int pf_maxpool_bwd_argmax(const uint8_t* Idx, const void* dY, void* dX, int B, int H, int W, int C,
+                                     int k, int stride, int pad, const pf_ctl_t* ctl, void* stream) {
+  PF_RUN_OP(pf::make_maxpool_bwd_idx_op(&op, Idx, dY, dX, B, H, W, C, k, stride, pad));
 }
 
 extern "C" int pf_avgpool_bwd(const void* dY, void* dX, int B, int HW, int C, const pf_ctl_t* ctl,

@@ -153,6 +153,10 @@ _SIGNATURES: dict[str, tuple] = {
     "pf_maxpool_bwd": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                                POINTER(PfCtl), c_void_p]),
     "pf_avgpool_bwd": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, POINTER(PfCtl), c_void_p]),
+    "pf_maxpool_argmax": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                                  POINTER(PfCtl), c_void_p]),
+    "pf_maxpool_bwd_argmax": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int,
+                                      c_int, POINTER(PfCtl), c_void_p]),
     "pf_softmax_xent": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_float, POINTER(PfCtl),
                                 c_void_p]),
     "pf_sgd_update": (c_int, [POINTER(SgdSegment), c_int, c_float, c_float, POINTER(PfCtl), c_void_p]),
@@ -172,6 +176,10 @@ _SIGNATURES: dict[str, tuple] = {
     "pf_chain_add_maxpool_bwd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int,
                                          c_int, c_int, c_int]),
     "pf_chain_add_avgpool_bwd": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int]),
+    "pf_chain_add_maxpool_argmax": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int,
+                                            c_int, c_int, c_int]),
+    "pf_chain_add_maxpool_bwd_argmax": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int,
+                                                c_int, c_int, c_int, c_int]),
     "pf_chain_add_softmax_xent": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int,
                                           c_float]),
     "pf_chain_add_sgd": (c_int, [c_void_p, POINTER(SgdSegment), c_int, c_float, c_float]),

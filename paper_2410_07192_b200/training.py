@@ -294,6 +294,7 @@ class TrainStem(TrainModule):
         i = self.idx
         ws = {f"s{i}.col": m1 * c.stem_kp, f"s{i}.z": m1 * c.stem_ch, f"s{i}.a": m1 * c.stem_ch,
               f"s{i}.stats": 4 * c.stem_ch, f"out{i}": batch * self.h2 * self.h2 * c.stem_ch,
+              f"s{i}.argmax": (batch * self.h2 * self.h2 * c.stem_ch + 1) // 2,  # uint8 in bf16 units
               "da": m1 * c.stem_ch, "dz": m1 * c.stem_ch}
         ws.update(self.grad_ws(batch))
         return ws
@@ -317,8 +318,10 @@ class TrainStem(TrainModule):
         r.im2col(x, 7, 2, 3, c.stem_kp, col)
         r.gemm(col, d["w.w"], z)
         r.bn_forward(z, d["g"], d["b"], st[:c.stem_ch], st[c.stem_ch:], a.view(m1, c.stem_ch), relu=True)
-        r.call("pf_chain_add_maxpool", a.data_ptr(), out.data_ptr(), b, self.h1, self.h1, c.stem_ch, 3, 2, 1)
-        self.saved = dict(col=col, z=z, a=a, st=st, b=b)
+        idx = ctx.buf(f"s{i}.argmax", (b * self.h2 * self.h2 * c.stem_ch + 1) // 2)
+        r.call("pf_chain_add_maxpool_argmax", a.data_ptr(), out.data_ptr(), idx.data_ptr(), b, self.h1, self.h1,
+               c.stem_ch, 3, 2, 1)
+        self.saved = dict(col=col, z=z, a=a, st=st, b=b, idx=idx)
         return out
 
     def record_backward(self, r: _Rec, dout):
@@ -326,8 +329,8 @@ class TrainStem(TrainModule):
         b = s["b"]
         m1 = b * self.h1 * self.h1
         da = ctx.buf("da", m1 * c.stem_ch).view(b, self.h1, self.h1, c.stem_ch)
-        r.call("pf_chain_add_maxpool_bwd", s["a"].data_ptr(), dout.data_ptr(), da.data_ptr(), b, self.h1, self.h1,
-               c.stem_ch, 3, 2, 1)
+        r.call("pf_chain_add_maxpool_bwd_argmax", s["idx"].data_ptr(), dout.data_ptr(), da.data_ptr(), b, self.h1,
+               self.h1, c.stem_ch, 3, 2, 1)
         dz = ctx.buf("dz", m1 * c.stem_ch).view(m1, c.stem_ch)
         g = {p.name: ctx.ws[f"g{i}.{p.name}"] for p in self.tparams()}
         gf = lambda nm: g[nm].view(-1)[:2 * c.stem_ch].view(torch.float32)  # noqa: E731

@@ -130,6 +130,33 @@ def test_pool_backward(K):
     assert rel(got, (d.float() / 49)[:, None, :].expand(4, 49, 2048)) < 1e-2
 
 
+@pytest.mark.parametrize("shape", [(2, 28, 28, 64), (3, 17, 15, 16), (64, 112, 112, 64)])
+def test_maxpool_argmax_path_is_bit_identical(K, shape):
+    """pf_maxpool_argmax writes the same pooled output as pf_maxpool plus the first-maximum
+    window positions; pf_maxpool_bwd_argmax (reads 8 index bytes per window) equals
+    pf_maxpool_bwd (re-scans every window) bit for bit, ties included."""
+    from paper_2410_07192_b200 import native
+
+    g = torch.Generator().manual_seed(9)
+    b, h, w, c = shape
+    x = bf(b, h, w, c, gen=g)
+    x[0, :4, :4, :8] = 1.0  # ties inside windows: the first maximum wins in both paths
+    x = x.cuda()
+    ho, wo = (h + 2 - 3) // 2 + 1, (w + 2 - 3) // 2 + 1
+    y_ref = K.maxpool(x, 3, 2, 1) if hasattr(K, "maxpool") else None
+    y = torch.empty(b, ho, wo, c, dtype=torch.bfloat16, device="cuda")
+    idx = torch.empty(b * ho * wo * c, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    native.call("pf_maxpool_argmax", x.data_ptr(), y.data_ptr(), idx.data_ptr(), b, h, w, c, 3, 2, 1, None, s)
+    if y_ref is not None:
+        assert torch.equal(y, y_ref)
+    dy = bf(b, ho, wo, c, gen=g).cuda()
+    dx = torch.empty_like(x)
+    native.call("pf_maxpool_bwd_argmax", idx.data_ptr(), dy.data_ptr(), dx.data_ptr(), b, h, w, c, 3, 2, 1, None, s)
+    torch.cuda.synchronize()
+    assert torch.equal(dx, K.maxpool_bwd(x, dy))
+
+
 def test_softmax_cross_entropy(K):
     g = torch.Generator().manual_seed(5)
     b, n = 24, 1000
