@@ -507,7 +507,8 @@ def run_training_depths(args, conf) -> None:
     _, hi_prio = torch.cuda.Stream.priority_range()
     streams = (torch.cuda.Stream(priority=hi_prio), torch.cuda.Stream(priority=hi_prio))
     free_b, total_b = torch.cuda.mem_get_info()
-    probe_model = resnet50_train(seed=0)
+    part = bool(args.train_partitioned)
+    probe_model = resnet50_train(seed=0, partitioned=part)
     profile = measure_train_profile(probe_model, conf["batch_sizes"])
     torch.cuda.synchronize()
     # the main job's peak with 8 microbatches in flight (stage 0 of the deepest pipeline)
@@ -520,6 +521,8 @@ def run_training_depths(args, conf) -> None:
     free_b, total_b = torch.cuda.mem_get_info()
     reserved = torch.cuda.max_memory_reserved()
     arena_bytes = int(min(max(0, total_b - reserved - (4 << 30)) * 0.9, conf["arena_cap"]))
+    if args.arena_cap_gb:  # a capped bubble free memory: partitioned training plans
+        arena_bytes = min(arena_bytes, int(args.arena_cap_gb * 2**30))
     executor = Executor(arena_bytes, job_seed=rank)
     n_total = args.warmup + args.steps
     results, stats_all = {}, []
@@ -528,7 +531,7 @@ def run_training_depths(args, conf) -> None:
             pcfg = pf.PipelineConfig(P, conf["micro"], tf_ms, tb_ms, pf.ScheduleKind.ONE_F_ONE_B, arena_bytes,
                                      arena_bytes, args.fill_fraction)
             engines = {s_: StageEngine(pcfg, s_, main_model, executor, streams=streams) for s_ in range(P)}
-            models = {s_: resnet50_train(seed=s_) for s_ in range(P)}
+            models = {s_: resnet50_train(seed=s_, partitioned=part) for s_ in range(P)}
             for m_ in models.values():
                 m_.profile = profile
             coords, items = {}, {}
@@ -584,6 +587,7 @@ def run_training_depths(args, conf) -> None:
             executor.gemm_samples = []
             n_rec0 = len(executor.records)
             launches0 = executor.kernel_launches + sum(e.launches for e in engines.values())
+            h2d0 = executor.h2d_bytes
             steps = [step(k) for k in range(args.warmup, n_total)]
             executor.timing = False
             recs = executor.records[n_rec0:]
@@ -614,6 +618,9 @@ def run_training_depths(args, conf) -> None:
                 "gemm_tflops_in_situ": tot.gemm_tflops, "gemm_launch_roofline": launch_roof,
                 "sgd_steps": int(sum(r_.batches_done for r_ in recs)),
                 "plan_stage0": pf.plan_to_dict(coords[0].executables["train-0"]),
+                "partitions_per_stage": {str(s_): len(coords[s_].executables[f"train-{s_}"].partitions)
+                                         for s_ in range(P)},
+                "h2d_bytes_per_step": (executor.h2d_bytes - h2d0) / max(1, len(steps)),
                 "ms_per_step": 1000 * tot.device_s / max(1, len(steps))}
             executor.work_source = None
             for m_ in models.values():
@@ -627,7 +634,10 @@ def run_training_depths(args, conf) -> None:
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random-init ResNet-50, N(0,1) 224x224 images, uniform labels)",
             "config": {"name": "c4", "workload": "ResNet-50 training fill (fwd+bwd+SGD per batch, train-mode BN) in "
-                       "the bubbles of a 1F1B GPT-style 8B main job at 2/4/8 stages (artificial neighbours)",
+                       "the bubbles of a 1F1B GPT-style 8B main job at 2/4/8 stages (artificial neighbours)"
+                       + (", 18-module partitioned training plans (batch-major phases, state written back "
+                          "per partition)" if part else ""),
+                       "train_partitioned": part, "arena_cap_gb": args.arena_cap_gb,
                        "depths": list(conf["depths"]), "batch_sizes": list(conf["batch_sizes"]),
                        "fill_fraction": args.fill_fraction, "arena_bytes": arena_bytes,
                        "t_fwd_ms": tf_ms, "t_bwd_ms": tb_ms,
@@ -819,6 +829,10 @@ def main() -> None:
     ap.add_argument("--throttle-ctas", type=int, default=THROTTLE_CTAS)
     ap.add_argument("--loss-iters", type=int, default=4,
                     help="nccl: iterations per deterministic fill-off / on / off loss-identity replay")
+    ap.add_argument("--train-partitioned", action="store_true",
+                    help="c4: ResNet-50 training with its 18 modules as plan nodes (partitioned across bubbles)")
+    ap.add_argument("--arena-cap-gb", type=float, default=None,
+                    help="cap the fill arena / bubble free memory (GB), e.g. to force multi-partition plans")
     ap.add_argument("--slowdown-pattern", default=None,
                     help="explicit fill-off (A) / fill-on (B) iteration order per stage, e.g. AABBBBAA")
     ap.add_argument("--slowdown-stages", default=None, help="comma-separated stages for the slowdown phase")

@@ -401,7 +401,9 @@ int pf_chain_launch(pf_chain_t* chain, const uint32_t* flag, uint32_t* abort, ui
  * to *staged_out (1 = staged). A run-ahead staging behind a batch that yielded is
  * therefore skipped and cannot overwrite the yielded batch's weights or workspace
  * (the region holds one partition at a time). No reference counterpart:
- * the reference charges partitions whole cycles (partition.py:118-124).              */
+ * the reference charges partitions whole cycles (partition.py:118-124). Copies may go
+ * either way (cudaMemcpyDefault): a partitioned training job writes the updated state of
+ * the resident partition back to its pinned blob and stages the next one in one graph. */
 typedef struct pf_staging pf_staging_t;
 int pf_staging_create(pf_staging_t** out, void* const* dst, const void* const* src,
                       const uint64_t* bytes, int n, const uint32_t* abort, uint32_t* staged_out);

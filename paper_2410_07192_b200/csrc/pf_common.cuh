@@ -102,6 +102,18 @@ __device__ __forceinline__ bool chain_aborted(const Ctl& c) {
   return c.abort != nullptr && ld_volatile_u32(c.abort) != 0u;
 }
 
+// The entry check made uniform across the CTA: thread 0 reads the abort word and the
+// decision goes through shared memory. Other CTAs of the same kernel set the word when they
+// see the bubble close, so per-thread reads at entry can disagree inside one CTA, and the
+// threads that stayed would wait at the next __syncthreads for the ones that returned
+// (found as an intermittent fill-stream stall in the SGD kernel of a resumed training
+// phase). `word` is a CTA-shared scratch word.
+__device__ __forceinline__ bool chain_aborted_cta(const Ctl& c, volatile uint32_t* word) {
+  if (threadIdx.x == 0) *word = chain_aborted(c) ? 1u : 0u;
+  __syncthreads();
+  return *word != 0u;
+}
+
 // Bubble flag values: 0 = closed (yield), 1 = open, v >= 2 = open but throttled to v CTAs:
 // in the bubble's last milliseconds the engine lowers the fill's power draw so the board's
 // power controller has raised the SM clock again when the main job resumes.

@@ -30,7 +30,8 @@ __global__ void __launch_bounds__(T) sgemm_kernel(const float* __restrict__ X, c
                                                   const float* __restrict__ bias, const float* __restrict__ R,
                                                   float* __restrict__ Y, int M, int N, int K, int gelu_on,
                                                   int tiles_n, int tiles, Ctl ctl) {
-  if (chain_aborted(ctl)) return;
+  __shared__ uint32_t s_abort;
+  if (chain_aborted_cta(ctl, &s_abort)) return;
   __shared__ float sA[2][BK][BM + 4];
   __shared__ float sB[2][BK][BN + 4];
   __shared__ int s_tile;

@@ -320,7 +320,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int lane = lane_id();
 
   pdl_enter();
-  if (chain_aborted(ctl)) return;  // uniform across the CTA: nothing allocated yet
+  // CTA-uniform (thread 0 decides; nothing allocated yet); tmem_base_smem[2] is scratch
+  if (chain_aborted_cta(ctl, tmem_base_smem + 2)) return;
   DIAG_INIT();
   if (threadIdx.x == 0 && p.stamp) atomicMin(&p.stamp[0], globaltimer_ns());
 

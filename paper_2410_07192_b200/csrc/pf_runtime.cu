@@ -605,7 +605,7 @@ int pf_staging_create(pf_staging_t** out, void* const* dst, const void* const* s
       if (bytes[i] == 0) continue;
       cudaGraphNode_t nd;
       rc = check_cuda(cudaGraphAddMemcpyNode1D(&nd, body, prev ? &prev : nullptr, prev ? 1 : 0, dst[i],
-                                               src[i], (size_t)bytes[i], cudaMemcpyHostToDevice),
+                                               src[i], (size_t)bytes[i], cudaMemcpyDefault),
                       "cudaGraphAddMemcpyNode1D (conditional body)");
       prev = nd;
     }

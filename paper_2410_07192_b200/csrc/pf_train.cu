@@ -564,7 +564,8 @@ constexpr int MAX_SGD_SEGS = 256;
 
 __global__ void __launch_bounds__(T) sgd_kernel(const SgdSeg* __restrict__ segs, int nseg, int units,
                                                 float lr, float mu, Ctl ctl) {
-  if (chain_aborted(ctl)) return;
+  __shared__ uint32_t s_abort;
+  if (chain_aborted_cta(ctl, &s_abort)) return;
   __shared__ int s_unit;
   __shared__ int s_first[MAX_SGD_SEGS];  // first unit of every segment: binary-searched in smem
   for (int i = threadIdx.x; i < nseg; i += T) s_first[i] = segs[i].first_unit;

@@ -109,6 +109,7 @@ class _Pending:
     has_resume: bool = False
     parts: list[int] = None  # partition of every batch (run-ahead appends partition part + 1)
     progress_key: tuple = ()  # (part, next sample, resume point, resume cursor) when enqueued
+    tp: Optional[list] = None  # partitioned training: [(batch index, phase index, start node)] enqueued
 
 
 class _Chain:
@@ -254,11 +255,17 @@ class Executor:
         self.progress = _Progress()
         self._cursor_now = -1
         self.starved = 0
+        self._tp_state = {"phase": 0, "resident": 0, "dirty": False} if self._tp else None
         self._in_host.tensor[:n].copy_(self.model.make_inputs(self.job_seed, item.entry.lo - 1, n))
         if self._aux_host is not None:
             self._aux_host.tensor[:n].copy_(self.model.make_aux(self.job_seed, item.entry.lo - 1, n))
         self._stage_partition(0)
         self.prewarm()
+
+    @property
+    def _tp(self) -> bool:
+        """Partitioned training (training.ResNetTrainPartitioned): batch-major phases."""
+        return bool(getattr(self.model, "partitioned", False))
 
     def _layout(self, cap: int) -> None:
         """Carve a new executable's region out of the arena; when the arena is full,
@@ -283,7 +290,7 @@ class Executor:
         w = sum(_pad256(model[i].weight_bytes()) for i in range(p.lo, p.hi))
         b = max([e.batch_size for e in p.per_bubble] + [1])
         need = dict(model.workspace(p.lo, p.hi, b))
-        if p.lo > 0:  # the partition's input, reloaded from the activation store (bf16 units)
+        if p.lo > 0 and not self._tp:  # the partition's input, reloaded from the activation store (bf16 units)
             need["in"] = b * model.boundary_elems(p.lo) * model.act_bytes() // 2
         return w, need
 
@@ -308,6 +315,8 @@ class Executor:
         self._gated: dict[int, ctypes.c_void_p] = {}  # partition -> gated run-ahead staging graph
         self.ws = {}
         bmax = max(e.batch_size for p in plan.partitions[:1] for e in p.per_bubble)
+        if self._tp:
+            bmax = max(bmax, self._tp_batch())
         in_dtype, in_shape = model.input_spec()
         self.in_dev = self.arena.alloc((max(bmax, 1), *in_shape), in_dtype)
         self._cap = cap
@@ -318,7 +327,16 @@ class Executor:
         self.aux_dev = self.arena.alloc((max(bmax, 1), *aux[1]), aux[0]) if aux else None
         self._store_dev = None
         self._store_host = None
-        if len(plan.partitions) > 1:
+        self._tp_act, self._tp_din = {}, {}
+        if self._tp:
+            # one batch in flight: the input boundary of every partition p > 0 (forward) and the
+            # gradient of that input (backward), b samples each, in HBM
+            b = self._tp_batch()
+            for k in range(1, len(plan.partitions)):
+                shape = (b, *model.boundary_shape(plan.partitions[k].lo))
+                self._tp_act[k] = self.arena.alloc(shape, torch.bfloat16)
+                self._tp_din[k] = self.arena.alloc(shape, torch.bfloat16)
+        elif len(plan.partitions) > 1:
             # one sample's activation at the widest inter-partition boundary. A partition
             # overwrites its input store in place sample by sample, which is safe only when
             # no boundary grows (BERT); otherwise partitions ping-pong between two stores.
@@ -417,18 +435,23 @@ class Executor:
 
     # ------------------------------------------------------------------ chains
 
-    def _chain(self, part_idx: int, cnt: int, flag: Optional[int] = None) -> _Chain:
+    def _chain(self, part_idx, cnt: int, flag: Optional[int] = None) -> _Chain:
+        """Recorded chain of one batch of `cnt` samples through partition `part_idx` (for
+        partitioned training: part_idx = (phase kind, partition))."""
         key = (part_idx, cnt, flag)
         ch = self._chains.get(key)
         if ch is not None:
             return ch
         model = self.model
-        part = self.plan.partitions[part_idx]
-        views, ws = self._part_layout(part_idx)
+        pidx = part_idx[1] if self._tp else part_idx
+        part = self.plan.partitions[pidx]
+        views, ws = self._part_layout(pidx)
         resident = {i: getattr(model[i], "dev", None) for i in views}
         for i, dev in views.items():  # record against the partition's region layout
             model[i].dev = dev
         try:
+            if self._tp:
+                return self._record_tp_chain(key, part_idx[0], pidx, cnt, flag, ws)
             return self._record_chain(key, part, cnt, flag, ws)
         finally:
             for i, dev in resident.items():
@@ -505,14 +528,65 @@ class Executor:
         self._chains[key] = ch
         return ch
 
-    def _write_back(self) -> None:
-        """Training jobs: copy the trained state of every module back to its pinned host
-        blob (copy stream, after the fill stream), so the next range -- or a restage after
-        an eviction -- continues from it."""
-        part = 0
+    def _record_tp_chain(self, key: tuple, kind: str, pidx: int, cnt: int, flag: Optional[int],
+                         ws: dict) -> _Chain:
+        """One phase of one batch of partitioned training (ResNetTrainPartitioned.record_phase):
+        input from the images (partition 0) or the partition's input store, gradient of its
+        output from the next partition's store, output / input gradient to the stores,
+        labels in and per-sample losses out for the loss phase."""
+        model = self.model
+        part = self.plan.partitions[pidx]
+        k = len(self.plan.partitions)
+        ch = _Chain()
+        ctx = ExecContext(self.stream, ws, chain=ch.h)
+        node = 0
+        if pidx == 0:
+            nb = cnt * model.input_bytes()
+            native.call("pf_chain_add_copy", ch.h, self.in_dev.data_ptr(), nb, self._in_host.ptr, nb, nb, 1, 1)
+            x = self.in_dev[:cnt]
+            node += 1
+        else:
+            x = self._tp_act[pidx][:cnt]
+        labels = loss = None
+        if kind == "L":
+            ab = cnt * self._aux_host.tensor[0].numel() * self._aux_host.tensor.element_size()
+            native.call("pf_chain_add_copy", ch.h, self.aux_dev.data_ptr(), ab, self._aux_host.ptr, ab, ab, 1, 3)
+            node += 1
+            labels = self.aux_dev[:cnt]
+            loss = ctx.fbuf("loss", cnt * 4).view(cnt, 4)
+        dout = self._tp_din[pidx + 1][:cnt] if kind == "B" else None
+        ctx.node = node
+        seg_ends, flops, nbytes, out = model.record_phase(kind, part.lo, part.hi, x, dout, labels, loss, ctx)
+        ch.seg_ends, ch.gemm_flops, ch.gemm_bytes = list(seg_ends), flops, nbytes
+        if kind == "F":  # the output boundary for the next partition
+            dst = self._tp_act[pidx + 1][:cnt]
+            nb = dst.numel() * 2
+            native.call("pf_chain_add_copy", ch.h, dst.data_ptr(), nb, out.data_ptr(), nb, nb, 1, 0)
+        elif pidx > 0:  # the gradient of the partition's input for the previous partition
+            dst = self._tp_din[pidx][:cnt]
+            nb = dst.numel() * 2
+            native.call("pf_chain_add_copy", ch.h, dst.data_ptr(), nb, out.data_ptr(), nb, nb, 1, 0)
+        if kind == "L":
+            rb = cnt * 16
+            native.call("pf_chain_add_copy", ch.h, self._results.ptr, rb, loss.data_ptr(), rb, rb, 1, 2)
+        _ = k
+        ch.finalize()
+        ch.seg_ends[-1] = len(ch.units)
+        native.call("pf_chain_set_desc", ch.h, self._desc.data_ptr())
+        native.call("pf_chain_set_stamps", ch.h, self._stamps.data_ptr())
+        base = self._ctl.data_ptr()
+        ch.build_graph(flag, base if flag else None, base + 4 * _CURSOR0 if flag else None, base + 4)
+        self._chains[key] = ch
+        return ch
+
+    def _write_back(self, part: int = 0) -> None:
+        """Training jobs: copy the trained state of every module of partition `part` back to
+        its pinned host blob (copy stream, after the fill stream), so the next range -- or a
+        restage after an eviction -- continues from it."""
+        p = self.plan.partitions[part]
         with torch.cuda.stream(self.copy_stream):
             self.copy_stream.wait_stream(self.stream)
-            for i in range(len(self.model)):
+            for i in range(p.lo, p.hi):
                 mod = self.model[i]
                 if mod.host is not None and mod.weight_bytes():
                     native.call("pf_stage_d2h", mod.host.ptr, self._module_ptr(part, i), mod.weight_bytes(),
@@ -534,6 +608,10 @@ class Executor:
             self._last_flag = flag_ptr or None
         if self.item is None or self.progress.finished:
             return
+        if self._tp:
+            for kind, pidx in self._tp_phases():
+                self._chain((kind, pidx), self._tp_batch(), self._last_flag)
+            return
         for pidx, part in enumerate(self.plan.partitions):  # every partition: switches record nothing
             for e in part.per_bubble:
                 if e.num_batches:
@@ -554,6 +632,9 @@ class Executor:
             if nxt is not None:
                 self.load(*nxt)
         if not self.busy:
+            return prev
+        if self._tp:
+            self._fill_tp(slot)
             return prev
         pr = self.progress
         if self._staged_part != pr.part:  # a run-ahead staged the next partition over this one
@@ -654,6 +735,221 @@ class Executor:
         self.kernel_launches += launches
         return prev
 
+    # ------------------------------------------------------------------ partitioned training
+
+    def _tp_phases(self) -> list[tuple[str, int]]:
+        """Phases of one batch over k partitions: F_0 .. F_{k-2}, L_{k-1}, B_{k-2} .. B_0."""
+        k = len(self.plan.partitions)
+        return [("F", p) for p in range(k - 1)] + [("L", k - 1)] + [("B", p) for p in range(k - 2, -1, -1)]
+
+    def _tp_batch(self) -> int:
+        """Every phase runs at the plan's largest batch size (one batch = one SGD step)."""
+        return max([e.batch_size for p in self.plan.partitions for e in p.per_bubble] + [8])
+
+    def _tp_cost(self, kind: str, pidx: int, b: int) -> float:
+        """Estimated phase time (us) from the profile: a partition's training time is its
+        layers' sum; a forward phase is a third of it, a loss / backward phase (forward
+        recomputed + backward + SGD) all of it."""
+        prof = getattr(self.model, "profile", None)
+        p = self.plan.partitions[pidx]
+        if prof is None or len(prof.layers) != len(self.model):
+            return 1.0
+        t = sum(prof.layers[i].exec_time_us(b) if b in prof.layers[i].exec_time_ms else 1 for i in range(p.lo, p.hi))
+        return t / 3.0 if kind == "F" else float(t)
+
+    def _tp_swap(self, old: int, new: int, dirty: bool, st: torch.cuda.Stream) -> None:
+        """Gated in-stream swap of the resident partition: write `old`'s state back to its
+        pinned blobs (when a backward phase updated it), then stage `new` in. Skipped on the
+        device if an earlier phase of this bubble yielded (pf_staging gate)."""
+        key = ("tp", old, new, dirty)
+        g = self._gated.get(key)
+        if g is None:
+            dst, src, nb = [], [], []
+            if dirty:
+                po = self.plan.partitions[old]
+                for i in range(po.lo, po.hi):
+                    if self.model[i].weight_bytes():
+                        dst.append(self.model[i].host.ptr)
+                        src.append(self._module_ptr(old, i))
+                        nb.append(self.model[i].weight_bytes())
+            pn = self.plan.partitions[new]
+            for i in range(pn.lo, pn.hi):
+                if self.model[i].weight_bytes():
+                    dst.append(self._module_ptr(new, i))
+                    src.append(self.model[i].host.ptr)
+                    nb.append(self.model[i].weight_bytes())
+            n = len(dst)
+            g = ctypes.c_void_p()
+            base = self._ctl.data_ptr()
+            native.call("pf_staging_create", ctypes.byref(g), (ctypes.c_void_p * max(n, 1))(*dst),
+                        (ctypes.c_void_p * max(n, 1))(*src), (ctypes.c_uint64 * max(n, 1))(*nb), n, base, base + 8)
+            self._gated[key] = g
+        native.call("pf_staging_launch", g, st.cuda_stream)
+        self.h2d_bytes += sum(self.model[i].weight_bytes() for i in range(self.plan.partitions[new].lo,
+                                                                           self.plan.partitions[new].hi))
+        if dirty:
+            self.d2h_bytes += sum(self.model[i].weight_bytes() for i in range(self.plan.partitions[old].lo,
+                                                                              self.plan.partitions[old].hi))
+
+    def _fill_tp(self, slot: BubbleSlot) -> None:
+        """Enqueue this bubble's phases of partitioned training: a resumed phase first, then
+        phases (swapping partitions in-stream when one changes) while the plan's time budget
+        for this bubble lasts."""
+        ts, phases, b = self._tp_state, self._tp_phases(), self._tp_batch()
+        budget = sum(e.num_batches * self._tp_cost("B", pi, b) for pi, p in enumerate(self.plan.partitions)
+                     for e in p.per_bubble[slot.index:slot.index + 1] if e.num_batches)
+        if budget <= 0:
+            return
+        n_total = self.item.entry.size
+        n_batches = -(-n_total // b)
+        pr = self.progress
+        queue: list[tuple[int, int, int]] = []  # (batch, phase, start node)
+        bi, ph = pr.next_sample // b, ts["phase"]
+        spent = 0.0
+        if pr.resume is not None:
+            queue.append((bi, ph, pr.resume[2]))
+            spent += self._tp_cost(*phases[ph], b)
+            ph += 1
+            if ph == len(phases):
+                bi, ph = bi + 1, 0
+        while bi < n_batches and len(queue) < MAX_BATCHES and (not queue or spent < budget):
+            queue.append((bi, ph, 0))
+            spent += self._tp_cost(*phases[ph], b)
+            ph += 1
+            if ph == len(phases):
+                bi, ph = bi + 1, 0
+        st = self.stream
+        base = self._ctl.data_ptr()
+        flag = slot.flag_ptr or None
+        self._last_flag = flag
+        dh = self._desc_host.tensor
+        in_b = self.model.input_bytes()
+        aux_b = self._aux_host.tensor[0].numel() * self._aux_host.tensor.element_size()
+        for q, (bj, pj, node) in enumerate(queue):
+            first = bj * b
+            dh[q, 0], dh[q, 1], dh[q, 2] = first * in_b, first * 16, first * aux_b
+        launches = 0
+        with torch.cuda.stream(st):
+            if slot.start_event is not None:
+                st.wait_event(slot.start_event)
+            if self._staged_event is not None:
+                st.wait_event(self._staged_event)
+            self._ctl[:3].zero_()
+            if pr.resume_zero is not None:
+                self._ctl[_CURSOR0 + pr.resume_zero] = 0
+                pr.resume_zero = None
+            native.call("pf_stage_h2d", self._desc.data_ptr(), self._desc_host.ptr, 8 * DESC_WORDS * len(queue),
+                        st.cuda_stream)
+            native.call("pf_read_globaltimer", base + 32, st.cuda_stream)
+            resident, dirty = ts["resident"], ts["dirty"]
+            for q, (bj, pj, node) in enumerate(queue):
+                kind, pidx = phases[pj]
+                if pidx != resident:
+                    self._tp_swap(resident, pidx, dirty, st)
+                    resident, dirty = pidx, False
+                    launches += 2
+                ch = self._chain((kind, pidx), b, flag)
+                if node > 0 or not self.use_graphs:
+                    native.call("pf_chain_launch", ch.h, flag, base if flag else None,
+                                base + 4 * _CURSOR0 if flag else None, base + 4, node, 0, 0, st.cuda_stream)
+                    launches += len(ch.units) - node + 1
+                else:
+                    native.call("pf_chain_graph_launch", ch.h, st.cuda_stream)
+                    launches += len(ch.units) + len(ch.seg_ends) + 2
+                dirty = dirty or kind != "F"
+            native.call("pf_read_globaltimer", base + 40, st.cuda_stream)
+            launches += 2
+        ev = torch.cuda.Event()
+        ev.record(st)
+        self.pending = _Pending(slot, [(bj * b, b, node) for bj, _, node in queue], ev, launches, pr.part,
+                                has_resume=pr.resume is not None, parts=[phases[pj][1] for _, pj, _ in queue],
+                                progress_key=(pr.part, pr.next_sample, pr.resume, self._cursor_now),
+                                tp=list(queue))
+        self.kernel_launches += launches
+
+    def _settle_tp(self, pend: _Pending, w: torch.Tensor, aborted: bool, done: int) -> BubbleRecord:
+        """Advance partitioned training: the first `done` phases completed; an interrupted
+        phase resumes at its first incomplete node; the resident partition is the one of the
+        last phase that started (a swap runs only behind completed phases)."""
+        ts, phases, b = self._tp_state, self._tp_phases(), self._tp_batch()
+        pr = self.progress
+        queue = pend.tp
+        ts0 = dict(ts)
+        ts1 = (ts0["resident"], ts0["dirty"])
+        rec = BubbleRecord(pend.slot.index, len(queue), done, 0, aborted, int(w[8:12].view(torch.int64)[0]),
+                           int(w[8:12].view(torch.int64)[1]), pend.launches, pend.part, 1.0, tag=pend.slot.tag)
+        k = len(self.plan.partitions)
+        frac = self._flops_frac
+        resident, dirty = ts1
+        for q, (bj, pj, node) in enumerate(queue):
+            kind, pidx = phases[pj]
+            if q > done:
+                break
+            if q == done and not aborted:
+                break
+            if pidx != resident:
+                resident, dirty = pidx, False
+            if q < done:
+                dirty = dirty or kind != "F"
+                # a phase's share of the step: forward a third of the partition, loss/backward two thirds
+                rec.sample_eq += b * frac[pidx] * (1.0 / 3.0 if kind == "F" else 2.0 / 3.0)
+                pr.resume = None
+                ph = pj + 1
+                if ph == len(phases):  # the batch's last phase: the SGD step is complete
+                    rec.samples_done += b
+                    rec.samples_completed += b
+                    pr.next_sample = (bj + 1) * b
+                    ph = 0
+                ts["phase"] = ph
+            else:  # the phase that yielded
+                ch = self._chains[((kind, pidx), b, pend.slot.flag_ptr or None)]
+                rec.last_work_end_ns = self._last_work_end(ch)
+                cur = w[_CURSOR0:_CURSOR0 + len(ch.units)]
+                resume_node = len(ch.units)
+                for j, (u, _) in enumerate(ch.units):
+                    if int(cur[j]) < u:
+                        resume_node = j
+                        break
+                dirty = dirty or (kind != "F" and resume_node > 0)
+                if resume_node >= len(ch.units):  # every node finished; only the end marker was skipped
+                    rec.sample_eq += b * frac[pidx] * (1.0 / 3.0 if kind == "F" else 2.0 / 3.0)
+                    pr.resume = None
+                    ph = pj + 1
+                    if ph == len(phases):
+                        rec.samples_done += b
+                        rec.samples_completed += b
+                        pr.next_sample = (bj + 1) * b
+                        ph = 0
+                    ts["phase"] = ph
+                else:
+                    pr.resume = (bj * b, b, max(resume_node, node))
+                    if not ch.units[resume_node][1]:
+                        pr.resume_zero = resume_node
+                    ts["phase"] = pj
+                    pr.next_sample = bj * b
+        ts["resident"], ts["dirty"] = resident, dirty
+        self._staged_part = resident
+        views, wsd = self._part_layout(resident)
+        for i in range(self.plan.partitions[resident].lo, self.plan.partitions[resident].hi):
+            self.model[i].dev = views[i]
+        self.ws = wsd
+        self._dev_views = dict(views)
+        self.samples_completed += rec.samples_completed
+        key_after = (pr.part, pr.next_sample, pr.resume, self._resume_cursor(pend, [], w))
+        self.starved = self.starved + 1 if (done == 0 and aborted and key_after == pend.progress_key) else 0
+        self._cursor_now = key_after[3]
+        n_total = self.item.entry.size
+        if pr.resume is None and pr.next_sample >= n_total:
+            pr.finished = True
+            if ts["dirty"]:
+                self._write_back(ts["resident"])
+                ts["dirty"] = False
+        self.records.append(rec)
+        if self.starved >= STARVE_LIMIT:
+            raise FillStarvation(f"no fill progress in {self.starved} consecutive bubbles (partitioned training, "
+                                 f"phase {ts['phase']}, resume point {pr.resume})")
+        return rec
+
     def _stage_in_stream(self, part: int, st: torch.cuda.Stream) -> None:
         """Run-ahead staging: copy partition `part`'s weights into the region on the fill
         stream itself, ordered after the previous partition's batches, as a gated graph
@@ -721,6 +1017,8 @@ class Executor:
         w = words.tensor
         aborted = int(w[0]) != 0
         done = int(w[1])
+        if pend.tp is not None:
+            return self._settle_tp(pend, w, aborted, done)
         ts = w[8:12].view(torch.int64)
         pr = self.progress
         rec = BubbleRecord(pend.slot.index, len(pend.batches), done, 0, aborted, int(ts[0]), int(ts[1]),

@@ -109,6 +109,17 @@ def _module_flops(model: FillSequential, i: int) -> float:
     return model[i].flops_per_sample()
 
 
+def _is_module_buffer(name: str, i: int) -> bool:
+    """Workspace buffers that belong to module i alone (its saved activations, statistics,
+    output and gradient buffers); every other name is scratch shared across modules."""
+    return name.startswith(f"s{i}.") or name == f"out{i}" or name.startswith(f"g{i}.")
+
+
+def _module_own_bytes(model, i: int, batch: int) -> int:
+    need = model.workspace(i, i + 1, batch)
+    return sum(2 * v for k, v in need.items() if _is_module_buffer(k, i))
+
+
 def measure_train_profile(model: FillSequential, batch_sizes: Sequence[int], reps: int = 4,
                           warmup: int = 2, name: str | None = None) -> ModelProfile:
     """Profile of a training fill job (forward + loss + backward + SGD per batch).
@@ -158,17 +169,32 @@ def measure_train_profile(model: FillSequential, batch_sizes: Sequence[int], rep
         finally:
             ex.close()
     layers = []
+    partitioned = getattr(model, "partitioned", False)
     for i in range(len(model)):
         w = model[i].weight_bytes()
         exec_ms, mem = {}, {}
         prev_t = 0.0
+        if partitioned:
+            # a partition keeps the saved activations and gradients of all its modules until its
+            # backward: charge them to the module's batch-independent bytes (at the largest batch
+            # size, conservative below it), so the planner's peak (sum of weight_bytes + the
+            # largest transient, partition.py:143-150) bounds what the executor carves
+            own = _module_own_bytes(model, i, sizes[-1])
+            w_plan = w + own
         for b in sizes:
-            need = model.workspace(0, len(model), b)
-            transient = sum(2 * v for v in need.values()) + b * model.input_bytes() + FIXED_TRANSIENT_BYTES
+            if partitioned:
+                need = model.workspace(i, i + 1, b)
+                shared = sum(2 * v for k, v in need.items() if not _is_module_buffer(k, i))
+                bnd = 2 * 2 * b * model.boundary_elems(i)  # input boundary + its gradient
+                transient = shared + bnd + b * model.input_bytes() + FIXED_TRANSIENT_BYTES
+            else:
+                need = model.workspace(0, len(model), b)
+                transient = sum(2 * v for v in need.values()) + b * model.input_bytes() + FIXED_TRANSIENT_BYTES
             t = max(step_ms[b] * flops[i] / total_f, prev_t, 1e-3)
-            exec_ms[b], mem[b] = t, w + transient
+            exec_ms[b] = t
+            mem[b] = (w_plan if partitioned else w) + transient
             prev_t = t
-        layers.append(LayerProfile(exec_time_ms=exec_ms, mem_bytes=mem, weight_bytes=w,
+        layers.append(LayerProfile(exec_time_ms=exec_ms, mem_bytes=mem, weight_bytes=w_plan if partitioned else w,
                                    flops_per_sample=flops[i]))
     params = sum(model[i].weight_bytes() // 10 for i in range(len(model)))
     prof = ModelProfile(name=name or f"{model.cfg.name}-train-b200", layers=tuple(layers), param_count=params,

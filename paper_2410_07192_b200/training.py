@@ -704,6 +704,114 @@ class ResNetTrainSequential(FillSequential):
         return ends, flops
 
 
+class ResNetTrainPartitioned(FillSequential):
+    """ResNet-50 training with its 18 modules as separate nodes, so a plan may split them
+    into partitions that run in different bubbles (BASELINE.json configs[3]: "fwd+bwd
+    partitioned across bubbles"; the reference profiles training as L layers plus an
+    optimizer pseudo-layer, workload.py:256-264). One batch is still one SGD step. The
+    executor runs it batch-major as 2k - 1 phases over the k partitions (record_phase):
+
+    * ``F`` p < k-1: forward of partition p from its input boundary, output boundary stored;
+    * ``L`` p = k-1: forward, loss, backward and SGD of the last partition;
+    * ``B`` p < k-1: the partition's forward recomputed from its stored input (activation
+      checkpointing at partition boundaries), backward with the stored gradient of its
+      output, SGD of its modules, gradient of its input stored for partition p - 1.
+
+    Every kernel is the one the single-node step (ResNetTrainSequential) records, on the same
+    inputs, so a multi-partition plan trains bit-identically to a single-partition one
+    (tests/test_train_gpu.py). Module state lives in one pinned blob per module and is
+    written back when its partition leaves the device."""
+
+    is_training = True
+    partitioned = True
+
+    @property
+    def blocks(self) -> list["TrainModule"]:
+        return list(self)
+
+    def input_spec(self):
+        c = self.cfg
+        return torch.bfloat16, (c.image, c.image, c.in_ch)
+
+    def boundary_shape(self, i):
+        return self.input_spec()[1] if i == 0 else tuple(self[i - 1].out_shape())
+
+    def result_shape(self):
+        return (4,)
+
+    def result_dtype(self):
+        return torch.float32
+
+    def result_view(self, x, cnt):
+        raise RuntimeError("training results are written by the loss phase")
+
+    def aux_spec(self):
+        return torch.int32, (4,)
+
+    def make_inputs(self, job_seed, first, count):
+        return synthetic_images(job_seed, first, count, self.cfg.image, self.cfg.in_ch)
+
+    def make_aux(self, job_seed, first, count):
+        return synthetic_labels(job_seed, first, count, self.cfg.classes)
+
+    def workspace(self, lo: int, hi: int, batch: int) -> dict[str, int]:
+        """Partition [lo, hi)'s workspace: its modules' buffers, the gradient ping-pong between
+        them, BatchNorm partials / scale / shift."""
+        need: dict[str, int] = {}
+        for i in range(lo, hi):
+            for k, v in self[i].workspace(batch).items():
+                need[k] = max(need.get(k, 0), v)
+        ins = [batch * _numel(self.boundary_shape(i)) for i in range(max(lo, 1), hi)]
+        for j in (0, 1):
+            need[f"grad{j}"] = max(ins + [8])
+        need["partial"] = max(need.get("partial", 0), 2 * MAX_PARTIALS * 2 * 2048)
+        need["scale"] = need["shift"] = 2 * 2048
+        need["loss"] = max(need.get("loss", 0), 2 * 4 * batch)
+        return need
+
+    def record_phase(self, kind: str, lo: int, hi: int, x, dout, labels, loss,
+                     ctx: ExecContext) -> tuple[list[int], dict, dict, Optional[torch.Tensor]]:
+        """Record one phase of partition [lo, hi) (see the class docstring). Returns (segment
+        ends, GEMM FLOPs per node, GEMM bytes per node, the tensor holding the partition's
+        output (F) or input gradient (L / B, None for the stem))."""
+        flops: dict[int, float] = {}
+        nbytes: dict[int, float] = {}
+        r = _Rec(ctx, flops, nbytes)
+        b = x.shape[0]
+        if b % 8:
+            raise ValueError("training batches must be a multiple of 8 samples")
+        mods = [self[i] for i in range(lo, hi)]
+        has_head = hi == len(self)
+        if (kind == "L") != has_head:
+            raise ValueError("the loss phase is the last partition's, and only its")
+        ends = []
+        y = x
+        for mod in mods[:-1] if has_head else mods:
+            y = mod.record_forward(r, y)
+            ends.append(ctx.node)
+        if kind == "F":
+            return ends, flops, nbytes, y
+        if has_head:
+            mods[-1].record_forward(r, y, labels, loss)
+            ends.append(ctx.node)
+            dy = mods[-1].record_backward(r)
+            ends.append(ctx.node)
+            rest = mods[:-1]
+        else:
+            dy = dout
+            rest = mods
+        for mod in reversed(rest):
+            dy = mod.record_backward(r, dy)
+            ends.append(ctx.node)
+        segs = []
+        for mod in mods:
+            segs.extend(mod.sgd_segments(ctx, b))
+        native.call("pf_chain_add_sgd", ctx.chain, K.sgd_segments(segs), len(segs), LR, MOMENTUM)
+        ctx.node += 1
+        ends.append(ctx.node)
+        return ends, flops, nbytes, dy
+
+
 def synthetic_labels(job_seed: int, first: int, count: int, classes: int) -> torch.Tensor:
     """int32 [count, 4], label of sample i at [i, 0] (depends only on (job_seed, i))."""
     i = torch.arange(first, first + count, dtype=torch.int64)
@@ -713,9 +821,12 @@ def synthetic_labels(job_seed: int, first: int, count: int, classes: int) -> tor
     return out
 
 
-def resnet50_train(cfg: ResNetConfig = RESNET50, seed: Optional[int] = 0, pinned: bool = True
-                   ) -> ResNetTrainSequential:
-    """ResNet-50 training job as the linearized fill model [stem, 16 bottlenecks, head]."""
+def resnet50_train(cfg: ResNetConfig = RESNET50, seed: Optional[int] = 0, pinned: bool = True,
+                   partitioned: bool = False):
+    """ResNet-50 training job as the linearized fill model [stem, 16 bottlenecks, head]:
+    one node wrapping the whole step (ResNetTrainSequential), or with `partitioned` the 18
+    modules as nodes a plan may split across bubbles (ResNetTrainPartitioned). Both draw
+    the same initial state from `seed`."""
     from .fillmodels import Bottleneck as _InferBlock  # shapes of the inference twin
 
     mods: list[FillModule] = [TrainStem(cfg)]
@@ -728,12 +839,12 @@ def resnet50_train(cfg: ResNetConfig = RESNET50, seed: Optional[int] = 0, pinned
             ch, h = blk.out_ch, blk.ho
     mods.append(TrainHead(cfg, len(mods), ch, h))
     _ = _InferBlock
-    seq = ResNetTrainSequential(cfg, [ResNetTrainStep(mods)])
+    seq = ResNetTrainPartitioned(cfg, mods) if partitioned else ResNetTrainSequential(cfg, [ResNetTrainStep(mods)])
     if seed is not None:
         seq.init_weights(seed, pinned=pinned)
     return seq
 
 
-__all__ = ["ResNetTrainSequential", "ResNetTrainStep", "resnet50_train", "synthetic_labels", "TrainStem", "TrainBottleneck",
+__all__ = ["ResNetTrainSequential", "ResNetTrainPartitioned", "ResNetTrainStep", "resnet50_train", "synthetic_labels", "TrainStem", "TrainBottleneck",
            "TrainHead", "LR", "MOMENTUM", "WEIGHT_DECAY"]
 _ = (ATOMIC, PREFIX, dataclass)

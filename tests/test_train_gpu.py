@@ -180,3 +180,93 @@ def test_resnet50_training_step_matches_torchvision_module_by_module():
     for k, v in report.items():
         tol = 1e-5 if k == "sgd update" else (2e-2 if ("fwd" in k or k == "loss") else 1.5e-1)
         assert v < tol, (k, v, report)
+
+
+def _partitioned_item(pf, model, samples, batch, free_fraction):
+    """A WorkItem whose plan splits the partitioned ResNet-50 training job: the bubbles'
+    free memory is `free_fraction` of the whole job's planner peak."""
+    from paper_2410_07192_b200.profiler import _is_module_buffer, _module_own_bytes
+    from paper_2410_07192_b200.profiles import JobKind, JobSpec, LayerProfile, ModelProfile
+
+    layers = []
+    for i in range(len(model)):
+        w = model[i].weight_bytes() + _module_own_bytes(model, i, batch)
+        need = model.workspace(i, i + 1, batch)
+        tr = sum(2 * v for k, v in need.items() if not _is_module_buffer(k, i))
+        layers.append(LayerProfile({batch: 0.001}, {batch: w + tr}, w, 1.0))
+    prof = ModelProfile("resnet50-train-part-test", tuple(layers), 1, frozenset({JobKind.TRAINING}))
+    peak = sum(lp.weight_bytes for lp in layers) + max(lp.transient_bytes(batch) for lp in layers)
+    free = int(free_fraction * peak)
+    cyc = pf.BubbleCycle((pf.BubbleSpec(2000, 2000, free, pf.BubbleKind.FWD_BWD),
+                          pf.BubbleSpec(1000, 1000, free, pf.BubbleKind.FILL_DRAIN)), 20_000, 0)
+    coord = pf.Coordinator(0, cyc, 1, batch_sizes=[batch], max_batches_per_bubble=1)
+    plan = coord.admit(JobSpec("t0", 0.0, prof, JobKind.TRAINING, samples))
+    return coord.request_work(0, 0.0), plan
+
+
+@pytest.mark.parametrize("preempt", [False, True])
+def test_partitioned_training_is_bit_identical_to_the_single_node_step(preempt):
+    """BASELINE configs[3]: a training job whose plan splits ResNet-50 into >= 2 partitions
+    that run in different bubbles (forward phases, the loss phase, backward phases with the
+    forward recomputed from the stored partition input, per-partition SGD, state written
+    back when a partition leaves the device) trains bit-identically to the single-node
+    step: same per-sample losses and the same fp32 masters after 3 SGD steps -- also when
+    timer-closed bubbles preempt phases mid-way and they resume."""
+    import ctypes
+
+    import paper_2410_07192_b200 as pf
+    from paper_2410_07192_b200 import native
+    from paper_2410_07192_b200.executor import BubbleSlot, Executor
+    from paper_2410_07192_b200.fillmodels import ResNetConfig
+    from paper_2410_07192_b200.training import resnet50_train
+
+    native.require_device()
+    cfg = ResNetConfig(image=64)
+    batch, steps, seed = 16, 3, 5
+    ref = resnet50_train(cfg, seed=11)
+    ex = Executor(8 << 30, job_seed=seed)
+    ex.load(_plan_item(pf, ref, batch * steps, batch), ref)
+    while ex.busy:
+        ex.fill(BubbleSlot(0, None, 0))
+    ex.settle()
+    torch.cuda.synchronize()
+    want_loss = ex.results().clone()
+    want = [m.state_host() for m in ref.blocks]
+    ex.close()
+
+    part = resnet50_train(cfg, seed=11, partitioned=True)
+    item, plan = _partitioned_item(pf, part, batch * steps, batch, 0.45)
+    assert len(plan.partitions) >= 2, plan
+    ex = Executor(8 << 30, job_seed=seed)
+    ex.load(item, part)
+    flag, comm = ctypes.c_void_p(), torch.cuda.Stream()
+    native.call("pf_flag_create", ctypes.byref(flag))
+    anchor = torch.zeros(1, dtype=torch.int64, device="cuda")
+    k = 0
+    while ex.busy and k < 4000:
+        if preempt:
+            with torch.cuda.stream(comm):
+                torch.cuda._sleep(300_000)
+            native.call("pf_read_globaltimer", anchor.data_ptr(), comm.cuda_stream)
+            native.call("pf_flag_write_on_stream", flag, 1, comm.cuda_stream)
+            ev = torch.cuda.Event()
+            ev.record(comm)
+            native.call("pf_flag_clear_at", flag, anchor.data_ptr(), 200_000 + 300_000 * (k % 4), None,
+                        comm.cuda_stream)
+            ex.fill(BubbleSlot(k % 2, ev, flag.value))
+        else:
+            ex.fill(BubbleSlot(k % 2, None, 0))
+        k += 1
+    ex.settle()
+    torch.cuda.synchronize()
+    assert not ex.busy, k
+    if preempt:
+        assert sum(r.aborted for r in ex.records) > 0, "no phase was preempted; shorten the bubbles"
+    got_loss = ex.results().clone()
+    got = [m.state_host() for m in part.blocks]
+    ex.close()
+    native.call("pf_flag_destroy", flag)
+    assert torch.equal(got_loss, want_loss)
+    for i, (a, b) in enumerate(zip(got, want)):
+        for name in a:
+            assert torch.equal(a[name], b[name]), (i, name)
