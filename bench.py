@@ -528,8 +528,17 @@ def run_training_depths(args, conf) -> None:
     results, stats_all = {}, []
     with ClockSampler(local) as clocks:
         for P in conf["depths"]:
-            pcfg = pf.PipelineConfig(P, conf["micro"], tf_ms, tb_ms, pf.ScheduleKind.ONE_F_ONE_B, arena_bytes,
-                                     arena_bytes, args.fill_fraction)
+            # bubble free memory the planner sees: the arena, less (partitioned training) the
+            # executor's allocations outside the partition region -- the boundary stores of every
+            # partition (one batch each way) and the batch inputs -- which the per-partition peak
+            # of the reference's memory model (partition.py:143-150) cannot express
+            plan_mem = arena_bytes
+            if part:
+                b_max = max(conf["batch_sizes"])
+                stores = sum(2 * 2 * b_max * probe_model.boundary_elems(i) for i in range(1, len(probe_model)))
+                plan_mem = max(arena_bytes // 4, arena_bytes - stores - b_max * probe_model.input_bytes() - (64 << 20))
+            pcfg = pf.PipelineConfig(P, conf["micro"], tf_ms, tb_ms, pf.ScheduleKind.ONE_F_ONE_B, plan_mem,
+                                     plan_mem, args.fill_fraction)
             engines = {s_: StageEngine(pcfg, s_, main_model, executor, streams=streams) for s_ in range(P)}
             models = {s_: resnet50_train(seed=s_, partitioned=part) for s_ in range(P)}
             for m_ in models.values():

@@ -927,6 +927,19 @@ class Executor:
                         pr.resume_zero = resume_node
                     ts["phase"] = pj
                     pr.next_sample = bj * b
+        if self.timing and done > 0 and not aborted:
+            # in-kernel stamps of the bubble's last phase: (FLOPs, ms, tag, batch, bytes) per GEMM node
+            bj, pj, _ = queue[done - 1]
+            ch = self._chains.get((phases[pj], b, pend.slot.flag_ptr or None))
+            if ch is not None and ch.gemm_flops:
+                native.call("pf_stage_d2h", self._stamps_host.ptr, self._stamps.data_ptr(), 16 * len(ch.units),
+                            self.stream.cuda_stream)
+                self.stream.synchronize()
+                sh = self._stamps_host.tensor
+                for nd, fl in ch.gemm_flops.items():
+                    t0, t1 = int(sh[nd, 0]), int(sh[nd, 1])
+                    if 0 < t0 < t1:
+                        self.gemm_samples.append((fl, (t1 - t0) / 1e6, pend.slot.tag, b, ch.gemm_bytes.get(nd, 0.0)))
         ts["resident"], ts["dirty"] = resident, dirty
         self._staged_part = resident
         views, wsd = self._part_layout(resident)
