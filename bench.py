@@ -84,6 +84,9 @@ FILL_FRACTION_NCCL = 0.95
 COOLDOWN_MS = 20.0
 THROTTLE_MS = 50.0
 THROTTLE_CTAS = 64
+TAIL_MIN_MS = None
+TAIL_FRAC = 1.0
+TAIL_FROM_FRAC = 0.0
 # main-job slowdown phase: A = fill-off, B = fill-on iteration of one stage; the first of each run is
 # discarded (it inherits the other mode's power state), leaving 4 off and 5 on per stage
 DEFAULT_SLOWDOWN_PATTERN = "AAABBBBBBAAA"
@@ -670,6 +673,30 @@ def run_training_depths(args, conf) -> None:
         dist.destroy_process_group()
 
 
+def tail_min_ms(args) -> float:
+    return args.throttle_ms if args.tail_min_ms is None else args.tail_min_ms
+
+
+def tail_on_stage(args, stage: int, stages: int) -> bool:
+    """Stage-aware tail: only stages from ceil(tail_from_frac x p) on get it. The composed
+    slowdown comes almost entirely from the later stages (their steady state is the critical
+    path): with the early stages' ops unaffected it moves by <= 0.1 point, with the last
+    stage's by 1.1."""
+    return stage >= math.ceil(args.tail_from_frac * stages - 1e-9)
+
+
+def set_tail(engine, args) -> None:
+    """The power-aware bubble tail of DESIGN.md §5.1 on a stage engine: bubbles longer than
+    tail_min_ms run their last min(throttle_ms, tail_frac x duration) on throttle_ctas CTAs."""
+    if not tail_on_stage(args, engine.stage, engine.cfg.num_stages):
+        engine.throttle_ns = 0
+        return
+    engine.throttle_ns = int(args.throttle_ms * 1e6)
+    engine.throttle_ctas = args.throttle_ctas
+    engine.throttle_min_ns = int(tail_min_ms(args) * 1e6)
+    engine.throttle_frac = args.tail_frac
+
+
 def measure_interference(args, stages, run_block, local, pcfg) -> dict:
     """Main-job slowdown with filling on vs off, from blocks of consecutive iterations.
 
@@ -836,6 +863,12 @@ def main() -> None:
     ap.add_argument("--throttle-ms", type=float, default=THROTTLE_MS,
                     help="throttle the fill to --throttle-ctas CTAs this long before every bubble's end")
     ap.add_argument("--throttle-ctas", type=int, default=THROTTLE_CTAS)
+    ap.add_argument("--tail-min-ms", type=float, default=TAIL_MIN_MS,
+                    help="bubbles no longer than this get no power tail (default: --throttle-ms)")
+    ap.add_argument("--tail-from-frac", type=float, default=TAIL_FROM_FRAC,
+                    help="only stages >= ceil(frac x stages) get the power tail (0: every stage)")
+    ap.add_argument("--tail-frac", type=float, default=TAIL_FRAC,
+                    help="a bubble's throttled tail is at most this share of it (its idle cooldown half of that)")
     ap.add_argument("--loss-iters", type=int, default=4,
                     help="nccl: iterations per deterministic fill-off / on / off loss-identity replay")
     ap.add_argument("--train-partitioned", action="store_true",
@@ -935,8 +968,9 @@ def main() -> None:
         if s not in coords:
             # the stage's Coordinator; a long-running fill job split into 16K-sample ranges
             # power-aware tail: bubbles longer than the throttle window keep an idle cooldown
-            cyc = with_cooldown(cycle or pf.build_bubble_cycle(cfg, s), int(args.cooldown_ms * 1000),
-                                int(args.throttle_ms * 1000))
+            cyc = cycle or pf.build_bubble_cycle(cfg, s)
+            if tail_on_stage(args, s, cfg.num_stages):
+                cyc = with_cooldown(cyc, int(args.cooldown_ms * 1000), int(tail_min_ms(args) * 1000), args.tail_frac / 2)
             coords[s] = pf.Coordinator(s, cyc, 1,
                                        pf.OrderingPolicy("concurrent", conf["chunk"]),
                                        batch_sizes=list(conf["batch_sizes"]),
@@ -1006,8 +1040,7 @@ def main() -> None:
             rank, max(period_us, sum(durs)), durs, [arena_bytes, arena_bytes], args.fill_fraction,
             unfillable_us=max(0, min(analytic.unfillable_us, period_us - sum(durs))))
         coordinator_for(rank, pcfg, measured_cycle)
-        eng.throttle_ns = int(args.throttle_ms * 1e6)
-        eng.throttle_ctas = args.throttle_ctas
+        set_tail(eng, args)
         eng.expected_ns = {k: d * 1000 for k, d in enumerate(durs)}
         characterization = {"measured_bubbles_us": durs, "measured_period_us": period_us,
                             "analytic_bubbles_us": [b.duration_us for b in analytic.bubbles],
@@ -1062,8 +1095,7 @@ def main() -> None:
             if s not in engines:
                 engines[s] = StageEngine(pcfg, s, main_model, executor, streams=shared_streams)
                 engines[s].op_stamps = True  # per-op stamps + SM clock, fill on and off alike
-                engines[s].throttle_ns = int(args.throttle_ms * 1e6)
-                engines[s].throttle_ctas = args.throttle_ctas
+                set_tail(engines[s], args)
                 coordinator_for(s, pcfg)
             return engines[s]
 
@@ -1303,6 +1335,8 @@ def main() -> None:
                          "max_batches_per_bubble": conf.get("max_batches", 16),
                          "fill_fraction": args.fill_fraction, "cooldown_ms": args.cooldown_ms,
                          "throttle_ms": args.throttle_ms, "throttle_ctas": args.throttle_ctas,
+                         "tail_min_ms": tail_min_ms(args), "tail_frac": args.tail_frac,
+                         "tail_from_frac": args.tail_from_frac,
                          "arena_bytes": arena_bytes,
                          "plans": {str(s): pf.plan_to_dict(c.executables[f"fill-{s}"]) for s, c in coords.items()}},
                 "stages_run": [t["stage"] for t in steps],

@@ -20,6 +20,69 @@ constexpr int MAX_NV = 8;  // 8 vectors x 8 bf16 x 32 lanes = 2048 columns
 // Normalise one row held as NV vectors of 8 per lane (vector j covers columns
 // (j*32 + lane)*8 .. +8), then write gamma/beta-scaled bf16. (Preloading gamma / beta with
 // the row cost 90 registers and occupancy: 15.6 -> 17.9 us per BERT-large LN, reverted.)
+// The same on packed fp32 pairs (FADD2 / FFMA2 / FMUL2, pf_common.cuh f2_*): the kernel is
+// issue-bound, not HBM-bound (ncu, BERT-large [16384, 1024]: 69 % issue active, 23 % DRAM
+// throughput), so halving the FP instructions per element is what moves it. x2[j][h] holds
+// columns (j*32 + lane)*8 + 2h, +1.
+template <int NV, bool RMS>
+__device__ __forceinline__ void norm_row_store2(const f32x2 (&x2)[NV][4], int cols, float eps,
+                                                const __nv_bfloat16* gamma, const __nv_bfloat16* beta,
+                                                __nv_bfloat16* y) {
+  const int lane = lane_id();
+  float mean = 0.f;
+  if (!RMS) {
+    f32x2 s0 = f2_splat(0.f), s1 = f2_splat(0.f);  // two chains for ILP
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      if ((j * 32 + lane) * 8 < cols) {
+        s0 = f2_add(s0, f2_add(x2[j][0], x2[j][1]));
+        s1 = f2_add(s1, f2_add(x2[j][2], x2[j][3]));
+      }
+    float a, b, c, d;
+    f2_unpack(s0, a, b);
+    f2_unpack(s1, c, d);
+    mean = warp_sum((a + b) + (c + d)) / (float)cols;
+  }
+  const f32x2 nm = f2_splat(-mean);
+  f32x2 q0 = f2_splat(0.f), q1 = f2_splat(0.f);
+#pragma unroll
+  for (int j = 0; j < NV; ++j)
+    if ((j * 32 + lane) * 8 < cols) {
+#pragma unroll
+      for (int h = 0; h < 4; h += 2) {
+        const f32x2 d0 = f2_add(x2[j][h], nm), d1 = f2_add(x2[j][h + 1], nm);
+        q0 = f2_fma(d0, d0, q0);
+        q1 = f2_fma(d1, d1, q1);
+      }
+    }
+  float a, b, c, d;
+  f2_unpack(q0, a, b);
+  f2_unpack(q1, c, d);
+  const f32x2 r2 = f2_splat(rsqrtf(warp_sum((a + b) + (c + d)) / (float)cols + eps));
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int col = (j * 32 + lane) * 8;
+    if (col < cols) {
+      const uint4 gu = __ldg(reinterpret_cast<const uint4*>(gamma + col));
+      uint4 bu = make_uint4(0, 0, 0, 0);
+      if (!RMS) bu = __ldg(reinterpret_cast<const uint4*>(beta + col));
+      const uint32_t gw[4] = {gu.x, gu.y, gu.z, gu.w};
+      const uint32_t bw[4] = {bu.x, bu.y, bu.z, bu.w};
+      uint32_t o[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const float2 g = unpack_bf16x2(gw[h]);
+        const float2 bb = unpack_bf16x2(bw[h]);
+        const f32x2 t = f2_mul(f2_add(x2[j][h], nm), r2);
+        float lo, hi;
+        f2_unpack(f2_fma(t, f2_pack(g.x, g.y), f2_pack(bb.x, bb.y)), lo, hi);
+        o[h] = pack_bf16x2(lo, hi);
+      }
+      *reinterpret_cast<uint4*>(y + col) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
 template <int NV, bool RMS>
 __device__ __forceinline__ void norm_row_store(float (&x)[NV][8], int cols, float eps,
                                                const __nv_bfloat16* gamma,
@@ -86,7 +149,7 @@ __global__ void __launch_bounds__(WARPS * 32) norm_kernel(const __nv_bfloat16* _
   }
   if (!atomic_unit_check(ctl)) return;
   if (row < rows) {
-    float x[NV][8];
+    f32x2 x2[NV][4];
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const uint32_t w[4] = {xa[j].x, xa[j].y, xa[j].z, xa[j].w};
@@ -94,16 +157,14 @@ __global__ void __launch_bounds__(WARPS * 32) norm_kernel(const __nv_bfloat16* _
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
         const float2 f = unpack_bf16x2(w[h]);
-        x[j][2 * h] = f.x;
-        x[j][2 * h + 1] = f.y;
+        x2[j][h] = f2_pack(f.x, f.y);
         if (R) {
           const float2 g = unpack_bf16x2(v[h]);
-          x[j][2 * h] += g.x;
-          x[j][2 * h + 1] += g.y;
+          x2[j][h] = f2_add(x2[j][h], f2_pack(g.x, g.y));
         }
       }
     }
-    norm_row_store<NV, RMS>(x, cols, eps, gamma, beta, Y + off);
+    norm_row_store2<NV, RMS>(x2, cols, eps, gamma, beta, Y + off);
   }
   atomic_unit_exit(ctl);
 }

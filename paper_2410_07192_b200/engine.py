@@ -362,6 +362,8 @@ class StageEngine:
         # raised the SM clock when the main job resumes
         self.throttle_ns = 0
         self.throttle_ctas = 0
+        self.throttle_min_ns = None  # bubbles shorter than this are not throttled (None: throttle_ns)
+        self.throttle_frac = 1.0  # a bubble's throttled tail is at most this share of it
         self.timer = torch.cuda.Stream(priority=hi)
 
     def set_anchor(self, lead_ms: float = 5.0) -> None:
@@ -394,15 +396,13 @@ class StageEngine:
                 start_ev = torch.cuda.Event()
                 start_ev.record(comm)
                 clear_idx = self.words.n
-                if (fill and self.throttle_ns > 0 and self.throttle_ctas >= 2
-                        and (end_us - start_us) * US > self.throttle_ns):
-                    # the bubble's last throttle_ns run throttled. Bubbles shorter than that are
-                    # not: the power controller needs ~40 ms to raise the clock after the power
-                    # drops (scripts/power_throttle.py), so the main job resumes at the clock it
-                    # left the bubble with whether a short bubble was filled or idle
+                tail = _throttle_tail(self, (end_us - start_us) * US)
+                if fill and tail > 0:
+                    # the bubble's last `tail` ns run throttled (bubbles shorter than the
+                    # threshold not at all: DESIGN.md §5.1)
                     self.timer.wait_event(start_ev)
                     native.call("pf_flag_throttle_at", flag, self.words.anchor.data_ptr(),
-                                int(base + end_us * US - self.throttle_ns), int(self.throttle_ctas),
+                                int(base + end_us * US - tail), int(self.throttle_ctas),
                                 self.timer.cuda_stream)
                     self.launches += 1
                 self.link.bubble_end(base + end_us * US, self.words.stamp_ptr())
@@ -491,6 +491,17 @@ class StageEngine:
 
 
 OP_PROBE_NS = 4000  # SM-clock probe before every stamped op (4 us of one thread)
+
+
+def _throttle_tail(engine, duration_ns: int) -> int:
+    """Throttled tail (ns) of a bubble of `duration_ns`: min(throttle_ns, throttle_frac x
+    duration) for bubbles longer than throttle_min_ns (default: throttle_ns), else 0."""
+    if engine.throttle_ns <= 0 or engine.throttle_ctas < 2 or duration_ns <= 0:
+        return 0
+    lo = engine.throttle_ns if engine.throttle_min_ns is None else engine.throttle_min_ns
+    if duration_ns <= lo:
+        return 0
+    return int(min(engine.throttle_ns, engine.throttle_frac * duration_ns))
 
 
 def op_timing(st: torch.Tensor, rec: IterationRecord) -> dict:
@@ -609,6 +620,8 @@ class NcclPipelineEngine:
         # measured duration (expected_ns, from the fill-off characterization) minus throttle_ns
         self.throttle_ns = 0
         self.throttle_ctas = 0
+        self.throttle_min_ns = None
+        self.throttle_frac = 1.0
         self.expected_ns: dict[int, int] = {}
         self.timer = torch.cuda.Stream(priority=hi)
 
@@ -648,10 +661,11 @@ class NcclPipelineEngine:
         start_ev.record(self.comm)
         k = 0 if kind is BubbleKind.FWD_BWD else 1
         exp = self.expected_ns.get(k, 0)
-        if fill and self.throttle_ns > 0 and self.throttle_ctas >= 2 and exp > self.throttle_ns:
+        tail = _throttle_tail(self, exp)
+        if fill and tail > 0:
             self.timer.wait_event(start_ev)
             native.call("pf_flag_throttle_at", flag, self.words.stamps.data_ptr() + 8 * set_idx,
-                        int(exp - self.throttle_ns), int(self.throttle_ctas), self.timer.cuda_stream)
+                        int(exp - tail), int(self.throttle_ctas), self.timer.cuda_stream)
             self.launches += 1
         got = None
         if end_recv is not None:

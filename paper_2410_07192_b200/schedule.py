@@ -215,9 +215,10 @@ def cycle_from_measurements(
     return BubbleCycle(bubbles, int(period_us), stage_id, int(unfillable_us))
 
 
-def with_cooldown(cycle: BubbleCycle, cooldown_us: int, min_duration_us: int = 0) -> BubbleCycle:
+def with_cooldown(cycle: BubbleCycle, cooldown_us: int, min_duration_us: int = 0,
+                  max_fraction: float = 1.0) -> BubbleCycle:
     """The same cycle with the usable time of every bubble longer than min_duration_us capped
-    at duration - cooldown_us.
+    at duration - min(cooldown_us, max_fraction * duration).
 
     Power-aware usable time: under the board power cap the SM clock the main
     job resumes at depends on the power the end of the preceding bubble drew. An idle tail
@@ -227,7 +228,9 @@ def with_cooldown(cycle: BubbleCycle, cooldown_us: int, min_duration_us: int = 0
     if cooldown_us <= 0:
         return cycle
     bubbles = tuple(b if b.duration_us <= min_duration_us else
-                    BubbleSpec(b.duration_us, max(0, min(b.usable_us, b.duration_us - int(cooldown_us))),
+                    BubbleSpec(b.duration_us,
+                               max(0, min(b.usable_us, b.duration_us - int(min(cooldown_us,
+                                                                             max_fraction * b.duration_us)))),
                                b.free_mem_bytes, b.kind) for b in cycle.bubbles)
     return BubbleCycle(bubbles, cycle.period_us, cycle.stage_id, cycle.unfillable_us)
 
