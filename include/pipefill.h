@@ -210,7 +210,8 @@ int pf_attention_f32(const float* QKV, float* O, int batch, int seq, int heads, 
  * ReLU / residual in its epilogue). Col[B*Ho*Wo, Kp], column (ky*kw + kx)*C + c,
  * zeros outside the image and in columns kh*kw*C..Kp; Kp % 8 == 0.
  * Atomic work units; pf_image_units(kind 0 = im2col with out_elems = rows*Kp,
- * kind 1 = pooling with out_elems = output pixels * C).                              */
+ * kind 1 = max pooling, kind 2 = average pooling, out_elems = output pixels * C): the
+ * launch's CTA count, capped at the kernel's resident CTAs per SM x SMs.              */
 int pf_im2col(const void* X, void* Col, int B, int H, int W, int C, int kh, int kw, int stride,
               int pad, int Kp, const pf_ctl_t* ctl, void* stream);
 /* k x k max pooling (padding never wins: -inf), C % 8 == 0.                           */

@@ -333,6 +333,21 @@ inline unsigned persistent_grid(long long items, int threads) {
   return (unsigned)(need < cap ? (need > 0 ? need : 1) : cap);
 }
 
+// The same, capped at the CTAs of `kernel` that are resident at once (its register and
+// shared-memory occupancy): a grid of 8 CTAs/SM for a kernel that fits 3 runs in ceil(8/3)
+// rounds with the last one partly idle (bn_bwd_apply: 74 registers).
+template <typename Kernel>
+inline unsigned persistent_grid_for(Kernel kernel, long long items, int threads) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0) != cudaSuccess || occ <= 0) {
+    (void)cudaGetLastError();
+    occ = 1;
+  }
+  const long long need = (items + threads - 1) / threads;
+  const long long cap = (long long)occ * device_sm_count();
+  return (unsigned)(need < cap ? (need > 0 ? need : 1) : cap);
+}
+
 // Poll the flag every PF_POLL_STRIDES grid strides (~64 x 592 CTAs x 256 items).
 #define PF_POLL_STRIDES 64
 

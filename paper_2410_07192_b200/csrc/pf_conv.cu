@@ -172,7 +172,9 @@ struct Im2colOp final : PreparedOp {
   int H = 0, W = 0, C = 0, Ho = 0, Wo = 0, kw = 0, stride = 1, pad = 0, K = 0, Kp = 0;
   long long n = 0;  // vectors (C % 8 == 0) or elements
   bool vec = true;
-  uint32_t units() const override { return blocks_for(n); }
+  uint32_t units() const override {
+    return persistent_grid_for(vec ? (void*)im2col_vec_kernel : (void*)im2col_small_c_kernel, n, THREADS);
+  }
   bool resumable() const override { return false; }
   int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
     const Im2colDiv dv{FastDiv((uint32_t)(Kp / 8)), FastDiv((uint32_t)C), FastDiv((uint32_t)kw),
@@ -193,7 +195,7 @@ struct MaxpoolOp final : PreparedOp {
   uint8_t* idx = nullptr;  // optional argmax output (training)
   int H = 0, W = 0, C = 0, Ho = 0, Wo = 0, k = 0, stride = 1, pad = 0;
   long long n = 0;
-  uint32_t units() const override { return blocks_for(n); }
+  uint32_t units() const override { return persistent_grid_for(maxpool_kernel, n, THREADS); }
   bool resumable() const override { return false; }
   int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
     maxpool_kernel<<<units(), THREADS, 0, s>>>(x, y, idx, H, W, C, k, stride, pad, n, FastDiv((uint32_t)(C / 8)),
@@ -208,7 +210,7 @@ struct AvgpoolOp final : PreparedOp {
   __nv_bfloat16* y = nullptr;
   int HW = 0, C = 0;
   long long n = 0;
-  uint32_t units() const override { return blocks_for(n); }
+  uint32_t units() const override { return persistent_grid_for(avgpool_kernel, n, THREADS); }
   bool resumable() const override { return false; }
   int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
     avgpool_kernel<<<units(), THREADS, 0, s>>>(x, y, HW, C, n, make_ctl(ctl));
@@ -335,7 +337,11 @@ extern "C" int pf_avgpool(const void* X, void* Y, int B, int HW, int C, const pf
 extern "C" int pf_image_units(int kind, long long out_elems, int C, uint32_t* out_units) {
   // kind 0: im2col (out_elems = rows * Kp), 1: maxpool / avgpool (out_elems = pixels * C)
   if (!out_units || out_elems <= 0 || C <= 0) return pf::set_error(PF_ERR_INVALID, "pf_image_units");
-  (void)C;  // every image kernel handles 8 output elements per item (im2col: Kp % 8 == 0)
-  *out_units = pf::conv::blocks_for(out_elems / 8);
+  // every image kernel handles 8 output elements per item (im2col: Kp % 8 == 0); the grid is
+  // capped at the kernel's resident CTAs. kind 0: im2col, 1: max pool, 2: average pool
+  using namespace pf::conv;
+  void* k = kind == 0 ? (C % 8 == 0 ? (void*)im2col_vec_kernel : (void*)im2col_small_c_kernel)
+                      : kind == 1 ? (void*)maxpool_kernel : (void*)avgpool_kernel;
+  *out_units = pf::persistent_grid_for(k, out_elems / 8, THREADS);
   return PF_OK;
 }

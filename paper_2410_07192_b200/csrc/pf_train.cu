@@ -98,7 +98,8 @@ __global__ void __launch_bounds__(T) transpose_kernel(const bf* __restrict__ X, 
 
 // mode 0: (sum x, sum x^2) of X.  mode 1: (sum dA, sum dA * xhat), dA = G * [Ymask > 0]
 // (Ymask may be null: no ReLU), xhat = (X - mean) * invstd.
-__global__ void __launch_bounds__(T) colstats_kernel(const bf* __restrict__ X, const bf* __restrict__ G,
+__global__ void __launch_bounds__(T, 4) colstats_kernel(  // 4 CTAs/SM: the grid is 4 x SMs (one wave)
+    const bf* __restrict__ X, const bf* __restrict__ G,
                                                      const bf* __restrict__ Ymask,
                                                      const float* __restrict__ mean,
                                                      const float* __restrict__ invstd, float* partial,
@@ -664,7 +665,7 @@ struct BnApplyOp final : PreparedOp {
   bf* y = nullptr;
   int C = 0, relu = 0;
   long long nvec = 0;
-  uint32_t units() const override { return blocks_for(nvec); }
+  uint32_t units() const override { return persistent_grid_for(bn_apply_kernel, nvec, T); }
   bool resumable() const override { return false; }
   int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
     bn_apply_kernel<<<units(), T, 0, s>>>(x, scale, shift, r, y, C, nvec, relu, FastDiv((uint32_t)(C / 8)),
@@ -680,7 +681,7 @@ struct BnBwdApplyOp final : PreparedOp {
   bf *dx = nullptr, *da = nullptr;
   int M = 0, C = 0;
   long long nvec = 0;
-  uint32_t units() const override { return blocks_for(nvec); }
+  uint32_t units() const override { return persistent_grid_for(bn_bwd_apply_kernel, nvec, T); }
   bool resumable() const override { return false; }
   int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
     bn_bwd_apply_kernel<<<units(), T, 0, s>>>(x, g, ymask, mean, invstd, gamma, dgamma, dbeta, dx, da, M, C,
@@ -695,7 +696,7 @@ struct Col2imOp final : PreparedOp {
   bf* dx = nullptr;
   int H = 0, W = 0, C = 0, Ho = 0, Wo = 0, kh = 0, kw = 0, stride = 1, pad = 0, Kp = 0;
   long long nvec = 0;
-  uint32_t units() const override { return blocks_for(nvec); }
+  uint32_t units() const override { return persistent_grid_for(col2im_kernel, nvec, T); }
   bool resumable() const override { return false; }
   int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
     col2im_kernel<<<units(), T, 0, s>>>(dcol, r, dx, H, W, C, Ho, Wo, kh, kw, stride, pad, Kp, nvec,
@@ -713,7 +714,7 @@ struct PoolBwdOp final : PreparedOp {
   int H = 0, W = 0, C = 0, Ho = 0, Wo = 0, k = 0, stride = 1, pad = 0, HW = 0;
   bool avg = false;
   long long nvec = 0;
-  uint32_t units() const override { return blocks_for(nvec); }
+  uint32_t units() const override { return persistent_grid_for(avg ? (void*)avgpool_bwd_kernel : idx ? (void*)maxpool_bwd_idx_kernel : (void*)maxpool_bwd_kernel, nvec, T); }
   bool resumable() const override { return false; }
   int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
     if (avg)

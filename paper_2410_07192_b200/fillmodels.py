@@ -766,7 +766,7 @@ class ResNetHead(FillModule):
         return [(1, 2.0 * (batch * self.in_ch + self.cfg.classes * self.in_ch + batch * self.cfg.classes))]
 
     def node_units(self, batch):
-        return [(K.image_units(1, batch * self.in_ch, self.in_ch), ATOMIC),
+        return [(K.image_units(2, batch * self.in_ch, self.in_ch), ATOMIC),
                 (K.gemm_units(batch, self.cfg.classes, self.in_ch), PREFIX)]
 
     def forward(self, x, ctx):
