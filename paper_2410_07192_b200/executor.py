@@ -37,7 +37,7 @@ from . import native
 from .arena import Arena, PinnedBuffer, device_view
 from .coordinator import WorkItem
 from .fillmodels import ExecContext, FillSequential
-from .planner import ExecutionPlan
+from .planner import BubblePlanEntry, ExecutionPlan, GreedyPlan, PartitionPlan
 
 _CTL_WORDS = 64 + 4096  # [0]=abort, [1]=batches done, [2]=run-ahead staged, [8..12)=timestamps (2 x u64),
 #                        [64..)=cursors
@@ -110,6 +110,7 @@ class _Pending:
     parts: list[int] = None  # partition of every batch (run-ahead appends partition part + 1)
     progress_key: tuple = ()  # (part, next sample, resume point, resume cursor) when enqueued
     tp: Optional[list] = None  # partitioned training: [(batch index, phase index, start node)] enqueued
+    greedy: Optional[list] = None  # Algorithm-1 plan: [(replica, lo, hi, start node)] of partition j
 
 
 class _Chain:
@@ -204,6 +205,7 @@ class Executor:
         # weight-partition stagings: (bytes, start event, end event) on the copy stream
         self.stagings: list[tuple[int, torch.cuda.Event, torch.cuda.Event]] = []
         self._aux_host: Optional[PinnedBuffer] = None
+        self._greedy: Optional[dict] = None  # Algorithm-1 execution state (load_greedy)
         self.starved = 0  # consecutive settled bubbles that enqueued work but made no progress
         self._cursor_now = -1  # the resume node's cursor as of the last settle
 
@@ -255,6 +257,7 @@ class Executor:
         self.progress = _Progress()
         self._cursor_now = -1
         self.starved = 0
+        self._greedy = None
         self._tp_state = {"phase": 0, "resident": 0, "dirty": False} if self._tp else None
         self._in_host.tensor[:n].copy_(self.model.make_inputs(self.job_seed, item.entry.lo - 1, n))
         if self._aux_host is not None:
@@ -636,6 +639,9 @@ class Executor:
         if self._tp:
             self._fill_tp(slot)
             return prev
+        if self._greedy is not None:
+            self._fill_greedy(slot)
+            return prev
         pr = self.progress
         if self._staged_part != pr.part:  # a run-ahead staged the next partition over this one
             self._stage_partition(pr.part)
@@ -734,6 +740,223 @@ class Executor:
                                 parts=parts, progress_key=(pr.part, pr.next_sample, pr.resume, self._cursor_now))
         self.kernel_launches += launches
         return prev
+
+    # ------------------------------------------------------------------ Algorithm-1 plans
+
+    def load_greedy(self, item: WorkItem, model: FillSequential, gplan: GreedyPlan, batch_size: int) -> None:
+        """Run a WorkItem's sample range with an Algorithm-1 plan (planner.greedy_pack_model,
+        the paper's Executor packer: partition.py:425-494) instead of its
+        DP ExecutionPlan. Algorithm 1 replicates the node list `num_replicas` times (one batch
+        of `batch_size` per replica) and cuts it into partitions; partition j runs in the j-th
+        bubble of the sequence, i.e. in bubble kind j mod P. A partition is a run of whole or
+        partial replicas: segment (replica r, layers [lo, hi)). A replica cut between two
+        partitions keeps its activation in slot r of the activation store. All weights stay
+        resident (one staging at load), so each node's memory fits as the plan assumed.
+        Results are those of the DP plan bit for bit (each sample's rows run the same kernels)."""
+        L = len(model)
+        per = tuple(BubblePlanEntry(batch_size, 1) for _ in range(max(1, len(item.plan.partitions[0].per_bubble))))
+        whole = PartitionPlan(0, L, per, item.plan.total_tps_us, 0)
+        carrier = WorkItem(item.entry, ExecutionPlan((whole,), item.plan.period_us, item.plan.total_tps_us),
+                           item.reuse, item.wall_s, item.busy_s)
+        self.load(carrier, model)  # one partition [0, L): every weight resident, workspace at batch_size
+        self.item = item
+        R = max(1, gplan.num_replicas)
+        parts, pos = [], 0
+        for nodes in gplan.partitions:
+            segs = []
+            for k in range(len(nodes)):
+                r, node = divmod(pos + k, L)
+                if segs and segs[-1][0] == r and segs[-1][2] == node:
+                    segs[-1] = (r, segs[-1][1], node + 1)
+                else:
+                    segs.append((r, node, node + 1))
+            parts.append(segs)
+            pos += len(nodes)
+        if pos != R * L:
+            raise ValueError(f"greedy plan covers {pos} of {R} x {L} nodes")
+        bnd = max([model.boundary_elems(i) for i in range(1, L)] + [1])
+        slot_b = batch_size * bnd * model.act_bytes()
+        # per-replica activation slots, and the staging buffer a segment's input is copied to
+        self._g_store = self.arena.alloc((max(1, R * slot_b // 2),), torch.bfloat16)
+        self._g_in = self.arena.alloc((max(1, slot_b // 2),), torch.bfloat16)
+        self._greedy = {"parts": parts, "R": R, "b": batch_size, "j": 0, "pass": 0, "resume": None,
+                        "slot_bytes": slot_b, "P": len(per)}
+
+    def _greedy_chain(self, lo: int, hi: int, cnt: int, flag: Optional[int]) -> _Chain:
+        key = (("G", lo, hi), cnt, flag)
+        ch = self._chains.get(key)
+        if ch is not None:
+            return ch
+        model = self.model
+        views, ws = self._part_layout(0)
+        for i, dev in views.items():
+            model[i].dev = dev
+        ch = _Chain()
+        ctx = ExecContext(self.stream, ws, chain=ch.h)
+        store = self._g_store.data_ptr()
+        if lo == 0:
+            nb = cnt * model.input_bytes()
+            native.call("pf_chain_add_copy", ch.h, self.in_dev.data_ptr(), nb, self._in_host.ptr, nb, nb, 1, 1)
+            x = self.in_dev[:cnt]
+        else:  # slot r of the store (desc in_off) -> the workspace
+            shape = model.boundary_shape(lo)
+            x = self._g_in[:cnt * model.boundary_elems(lo) * model.act_bytes() // 2].view(
+                model.act_dtype()).view(cnt, *shape)
+            nb = cnt * model.boundary_elems(lo) * model.act_bytes()
+            native.call("pf_chain_add_copy", ch.h, x.data_ptr(), nb, store, nb, nb, 1, 1)
+        ctx.node = 1
+        for i in range(lo, hi):
+            before = ctx.node
+            x = model[i](x, ctx)
+            for node, fl in model[i].gemm_node_flops(cnt):
+                ch.gemm_flops[before + node] = fl
+            if (i - lo + 1) % _SEG_MODULES == 0 or i == hi - 1:
+                ch.seg_ends.append(ctx.node)
+        if hi == len(model):
+            src, spitch, width, rows = model.result_view(x, cnt)
+            native.call("pf_chain_add_copy", ch.h, self._results.ptr, width, src, spitch, width, rows, 2)
+        else:  # -> slot r of the store (desc out_off)
+            nb = cnt * model.boundary_elems(hi) * model.act_bytes()
+            native.call("pf_chain_add_copy", ch.h, store, nb, x.data_ptr(), nb, nb, 1, 2)
+        ch.finalize()
+        ch.seg_ends[-1] = len(ch.units)
+        native.call("pf_chain_set_desc", ch.h, self._desc.data_ptr())
+        native.call("pf_chain_set_stamps", ch.h, self._stamps.data_ptr())
+        base = self._ctl.data_ptr()
+        ch.build_graph(flag, base if flag else None, base + 4 * _CURSOR0 if flag else None, base + 4)
+        self._chains[key] = ch
+        return ch
+
+    def _greedy_batch(self, r: int) -> tuple[int, int]:
+        """(first sample, count) of replica r of the current pass (0 count past the range)."""
+        g = self._greedy
+        first = (g["pass"] * g["R"] + r) * g["b"]
+        return first, max(0, min(g["b"], self.item.entry.size - first))
+
+    def _fill_greedy(self, slot: BubbleSlot) -> None:
+        """Enqueue partition j's segments if this bubble is its bubble kind (j mod P);
+        partitions of zero-length bubbles are empty and are skipped."""
+        g = self._greedy
+        while g["j"] < len(g["parts"]) and not g["parts"][g["j"]]:
+            g["j"] += 1  # an empty partition (Algorithm 1 emits them for zero-length bubbles)
+        if g["j"] >= len(g["parts"]):
+            g["j"], g["pass"] = 0, g["pass"] + 1
+        if g["pass"] * g["R"] * g["b"] >= self.item.entry.size and g["resume"] is None:
+            self.progress.finished = True  # the last pass's remaining partitions hold no samples
+            return
+        if slot.index != g["j"] % g["P"]:
+            return
+        segs = g["parts"][g["j"]]
+        start = 0 if g["resume"] is None else g["resume"][0]
+        queue = []
+        for k in range(start, len(segs)):
+            r, lo, hi = segs[k]
+            first, cnt = self._greedy_batch(r)
+            node = g["resume"][1] if (g["resume"] is not None and k == start) else 0
+            if cnt > 0:
+                queue.append((k, r, lo, hi, first, cnt, node))
+        if not queue:
+            g["j"] += 1
+            g["resume"] = None
+            return
+        model, st, base = self.model, self.stream, self._ctl.data_ptr()
+        flag = slot.flag_ptr or None
+        self._last_flag = flag
+        res_b = self._results.tensor.element_size() * _numel(model.result_shape())
+        dh = self._desc_host.tensor
+        for q, (k, r, lo, hi, first, cnt, node) in enumerate(queue):
+            dh[q, 0] = first * model.input_bytes() if lo == 0 else r * g["slot_bytes"]
+            dh[q, 1] = first * res_b if hi == len(model) else r * g["slot_bytes"]
+            dh[q, 2] = 0
+            if lo == 0 and node == 0:
+                self.h2d_bytes += cnt * model.input_bytes()
+            if hi == len(model):
+                self.d2h_bytes += cnt * res_b
+        launches = 0
+        with torch.cuda.stream(st):
+            if slot.start_event is not None:
+                st.wait_event(slot.start_event)
+            if self._staged_event is not None:
+                st.wait_event(self._staged_event)
+            self._ctl[:3].zero_()
+            if self.progress.resume_zero is not None:
+                self._ctl[_CURSOR0 + self.progress.resume_zero] = 0
+                self.progress.resume_zero = None
+            native.call("pf_stage_h2d", self._desc.data_ptr(), self._desc_host.ptr, 8 * DESC_WORDS * len(queue),
+                        st.cuda_stream)
+            native.call("pf_read_globaltimer", base + 32, st.cuda_stream)
+            for k, r, lo, hi, first, cnt, node in queue:
+                ch = self._greedy_chain(lo, hi, cnt, flag)
+                if node > 0 or not self.use_graphs:
+                    native.call("pf_chain_launch", ch.h, flag, base if flag else None,
+                                base + 4 * _CURSOR0 if flag else None, base + 4, node, 0, 0, st.cuda_stream)
+                    launches += len(ch.units) - node + 1
+                else:
+                    native.call("pf_chain_graph_launch", ch.h, st.cuda_stream)
+                    launches += len(ch.units) + len(ch.seg_ends) + 2
+            native.call("pf_read_globaltimer", base + 40, st.cuda_stream)
+            launches += 2
+        ev = torch.cuda.Event()
+        ev.record(st)
+        self.pending = _Pending(slot, [(first, cnt, node) for _, _, _, _, first, cnt, node in queue], ev, launches, 0,
+                                progress_key=(g["pass"], g["j"], g["resume"], self._cursor_now), greedy=list(queue))
+        self.kernel_launches += launches
+
+    def _settle_greedy(self, pend: _Pending, w: torch.Tensor, aborted: bool, done: int) -> BubbleRecord:
+        g = self._greedy
+        queue = pend.greedy
+        ts = w[8:12].view(torch.int64)
+        rec = BubbleRecord(pend.slot.index, len(queue), done, 0, aborted, int(ts[0]), int(ts[1]), pend.launches, 0,
+                           1.0, tag=pend.slot.tag)
+        L = len(self.model)
+        prof = getattr(self.model, "profile", None)
+        cost = ([prof.layers[i].exec_time_ms[max(prof.batch_sizes)] for i in range(L)]
+                if prof is not None and len(prof.layers) == L else [self.model[i].flops_per_sample() for i in range(L)])
+        total = sum(cost) or 1.0
+        g_resume = None
+        for q, (k, r, lo, hi, first, cnt, node) in enumerate(queue):
+            if q < done:
+                rec.sample_eq += cnt * sum(cost[lo:hi]) / total
+                rec.samples_done += cnt
+                if hi == L:
+                    rec.samples_completed += cnt
+                continue
+            if q == done and aborted:
+                ch = self._chains[(("G", lo, hi), cnt, pend.slot.flag_ptr or None)]
+                rec.last_work_end_ns = self._last_work_end(ch)
+                cur = w[_CURSOR0:_CURSOR0 + len(ch.units)]
+                resume_node = len(ch.units)
+                for j, (u, _) in enumerate(ch.units):
+                    if int(cur[j]) < u:
+                        resume_node = j
+                        break
+                if resume_node >= len(ch.units):  # every node finished; only the end marker was skipped
+                    rec.sample_eq += cnt * sum(cost[lo:hi]) / total
+                    if hi == L:
+                        rec.samples_completed += cnt
+                    g_resume = (k + 1, 0) if k + 1 < len(g["parts"][g["j"]]) else None
+                else:
+                    g_resume = (k, max(resume_node, node))
+                    if not ch.units[resume_node][1]:
+                        self.progress.resume_zero = resume_node
+                break
+        if g_resume is None and (done >= len(queue) or (aborted and done < len(queue) and
+                                                        queue[done][0] + 1 >= len(g["parts"][g["j"]]))):
+            g["j"] += 1  # partition j finished in this bubble
+            g["resume"] = None
+        else:
+            g["resume"] = g_resume
+        self.samples_completed += rec.samples_completed
+        self.starved = self.starved + 1 if (done == 0 and aborted and g["resume"] == pend.progress_key[2]) else 0
+        if g["j"] >= len(g["parts"]):
+            g["j"], g["pass"] = 0, g["pass"] + 1
+        if g["pass"] * g["R"] * g["b"] >= self.item.entry.size and g["resume"] is None:
+            self.progress.finished = True
+        self.records.append(rec)
+        if self.starved >= STARVE_LIMIT:
+            raise FillStarvation(f"no fill progress in {self.starved} consecutive bubbles (greedy plan, "
+                                 f"partition {g['j']}, resume {g['resume']})")
+        return rec
 
     # ------------------------------------------------------------------ partitioned training
 
@@ -1032,6 +1255,8 @@ class Executor:
         done = int(w[1])
         if pend.tp is not None:
             return self._settle_tp(pend, w, aborted, done)
+        if pend.greedy is not None:
+            return self._settle_greedy(pend, w, aborted, done)
         ts = w[8:12].view(torch.int64)
         pr = self.progress
         rec = BubbleRecord(pend.slot.index, len(pend.batches), done, 0, aborted, int(ts[0]), int(ts[1]),

@@ -157,3 +157,64 @@ def test_executor_preemption_resume_is_exact(pf, multi):
         assert any(r.ran_ahead for r in ex.records)
     ex.close()
     native.call("pf_flag_destroy", flag)
+
+
+@pytest.mark.parametrize("preempt", [False, True])
+def test_greedy_algorithm1_plan_matches_the_dp_plan(pf, preempt):
+    """An Algorithm-1 plan (planner.greedy_pack_model, partition.py:425-494)
+    executed for real: 3 replicas of the node list packed into two bubbles, partitions that
+    cut a replica in the middle (its activation kept in a store slot), partition j in bubble
+    kind j mod 2. Results equal the DP single-partition run bit for bit -- also when timer-
+    closed bubbles preempt segments mid-way."""
+    from paper_2410_07192_b200.executor import BubbleSlot, Executor
+    from paper_2410_07192_b200.fillmodels import bert
+    from paper_2410_07192_b200.planner import greedy_pack_model
+    from paper_2410_07192_b200.profiles import JobKind, JobSpec, LayerProfile, ModelProfile
+
+    model = bert(tiny_cfg(), seed=8)
+    b, n = 8, 60
+    layers = tuple(LayerProfile({b: 0.01}, {b: model[i].weight_bytes() + (8 << 20)}, model[i].weight_bytes(), 1.0)
+                   for i in range(len(model)))
+    prof = ModelProfile("tiny-greedy", layers, 1, frozenset({JobKind.BATCH_INFERENCE}))
+    cyc = pf.BubbleCycle((pf.BubbleSpec(100, 100, 8_000_000_000, pf.BubbleKind.FWD_BWD),
+                          pf.BubbleSpec(60, 60, 8_000_000_000, pf.BubbleKind.FILL_DRAIN)), 10_000, 0)
+    gplan = greedy_pack_model(prof, cyc, b)
+    assert gplan.num_replicas == 3 and len(gplan.partitions) >= 2, gplan
+    coord = pf.Coordinator(0, cyc, 1, batch_sizes=[b])
+    coord.admit(JobSpec("g", 0.0, prof, JobKind.BATCH_INFERENCE, n))
+    item = coord.request_work(0, 0.0)
+
+    ex0 = Executor(256 << 20, job_seed=4)
+    ex0.load(item, model)
+    run_to_completion(ex0, lambda k: BubbleSlot(k % 2, None, 0))
+    ref = ex0.results().clone()
+    ex0.close()
+
+    ex = Executor(256 << 20, job_seed=4)
+    ex.load_greedy(item, model, gplan, b)
+    if preempt:
+        flag = ctypes.c_void_p()
+        native_call = __import__("paper_2410_07192_b200.native", fromlist=["call"]).call
+        native_call("pf_flag_create", ctypes.byref(flag))
+        anchor = torch.zeros(1, dtype=torch.int64, device="cuda")
+        comm = torch.cuda.Stream()
+
+        def bubble(k):
+            with torch.cuda.stream(comm):
+                torch.cuda._sleep(400_000)
+            native_call("pf_read_globaltimer", anchor.data_ptr(), comm.cuda_stream)
+            native_call("pf_flag_write_on_stream", flag, 1, comm.cuda_stream)
+            ev = torch.cuda.Event()
+            ev.record(comm)
+            native_call("pf_flag_clear_at", flag, anchor.data_ptr(), 60_000 + 120_000 * (k % 4), None,
+                        comm.cuda_stream)
+            return BubbleSlot(k % 2, ev, flag.value)
+        run_to_completion(ex, bubble, max_bubbles=3000)
+        assert sum(r.aborted for r in ex.records) > 0
+    else:
+        run_to_completion(ex, lambda k: BubbleSlot(k % 2, None, 0))
+    assert ex.samples_completed == n
+    assert torch.equal(ex.results(), ref)
+    ex.close()
+    if preempt:
+        native_call("pf_flag_destroy", flag)
