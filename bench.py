@@ -1281,7 +1281,7 @@ def main() -> None:
     executor.timing = False
     traffic, traffic_src = None, None
     try:  # DRAM bytes per GEMM launch from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r02", "gemm_traffic.json")) as fh:
             tdoc = json.load(fh)
         traffic, traffic_src = tdoc["per_launch_dram_bytes"], tdoc["source"]
     except (OSError, KeyError, ValueError):
