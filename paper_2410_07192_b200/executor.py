@@ -761,19 +761,7 @@ class Executor:
         self.load(carrier, model)  # one partition [0, L): every weight resident, workspace at batch_size
         self.item = item
         R = max(1, gplan.num_replicas)
-        parts, pos = [], 0
-        for nodes in gplan.partitions:
-            segs = []
-            for k in range(len(nodes)):
-                r, node = divmod(pos + k, L)
-                if segs and segs[-1][0] == r and segs[-1][2] == node:
-                    segs[-1] = (r, segs[-1][1], node + 1)
-                else:
-                    segs.append((r, node, node + 1))
-            parts.append(segs)
-            pos += len(nodes)
-        if pos != R * L:
-            raise ValueError(f"greedy plan covers {pos} of {R} x {L} nodes")
+        parts = greedy_segments(gplan, L)
         bnd = max([model.boundary_elems(i) for i in range(1, L)] + [1])
         slot_b = batch_size * bnd * model.act_bytes()
         # per-replica activation slots, and the staging buffer a segment's input is copied to
@@ -1406,6 +1394,30 @@ class Executor:
         for buf in (self._ctl_host, self._desc_host, self._stamps_host):
             buf.close()
         self.arena.close()
+
+
+def greedy_segments(gplan: GreedyPlan, num_layers: int) -> list[list[tuple[int, int, int]]]:
+    """Segments (replica r, layers [lo, hi)) of every partition of an Algorithm-1 plan: the
+    plan's partitions cut the node list replicated `num_replicas` times (partition.py:453-479)
+    into consecutive runs, so partition j covers positions [p_j, p_j+1) of that list."""
+    L = num_layers
+    R = max(1, gplan.num_replicas)
+    parts, pos = [], 0
+    for nodes in gplan.partitions:
+        segs: list[tuple[int, int, int]] = []
+        for k, n in enumerate(nodes):
+            r, node = divmod(pos + k, L)
+            if node != n:
+                raise ValueError(f"greedy partition node {n} at position {pos + k} of a {L}-node list")
+            if segs and segs[-1][0] == r and segs[-1][2] == node:
+                segs[-1] = (r, segs[-1][1], node + 1)
+            else:
+                segs.append((r, node, node + 1))
+        parts.append(segs)
+        pos += len(nodes)
+    if pos != R * L:
+        raise ValueError(f"greedy plan covers {pos} of {R} x {L} nodes")
+    return parts
 
 
 def _close_layout(saved: dict) -> None:

@@ -58,3 +58,36 @@ def test_with_cooldown_caps_usable_time_only():
     cd = with_cooldown(cyc, 10_000, 50_000)
     assert cd.bubbles[0] == cyc.bubbles[0]
     assert cd.bubbles[1].usable_us == cyc.bubbles[1].duration_us - 10_000
+
+
+def test_greedy_segments_cut_replicas_at_partition_boundaries():
+    from paper_2410_07192_b200.executor import greedy_segments
+    from paper_2410_07192_b200.planner import GreedyPlan, greedy_pack
+
+    g = GreedyPlan(((0, 1, 2, 3, 0, 1, 2, 3, 0), (1, 2, 3)), 3)
+    assert greedy_segments(g, 4) == [[(0, 0, 4), (1, 0, 4), (2, 0, 1)], [(2, 1, 4)]]
+    # empty partitions (zero-length bubbles) stay empty; every node is covered once
+    plan = greedy_pack([500, 0, 300], [10**9] * 3, [(100, 1)] * 5)
+    segs = greedy_segments(plan, 5)
+    covered = sorted((r, i) for part in segs for r, lo, hi in part for i in range(lo, hi))
+    assert covered == [(r, i) for r in range(plan.num_replicas) for i in range(5)]
+    assert any(part == [] for part in segs)
+
+
+def test_power_tail_rules():
+    import argparse
+
+    import bench
+    from paper_2410_07192_b200.engine import _throttle_tail
+
+    args = argparse.Namespace(tail_from_frac=0.375, throttle_ms=50.0, throttle_ctas=64, tail_min_ms=None,
+                              tail_frac=1.0, cooldown_ms=20.0)
+    assert [bench.tail_on_stage(args, s, 8) for s in range(8)] == [False] * 3 + [True] * 5
+    assert [bench.tail_on_stage(args, s, 4) for s in range(4)] == [False, False, True, True]
+
+    class E:
+        throttle_ns, throttle_ctas, throttle_min_ns, throttle_frac = 50_000_000, 64, None, 1.0
+    assert _throttle_tail(E, 40_000_000) == 0  # shorter than the window: not throttled
+    assert _throttle_tail(E, 120_000_000) == 50_000_000
+    E.throttle_min_ns, E.throttle_frac = 20_000_000, 0.6
+    assert _throttle_tail(E, 40_000_000) == 24_000_000
