@@ -80,16 +80,18 @@ FILL_FRACTION_NCCL = 0.95
 # board's power controller lets it start at up to 1965 MHz, after a bubble filled at full power at
 # ~1600. The last THROTTLE_MS of every bubble longer than that run on THROTTLE_CTAS CTAs and the
 # last COOLDOWN_MS idle. Measured on B200 (profiles/r02_power_sweep.md): composed 8-stage
-# main-job slowdown +3.5-4.6 % without; with (20 ms idle, 50 ms at 64 CTAs) +1.6 %, at ~16 % less fill.
-COOLDOWN_MS = 20.0
-THROTTLE_MS = 50.0
+# main-job slowdown +3.5-4.6 % without; with a tail of 50-60 ms at 48-64 CTAs and 15-25 ms idle about
+# +2 % (run-to-run spread +-0.7 points), at ~16 % less fill (profiles/r02/power_sweep.md).
+COOLDOWN_MS = 25.0
+THROTTLE_MS = 60.0
 THROTTLE_CTAS = 64
 TAIL_MIN_MS = None
 TAIL_FRAC = 1.0
 TAIL_FROM_FRAC = 0.0
 # main-job slowdown phase: A = fill-off, B = fill-on iteration of one stage; the first of each run is
-# discarded (it inherits the other mode's power state), leaving 4 off and 5 on per stage
-DEFAULT_SLOWDOWN_PATTERN = "AAABBBBBBAAA"
+# discarded (it inherits the other mode's power state), leaving 6 off and 7 on per stage (the
+# power-state noise makes single runs of the shorter AAABBBBBBAAA pattern spread by +-0.7 points)
+DEFAULT_SLOWDOWN_PATTERN = "AAAABBBBBBBBAAAA"
 
 
 def load_peaks() -> dict:
