@@ -88,6 +88,7 @@ THROTTLE_CTAS = 64
 TAIL_MIN_MS = None
 TAIL_FRAC = 1.0
 TAIL_FROM_FRAC = 0.0
+LATE_COOLDOWN_MS = None
 # main-job slowdown phase: A = fill-off, B = fill-on iteration of one stage; the first of each run is
 # discarded (it inherits the other mode's power state), leaving 6 off and 7 on per stage (the
 # power-state noise makes single runs of the shorter AAABBBBBBAAA pattern spread by +-0.7 points)
@@ -687,6 +688,13 @@ def tail_on_stage(args, stage: int, stages: int) -> bool:
     return stage >= math.ceil(args.tail_from_frac * stages - 1e-9)
 
 
+def stage_cooldown_ms(args, stage: int, stages: int) -> float:
+    """Idle tail of a stage's bubbles: --late-cooldown-ms for the last quarter of the stages
+    (the last stage's steady state is the pipeline's critical path)."""
+    late = args.late_cooldown_ms is not None and stage >= math.ceil(0.75 * stages - 1e-9)
+    return args.late_cooldown_ms if late else args.cooldown_ms
+
+
 def set_tail(engine, args) -> None:
     """The power-aware bubble tail of DESIGN.md §5.1 on a stage engine: bubbles longer than
     tail_min_ms run their last min(throttle_ms, tail_frac x duration) on throttle_ctas CTAs."""
@@ -867,6 +875,8 @@ def main() -> None:
     ap.add_argument("--throttle-ctas", type=int, default=THROTTLE_CTAS)
     ap.add_argument("--tail-min-ms", type=float, default=TAIL_MIN_MS,
                     help="bubbles no longer than this get no power tail (default: --throttle-ms)")
+    ap.add_argument("--late-cooldown-ms", type=float, default=LATE_COOLDOWN_MS,
+                    help="idle tail for the last quarter of the stages (default: --cooldown-ms)")
     ap.add_argument("--tail-from-frac", type=float, default=TAIL_FROM_FRAC,
                     help="only stages >= ceil(frac x stages) get the power tail (0: every stage)")
     ap.add_argument("--tail-frac", type=float, default=TAIL_FRAC,
@@ -972,7 +982,8 @@ def main() -> None:
             # power-aware tail: bubbles longer than the throttle window keep an idle cooldown
             cyc = cycle or pf.build_bubble_cycle(cfg, s)
             if tail_on_stage(args, s, cfg.num_stages):
-                cyc = with_cooldown(cyc, int(args.cooldown_ms * 1000), int(tail_min_ms(args) * 1000), args.tail_frac / 2)
+                cyc = with_cooldown(cyc, int(stage_cooldown_ms(args, s, cfg.num_stages) * 1000),
+                                    int(tail_min_ms(args) * 1000), args.tail_frac / 2)
             coords[s] = pf.Coordinator(s, cyc, 1,
                                        pf.OrderingPolicy("concurrent", conf["chunk"]),
                                        batch_sizes=list(conf["batch_sizes"]),
@@ -1338,7 +1349,7 @@ def main() -> None:
                          "fill_fraction": args.fill_fraction, "cooldown_ms": args.cooldown_ms,
                          "throttle_ms": args.throttle_ms, "throttle_ctas": args.throttle_ctas,
                          "tail_min_ms": tail_min_ms(args), "tail_frac": args.tail_frac,
-                         "tail_from_frac": args.tail_from_frac,
+                         "tail_from_frac": args.tail_from_frac, "late_cooldown_ms": args.late_cooldown_ms,
                          "arena_bytes": arena_bytes,
                          "plans": {str(s): pf.plan_to_dict(c.executables[f"fill-{s}"]) for s, c in coords.items()}},
                 "stages_run": [t["stage"] for t in steps],
