@@ -1386,6 +1386,11 @@ def main() -> None:
             "fill_samples_completed": int(tot.samples_completed),
             "value_definition": "sample-equivalents/s: completed batches x share of the model's FLOPs in "
                                 "the batch's partition, over device time of the timed iterations",
+            "parity": {"tolerance": "bf16 path rel 2e-2 (north star), measured as max|got - ref| / max|ref| "
+                                    "against the CPU fp32 oracle (oracle/fill_ref.py): a norm-wise bound, "
+                                    "lenient for small outputs; fp32 path rel 1e-4",
+                       "evidence": "tests/test_kernels_gpu.py (BERT-base/large shapes), tests/test_executor_gpu.py "
+                                   "(whole model through the executor), __graft_entry__.smoke()"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak if peak else None, "traffic": traffic,
                          "traffic_source": traffic_src,
