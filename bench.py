@@ -1104,13 +1104,37 @@ def main() -> None:
         losses_off, losses, losses_off2 = obj[0]
         del snap
     else:
+        characterizations: dict[int, dict] = {}
+
         def engine_for(s: int) -> StageEngine:
             if s not in engines:
                 engines[s] = StageEngine(pcfg, s, main_model, executor, streams=shared_streams)
                 engines[s].op_stamps = True  # per-op stamps + SM clock, fill on and off alike
                 set_tail(engines[s], args)
-                coordinator_for(s, pcfg)
+                coordinator_for(s, pcfg, measured_cycle(s))
             return engines[s]
+
+        def measured_cycle(s: int):
+            """Bubble characterization of stage s from fill-off iterations:
+            durations from the flag stamps, free memory from the main job's allocated bytes at
+            every BUBBLE, capped at the arena (the fill cannot use more). Plans are made from
+            it instead of the analytic build_bubble_cycle (pipeline.py:200-216)."""
+            from paper_2410_07192_b200.engine import characterize_stage
+
+            _, rep = characterize_stage(engines[s], iterations=2, fill_fraction=args.fill_fraction)
+            free = [min(arena_bytes, int(f)) for f in rep["free_mem_bytes"]]
+            analytic = pf.build_bubble_cycle(pcfg, s)
+            durs = [d if a > 0 else 0 for d, a in zip(rep["measured_bubbles_us"],
+                                                       [b.duration_us for b in analytic.bubbles])]
+            period = max(rep["measured_period_us"], sum(durs))
+            cyc = pf.cycle_from_measurements(s, period, durs, free, args.fill_fraction,
+                                             unfillable_us=max(0, min(analytic.unfillable_us, period - sum(durs))))
+            characterizations[s] = {k: rep[k] for k in ("measured_bubbles_us", "analytic_bubbles_us",
+                                                        "measured_period_us", "free_mem_bytes",
+                                                        "main_job_allocated_bytes", "insitu_t_fwd_ms",
+                                                        "insitu_t_bwd_ms")}
+            characterizations[s]["planned_free_mem_bytes"] = free
+            return cyc
 
         def stage_of(k: int) -> int:
             return (rank + k * world) % P_STAGES if conf["rotate"] else (rank + 3) % P_STAGES
@@ -1189,7 +1213,11 @@ def main() -> None:
         recs = executor.records[n_rec0:]
         launches = executor.kernel_launches + sum(e.launches for e in engines.values()) - launches0
         losses, losses_off, losses_off2 = [], [], []
-        characterization = {"bubbles": "analytic timeline with measured t_fwd/t_bwd (artificial neighbours)"}
+        characterization = {"method": "per stage, 2 fill-off iterations: bubble durations from the flag stamps, "
+                                      "free memory from memory_allocated() at each BUBBLE (capped at the arena); "
+                                      "the neighbours' arrivals follow the analytic timeline of the measured "
+                                      "t_fwd/t_bwd (artificial neighbours)",
+                            "per_stage": {str(k): v for k, v in sorted(characterizations.items())}}
         # main-job interference, after (and outside) the timed region: every stage the timed
         # steps visited runs fill-off and fill-on iterations interleaved ABBA (off on on off ...)
         def run_block(s_: int, modes: list) -> list[dict]:
