@@ -865,7 +865,12 @@ def main() -> None:
                     help=f"share of each bubble the planner may fill (reference default 0.68; here "
                          f"{FILL_FRACTION} emulated, {FILL_FRACTION_NCCL} nccl)")
     ap.add_argument("--optimizer-offload", action="store_true",
-                    help="main job keeps its AdamW moments in pinned host memory between steps")
+                    help="main job keeps its AdamW moments in pinned host memory between steps and "
+                         "lends their device buffer to the fill in the bubbles between (DESIGN.md §3.3)")
+    ap.add_argument("--stage", type=int, default=None,
+                    help="every timed iteration runs stage (rank + STAGE) mod 8 instead of rotating over stages")
+    ap.add_argument("--no-loan", action="store_true",
+                    help="with --optimizer-offload: free the moments' device blocks instead of lending them")
     ap.add_argument("--max-batches", type=int, default=None,
                     help="Coordinator max_batches_per_bubble (overrides the config's)")
     ap.add_argument("--cooldown-ms", type=float, default=COOLDOWN_MS,
@@ -899,6 +904,9 @@ def main() -> None:
     conf = dict(CONFIGS[args.config])
     if args.max_batches is not None:
         conf["max_batches"] = args.max_batches
+    if args.stage is not None:
+        conf["rotate"] = False
+        conf["stage"] = args.stage
     if args.batch_sizes:
         conf["batch_sizes"] = tuple(int(b) for b in args.batch_sizes.split(","))
     args.fill = args.fill or conf["fill"]
@@ -946,7 +954,7 @@ def main() -> None:
     if args.optimizer_offload and args.pipeline == "nccl":
         raise SystemExit("--optimizer-offload is implemented for the emulated engine (StageEngine) only")
     if args.optimizer_offload:  # AdamW moments in pinned host memory between steps
-        main_model.enable_optimizer_offload(h2d_gbs=measure_h2d_gbs())
+        main_model.enable_optimizer_offload(h2d_gbs=measure_h2d_gbs(), loan=not args.no_loan)
 
     # ---- fill job: BERT with a B200-measured profile
     fcfg = BERT_LARGE if args.fill == "bert_large" else BERT_BASE
@@ -968,10 +976,14 @@ def main() -> None:
     reserved = torch.cuda.max_memory_reserved()
     free_mem = int(max(0, total_b - reserved - (4 << 30)) * 0.9)  # safety margin
     arena_bytes = min(free_mem, conf["arena_cap"])
+    if args.arena_cap_gb:  # a main job that leaves less HBM free (the memory-loan runs)
+        arena_bytes = min(arena_bytes, int(args.arena_cap_gb * 2**30))
     pcfg = pf.PipelineConfig(P_STAGES, M_MICRO, tf_ms, tb_ms, sched, arena_bytes, arena_bytes,
                              args.fill_fraction)
 
     executor = Executor(arena_bytes, job_seed=rank)
+    if main_model.offload is not None and main_model.offload.loan:
+        main_model.offload.borrower = executor  # the moments' buffer is lent between steps
     coords: dict[int, pf.Coordinator] = {}
     engines: dict[int, object] = {}
     items: dict[int, object] = {}
@@ -993,6 +1005,8 @@ def main() -> None:
 
     def next_work():
         s = items["stage"]
+        if s in engines and hasattr(engines[s], "loan_kinds"):
+            executor.loan_kinds = engines[s].loan_kinds()  # the plan's bubbles planned with the loan
         prev = items.get("item")
         if prev is not None and not executor.busy:
             coords[s].on_range_done(0, prev, 0.0)
@@ -1123,6 +1137,10 @@ def main() -> None:
 
             _, rep = characterize_stage(engines[s], iterations=2, fill_fraction=args.fill_fraction)
             free = [min(arena_bytes, int(f)) for f in rep["free_mem_bytes"]]
+            # bubble kinds inside the optimizer-state loan window get the lent bytes on top
+            lent = engines[s].loan_kinds()
+            off_ = main_model.offload
+            free = [f + (off_.device_buf.numel() if k in lent else 0) for k, f in enumerate(free)]
             analytic = pf.build_bubble_cycle(pcfg, s)
             durs = [d if a > 0 else 0 for d, a in zip(rep["measured_bubbles_us"],
                                                        [b.duration_us for b in analytic.bubbles])]
@@ -1134,10 +1152,11 @@ def main() -> None:
                                                         "main_job_allocated_bytes", "insitu_t_fwd_ms",
                                                         "insitu_t_bwd_ms")}
             characterizations[s]["planned_free_mem_bytes"] = free
+            characterizations[s]["loan_kinds"] = sorted(lent)
             return cyc
 
         def stage_of(k: int) -> int:
-            return (rank + k * world) % P_STAGES if conf["rotate"] else (rank + 3) % P_STAGES
+            return (rank + k * world) % P_STAGES if conf["rotate"] else (rank + conf.get("stage", 3)) % P_STAGES
 
         def run_step(k: int, fill: bool, stage: int | None = None) -> dict:
             s = stage_of(k) if stage is None else stage
@@ -1406,7 +1425,10 @@ def main() -> None:
             "bubble_characterization": characterization,
             "optimizer_offload": None if main_model.offload is None else {
                 "state_bytes": main_model.offload.state_bytes, "lead_ms": main_model.offload.lead_us / 1e3,
-                "h2d_gbs": main_model.offload.h2d_gbs, "transfers": main_model.offload.transfers},
+                "h2d_gbs": main_model.offload.h2d_gbs, "transfers": main_model.offload.transfers,
+                "loan": None if not main_model.offload.loan else {
+                    "bytes": main_model.offload.device_buf.numel(), "loans": main_model.offload.loans,
+                    "loan_batches": executor.loan_batches, "rollbacks": executor.loan_rollbacks}},
             "weight_staging": staging,
             "bubbles_preempted": sum(1 for r in recs if r.aborted),
             "bubbles_filled": len(recs),

@@ -102,10 +102,11 @@ class GPTStage(nn.Module):
         self._saved: dict[int, tuple[torch.Tensor, torch.Tensor]] = {}
         self.offload: Optional[OptimizerOffload] = None
 
-    def enable_optimizer_offload(self, h2d_gbs: float = 50.0) -> "OptimizerOffload":
+    def enable_optimizer_offload(self, h2d_gbs: float = 50.0, loan: bool = False) -> "OptimizerOffload":
         """Keep AdamW's moment estimates in pinned host memory between optimizer steps
-        (PAPER.md:427): the bubbles before the step see that much more free HBM."""
-        self.offload = OptimizerOffload(self.opt, h2d_gbs)
+        (PAPER.md:427): the bubbles before the step see that much more free HBM (with
+        `loan`, lent to the fill executor set as `offload.borrower`)."""
+        self.offload = OptimizerOffload(self.opt, h2d_gbs, loan=loan)
         return self.offload
 
     def forward_mb(self, mb: int, x: torch.Tensor) -> torch.Tensor:
@@ -138,6 +139,8 @@ class GPTStage(nn.Module):
         """Device copies of parameters and the full optimizer state (to replay iterations)."""
         import copy
 
+        if self.offload is not None and not self.offload.resident:  # moments back on the device
+            self.offload.wait_resident(torch.cuda.current_stream())
         torch.cuda.synchronize()
         params = [p.detach().clone() for p in self.parameters()]
         return {"params": params, "opt": copy.deepcopy(self.opt.state_dict())}
@@ -158,6 +161,29 @@ class GPTStage(nn.Module):
         torch.cuda.synchronize()
 
 
+def _pad256(n: int) -> int:
+    return (n + 255) // 256 * 256
+
+
+def loan_window_kinds(timeline, period_us: int, lead_us: int) -> set[int]:
+    """StageEngine.loan_kinds on a steady-state timeline [(Instr, start_us, end_us)]."""
+    compute = [(ins, st, en) for ins, st, en in timeline if ins.op != "BUBBLE"]
+    step_end = max(en for _, _, en in compute)
+    prefetch_at = min((st for _, st, _ in compute if st >= step_end - lead_us), default=step_end)
+    copy_us = lead_us / 1.25
+    inside, outside = set(), set()
+    for ins, st, en in timeline:
+        if ins.op != "BUBBLE":
+            continue
+        kind = 0 if ins.kind is BubbleKind.FWD_BWD else 1
+        after_step = st >= step_end
+        since_copy_out = st - step_end if after_step else st - (step_end - period_us)
+        # the fill may wait for the copy-out for at most a tenth of the bubble
+        ok = since_copy_out + 0.1 * (en - st) >= copy_us and (after_step or st < prefetch_at)
+        (inside if ok else outside).add(kind)
+    return inside - outside
+
+
 class OptimizerOffload:
     """Main-job optimizer-state offload.
 
@@ -168,12 +194,18 @@ class OptimizerOffload:
     ``StageEngine.run_iteration`` ``lead_us`` ahead of the step). The step waits for the
     copy-back (``wait_resident``). Copies are exact, so the main job's parameters and
     losses are bitwise those of a run without offload. The bubbles that fall between
-    eviction and prefetch have ``state_bytes`` more free HBM, which is what the fill job's
-    arena can be sized from."""
+    eviction and prefetch have ``state_bytes`` more free HBM.
+
+    Loan mode (``loan=True``): the moments live in one device buffer (``device_buf``, the
+    states are views of it) that is not freed but *lent* to a borrower (the fill
+    ``Executor``) between the copy-out and the prefetch: ``borrower.lend(device_buf,
+    evicted)`` after the step, ``borrower.revoke()`` before the copy-back, which waits on
+    the event revoke returns. The fill's plans for the bubbles in that window get the
+    buffer's bytes as extra free memory."""
 
     KEYS = ("exp_avg", "exp_avg_sq")
 
-    def __init__(self, opt: torch.optim.Optimizer, h2d_gbs: float = 50.0):
+    def __init__(self, opt: torch.optim.Optimizer, h2d_gbs: float = 50.0, loan: bool = False):
         self.opt = opt
         self.stream = torch.cuda.Stream()
         self.host: dict[tuple[int, str], torch.Tensor] = {}
@@ -182,6 +214,34 @@ class OptimizerOffload:
         self.resident = True  # states on the device (before the first step they do not exist)
         self.state_bytes = 0
         self.transfers = 0
+        self.loan = loan
+        self.borrower = None  # loan mode: object with lend(buf, ready_event) / revoke() -> event
+        self.device_buf: Optional[torch.Tensor] = None
+        self.host_buf: Optional[torch.Tensor] = None
+        self._views: dict[tuple[int, str], torch.Tensor] = {}
+        self._lent = False
+        self.loans = 0
+
+    def _adopt(self) -> None:
+        """Loan mode: every moment becomes a view of `device_buf` (allocated at the first
+        step; states replaced since -- restore(), load_state_dict -- are copied into their
+        views on the current stream)."""
+        specs = [(p, st, k) for p, st in self._states() for k in self.KEYS if st.get(k) is not None]
+        if self.device_buf is None:
+            total = sum(_pad256(st[k].numel() * st[k].element_size()) for _, st, k in specs)
+            self.device_buf = torch.empty(total, dtype=torch.uint8, device=specs[0][0].device)
+            self.host_buf = torch.empty(total, dtype=torch.uint8, pin_memory=True)
+            off = 0
+            for p, st, k in specs:
+                t = st[k]
+                nb = t.numel() * t.element_size()
+                self._views[(id(p), k)] = self.device_buf[off:off + nb].view(t.dtype).view(t.shape)
+                off += _pad256(nb)
+        for p, st, k in specs:
+            v = self._views[(id(p), k)]
+            if st[k].data_ptr() != v.data_ptr():
+                v.copy_(st[k])
+                st[k] = v
 
     def _states(self):
         for group in self.opt.param_groups:
@@ -196,6 +256,25 @@ class OptimizerOffload:
         return int(1.25 * self.state_bytes / (self.h2d_gbs * 1e3))
 
     def evict(self, main: torch.cuda.Stream) -> None:
+        if self.loan:
+            with torch.cuda.stream(main):
+                self._adopt()
+            ev = torch.cuda.Event()
+            ev.record(main)
+            self.stream.wait_event(ev)
+            with torch.cuda.stream(self.stream):
+                self.host_buf.copy_(self.device_buf, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(self.stream)
+            self.state_bytes = self.device_buf.numel()
+            self.resident = False
+            self._ready = None
+            self.transfers += 1
+            if self.borrower is not None:
+                self.borrower.lend(self.device_buf, done)
+                self._lent = True
+                self.loans += 1
+            return
         ev = torch.cuda.Event()
         ev.record(main)
         self.stream.wait_event(ev)
@@ -228,6 +307,16 @@ class OptimizerOffload:
             ev = torch.cuda.Event()
             ev.record(after)
             self.stream.wait_event(ev)
+        if self.loan:
+            if self._lent:  # the borrower's last use of the buffer comes first
+                self.stream.wait_event(self.borrower.revoke())
+                self._lent = False
+            with torch.cuda.stream(self.stream):
+                self.device_buf.copy_(self.host_buf, non_blocking=True)
+                self._ready = torch.cuda.Event()
+                self._ready.record(self.stream)
+            self.transfers += 1
+            return
         with torch.cuda.stream(self.stream):
             for p, st in self._states():
                 for k in self.KEYS:
@@ -243,6 +332,9 @@ class OptimizerOffload:
             return
         self.prefetch()  # no-op when run_iteration already issued it
         main.wait_event(self._ready)
+        if self.loan:
+            self.resident = True
+            return
         for _, st in self._states():
             for k in self.KEYS:
                 if st.get(k) is not None:
@@ -461,6 +553,18 @@ class StageEngine:
             prev_end_us = end_us
         self.records.append(rec)
         return rec
+
+    def loan_kinds(self) -> set[int]:
+        """Bubble kinds (0 fwd-bwd, 1 fill-drain) whose every bubble falls inside the
+        optimizer-state loan window of this stage's iteration: from the end of the copy-out
+        after the step (`lead_us` / 1.25 after it, the transfer time) to the copy-back, which
+        run_iteration issues `lead_us` ahead of the step. A bubble that opens more than a tenth
+        of its length before the copy-out ends is outside: the fill would wait for the copy
+        (DESIGN.md §3.3)."""
+        off = self.model.offload
+        if off is None or not off.loan or not off.state_bytes:
+            return set()
+        return loan_window_kinds(self.timeline, self.cfg.period_us, off.lead_us)
 
     def _last_compute(self) -> Instr:
         return [ins for ins, _, _ in self.timeline if ins.op != "BUBBLE"][-1]

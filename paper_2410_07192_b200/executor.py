@@ -97,6 +97,7 @@ class _Progress:
     resume: Optional[tuple[int, int, int]] = None  # (first sample, count, node) of a yielded batch
     resume_zero: Optional[int] = None  # atomic node whose cursor must be reset before the resume
     finished: bool = False
+    resume_epoch: int = 0  # loan epoch the yielded batch ran in (a loan batch resumes only in it)
 
 
 @dataclass
@@ -111,6 +112,7 @@ class _Pending:
     progress_key: tuple = ()  # (part, next sample, resume point, resume cursor) when enqueued
     tp: Optional[list] = None  # partitioned training: [(batch index, phase index, start node)] enqueued
     greedy: Optional[list] = None  # Algorithm-1 plan: [(replica, lo, hi, start node)] of partition j
+    loan_epoch: int = 0
 
 
 class _Chain:
@@ -208,13 +210,29 @@ class Executor:
         self._greedy: Optional[dict] = None  # Algorithm-1 execution state (load_greedy)
         self.starved = 0  # consecutive settled bubbles that enqueued work but made no progress
         self._cursor_now = -1  # the resume node's cursor as of the last settle
+        # memory loan (lend / revoke): HBM the main job does not need between two points of its
+        # iteration (the offloaded optimizer moments' device buffer, engine.OptimizerOffload).
+        # Bubble kinds in `loan_kinds` are planned with the loan added to their free memory;
+        # batches larger than what the arena's region holds (`_base_b`) take their transient
+        # workspace from the loan and run only while it is held
+        self.loan_kinds: set[int] = set()
+        self._loan: Optional[torch.Tensor] = None  # uint8 device buffer while lent
+        self._loan_buf: Optional[torch.Tensor] = None  # the buffer chains were recorded against
+        self._loan_ready: Optional[torch.cuda.Event] = None
+        self._loan_epoch = 0
+        self._base_b: dict[int, int] = {}  # partition -> largest batch the region's workspace holds
+        self._loan_ws: dict[tuple[int, int], dict] = {}
+        self._loan_copy: Optional[torch.cuda.Event] = None  # last staging into the loan
+        self.loan_batches = 0  # batches enqueued on the loan
+        self.loan_rollbacks = 0  # yielded loan batches restarted after a revoke
 
     # ------------------------------------------------------------------ loading
 
     _LAYOUT_ATTRS = ("_ctl", "_desc", "_stamps", "_region", "ws", "in_dev", "_cap", "_in_host", "_aux_host",
                      "aux_dev",
                      "_results", "_store_dev", "_store_host", "_flops_frac", "_staged_part",
-                     "_staged_event", "_chains", "model", "plan", "_dev_views", "_part_layouts", "_gated")
+                     "_staged_event", "_chains", "model", "plan", "_dev_views", "_part_layouts", "_gated",
+                     "_base_b", "_loan_ws")
 
     def _save_layout(self) -> None:
         if self._layout_key is not None:
@@ -291,11 +309,111 @@ class Executor:
         (Σ weights + max transient, partition.py:143-150 / profiler._module_mem)."""
         model, p = self.model, self.plan.partitions[part]
         w = sum(_pad256(model[i].weight_bytes()) for i in range(p.lo, p.hi))
-        b = max([e.batch_size for e in p.per_bubble] + [1])
+        b = self._base_b.get(part) or max([e.batch_size for e in p.per_bubble] + [1])
+        return w, self._ws_need(part, b)
+
+    def _ws_need(self, part: int, b: int) -> dict[str, int]:
+        model, p = self.model, self.plan.partitions[part]
         need = dict(model.workspace(p.lo, p.hi, b))
         if p.lo > 0 and not self._tp:  # the partition's input, reloaded from the activation store (bf16 units)
             need["in"] = b * model.boundary_elems(p.lo) * model.act_bytes() // 2
-        return w, need
+        return need
+
+    def _plan_base_b(self) -> dict[int, int]:
+        """Per partition: the largest batch its region workspace is sized for -- the plan's
+        batch sizes in bubble kinds planned without the loan (all kinds when there is no
+        loan). Loan kinds' larger batches take their workspace from the loan."""
+        out = {}
+        loan_ok = bool(self.loan_kinds) and not self.model.is_training and not self._tp
+        for k, p in enumerate(self.plan.partitions):
+            sizes = [e.batch_size for j, e in enumerate(p.per_bubble) if e.num_batches] or [1]
+            base = [e.batch_size for j, e in enumerate(p.per_bubble)
+                    if e.num_batches and not (loan_ok and j in self.loan_kinds)]
+            if base:
+                out[k] = max(base)
+                continue
+            # every bubble is planned with the loan: the region holds the largest power-of-two
+            # batch (<= the planned ones) whose weights + workspace fit 90 % of the arena; if
+            # not even one sample's does, the partition lives in the loan (0: weights and
+            # workspace in the lent buffer, restaged every time the loan is granted)
+            w = sum(_pad256(self.model[i].weight_bytes()) for i in range(p.lo, p.hi))
+            b = max(sizes)
+            fits = lambda b_: w + sum(_pad256(2 * v) for v in self._ws_need(k, b_).values()) <= 0.9 * self.arena.capacity
+            while b > 1 and not fits(b):
+                b //= 2
+            out[k] = b if fits(b) else 0
+        return out
+
+    def _on_loan(self, part: int) -> bool:
+        """Partition `part` is loan-resident (weights + workspace in the lent buffer)."""
+        return self._base_b.get(part, 1) == 0
+
+    def _backing(self, part: int) -> torch.Tensor:
+        """bf16 storage partition `part`'s weights and workspace are laid out in."""
+        if self._on_loan(part):
+            if self._loan_buf is None:
+                raise native.ArenaExhausted(f"partition {part} needs the loan, which was never granted")
+            return self._loan_buf.view(torch.bfloat16)
+        return self._region
+
+    def _loan_workspace(self, part: int, b: int) -> dict:
+        """Workspace views of a batch of b samples through partition `part` inside the lent
+        buffer (the chains recorded with them are valid as long as the buffer is)."""
+        ws = self._loan_ws.get((part, b))
+        if ws is not None:
+            return ws
+        buf = self._loan_buf
+        need = self._ws_need(part, b)
+        total = sum(_pad256(2 * v) for v in need.values())
+        if buf is None or total > buf.numel():
+            raise native.ArenaExhausted(f"loan of {0 if buf is None else buf.numel()} B cannot hold the "
+                                        f"{total} B workspace of batch {b} (partition {part})")
+        ws, off = {}, 0
+        for k, v in need.items():
+            ws[k] = buf[off:off + 2 * v].view(torch.bfloat16)
+            off += _pad256(2 * v)
+        self._loan_ws[(part, b)] = ws
+        return ws
+
+    def lend(self, buf: torch.Tensor, ready: Optional[torch.cuda.Event]) -> None:
+        """The main job lends `buf` (uint8, device) until `revoke`; the fill stream uses it only
+        after `ready` (the main job's last use of it)."""
+        if self._loan_buf is not None and (buf.data_ptr() != self._loan_buf.data_ptr()
+                                           or buf.numel() != self._loan_buf.numel()):
+            self.stream.synchronize()
+            self._drop_chains()  # chains recorded against another loan buffer
+            self._loan_ws = {}
+        first = self._loan_buf is None
+        self._loan_buf = buf
+        self._loan = buf
+        self._loan_ready = ready
+        self._loan_epoch += 1
+        if first:
+            self.prewarm()  # record the loan batch sizes' chains now, not in a bubble
+
+    def _batch_cap(self, part: int, planned: int, num: int) -> tuple[int, int]:
+        """A planned (batch size, batches), capped at the region's workspace while the loan
+        is not usable -- with proportionally more batches, so the bubble stays filled."""
+        cap = self._base_b.get(part, planned)
+        if planned <= cap or self._loan is not None or cap == 0:
+            return planned, num
+        return cap, min((MAX_BATCHES - 1) // 2, -(-num * planned // cap))
+
+    def revoke(self) -> torch.cuda.Event:
+        """End the loan: returns an event after the last fill work enqueued so far (kernels
+        yield at the bubble's end, so it fires within the yield latency of the bubble's end).
+        The lender's next write to the buffer waits on it. A batch that yielded on the loan is
+        restarted (from its first node) the next time it runs."""
+        self._loan = None
+        self._loan_ready = None
+        if self._staged_part is not None and self.plan is not None and self._on_loan(self._staged_part):
+            self._staged_part = None  # restaged into the next loan
+        if self._loan_copy is not None:  # a loan-resident staging's copies precede the return
+            self.stream.wait_event(self._loan_copy)
+            self._loan_copy = None
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
+        return ev
 
     def _carve(self, cap: int) -> None:
         """Arena: control block | partition region | ids | store. The partition region
@@ -305,12 +423,16 @@ class Executor:
         plan, model = self.plan, self.model
         self._chains = {}
         self._dev_views = {}
+        self._loan_ws = {}
+        self._base_b = self._plan_base_b()
         self._ctl = self.arena.alloc((_CTL_WORDS,), torch.int32)
         self._ctl.zero_()
         self._desc = self.arena.alloc((MAX_BATCHES, DESC_WORDS), torch.int64)
         self._stamps = self.arena.alloc((MAX_NODES, 2), torch.int64)
-        region = 0
+        region = 256
         for k in range(len(plan.partitions)):
+            if self._on_loan(k):
+                continue
             w, need = self._part_need(k)
             region = max(region, w + sum(_pad256(2 * v) for v in need.values()))
         self._region = self.arena.alloc((region // 2,), torch.bfloat16)
@@ -381,7 +503,8 @@ class Executor:
         if lay is not None:
             return lay
         p = self.plan.partitions[part]
-        base = self._region.data_ptr()
+        backing = self._backing(part)
+        base = backing.data_ptr()
         ptr = base
         views: dict[int, dict] = {}
         for i in range(p.lo, p.hi):
@@ -392,7 +515,7 @@ class Executor:
         off = (ptr - base) // 2
         ws: dict[str, torch.Tensor] = {}
         for k, v in need.items():
-            ws[k] = self._region[off:off + v]
+            ws[k] = backing[off:off + v]
             off += _pad256(2 * v) // 2
         lay = (views, ws)
         self._part_layouts[part] = lay
@@ -401,7 +524,7 @@ class Executor:
     def _module_ptr(self, part: int, i: int) -> int:
         """Device address of module i's staged state inside the region."""
         p = self.plan.partitions[part]
-        ptr = self._region.data_ptr()
+        ptr = self._backing(part).data_ptr()
         for j in range(p.lo, i):
             ptr += _pad256(self.model[j].weight_bytes())
         return ptr
@@ -412,12 +535,16 @@ class Executor:
         fill stream waits on the staging event before the partition's first batch."""
         if self._staged_part == part:
             return
+        if self._on_loan(part) and self._loan is None:
+            return  # staged when the loan is granted (fill)
         p = self.plan.partitions[part]
         views, ws = self._part_layout(part)
         e0 = torch.cuda.Event(enable_timing=True)
         staged = 0
         with torch.cuda.stream(self.copy_stream):
             self.copy_stream.wait_stream(self.stream)
+            if self._on_loan(part) and self._loan_ready is not None:
+                self.copy_stream.wait_event(self._loan_ready)
             e0.record(self.copy_stream)
             for i in range(p.lo, p.hi):
                 mod = self.model[i]
@@ -432,6 +559,8 @@ class Executor:
         ev.record(self.copy_stream)
         self._staged_event = ev
         self._staged_part = part
+        if self._on_loan(part):
+            self._loan_copy = ev
         self.stagings.append((staged, e0, ev))
         self.ws = ws
         self._dev_views = dict(views)
@@ -449,6 +578,8 @@ class Executor:
         pidx = part_idx[1] if self._tp else part_idx
         part = self.plan.partitions[pidx]
         views, ws = self._part_layout(pidx)
+        if not self._tp and 0 < self._base_b.get(pidx, cnt) < cnt:
+            ws = self._loan_workspace(pidx, cnt)  # a loan batch
         resident = {i: getattr(model[i], "dev", None) for i in views}
         for i, dev in views.items():  # record against the partition's region layout
             model[i].dev = dev
@@ -617,7 +748,7 @@ class Executor:
             return
         for pidx, part in enumerate(self.plan.partitions):  # every partition: switches record nothing
             for e in part.per_bubble:
-                if e.num_batches:
+                if e.num_batches and (self._loan_buf is not None or e.batch_size <= self._base_b.get(pidx, 1 << 30)):
                     self._chain(pidx, e.batch_size, self._last_flag)
 
     # ------------------------------------------------------------------ bubbles
@@ -643,8 +774,16 @@ class Executor:
             self._fill_greedy(slot)
             return prev
         pr = self.progress
+        if self._on_loan(pr.part) and self._loan is None:
+            return prev  # loan-resident partition, loan not held: nothing to run
         if self._staged_part != pr.part:  # a run-ahead staged the next partition over this one
             self._stage_partition(pr.part)
+        if (pr.resume is not None and pr.resume[1] > self._base_b.get(pr.part, pr.resume[1])
+                and (self._loan is None or pr.resume_epoch != self._loan_epoch)):
+            # a batch yielded on the loan, which has been returned since: its workspace is
+            # gone, so it restarts from its first node (cursors are re-zeroed by the chain)
+            pr.next_sample, pr.resume, pr.resume_zero = pr.resume[0], None, None
+            self.loan_rollbacks += 1
         part = self.plan.partitions[pr.part]
         entry = part.per_bubble[slot.index] if slot.index < len(part.per_bubble) else None
         n_total = self.item.entry.size
@@ -655,10 +794,11 @@ class Executor:
             batches.append(pr.resume)
         start = pr.next_sample
         if entry.num_batches > 0:
-            for _ in range(entry.num_batches - (1 if pr.resume is not None else 0)):
+            bsz, nb = self._batch_cap(pr.part, entry.batch_size, entry.num_batches)
+            for _ in range(nb - (1 if pr.resume is not None else 0)):
                 if start >= n_total:
                     break
-                cnt = min(entry.batch_size, n_total - start)
+                cnt = min(bsz, n_total - start)
                 batches.append((start, cnt, 0))
                 start += cnt
         if not batches:
@@ -666,15 +806,16 @@ class Executor:
         parts = [pr.part] * len(batches)
         ahead = pr.part + 1
         if (self.run_ahead and not self.model.is_training and start >= n_total and ahead < len(self.plan.partitions)
-                and len(batches) < MAX_BATCHES):
+                and len(batches) < MAX_BATCHES and not self._on_loan(pr.part) and not self._on_loan(ahead)):
             nxt = self.plan.partitions[ahead]
             e2 = nxt.per_bubble[slot.index] if slot.index < len(nxt.per_bubble) else None
             s2 = 0
             if e2 is not None:
-                for _ in range(min(e2.num_batches, MAX_BATCHES - len(batches))):
+                bsz2, nb2 = self._batch_cap(ahead, e2.batch_size, e2.num_batches)
+                for _ in range(min(nb2, MAX_BATCHES - len(batches))):
                     if s2 >= n_total:
                         break
-                    cnt = min(e2.batch_size, n_total - s2)
+                    cnt = min(bsz2, n_total - s2)
                     batches.append((s2, cnt, 0))
                     parts.append(ahead)
                     s2 += cnt
@@ -714,6 +855,12 @@ class Executor:
                 st.wait_event(slot.start_event)
             if self._staged_event is not None:
                 st.wait_event(self._staged_event)
+            on_loan = sum(1 for k, (_, c, _) in enumerate(batches) if c > self._base_b.get(parts[k], c))
+            if on_loan:
+                self.loan_batches += on_loan
+                if self._loan_ready is not None:  # the main job's last use of the lent buffer
+                    st.wait_event(self._loan_ready)
+                    self._loan_ready = None
             self._ctl[:3].zero_()  # fresh bubble: abort word, done counter, run-ahead staged
             if pr.resume_zero is not None:
                 self._ctl[_CURSOR0 + pr.resume_zero] = 0
@@ -737,7 +884,8 @@ class Executor:
         ev = torch.cuda.Event()
         ev.record(st)
         self.pending = _Pending(slot, batches, ev, launches, pr.part, has_resume=pr.resume is not None,
-                                parts=parts, progress_key=(pr.part, pr.next_sample, pr.resume, self._cursor_now))
+                                parts=parts, progress_key=(pr.part, pr.next_sample, pr.resume, self._cursor_now),
+                                loan_epoch=self._loan_epoch)
         self.kernel_launches += launches
         return prev
 
@@ -1309,6 +1457,7 @@ class Executor:
                         completed_last += cnt
                 else:
                     pr.resume = (first, cnt, max(resume_node, node))
+                    pr.resume_epoch = pend.loan_epoch
                     if not ch.units[resume_node][1]:
                         pr.resume_zero = resume_node  # atomic: re-run the whole node
                 break

@@ -218,3 +218,93 @@ def test_greedy_algorithm1_plan_matches_the_dp_plan(pf, preempt):
     ex.close()
     if preempt:
         native_call("pf_flag_destroy", flag)
+
+
+def plan_item_per_kind(pf, model, samples, free_fwd, free_drain, sizes=(4, 16)):
+    """plan_item with a different free memory per bubble kind (the loan's effect)."""
+    from paper_2410_07192_b200.profiles import JobSpec, LayerProfile, ModelProfile, JobKind
+
+    layers = []
+    for i in range(len(model)):
+        w = model[i].weight_bytes()
+        layers.append(LayerProfile({b: 0.005 + 0.0005 * b for b in sizes}, {b: w + 1_000_000 * b for b in sizes}, w, 1.0))
+    prof = ModelProfile("tiny", tuple(layers), 1, frozenset({JobKind.BATCH_INFERENCE}))
+    cyc = pf.BubbleCycle((pf.BubbleSpec(1000, 1000, free_fwd, pf.BubbleKind.FWD_BWD),
+                          pf.BubbleSpec(500, 500, free_drain, pf.BubbleKind.FILL_DRAIN)), 10_000, 0)
+    coord = pf.Coordinator(0, cyc, 1)
+    plan = coord.admit(JobSpec("j0", 0.0, prof, JobKind.BATCH_INFERENCE, samples))
+    return coord.request_work(0, 0.0), plan
+
+
+@pytest.mark.parametrize("resident", [False, True])
+def test_executor_memory_loan_is_exact_and_returned(pf, resident):
+    """Memory loan: the fwd-bwd bubbles are planned with more free memory
+    (a lent buffer). resident=False: they run larger batches whose workspace lives in the
+    loan; the fill-drain bubbles run region-sized batches. resident=True: the arena cannot
+    hold the model at all, so the plan's one partition runs only in the fwd-bwd bubbles
+    with its weights and workspace in the loan, restaged at every grant. The lender takes
+    the buffer back after every fwd-bwd bubble (revoke) and scribbles over it; bubbles
+    close mid-batch, so loan batches yield and must restart. Results equal an
+    unpreempted, loan-free run bit for bit."""
+    from paper_2410_07192_b200 import native
+    from paper_2410_07192_b200.executor import BubbleSlot, Executor
+    from paper_2410_07192_b200.fillmodels import bert
+
+    model = bert(tiny_cfg(), seed=8)
+    w = sum(model[i].weight_bytes() for i in range(len(model)))
+    item, plan = plan_item_per_kind(pf, model, samples=96, free_fwd=8_000_000_000,
+                                    free_drain=(w // 4) if resident else w + 8_000_000)
+    assert len(plan.partitions) == 1
+    want = [16, 0] if resident else [16, 4]
+    assert [e.batch_size for e in plan.partitions[0].per_bubble] == want, plan
+    ex0 = Executor(256 << 20, job_seed=4)
+    ex0.load(item, model)
+    run_to_completion(ex0, lambda k: BubbleSlot(k % 2, None, 0))
+    ref = ex0.results().clone()
+    ex0.close()
+
+    flag = ctypes.c_void_p()
+    native.call("pf_flag_create", ctypes.byref(flag))
+    anchor = torch.zeros(1, dtype=torch.int64, device="cuda")
+    comm = torch.cuda.Stream()
+    lender = torch.cuda.Stream()
+    loan = torch.zeros(64 << 20, dtype=torch.uint8, device="cuda")
+    ex = Executor((w // 2) if resident else (256 << 20), job_seed=4)
+    ex.loan_kinds = {0}
+    ex.load(item, model)
+    assert ex._on_loan(0) == resident
+
+    def bubble(k):
+        kind = k % 2
+        if kind == 0:  # the lender's copy-out done: lend for the fwd-bwd bubble
+            ready = torch.cuda.Event()
+            ready.record(lender)
+            ready.synchronize()
+            ex.lend(loan, ready)
+        with torch.cuda.stream(comm):
+            torch.cuda._sleep(300_000)
+        native.call("pf_read_globaltimer", anchor.data_ptr(), comm.cuda_stream)
+        native.call("pf_flag_write_on_stream", flag, 1, comm.cuda_stream)
+        ev = torch.cuda.Event()
+        ev.record(comm)
+        native.call("pf_flag_clear_at", flag, anchor.data_ptr(), 60_000 + 90_000 * (k % 5), None, comm.cuda_stream)
+        return BubbleSlot(kind, ev, flag.value)
+
+    k = 0
+    while ex.busy and k < 3000:
+        ex.fill(bubble(k))
+        if k % 2 == 0:  # take the buffer back and overwrite it (the moments' copy-back)
+            lender.wait_event(ex.revoke())
+            with torch.cuda.stream(lender):
+                loan.fill_(0xA5)
+        k += 1
+    ex.settle()
+    torch.cuda.synchronize()
+    assert not ex.busy
+    assert ex.loan_batches > 0
+    assert ex.loan_rollbacks > 0, "no loan batch yielded across a revoke; vary the bubbles"
+    assert torch.equal(ex.results(), ref), (k, ex.loan_batches, ex.loan_rollbacks)
+    if resident:  # the weights were staged into every loan the fill used
+        assert len(ex.stagings) > 3, len(ex.stagings)
+    ex.close()
+    native.call("pf_flag_destroy", flag)

@@ -91,3 +91,21 @@ def test_cycle_from_measurements_uses_reference_usable_rule():
     assert cyc.bubbles[1].kind is BubbleKind.FILL_DRAIN and cyc.stage_id == 3
     with pytest.raises(ValueError):
         cycle_from_measurements(0, 10, [20], [1])  # bubbles exceed the period
+
+
+def test_loan_window_kinds_8_stage_1f1b():
+    """Optimizer-state loan window (engine.loan_window_kinds): the fwd-bwd
+    bubble of stages 0-6 opens after the previous step's copy-out and before the copy-back;
+    the fill-drain bubble opens at the step, before the copy-out has finished."""
+    import paper_2410_07192_b200 as pf
+    from paper_2410_07192_b200.engine import loan_window_kinds
+    from paper_2410_07192_b200.schedule import steady_state_timeline
+
+    cfg = pf.PipelineConfig(8, 8, 12.0, 24.0, pf.ScheduleKind.ONE_F_ONE_B, 1, 1, 0.9)
+    got = [loan_window_kinds(steady_state_timeline(cfg, s), cfg.period_us, 94_000) for s in range(8)]
+    assert got == [{0}] * 7 + [set()]
+    # a copy-back issued earlier than the fwd-bwd bubble closes the window for it
+    got = [loan_window_kinds(steady_state_timeline(cfg, s), cfg.period_us, 400_000) for s in range(8)]
+    assert all(0 not in g for g in got[:3]), got
+    # no transfer time: the fill-drain bubble right after the step is inside too
+    assert loan_window_kinds(steady_state_timeline(cfg, 3), cfg.period_us, 0) == {0, 1}
