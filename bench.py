@@ -1305,6 +1305,16 @@ def main() -> None:
         slow["max"] = interference["pipeline"]["slowdown"]
         slow["noise_floor_stage_compute"] = slow["noise_floor"]
         slow["noise_floor"] = interference["pipeline"]["noise_floor"]
+        if world > 1:
+            # every rank is an independent replica of the same emulated pipeline: the
+            # headline is the mean of the N measurements, each listed
+            per_rank = [None] * world
+            dist.all_gather_object(per_rank, (interference["pipeline"]["slowdown"], interference["pipeline"]["noise_floor"]))
+            slow["per_rank"] = [v[0] for v in per_rank]
+            slow["per_rank_noise_floor"] = [v[1] for v in per_rank]
+            slow["max_over_ranks"] = max(slow["per_rank"])
+            slow["max"] = statistics.mean(slow["per_rank"])
+            slow["noise_floor"] = statistics.mean(x for x in slow["per_rank_noise_floor"] if x is not None)
     yield_stats = yield_latency(steps, by_tag)
     # roofline samples: GEMMs of bubbles that ran at full width -- bubbles no longer than the
     # throttle window, or whose fill ended before the window opened; the
@@ -1413,6 +1423,8 @@ def main() -> None:
                 "Not the emulated stage's own iteration time: its artificial neighbours' fixed arrival times absorb "
                 "its slowdown in its idle gaps (main_job_iteration_slowdown). noise floor = the same composition "
                 "from the two halves of the fill-off iterations"
+                + ("; with N > 1 ranks (independent replicas) the mean of their N measurements "
+                   "(main_job_slowdown_detail.per_rank)" if world > 1 else "")
                 if args.pipeline == "emulated" else
                 "max over pipeline stages (ranks) of mean(fill-on) / mean(fill-off) main-job iteration time - 1"),
             "main_job_iteration_slowdown": interference.get("iteration_slowdown"),
