@@ -24,30 +24,35 @@ constexpr int MAX_NV = 8;  // 8 vectors x 8 bf16 x 32 lanes = 2048 columns
 // issue-bound, not HBM-bound (ncu, BERT-large [16384, 1024]: 69 % issue active, 23 % DRAM
 // throughput), so halving the FP instructions per element is what moves it. x2[j][h] holds
 // columns (j*32 + lane)*8 + 2h, +1.
-template <int NV, bool RMS>
-__device__ __forceinline__ void norm_row_store2(const f32x2 (&x2)[NV][4], int cols, float eps,
-                                                const __nv_bfloat16* gamma, const __nv_bfloat16* beta,
-                                                __nv_bfloat16* y) {
+//
+// FULL (cols == NV * 256, every lane owns NV whole vectors): the per-vector column guards
+// compile away. With them the BERT-large row (NV 4) compiled to 920 SASS instructions per
+// warp: a BSSY/BSYNC pair, predicated pair moves and register spills around every guarded
+// vector, plus an IEEE-division slow path for "/ cols" (replaced by * inv_cols).
+template <int NV, bool RMS, bool FULL>
+__device__ __forceinline__ void norm_row_store2(const f32x2 (&x2)[NV][4], int cols, float inv_cols,
+                                                float eps, const __nv_bfloat16* gamma,
+                                                const __nv_bfloat16* beta, __nv_bfloat16* y) {
   const int lane = lane_id();
   float mean = 0.f;
   if (!RMS) {
     f32x2 s0 = f2_splat(0.f), s1 = f2_splat(0.f);  // two chains for ILP
 #pragma unroll
     for (int j = 0; j < NV; ++j)
-      if ((j * 32 + lane) * 8 < cols) {
+      if (FULL || (j * 32 + lane) * 8 < cols) {
         s0 = f2_add(s0, f2_add(x2[j][0], x2[j][1]));
         s1 = f2_add(s1, f2_add(x2[j][2], x2[j][3]));
       }
     float a, b, c, d;
     f2_unpack(s0, a, b);
     f2_unpack(s1, c, d);
-    mean = warp_sum((a + b) + (c + d)) / (float)cols;
+    mean = warp_sum((a + b) + (c + d)) * inv_cols;
   }
   const f32x2 nm = f2_splat(-mean);
   f32x2 q0 = f2_splat(0.f), q1 = f2_splat(0.f);
 #pragma unroll
   for (int j = 0; j < NV; ++j)
-    if ((j * 32 + lane) * 8 < cols) {
+    if (FULL || (j * 32 + lane) * 8 < cols) {
 #pragma unroll
       for (int h = 0; h < 4; h += 2) {
         const f32x2 d0 = f2_add(x2[j][h], nm), d1 = f2_add(x2[j][h + 1], nm);
@@ -58,11 +63,11 @@ __device__ __forceinline__ void norm_row_store2(const f32x2 (&x2)[NV][4], int co
   float a, b, c, d;
   f2_unpack(q0, a, b);
   f2_unpack(q1, c, d);
-  const f32x2 r2 = f2_splat(rsqrtf(warp_sum((a + b) + (c + d)) / (float)cols + eps));
+  const f32x2 r2 = f2_splat(rsqrtf(warp_sum((a + b) + (c + d)) * inv_cols + eps));
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
     const int col = (j * 32 + lane) * 8;
-    if (col < cols) {
+    if (FULL || col < cols) {
       const uint4 gu = __ldg(reinterpret_cast<const uint4*>(gamma + col));
       uint4 bu = make_uint4(0, 0, 0, 0);
       if (!RMS) bu = __ldg(reinterpret_cast<const uint4*>(beta + col));
@@ -122,14 +127,14 @@ __device__ __forceinline__ void norm_row_store(float (&x)[NV][8], int cols, floa
   }
 }
 
-template <int NV, bool RMS>
+template <int NV, bool RMS, bool FULL>
 __global__ void __launch_bounds__(WARPS * 32, 10) norm_kernel(  // 10 CTAs/SM: 16384 BERT rows in 2.8 waves, not 3.07
     const __nv_bfloat16* __restrict__ X,
                                                           const __nv_bfloat16* __restrict__ R,
                                                           const __nv_bfloat16* __restrict__ gamma,
                                                           const __nv_bfloat16* __restrict__ beta,
                                                           __nv_bfloat16* __restrict__ Y, int rows,
-                                                          int cols, float eps, Ctl ctl) {
+                                                          int cols, float inv_cols, float eps, Ctl ctl) {
   static_assert(ROWS_PER_WARP == 1, "one row per warp");
   pdl_enter();
   const int lane = lane_id();
@@ -142,7 +147,7 @@ __global__ void __launch_bounds__(WARPS * 32, 10) norm_kernel(  // 10 CTAs/SM: 1
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const int c = (j * 32 + lane) * 8;
-      if (c < cols) {
+      if (FULL || c < cols) {
         xa[j] = __ldg(reinterpret_cast<const uint4*>(X + off + c));
         if (R) ra[j] = __ldg(reinterpret_cast<const uint4*>(R + off + c));
       }
@@ -165,7 +170,96 @@ __global__ void __launch_bounds__(WARPS * 32, 10) norm_kernel(  // 10 CTAs/SM: 1
         }
       }
     }
-    norm_row_store2<NV, RMS>(x2, cols, eps, gamma, beta, Y + off);
+    norm_row_store2<NV, RMS, FULL>(x2, cols, inv_cols, eps, gamma, beta, Y + off);
+  }
+  atomic_unit_exit(ctl);
+}
+
+// bf16 pair -> fp32 pair in two integer ops (shl / and) written straight into a register
+// pair, ready for the f32x2 instructions (no PRMT + shift + pair moves).
+__device__ __forceinline__ f32x2 bf2_f2(uint32_t w) {
+  f32x2 r;
+  asm("{\n\t.reg .b32 lo, hi;\n\tshl.b32 lo, %1, 16;\n\tand.b32 hi, %1, 0xffff0000;\n\t"
+      "mov.b64 %0, {lo, hi};\n\t}"
+      : "=l"(r)
+      : "r"(w));
+  return r;
+}
+
+// The BERT LayerNorms (residual already added by the producing GEMM's epilogue) on full
+// rows (cols == NV * 256): the row stays packed bf16 in registers (NV x uint4: 16 registers
+// for 1024 columns instead of 32 fp32) and is re-expanded by bf2_f2 in each of the three
+// passes. Same arithmetic, same order as norm_kernel + norm_row_store2, so bitwise the same
+// output (scripts/ln_bench.py digests). norm_kernel at 10 CTAs/SM (48 registers) spilled
+// 35 times and ran ~690 SASS instructions per 1024-column row; this kernel at 8 CTAs/SM
+// (64 registers, no spills) ~500. B200, [16384, 1024] with the input in L2 (as in situ, right
+// after the producing GEMM): 18.4 -> 12.2 us; from HBM 22.5 -> 18.4 us
+// (profiles/r02/s53_ln_bench.txt). PF_LN_MINB=10 / 0 select the 10-CTA build / norm_kernel.
+template <int NV, bool RMS, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB) norm_packed_kernel(
+    const __nv_bfloat16* __restrict__ X, const __nv_bfloat16* __restrict__ gamma,
+    const __nv_bfloat16* __restrict__ beta, __nv_bfloat16* __restrict__ Y, int rows,
+    float inv_cols, float eps, Ctl ctl) {
+  constexpr int COLS = NV * 256;
+  pdl_enter();
+  const int lane = lane_id();
+  const int row = blockIdx.x * ROWS_PER_CTA + warp_id();
+  const size_t off = (size_t)row * COLS;
+  uint4 xa[NV];
+  if (row < rows) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) xa[j] = __ldg(reinterpret_cast<const uint4*>(X + off + (j * 32 + lane) * 8));
+  }
+  if (!atomic_unit_check(ctl)) return;
+  if (row < rows) {
+    float mean = 0.f;
+    if (!RMS) {
+      f32x2 s0 = f2_splat(0.f), s1 = f2_splat(0.f);
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        s0 = f2_add(s0, f2_add(bf2_f2(xa[j].x), bf2_f2(xa[j].y)));
+        s1 = f2_add(s1, f2_add(bf2_f2(xa[j].z), bf2_f2(xa[j].w)));
+      }
+      float a, b, c, d;
+      f2_unpack(s0, a, b);
+      f2_unpack(s1, c, d);
+      mean = warp_sum((a + b) + (c + d)) * inv_cols;
+    }
+    const f32x2 nm = f2_splat(-mean);
+    f32x2 q0 = f2_splat(0.f), q1 = f2_splat(0.f);
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const uint32_t w[4] = {xa[j].x, xa[j].y, xa[j].z, xa[j].w};
+#pragma unroll
+      for (int h = 0; h < 4; h += 2) {
+        const f32x2 d0 = f2_add(bf2_f2(w[h]), nm), d1 = f2_add(bf2_f2(w[h + 1]), nm);
+        q0 = f2_fma(d0, d0, q0);
+        q1 = f2_fma(d1, d1, q1);
+      }
+    }
+    float a, b, c, d;
+    f2_unpack(q0, a, b);
+    f2_unpack(q1, c, d);
+    const f32x2 r2 = f2_splat(rsqrtf(warp_sum((a + b) + (c + d)) * inv_cols + eps));
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int col = (j * 32 + lane) * 8;
+      const uint4 gu = __ldg(reinterpret_cast<const uint4*>(gamma + col));
+      uint4 bu = make_uint4(0, 0, 0, 0);
+      if (!RMS) bu = __ldg(reinterpret_cast<const uint4*>(beta + col));
+      const uint32_t w[4] = {xa[j].x, xa[j].y, xa[j].z, xa[j].w};
+      const uint32_t gw[4] = {gu.x, gu.y, gu.z, gu.w};
+      const uint32_t bw[4] = {bu.x, bu.y, bu.z, bu.w};
+      uint32_t o[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const f32x2 t = f2_mul(f2_add(bf2_f2(w[h]), nm), r2);
+        float lo, hi;
+        f2_unpack(f2_fma(t, bf2_f2(gw[h]), bf2_f2(bw[h])), lo, hi);
+        o[h] = pack_bf16x2(lo, hi);
+      }
+      *reinterpret_cast<uint4*>(Y + off + col) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
   }
   atomic_unit_exit(ctl);
 }
@@ -293,15 +387,31 @@ struct NormOp final : PreparedOp {
   uint32_t units() const override { return (uint32_t)grid_for(rows); }
   bool resumable() const override { return false; }
   int run(const pf_ctl_t* ctl, cudaStream_t s, const LaunchArgs&) override {
-    if (rms) {
-      PF_NV_DISPATCH(nv_for(cols), PF_CUDA(launch_pdl(norm_kernel<NV, true>, dim3(grid_for(rows)),
-                                                      dim3(WARPS * 32), 0, s, x, r, g, nullptr, y,
-                                                      rows, cols, eps, make_ctl(ctl))));
+    const float inv_cols = 1.f / (float)cols;
+    const bool full = cols % 256 == 0;
+    const __nv_bfloat16* bb = rms ? nullptr : b;
+#define PF_NORM_LAUNCH(RMSV, FULLV)                                                             \
+  PF_NV_DISPATCH(nv_for(cols), PF_CUDA(launch_pdl(norm_kernel<NV, RMSV, FULLV>, dim3(grid_for(rows)), \
+                                                  dim3(WARPS * 32), 0, s, x, r, g, bb, y, rows, cols, \
+                                                  inv_cols, eps, make_ctl(ctl))))
+    static const int minb = getenv("PF_LN_MINB") ? atoi(getenv("PF_LN_MINB")) : 8;  // 0: norm_kernel
+    if (full && !r && minb != 0) {  // the packed full-row kernel (the BERT LayerNorms)
+#define PF_NORM_PACKED(RMSV, MB)                                                                  \
+  PF_NV_DISPATCH(nv_for(cols), PF_CUDA(launch_pdl(norm_packed_kernel<NV, RMSV, MB>, dim3(grid_for(rows)), \
+                                                  dim3(WARPS * 32), 0, s, x, g, bb, y, rows, inv_cols,  \
+                                                  eps, make_ctl(ctl))))
+      if (minb == 8) {
+        if (rms) { PF_NORM_PACKED(true, 8); } else { PF_NORM_PACKED(false, 8); }
+      } else {
+        if (rms) { PF_NORM_PACKED(true, 10); } else { PF_NORM_PACKED(false, 10); }
+      }
+#undef PF_NORM_PACKED
+    } else if (rms) {
+      if (full) { PF_NORM_LAUNCH(true, true); } else { PF_NORM_LAUNCH(true, false); }
     } else {
-      PF_NV_DISPATCH(nv_for(cols), PF_CUDA(launch_pdl(norm_kernel<NV, false>, dim3(grid_for(rows)),
-                                                      dim3(WARPS * 32), 0, s, x, r, g, b, y, rows,
-                                                      cols, eps, make_ctl(ctl))));
+      if (full) { PF_NORM_LAUNCH(false, true); } else { PF_NORM_LAUNCH(false, false); }
     }
+#undef PF_NORM_LAUNCH
     PF_CUDA(cudaGetLastError());
     return PF_OK;
   }
