@@ -85,6 +85,7 @@ FILL_FRACTION_NCCL = 0.95
 COOLDOWN_MS = 25.0
 THROTTLE_MS = 60.0
 THROTTLE_CTAS = 64
+SHORT_CTAS = 0
 TAIL_MIN_MS = None
 TAIL_FRAC = 1.0
 TAIL_FROM_FRAC = 0.0
@@ -705,6 +706,7 @@ def set_tail(engine, args) -> None:
     engine.throttle_ctas = args.throttle_ctas
     engine.throttle_min_ns = int(tail_min_ms(args) * 1e6)
     engine.throttle_frac = args.tail_frac
+    engine.short_ctas = args.short_ctas
 
 
 def measure_interference(args, stages, run_block, local, pcfg) -> dict:
@@ -878,6 +880,8 @@ def main() -> None:
     ap.add_argument("--throttle-ms", type=float, default=THROTTLE_MS,
                     help="throttle the fill to --throttle-ctas CTAs this long before every bubble's end")
     ap.add_argument("--throttle-ctas", type=int, default=THROTTLE_CTAS)
+    ap.add_argument("--short-ctas", type=int, default=SHORT_CTAS,
+                    help="bubbles not longer than the tail threshold run whole on this many CTAs (0: all)")
     ap.add_argument("--tail-min-ms", type=float, default=TAIL_MIN_MS,
                     help="bubbles no longer than this get no power tail (default: --throttle-ms)")
     ap.add_argument("--late-cooldown-ms", type=float, default=LATE_COOLDOWN_MS,
@@ -1405,7 +1409,7 @@ def main() -> None:
                          "max_batches_per_bubble": conf.get("max_batches", 16),
                          "fill_fraction": args.fill_fraction, "cooldown_ms": args.cooldown_ms,
                          "throttle_ms": args.throttle_ms, "throttle_ctas": args.throttle_ctas,
-                         "tail_min_ms": tail_min_ms(args), "tail_frac": args.tail_frac,
+                         "tail_min_ms": tail_min_ms(args), "tail_frac": args.tail_frac, "short_ctas": args.short_ctas,
                          "tail_from_frac": args.tail_from_frac, "late_cooldown_ms": args.late_cooldown_ms,
                          "arena_bytes": arena_bytes,
                          "plans": {str(s): pf.plan_to_dict(c.executables[f"fill-{s}"]) for s, c in coords.items()}},

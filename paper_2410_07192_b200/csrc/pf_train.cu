@@ -182,24 +182,24 @@ __device__ __forceinline__ void sum_partials(const float* __restrict__ partial, 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double a = 0.0, b = 0.0;
   if (c < C) {
-    // loads of 4 partial rows in flight per warp, accumulated in row order (deterministic)
+    // loads of 8 partial rows in flight per warp (predicated), accumulated in row order
+    // (deterministic): the 592 rows of a 4-CTAs-per-SM colstats grid over 32 warps are 3
+    // rounds of L2 latency instead of ~6 with 4 in flight (the kernel is latency-bound:
+    // tiny grids, ~10 us each; 16 in flight spills at the 64-register budget of FT = 1024)
     int p = w;
-    for (; p + 3 * (FT / 32) < P; p += 4 * (FT / 32)) {
-      float x[4], y[4];
+    for (; p < P; p += 8 * (FT / 32)) {
+      float x[8], y[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        x[u] = partial[(size_t)(p + u * (FT / 32)) * 2 * C + c];
-        y[u] = partial[(size_t)(p + u * (FT / 32)) * 2 * C + C + c];
+      for (int u = 0; u < 8; ++u) {
+        const int q = p + u * (FT / 32);
+        x[u] = q < P ? partial[(size_t)q * 2 * C + c] : 0.f;
+        y[u] = q < P ? partial[(size_t)q * 2 * C + C + c] : 0.f;
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         a += x[u];
         b += y[u];
       }
-    }
-    for (; p < P; p += FT / 32) {
-      a += partial[(size_t)p * 2 * C + c];
-      b += partial[(size_t)p * 2 * C + C + c];
     }
   }
   red[0][w][lane] = a;

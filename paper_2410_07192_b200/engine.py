@@ -456,6 +456,7 @@ class StageEngine:
         self.throttle_ctas = 0
         self.throttle_min_ns = None  # bubbles shorter than this are not throttled (None: throttle_ns)
         self.throttle_frac = 1.0  # a bubble's throttled tail is at most this share of it
+        self.short_ctas = 0  # bubbles not longer than throttle_min_ns run whole on this many CTAs (0: full)
         self.timer = torch.cuda.Stream(priority=hi)
 
     def set_anchor(self, lead_ms: float = 5.0) -> None:
@@ -488,14 +489,12 @@ class StageEngine:
                 start_ev = torch.cuda.Event()
                 start_ev.record(comm)
                 clear_idx = self.words.n
-                tail = _throttle_tail(self, (end_us - start_us) * US)
+                tail, ctas = _throttle_tail(self, (end_us - start_us) * US)
                 if fill and tail > 0:
-                    # the bubble's last `tail` ns run throttled (bubbles shorter than the
-                    # threshold not at all: DESIGN.md §5.1)
+                    # the bubble's last `tail` ns run throttled
                     self.timer.wait_event(start_ev)
                     native.call("pf_flag_throttle_at", flag, self.words.anchor.data_ptr(),
-                                int(base + end_us * US - tail), int(self.throttle_ctas),
-                                self.timer.cuda_stream)
+                                int(base + end_us * US - tail), int(ctas), self.timer.cuda_stream)
                     self.launches += 1
                 self.link.bubble_end(base + end_us * US, self.words.stamp_ptr())
                 end_ev = torch.cuda.Event()
@@ -597,15 +596,18 @@ class StageEngine:
 OP_PROBE_NS = 4000  # SM-clock probe before every stamped op (4 us of one thread)
 
 
-def _throttle_tail(engine, duration_ns: int) -> int:
-    """Throttled tail (ns) of a bubble of `duration_ns`: min(throttle_ns, throttle_frac x
-    duration) for bubbles longer than throttle_min_ns (default: throttle_ns), else 0."""
+def _throttle_tail(engine, duration_ns: int) -> tuple[int, int]:
+    """(throttled tail in ns, CTAs) of a bubble of `duration_ns`: min(throttle_ns,
+    throttle_frac x duration) on throttle_ctas for bubbles longer than throttle_min_ns
+    (default: throttle_ns); shorter bubbles run whole on short_ctas when that is set (too
+    short for an idle tail to let the clock recover), else unthrottled."""
     if engine.throttle_ns <= 0 or engine.throttle_ctas < 2 or duration_ns <= 0:
-        return 0
+        return 0, 0
     lo = engine.throttle_ns if engine.throttle_min_ns is None else engine.throttle_min_ns
     if duration_ns <= lo:
-        return 0
-    return int(min(engine.throttle_ns, engine.throttle_frac * duration_ns))
+        short = getattr(engine, "short_ctas", 0)
+        return (int(duration_ns), short) if short >= 2 else (0, 0)
+    return int(min(engine.throttle_ns, engine.throttle_frac * duration_ns)), engine.throttle_ctas
 
 
 def op_timing(st: torch.Tensor, rec: IterationRecord) -> dict:
@@ -726,6 +728,7 @@ class NcclPipelineEngine:
         self.throttle_ctas = 0
         self.throttle_min_ns = None
         self.throttle_frac = 1.0
+        self.short_ctas = 0
         self.expected_ns: dict[int, int] = {}
         self.timer = torch.cuda.Stream(priority=hi)
 
@@ -765,11 +768,11 @@ class NcclPipelineEngine:
         start_ev.record(self.comm)
         k = 0 if kind is BubbleKind.FWD_BWD else 1
         exp = self.expected_ns.get(k, 0)
-        tail = _throttle_tail(self, exp)
+        tail, ctas = _throttle_tail(self, exp)
         if fill and tail > 0:
             self.timer.wait_event(start_ev)
             native.call("pf_flag_throttle_at", flag, self.words.stamps.data_ptr() + 8 * set_idx,
-                        int(exp - tail), int(self.throttle_ctas), self.timer.cuda_stream)
+                        int(exp - tail), int(ctas), self.timer.cuda_stream)
             self.launches += 1
         got = None
         if end_recv is not None:

@@ -87,7 +87,10 @@ def test_power_tail_rules():
 
     class E:
         throttle_ns, throttle_ctas, throttle_min_ns, throttle_frac = 50_000_000, 64, None, 1.0
-    assert _throttle_tail(E, 40_000_000) == 0  # shorter than the window: not throttled
-    assert _throttle_tail(E, 120_000_000) == 50_000_000
+    assert _throttle_tail(E, 40_000_000) == (0, 0)  # shorter than the window: not throttled
+    assert _throttle_tail(E, 120_000_000) == (50_000_000, 64)
+    E.short_ctas = 32  # ... unless short bubbles run whole on fewer CTAs
+    assert _throttle_tail(E, 40_000_000) == (40_000_000, 32)
+    E.short_ctas = 0
     E.throttle_min_ns, E.throttle_frac = 20_000_000, 0.6
-    assert _throttle_tail(E, 40_000_000) == 24_000_000
+    assert _throttle_tail(E, 40_000_000) == (24_000_000, 64)
