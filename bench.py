@@ -1320,17 +1320,20 @@ def main() -> None:
             slow["max"] = statistics.mean(slow["per_rank"])
             slow["noise_floor"] = statistics.mean(x for x in slow["per_rank_noise_floor"] if x is not None)
     yield_stats = yield_latency(steps, by_tag)
-    # roofline samples: GEMMs of bubbles that ran at full width -- bubbles no longer than the
-    # throttle window, or whose fill ended before the window opened; the
-    # throttled tail's GEMMs run on throttle_ctas of the 148 SMs by design
-    thr_ns = int(args.throttle_ms * 1e6)
-    full_width = set()
+    # roofline samples: GEMM launches that ran at full width, i.e. ended before their bubble's
+    # throttled part began: the tail of a long bubble and the whole of a
+    # short one run on throttle_ctas / short_ctas of the 148 SMs by design. Samples are the
+    # first and the last batch of every bubble (in-kernel %globaltimer stamps).
+    from paper_2410_07192_b200.engine import _throttle_tail
+
+    throttle_start = {}
     for t in steps:
+        eng = engines.get(t["stage"]) if isinstance(engines, dict) else None
         for kind, t_set, t_clr, tag in t["bubbles"]:
-            r = by_tag.get(tag)
-            if r is not None and (thr_ns <= 0 or t_clr - t_set <= thr_ns or r.fill_end_ns <= t_clr - thr_ns):
-                full_width.add(tag)
-    gemm_full = [g for g in executor.gemm_samples if g[2] in full_width]
+            tail = _throttle_tail(eng, t_clr - t_set)[0] if eng is not None else 0
+            throttle_start[tag] = t_clr - tail
+    gemm_full = [g for g in executor.gemm_samples
+                 if len(g) > 5 and g[2] in throttle_start and g[5] <= throttle_start[g[2]]]
     gemm_all = list(executor.gemm_samples)
     stats = FillStats(
         sample_equivalents=sum(r.sample_eq for r in recs),
@@ -1463,8 +1466,8 @@ def main() -> None:
                          "kernel": "pf_gemm (tcgen05)", "launches_timed": gemm_launches,
                          "by_batch_size": gemm_by_batch,
                          "sampling": "in-kernel %globaltimer span (first CTA start -> last working CTA end) of "
-                                     "every GEMM node of the last batch of each completed bubble that ran at "
-                                     "full width (not in the throttled bubble tail)",
+                                     "every GEMM node of the first and the last batch of each bubble, kept when "
+                                     "it ended before the bubble's throttled part began (full width: 148 SMs)",
                          **gemm_launch_roofline(gemm_full, peaks),
                          "achieved_incl_throttled_tail": gemm_all_tflops,
                          "launches_incl_throttled_tail": len(gemm_all),

@@ -180,7 +180,8 @@ class Executor:
         self.timing = False  # live per-GEMM device timing (bench roofline)
         # (flops, ms, bubble tag, batch size, minimum DRAM bytes) of every GEMM node of the last
         # batch of each completed bubble (in-kernel stamps)
-        self.gemm_samples: list[tuple[float, float, object, int, float]] = []
+        # (FLOPs, ms, bubble tag, batch size, bytes, end %globaltimer ns) per timed GEMM node
+        self.gemm_samples: list[tuple] = []
         # called when the executor runs out of work at a bubble: returns the next
         # (WorkItem, model) from the stage's Coordinator, or None
         self.work_source: Optional[Callable[[], Optional[tuple[WorkItem, FillSequential]]]] = None
@@ -189,6 +190,10 @@ class Executor:
         self._gated: dict[int, ctypes.c_void_p] = {}
         self._ahead_staging: Optional[int] = None  # index in self.stagings of the last run-ahead copy
         self._stamps_host = PinnedBuffer((MAX_NODES, 2), torch.int64)
+        # timing mode: the GEMM stamps of each bubble's FIRST batch, copied out right after it
+        # (before batch 2 overwrites the chain's stamp slots): with the power-aware tail a
+        # long bubble's last batch runs throttled, its first at full width
+        self._stamps_first_host = PinnedBuffer((MAX_NODES, 2), torch.int64)
         self._chains: dict[tuple[int, int], _Chain] = {}
         self._staged_event: Optional[torch.cuda.Event] = None
         self._staged_part: Optional[int] = None
@@ -879,6 +884,9 @@ class Executor:
                 else:
                     native.call("pf_chain_graph_launch", ch.h, st.cuda_stream)
                     launches += len(ch.units) + len(ch.seg_ends) + 2
+                if k == 0 and node == 0 and self.timing and len(batches) > 1 and ch.gemm_flops:
+                    native.call("pf_stage_d2h", self._stamps_first_host.ptr, self._stamps.data_ptr(),
+                                16 * len(ch.units), st.cuda_stream)
             native.call("pf_read_globaltimer", base + 40, st.cuda_stream)
             launches += 2
         ev = torch.cuda.Event()
@@ -1397,6 +1405,16 @@ class Executor:
         pr = self.progress
         rec = BubbleRecord(pend.slot.index, len(pend.batches), done, 0, aborted, int(ts[0]), int(ts[1]),
                            pend.launches, pend.part, self._flops_frac[pend.part], tag=pend.slot.tag)
+        if self.timing and done > 0 and len(pend.batches) > 1 and pend.batches[0][2] == 0:
+            # the first batch's GEMM stamps (copied out after it ran, see fill)
+            ch0 = self._chains.get(((pend.parts or [pend.part])[0], pend.batches[0][1], pend.slot.flag_ptr or None))
+            if ch0 is not None and ch0.gemm_flops:
+                sh = self._stamps_first_host.tensor
+                for node, fl in ch0.gemm_flops.items():
+                    t0, t1 = int(sh[node, 0]), int(sh[node, 1])
+                    if 0 < t0 < t1:
+                        self.gemm_samples.append((fl, (t1 - t0) / 1e6, pend.slot.tag, pend.batches[0][1],
+                                                  ch0.gemm_bytes.get(node, 0.0), t1))
         if self.timing and done > 0 and not aborted:
             # in-kernel stamps of the bubble's last batch: (FLOPs, ms) of every GEMM node
             last_cnt = pend.batches[len(pend.batches) - 1][1]
@@ -1412,7 +1430,7 @@ class Executor:
                     t0, t1 = int(sh[node, 0]), int(sh[node, 1])
                     if 0 < t0 < t1:
                         self.gemm_samples.append((fl, (t1 - t0) / 1e6, pend.slot.tag, last_cnt,
-                                                  ch.gemm_bytes.get(node, 0.0)))
+                                                  ch.gemm_bytes.get(node, 0.0), t1))
         n_total = self.item.entry.size
         samples = 0
         parts = pend.parts or [pend.part] * len(pend.batches)
@@ -1540,7 +1558,7 @@ class Executor:
         self._layouts = {}
         self._chains = {}
         self._gated = {}
-        for buf in (self._ctl_host, self._desc_host, self._stamps_host):
+        for buf in (self._ctl_host, self._desc_host, self._stamps_host, self._stamps_first_host):
             buf.close()
         self.arena.close()
 
