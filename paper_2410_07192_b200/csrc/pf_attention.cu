@@ -68,6 +68,10 @@ __device__ __forceinline__ bool mbar_try_wait_hint(uint64_t* bar, uint32_t parit
   return done != 0;
 }
 
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
 __device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 #ifdef PF_ATT_DIAG
@@ -245,7 +249,9 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
       const int b = u / heads;
       const float* mrow = mask_add ? mask_add + (size_t)b * seq : nullptr;
       const uint32_t tS = tmem + lane_base + s * 128 + half * 64;
-      uint8_t* blk = smem + s * STAGE_BYTES + half * TILE_BYTES + row * 128;  // K-block `half`
+      // K-block `half` of P, as a shared-window address: explicit st.shared (STS) instead of
+      // generic stores (ST.E), which ncu showed stalling the softmax warps
+      const uint32_t blk_s = smem_u32(smem + s * STAGE_BYTES + half * TILE_BYTES + row * 128);
       float sum = 0.f;
       if constexpr (FULL) {
         // max of the raw scores (scale > 0 commutes with max), then p = 2^(s*c - max*c)
@@ -281,8 +287,8 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int chunk = c * 4 + q;
-            *reinterpret_cast<uint4*>(blk + ((chunk ^ (row & 7)) << 4)) =
-                make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+            st_shared_v4(blk_s + ((chunk ^ (row & 7)) << 4), packed[4 * q], packed[4 * q + 1],
+                         packed[4 * q + 2], packed[4 * q + 3]);
           }
         }
       } else {
@@ -326,8 +332,8 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int chunk = c * 4 + q;
-            *reinterpret_cast<uint4*>(blk + ((chunk ^ (row & 7)) << 4)) =
-                make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+            st_shared_v4(blk_s + ((chunk ^ (row & 7)) << 4), packed[4 * q], packed[4 * q + 1],
+                         packed[4 * q + 2], packed[4 * q + 3]);
           }
         }
       }
