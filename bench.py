@@ -707,6 +707,7 @@ def set_tail(engine, args) -> None:
     engine.throttle_min_ns = int(tail_min_ms(args) * 1e6)
     engine.throttle_frac = args.tail_frac
     engine.short_ctas = args.short_ctas
+    engine.short_window_ns = None if args.short_window_ms is None else int(args.short_window_ms * 1e6)
 
 
 def measure_interference(args, stages, run_block, local, pcfg) -> dict:
@@ -880,6 +881,8 @@ def main() -> None:
     ap.add_argument("--throttle-ms", type=float, default=THROTTLE_MS,
                     help="throttle the fill to --throttle-ctas CTAs this long before every bubble's end")
     ap.add_argument("--throttle-ctas", type=int, default=THROTTLE_CTAS)
+    ap.add_argument("--short-window-ms", type=float, default=None,
+                    help="throttle only the last this-many ms of a short bubble (default: all of it)")
     ap.add_argument("--short-ctas", type=int, default=SHORT_CTAS,
                     help="bubbles not longer than the tail threshold run whole on this many CTAs (0: all)")
     ap.add_argument("--tail-min-ms", type=float, default=TAIL_MIN_MS,
@@ -1412,7 +1415,7 @@ def main() -> None:
                          "max_batches_per_bubble": conf.get("max_batches", 16),
                          "fill_fraction": args.fill_fraction, "cooldown_ms": args.cooldown_ms,
                          "throttle_ms": args.throttle_ms, "throttle_ctas": args.throttle_ctas,
-                         "tail_min_ms": tail_min_ms(args), "tail_frac": args.tail_frac, "short_ctas": args.short_ctas,
+                         "tail_min_ms": tail_min_ms(args), "tail_frac": args.tail_frac, "short_ctas": args.short_ctas, "short_window_ms": args.short_window_ms,
                          "tail_from_frac": args.tail_from_frac, "late_cooldown_ms": args.late_cooldown_ms,
                          "arena_bytes": arena_bytes,
                          "plans": {str(s): pf.plan_to_dict(c.executables[f"fill-{s}"]) for s, c in coords.items()}},

@@ -457,6 +457,7 @@ class StageEngine:
         self.throttle_min_ns = None  # bubbles shorter than this are not throttled (None: throttle_ns)
         self.throttle_frac = 1.0  # a bubble's throttled tail is at most this share of it
         self.short_ctas = 0  # bubbles not longer than throttle_min_ns run whole on this many CTAs (0: full)
+        self.short_window_ns = None  # ... or only their last short_window_ns
         self.timer = torch.cuda.Stream(priority=hi)
 
     def set_anchor(self, lead_ms: float = 5.0) -> None:
@@ -606,7 +607,9 @@ def _throttle_tail(engine, duration_ns: int) -> tuple[int, int]:
     lo = engine.throttle_ns if engine.throttle_min_ns is None else engine.throttle_min_ns
     if duration_ns <= lo:
         short = getattr(engine, "short_ctas", 0)
-        return (int(duration_ns), short) if short >= 2 else (0, 0)
+        window = getattr(engine, "short_window_ns", None)
+        span = int(duration_ns) if window is None else int(min(duration_ns, window))
+        return (span, short) if short >= 2 else (0, 0)
     return int(min(engine.throttle_ns, engine.throttle_frac * duration_ns)), engine.throttle_ctas
 
 
@@ -729,6 +732,7 @@ class NcclPipelineEngine:
         self.throttle_min_ns = None
         self.throttle_frac = 1.0
         self.short_ctas = 0
+        self.short_window_ns = None
         self.expected_ns: dict[int, int] = {}
         self.timer = torch.cuda.Stream(priority=hi)
 
