@@ -50,7 +50,10 @@ CONFIGS = {
            "batch_sizes": FILL_BATCH_SIZES, "arena_cap": 24 << 30, "chunk": 16384, "rotate": True},
     # configs[0]: the reference's CPU-runnable case, on the GPU
     "c1": {"stages": 4, "micro": 8, "schedule": "1f1b", "main": "gpt2small", "fill": "bert_base",
-           "batch_sizes": (32,), "arena_cap": 24 << 30, "chunk": 16384, "rotate": True},
+           "batch_sizes": (32,), "arena_cap": 24 << 30, "chunk": 16384, "rotate": True,
+           # the 124M-parameter main job never reaches the power cap (untailed fill: -0.1 %
+           # slowdown), so its short bubbles are filled at full width
+           "short_ctas": 0},
     # configs[2]: fill weights (0.67 GB) exceed the bubble free memory given to the fill job.
     # A rank stays on one stage ((rank + 3) mod 8: stage 3 at N=1 has both bubble kinds)
     # so a range progresses through the plan's partitions across iterations.
@@ -883,8 +886,9 @@ def main() -> None:
     ap.add_argument("--throttle-ctas", type=int, default=THROTTLE_CTAS)
     ap.add_argument("--short-window-ms", type=float, default=None,
                     help="throttle only the last this-many ms of a short bubble (default: all of it)")
-    ap.add_argument("--short-ctas", type=int, default=SHORT_CTAS,
-                    help="bubbles not longer than the tail threshold run whole on this many CTAs (0: all)")
+    ap.add_argument("--short-ctas", type=int, default=None,
+                    help="bubbles not longer than the tail threshold run whole on this many CTAs (0: all; "
+                         f"default {SHORT_CTAS}, c1: 0)")
     ap.add_argument("--tail-min-ms", type=float, default=TAIL_MIN_MS,
                     help="bubbles no longer than this get no power tail (default: --throttle-ms)")
     ap.add_argument("--late-cooldown-ms", type=float, default=LATE_COOLDOWN_MS,
@@ -909,6 +913,8 @@ def main() -> None:
     if args.fill_fraction is None:
         args.fill_fraction = FILL_FRACTION_NCCL if args.pipeline == "nccl" else FILL_FRACTION
     conf = dict(CONFIGS[args.config])
+    if args.short_ctas is None:
+        args.short_ctas = conf.get("short_ctas", SHORT_CTAS)
     if args.max_batches is not None:
         conf["max_batches"] = args.max_batches
     if args.stage is not None:
