@@ -91,6 +91,10 @@ def test_power_tail_rules():
     assert _throttle_tail(E, 120_000_000) == (50_000_000, 64)
     E.short_ctas = 32  # ... unless short bubbles run whole on fewer CTAs
     assert _throttle_tail(E, 40_000_000) == (40_000_000, 32)
-    E.short_ctas = 0
+    E.short_window_ns = 30_000_000  # ... or only their last 30 ms
+    assert _throttle_tail(E, 40_000_000) == (30_000_000, 32)
+    assert _throttle_tail(E, 20_000_000) == (20_000_000, 32)
+    assert _throttle_tail(E, 120_000_000) == (50_000_000, 64)  # long bubbles: unchanged
+    E.short_ctas, E.short_window_ns = 0, None
     E.throttle_min_ns, E.throttle_frac = 20_000_000, 0.6
     assert _throttle_tail(E, 40_000_000) == (24_000_000, 64)
