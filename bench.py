@@ -550,6 +550,8 @@ def run_training_depths(args, conf) -> None:
             pcfg = pf.PipelineConfig(P, conf["micro"], tf_ms, tb_ms, pf.ScheduleKind.ONE_F_ONE_B, plan_mem,
                                      plan_mem, args.fill_fraction)
             engines = {s_: StageEngine(pcfg, s_, main_model, executor, streams=streams) for s_ in range(P)}
+            for e_ in engines.values():
+                e_.op_stamps = True  # per-op stamps for the composed slowdown
             models = {s_: resnet50_train(seed=s_, partitioned=part) for s_ in range(P)}
             for m_ in models.values():
                 m_.profile = profile
@@ -629,10 +631,47 @@ def run_training_depths(args, conf) -> None:
                 device_s=sum(t["step_end"] - t["start"] for t in steps) / 1e9)
             tot = aggregate(st, device=torch.device("cuda", local))
             stats_all.append(tot)
+
+            def run_block(s_: int, modes: list) -> list[dict]:
+                """Consecutive iterations of stage s_ from one anchor, fill on or off per
+                iteration (as for configs[1]); the executor holds stage s_'s training job."""
+                if current["stage"] != s_:
+                    executor.settle()
+                    nxt = next_work(s_) if items.get(s_) is None else (items[s_], models[s_])
+                    if nxt is not None:
+                        executor.load(*nxt)
+                    executor.prewarm(engines[s_].words.flag.value)
+                    executor.work_source = lambda s__=s_: next_work(s__)
+                    current["stage"] = s_
+                    torch.cuda.synchronize()
+                eng = engines[s_]
+                executor.settle()
+                eng.reset_stamps()
+                eng.set_anchor()
+                recs_ = [eng.run_iteration(i, fill=(m == "on")) for i, m in enumerate(modes)]
+                executor.settle()
+                out = []
+                for r_ in recs_:
+                    t = eng.record_timing(r_)
+                    t["stage"] = s_
+                    out.append(t)
+                return out
+
+            # main-job slowdown as for configs[1]: the p-stage pipeline composed from per-op
+            # device times, fill on vs off (the per-stage iteration time of the emulation hides
+            # a stage's slowdown in its idle gaps); after the timed region
+            interf = measure_interference(args, list(range(P)), run_block, local, pcfg)
+            comp = interf.get("pipeline") or {}
             results[str(P)] = {
                 "images_per_s": tot.value, "bubble_time_filled": tot.bubble_filled,
                 "bubble_time_filled_of_total_idle": tot.idle_filled,
-                "main_job_slowdown": slowdown_stats(on_iter, off)["max"],
+                "main_job_slowdown": comp.get("slowdown"),
+                "main_job_slowdown_noise_floor": comp.get("noise_floor"),
+                "main_job_slowdown_definition": "composed p-stage pipeline iteration time from per-op device "
+                                                "stamps, fill on / off - 1 (DESIGN.md §5.1)",
+                "main_job_slowdown_stage_compute": interf["slowdown"],
+                "interference_per_stage": interf["per_stage"],
+                "main_job_iteration_slowdown": slowdown_stats(on_iter, off),
                 "main_job_slowdown_detail": slowdown_stats(on_iter, off),
                 "gemm_tflops_in_situ": tot.gemm_tflops, "gemm_launch_roofline": launch_roof,
                 "sgd_steps": int(sum(r_.batches_done for r_ in recs)),
@@ -664,6 +703,8 @@ def run_training_depths(args, conf) -> None:
             "per_pipeline_depth": results,
             "bubble_time_filled": deepest["bubble_time_filled"],
             "main_job_slowdown": deepest["main_job_slowdown"],
+            "main_job_slowdown_definition": deepest["main_job_slowdown_definition"],
+            "main_job_slowdown_per_depth": {d_: r_["main_job_slowdown"] for d_, r_ in results.items()},
             "roofline": {"bound": "tensor", "achieved": deepest["gemm_tflops_in_situ"], "peak": peak,
                          "unit": "TFLOP/s", "frac": deepest["gemm_tflops_in_situ"] / peak, "traffic": None,
                          "kernel": "pf_gemm + pf_gemm_splitk (tcgen05)",
