@@ -88,7 +88,7 @@ FILL_FRACTION_NCCL = 0.95
 COOLDOWN_MS = 25.0
 THROTTLE_MS = 60.0
 THROTTLE_CTAS = 64
-SHORT_CTAS = 48  # bubbles <= the tail threshold run whole on 48 CTAs (round 2)
+SHORT_CTAS = 32  # bubbles <= the tail threshold run whole on 32 CTAs (round 2)
 TAIL_MIN_MS = None
 TAIL_FRAC = 1.0
 TAIL_FROM_FRAC = 0.0
