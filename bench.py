@@ -82,9 +82,11 @@ FILL_FRACTION_NCCL = 0.95
 # Power-aware bubble tail: the main job runs power-capped; after an idle bubble the
 # board's power controller lets it start at up to 1965 MHz, after a bubble filled at full power at
 # ~1600. The last THROTTLE_MS of every bubble longer than that run on THROTTLE_CTAS CTAs and the
-# last COOLDOWN_MS idle. Measured on B200 (profiles/r02_power_sweep.md): composed 8-stage
-# main-job slowdown +3.5-4.6 % without; with a tail of 50-60 ms at 48-64 CTAs and 15-25 ms idle about
-# +2 % (run-to-run spread +-0.7 points), at ~16 % less fill (profiles/r02/power_sweep.md).
+# last COOLDOWN_MS idle; shorter bubbles run whole on SHORT_CTAS CTAs (an untailed short bubble
+# leaves the clock depressed for the ~60 ms of main-job compute after it). Measured on B200:
+# composed 8-stage main-job slowdown +3.5-4.6 % without any policy; with the tail alone +1.5 to
+# +2.9 % (profiles/r02/power_sweep.md); with short bubbles on 32 CTAs too +0.99 to +1.76 %
+# (8 runs, profiles/r02/final5, short/), at ~26 % less fill than without any policy.
 COOLDOWN_MS = 25.0
 THROTTLE_MS = 60.0
 THROTTLE_CTAS = 64
