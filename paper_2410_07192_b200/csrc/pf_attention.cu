@@ -271,6 +271,10 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
         s_red[half][row] = mx;
         softmax_bar();
         const float nmx = -fmaxf(s_red[0][row], s_red[1][row]) * scale_log2;
+        // exponent arguments and row sums on packed fp32 pairs (FFMA2 / FADD2): two FP
+        // instructions per key pair instead of four around the two MUFU.EX2
+        const f32x2 sc2 = f2_splat(scale_log2), nm2 = f2_splat(nmx);
+        f32x2 sum2 = f2_splat(0.f);
 #pragma unroll 1
         for (int c = 0; c < 2; ++c) {
           uint32_t r[32];
@@ -279,9 +283,10 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
           uint32_t packed[16];
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
-            const float p0 = fast_ex2(fmaf(__uint_as_float(r[j]), scale_log2, nmx));
-            const float p1 = fast_ex2(fmaf(__uint_as_float(r[j + 1]), scale_log2, nmx));
-            sum += p0 + p1;
+            float a0, a1;
+            f2_unpack(f2_fma(f2_pack(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), sc2, nm2), a0, a1);
+            const float p0 = fast_ex2(a0), p1 = fast_ex2(a1);
+            sum2 = f2_add(sum2, f2_pack(p0, p1));
             packed[j / 2] = pack_bf16x2(p0, p1);
           }
 #pragma unroll
@@ -290,6 +295,11 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
             st_shared_v4(blk_s + ((chunk ^ (row & 7)) << 4), packed[4 * q], packed[4 * q + 1],
                          packed[4 * q + 2], packed[4 * q + 3]);
           }
+        }
+        {
+          float lo, hi;
+          f2_unpack(sum2, lo, hi);
+          sum = lo + hi;
         }
       } else {
         float mx = -INFINITY;
