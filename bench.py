@@ -354,6 +354,7 @@ def run_service_sweep(args, conf) -> None:
     from paper_2410_07192_b200.fillmodels import BERT_BASE, BERT_LARGE, bert, resnet50
     from paper_2410_07192_b200.metrics import slowdown_stats
     from paper_2410_07192_b200.profiler import measure_profile
+    from paper_2410_07192_b200.schedule import with_cooldown
     from paper_2410_07192_b200.service import (FillService, ServiceConfig, predict, write_plan, write_report,
                                                write_sweep)
 
@@ -373,6 +374,8 @@ def run_service_sweep(args, conf) -> None:
     streams = (torch.cuda.Stream(priority=hi_prio), torch.cuda.Stream(priority=hi_prio))
     pcfg = pf.PipelineConfig(P, M, tf_ms, tb_ms, pf.ScheduleKind.ONE_F_ONE_B, 1, 1, args.fill_fraction)
     engines = [StageEngine(pcfg, s, main_model, None, streams=streams) for s in range(P)]
+    for e_ in engines:
+        set_tail(e_, args)  # the power-aware policy of configs[1]
     period_s = pcfg.period_us / 1e6
     jobs = [pf.JobSpec(f"j{i}-{name}", a * period_s, profiles[name], pf.JobKind.BATCH_INFERENCE, n)
             for i, (name, n, a) in enumerate(conf["jobs"])]
@@ -403,6 +406,10 @@ def run_service_sweep(args, conf) -> None:
             cap = int(cap_gb * 2**30)
             ccfg = pf.PipelineConfig(P, M, tf_ms, tb_ms, pf.ScheduleKind.ONE_F_ONE_B, cap, cap, args.fill_fraction)
             scfg = ServiceConfig(ccfg, "avg_jct", SJF, tuple(conf["batch_sizes"]), conf["max_batches"])
+            # the planners see the same idle tails as configs[1]'s Coordinators
+            cycles = [with_cooldown(pf.build_bubble_cycle(ccfg, s), int(stage_cooldown_ms(args, s, P) * 1000),
+                                    int(tail_min_ms(args) * 1000), args.tail_frac / 2)
+                      if tail_on_stage(args, s, P) else pf.build_bubble_cycle(ccfg, s) for s in range(P)]
             executors = [Executor(cap, job_seed=s) for s in range(P)]
             steps = []
 
@@ -413,9 +420,9 @@ def run_service_sweep(args, conf) -> None:
                 return t
 
             svc = FillService(scfg, registry, executors, run_iteration,
-                              flag_of=lambda s: engines[s].words.flag.value)
+                              flag_of=lambda s: engines[s].words.flag.value, cycles=cycles)
             rep = svc.run(jobs, max_rounds=60)
-            pred = predict(scfg, jobs)
+            pred = predict(scfg, jobs, cycles=cycles)
             for jid, res in rep.per_job.items():
                 res.predicted_completion_s = pred.get(jid)
             recs = [r for ex in executors for r in ex.records]
